@@ -1,0 +1,108 @@
+"""Oracle for the merge-tree / 0-dim persistence hot path -- TEST INFRASTRUCTURE.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s
+``cpu_baseline`` / ``--impl reference`` legs may import anything under
+``oracle/``.  The product package ``paper_2301_10838_b200`` never imports it,
+and this package never imports the product (they share no code; the only
+common input is the seeded field generator module ``synthfields``, which
+holds none of the method's arithmetic).
+
+Contents
+--------
+- ``merge_tree``  : O1, serial Kruskal/union-find with elder-rule pairing,
+                    plain C (``mt_oracle.c``), PAPER.md:139-148 + 180-200.
+- ``brute``       : O2, the triplet definition read literally by BFS over
+                    sublevel sets, tiny inputs only.
+- ``alg1``        : O3, the paper's Alg. 1-5 executed serially with the root
+                    guard readings of DESIGN.md (R4/R5), any edge order.
+- ``invariants``  : structural checks I1-I5 of DESIGN.md.
+
+Pins (tests/test_oracle_pins.py): O1 == O2 on exhaustive/random tiny grids;
+golden examples (tests/golden/*.txt, each cited); closed-form families
+(checkerboard, constant, ramp); scipy.ndimage.label Betti-0 counts at sampled
+thresholds.  No function here is "parity unpinned".
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+import threading
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "mt_oracle.c")
+_SO = os.path.join(_HERE, "libmt_oracle.so")
+_lock = threading.Lock()
+_lib = None
+
+PAIR_DTYPE = np.dtype([("birth_v", "<u4"), ("death_v", "<u4"), ("birth", "<f4"), ("death", "<f4")])
+
+OK, INVALID, TOO_LARGE, NONFINITE, NOMEM = 0, 1, 2, 3, 8
+
+
+class OracleError(RuntimeError):
+    def __init__(self, status):
+        super().__init__(f"oracle status {status}")
+        self.status = status
+
+
+def build(force: bool = False) -> str:
+    """Compile the C oracle with gcc (no -ffast-math: IEEE compares matter)."""
+    if force or not os.path.exists(_SO) or os.path.getmtime(_SO) < os.path.getmtime(_SRC):
+        tmp = _SO + f".tmp{os.getpid()}"
+        subprocess.check_call(["gcc", "-O2", "-std=c11", "-fPIC", "-shared", "-fno-fast-math",
+                               "-ffp-contract=off", _SRC, "-o", tmp, "-lm"])
+        os.replace(tmp, _SO)
+    return _SO
+
+
+def _load():
+    global _lib
+    with _lock:
+        if _lib is None:
+            lib = ctypes.CDLL(build())
+            lib.oracle_merge_tree.restype = ctypes.c_int
+            lib.oracle_merge_tree.argtypes = [
+                ctypes.c_void_p, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32,
+                ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p,
+                ctypes.POINTER(ctypes.c_uint64), ctypes.POINTER(ctypes.c_uint64)]
+            _lib = lib
+    return _lib
+
+
+def merge_tree(f: np.ndarray, dims, conn: int = 6, split: bool = False, want_pairs: bool = True):
+    """O1.  ``f``: float32 values, x fastest, ``dims`` = (nx, ny, nz).
+
+    Returns ``(T, pairs, n_pairs, n_ess)`` with ``T`` a uint64 array
+    (s << 32 | v) and ``pairs`` a PAIR_DTYPE array: finite pairs ascending by
+    birth vertex, then essential classes ascending (death = +inf).
+    """
+    lib = _load()
+    nx, ny, nz = (int(d) for d in dims)
+    f = np.ascontiguousarray(f, dtype=np.float32).reshape(-1)
+    n = nx * ny * nz
+    if f.size != n:
+        raise ValueError("f size does not match dims")
+    T = np.empty(n, dtype=np.uint64)
+    pairs = np.empty(n if want_pairs else 0, dtype=PAIR_DTYPE)
+    npairs, ness = ctypes.c_uint64(0), ctypes.c_uint64(0)
+    st = lib.oracle_merge_tree(f.ctypes.data if n else None, nx, ny, nz, int(conn), int(bool(split)),
+                               T.ctypes.data if n else None,
+                               pairs.ctypes.data if (want_pairs and n) else None,
+                               ctypes.byref(npairs), ctypes.byref(ness))
+    if st != OK:
+        raise OracleError(st)
+    k = npairs.value + ness.value
+    return T, (pairs[:k] if want_pairs else None), npairs.value, ness.value
+
+
+def unpack(T: np.ndarray):
+    """(s, v) halves of packed cells (s high, v low -- reading R11)."""
+    T = np.asarray(T, dtype=np.uint64)
+    return (T >> np.uint64(32)).astype(np.uint32), (T & np.uint64(0xFFFFFFFF)).astype(np.uint32)
+
+
+def pack(s, v):
+    return (np.asarray(s, dtype=np.uint64) << np.uint64(32)) | np.asarray(v, dtype=np.uint64)

@@ -1,0 +1,240 @@
+/*
+ * oracle/mt_oracle.c -- O1: serial union-find (Kruskal-style) merge tree +
+ * elder-rule 0-dimensional persistence pairs, written from the paper's plain
+ * definitions.  TEST INFRASTRUCTURE ONLY: nothing under paper_2301_10838_b200/
+ * may include, link or call this file; only tests/, __graft_entry__.smoke()
+ * and bench.py's cpu_baseline / --impl reference legs may.  It shares no code,
+ * header, table or constant with the CUDA path.
+ *
+ * What it computes (PAPER.md = /root/reference/PAPER.md):
+ *   - merge tree of f on a graph G=(V,E), sublevel sets G_c = {v : f(v) <= c}
+ *     (Sec. 2.1 "Merge Trees");
+ *   - computed "in O(m log n) time ... using the union-find data structure.
+ *     First, one sorts the vertices by values of the function.  Then the
+ *     algorithm goes over the sorted vertices ... (1) local minimum creates a
+ *     new component; (2) belongs to exactly one component; (3) multiple
+ *     components are merged";
+ *   - emitted as the normalized, minimal triplet representation
+ *     (Sec. 2.1 "Triplet merge trees"): one triplet (u,s,v)
+ *     per vertex u, v = deepest vertex of u's component of G_{f(s)};
+ *     (u,u,u) for the minimum of each connected component;
+ *   - persistence pairs (f(a), f(b)), one per branch (a = minimum,
+ *     b = saddle); which branch ends at a saddle follows the
+ *     branch semantics "a branch ... is created and ... merged with an older
+ *     component": the younger (higher) minimum dies.
+ *
+ * Readings: ties in f are broken by vertex
+ * id ascending (R1, simulation of simplicity); -0.0 == +0.0 as IEEE values
+ * (R2); NaN/Inf rejected (R3); split tree = merge tree of -f with the same
+ * ascending-id tie break (R16); grid ids x-fastest (R10); 4-/6-neighbour grid
+ * graph without periodic faces (R9).  Comparisons are plain IEEE float
+ * compares (no bit tricks); build WITHOUT -ffast-math.
+ *
+ * Packing of the output cell ("a pair can be packed into a
+ * 64-bit integer"): T[u] = (uint64)s << 32 | v  (reading R11: s high).
+ */
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+#include <math.h>
+
+#define OR_OK 0
+#define OR_INVALID 1
+#define OR_TOO_LARGE 2
+#define OR_NONFINITE 3
+#define OR_NOMEM 8
+
+typedef struct {
+    uint32_t birth_v, death_v;
+    float birth, death;
+} oracle_pair;
+
+typedef struct {
+    float g;     /* g = f (merge tree) or -f (split tree) */
+    uint32_t id; /* vertex id, the tie break */
+} vkey;
+
+/* less(a,b) := g(a) < g(b) || (g(a) == g(b) && a < b)    (reading R1) */
+static int key_less(float ga, uint32_t a, float gb, uint32_t b) {
+    if (ga < gb) return 1;
+    if (ga == gb && a < b) return 1;
+    return 0;
+}
+
+static int cmp_vkey(const void *pa, const void *pb) {
+    const vkey *a = (const vkey *)pa, *b = (const vkey *)pb;
+    if (key_less(a->g, a->id, b->g, b->id)) return -1;
+    if (key_less(b->g, b->id, a->g, a->id)) return 1;
+    return 0;
+}
+
+/* Disjoint sets: parent pointers, find with path halving,
+ * union by size. */
+static uint32_t ds_find(uint32_t *parent, uint32_t x) {
+    while (parent[x] != x) {
+        parent[x] = parent[parent[x]];
+        x = parent[x];
+    }
+    return x;
+}
+
+/* Grid neighbours of u: +-x, +-y, +-z inside the box (reading R9, R10). */
+static int grid_neighbours(uint64_t u, uint32_t nx, uint32_t ny, uint32_t nz, uint32_t out[6]) {
+    uint64_t x = u % nx, y = (u / nx) % ny, z = u / ((uint64_t)nx * ny);
+    uint64_t sxy = (uint64_t)nx * ny;
+    int k = 0;
+    if (x > 0) out[k++] = (uint32_t)(u - 1);
+    if (x + 1 < nx) out[k++] = (uint32_t)(u + 1);
+    if (y > 0) out[k++] = (uint32_t)(u - nx);
+    if (y + 1 < ny) out[k++] = (uint32_t)(u + nx);
+    if (z > 0) out[k++] = (uint32_t)(u - sxy);
+    if (z + 1 < nz) out[k++] = (uint32_t)(u + sxy);
+    return k;
+}
+
+/*
+ * oracle_merge_tree: returns OR_* status.
+ *   f        : n = nx*ny*nz float32 values, x fastest
+ *   conn     : 4 (2D, nz must be 1) or 6
+ *   split    : 0 = merge (join) tree of f; 1 = split tree (merge tree of -f)
+ *   T        : out, n words (s << 32 | v), may be NULL
+ *   pairs    : out, capacity >= n records, may be NULL; finite pairs by
+ *              ascending birth vertex, then essential classes by ascending
+ *              vertex (death_v = birth_v, death = +inf)
+ *   n_pairs, n_ess : out counts
+ */
+int oracle_merge_tree(const float *f, uint32_t nx, uint32_t ny, uint32_t nz, int conn, int split,
+                      uint64_t *T, oracle_pair *pairs, uint64_t *n_pairs, uint64_t *n_ess) {
+    if (!f && (uint64_t)nx * ny * nz) return OR_INVALID;
+    if (conn != 4 && conn != 6) return OR_INVALID;
+    if (conn == 4 && nz != 1) return OR_INVALID;
+    uint64_t n = (uint64_t)nx * ny * nz;
+    if (n > 4294967295ull) return OR_TOO_LARGE; /* 32-bit ids */
+    if (n_pairs) *n_pairs = 0;
+    if (n_ess) *n_ess = 0;
+    if (n == 0) return OR_OK;
+    for (uint64_t i = 0; i < n; i++)
+        if (!isfinite(f[i])) return OR_NONFINITE;
+
+    vkey *order = (vkey *)malloc(n * sizeof(vkey));
+    uint32_t *parent = (uint32_t *)malloc(n * sizeof(uint32_t));
+    uint32_t *size = (uint32_t *)malloc(n * sizeof(uint32_t));
+    uint32_t *cmin = (uint32_t *)malloc(n * sizeof(uint32_t));  /* deepest vertex of a set (valid at roots) */
+    uint32_t *death = (uint32_t *)malloc(n * sizeof(uint32_t)); /* saddle where a minimum's branch ends */
+    uint8_t *done = (uint8_t *)calloc(n, 1);                      /* swept already <=> less(w, u) */
+    uint64_t *Tl = T ? T : (uint64_t *)malloc(n * sizeof(uint64_t));
+    if (!order || !parent || !size || !cmin || !death || !done || !Tl) {
+        free(order); free(parent); free(size); free(cmin); free(death); free(done);
+        if (!T) free(Tl);
+        return OR_NOMEM;
+    }
+    float *g = (float *)malloc(n * sizeof(float)); /* g by vertex id */
+    if (!g) { free(order); free(parent); free(size); free(cmin); free(death); free(done); if (!T) free(Tl); return OR_NOMEM; }
+
+    for (uint64_t i = 0; i < n; i++) {
+        g[i] = split ? -f[i] : f[i];
+        order[i].g = g[i];
+        order[i].id = (uint32_t)i;
+        death[i] = UINT32_MAX;
+    }
+    /* "First, one sorts the vertices by values of the function". */
+    qsort(order, n, sizeof(vkey), cmp_vkey);
+
+    uint32_t nb[6], R[6];
+    for (uint64_t k = 0; k < n; k++) {
+        uint32_t u = order[k].id;
+        int deg = grid_neighbours(u, nx, ny, nz, nb);
+        /* R = distinct components of the lower neighbours of u */
+        int nr = 0;
+        for (int j = 0; j < deg; j++) {
+            uint32_t w = nb[j];
+            if (!done[w]) continue; /* not yet in the sublevel set <=> !less(w,u) */
+            uint32_t r = ds_find(parent, w);
+            int dup = 0;
+            for (int t = 0; t < nr; t++) dup |= (R[t] == r);
+            if (!dup) R[nr++] = r;
+        }
+        done[u] = 1;
+        if (nr == 0) {
+            /* (1) local minimum: "creates a new connected component" */
+            parent[u] = u;
+            size[u] = 1;
+            cmin[u] = u;
+            continue;
+        }
+        /* m* = deepest vertex over the merged components (the oldest branch). */
+        uint32_t mstar = cmin[R[0]];
+        for (int t = 1; t < nr; t++) {
+            uint32_t m = cmin[R[t]];
+            if (key_less(g[m], m, g[mstar], mstar)) mstar = m;
+        }
+        /* (3) merge: every younger minimum's branch ends at saddle u, merged
+         * into the branch of m* (elder rule; triplet (m, u, m*)). */
+        for (int t = 0; t < nr; t++) {
+            uint32_t m = cmin[R[t]];
+            if (m != mstar) {
+                Tl[m] = ((uint64_t)u << 32) | mstar;
+                death[m] = u;
+            }
+        }
+        /* u itself: (u, u, m*) -- m* is the deepest vertex of u's component
+         * of G_{f(u)} (minimality). */
+        Tl[u] = ((uint64_t)u << 32) | mstar;
+        /* union u and all of R, the union's deepest vertex is m* */
+        uint32_t root = R[0];
+        for (int t = 1; t < nr; t++) {
+            uint32_t a = root, b = R[t];
+            if (size[a] < size[b]) { uint32_t tmp = a; a = b; b = tmp; }
+            parent[b] = a;
+            size[a] += size[b];
+            root = a;
+        }
+        parent[u] = root;
+        size[root] += 1;
+        cmin[root] = mstar;
+    }
+    /* Survivors: the minimum of each connected component, triplet (m,m,m)
+     * (PAPER.md:190-191), essential class (f(m), +inf). */
+    uint64_t np = 0, ne = 0;
+    /* The deepest vertex of each final set is a minimum that never died:
+     * exactly one per connected component. */
+    for (uint64_t u = 0; u < n; u++) {
+        uint32_t r = ds_find(parent, (uint32_t)u);
+        if (cmin[r] == u) Tl[u] = ((uint64_t)u << 32) | u;
+    }
+    if (pairs) {
+        for (uint64_t u = 0; u < n; u++) {
+            if (death[u] != UINT32_MAX) {
+                pairs[np].birth_v = (uint32_t)u;
+                pairs[np].death_v = death[u];
+                pairs[np].birth = f[u];          /* values copied from the input f (reading R14) */
+                pairs[np].death = f[death[u]];
+                np++;
+            }
+        }
+        for (uint64_t u = 0; u < n; u++) {
+            uint32_t r = ds_find(parent, (uint32_t)u);
+            if (cmin[r] == u) {
+                pairs[np + ne].birth_v = (uint32_t)u;
+                pairs[np + ne].death_v = (uint32_t)u;
+                pairs[np + ne].birth = f[u];
+                pairs[np + ne].death = INFINITY;
+                ne++;
+            }
+        }
+    } else {
+        for (uint64_t u = 0; u < n; u++) {
+            if (death[u] != UINT32_MAX) np++;
+            else if (cmin[ds_find(parent, (uint32_t)u)] == u) ne++;
+        }
+    }
+    if (n_pairs) *n_pairs = np;
+    if (n_ess) *n_ess = ne;
+
+    free(order); free(parent); free(size); free(cmin); free(death); free(done); free(g);
+    if (!T) free(Tl);
+    return OR_OK;
+}
+
+/* Version tag so the Python loader can detect a stale build. */
+int oracle_abi_version(void) { return 1; }
