@@ -1,0 +1,353 @@
+#!/usr/bin/env python
+"""bench.py -- merge tree + 0-dim persistence diagram throughput on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c5] [--impl mt|reference]
+
+A step is one pass of the whole hot path (keys, steepest-descent
+init, CAS edge merge, repair, diagram) over one synthetic field: mt_compute +
+mt_diagram through the C ABI, inputs resident in HBM.  ``value`` is
+Mvertices/s over all ranks; ``e2e`` repeats the step through the public API
+with pinned HOST buffers (H2D of f, D2H of the triplet store and the diagram
+inside the timed region).  ``roofline`` reports the dominant kernel's
+algorithmic bytes per CUDA-event-timed
+launch against the measured HBM copy bandwidth.  ``cpu_baseline`` times the
+oracle O1 (serial C, 1 core) on a bounded sub-block of the same field.
+
+--impl reference times the oracle itself (the only "reference" this paper-only
+build has) on bounded samples of the same workload.
+Under torchrun (N > 1) every rank runs its own replica of the workload (the
+slab decomposition of SURVEY.md 8e is not built yet), reported as weak scaling.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "merge tree + 0-dim diagram Mvertices/s at 1/2/4/8 B200; % of HBM roofline"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--config", default="c5", choices=["c1", "c2", "c3", "c4", "c5"])
+    p.add_argument("--scale", type=int, default=None, help="override the grid edge (debug)")
+    p.add_argument("--impl", default="mt", choices=["mt", "reference"])
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--split", action="store_true", help="split tree (MT_FLAG_SPLIT_TREE)")
+    return p.parse_args()
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index: int):
+        self.dev = device_index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        self.lines = []
+        if self.proc is not None:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except Exception:
+                self.proc.kill()
+                out = ""
+            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+
+    def summary(self):
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in getattr(self, "lines", []):
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax = float(parts[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def field_for(cfg, scale, device):
+    from paper_2301_10838_b200 import fields
+    return fields.make(cfg, scale=scale, device=device)
+
+
+def oracle_rate(f, dims, conn, planes, split=False):
+    """O1 on the first `planes` z-planes (2D: rows) of the field; returns (Mv/s, n, seconds)."""
+    import oracle
+    nx, ny, nz = dims
+    if nz > 1:
+        sub_dims = (nx, ny, min(planes, nz))
+    else:
+        sub_dims = (nx, min(max(1, planes * 64), ny), 1)
+    n = sub_dims[0] * sub_dims[1] * sub_dims[2]
+    sub = np.ascontiguousarray(f[:n])
+    conn = 4 if sub_dims[2] == 1 else conn
+    t0 = time.perf_counter()
+    oracle.merge_tree(sub, sub_dims, conn=conn, split=split)
+    dt = time.perf_counter() - t0
+    return n / dt / 1e6, n, dt, sub_dims
+
+
+def cpu_sample_planes(cfg, target_s):
+    # oracle throughput is ~1-2 Mv/s on one core; pick the number of planes that
+    # gives about target_s seconds of work
+    from paper_2301_10838_b200.fields import CONFIGS
+    nx, ny, nz = CONFIGS[cfg]["dims"]
+    per_plane = nx * ny if nz > 1 else nx * 64
+    rate = 1.3e6
+    return max(1, int(target_s * rate / per_plane))
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the oracle O1 timed on bounded samples of the workload."""
+    if rank != 0:
+        return
+    import oracle  # noqa: F401  (test infrastructure; the one place bench executes it besides cpu_baseline)
+    f, dims, conn = field_for(args.config, args.scale, "cuda" if args.config == "c5" and _has_cuda() else "cpu")
+    planes = cpu_sample_planes(args.config, 3.0)
+    for _ in range(args.warmup):
+        oracle_rate(f, dims, conn, planes, args.split)
+    times, nv = [], 0
+    for _ in range(args.steps):
+        r, n, dt, sub = oracle_rate(f, dims, conn, planes, args.split)
+        times.append(dt)
+        nv = n
+    total = sum(times)
+    value = nv * args.steps / total / 1e6
+    cores = 1
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "Mvertices/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic", "config": _config(args, dims, conn),
+        "cpu_baseline": {"value": value, "unit": "Mvertices/s", "cores": cores, "kind": "oracle",
+                         "sample": f"O1 (serial C union-find) on the first {sub} sub-grid of the "
+                                   f"{args.config} field per step"},
+        "e2e": {"value": value, "unit": "Mvertices/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def _has_cuda():
+    import torch
+    return torch.cuda.is_available()
+
+
+def _config(args, dims, conn):
+    from paper_2301_10838_b200.fields import CONFIGS
+    return {"workload": f"{args.config}: {CONFIGS[args.config]['name']}" + (" (split tree)" if args.split else ""),
+            "dims": list(dims), "connectivity": conn, "vertices": int(np.prod(dims)),
+            "l2_policy": "inputs larger than L2 + 512 MiB L2 flush before every timed step",
+            "parallelism": f"replicas{args.gpus}" if args.gpus > 1 else "single"}
+
+
+# algorithmic bytes per vertex / per record of each kernel
+ALG_BYTES = {
+    "init_descent": lambda n, rec: 12 * n,          # read f (4) + write T (8)
+    "merge_edges": lambda n, rec: 12 * n,           # read f (4) + read T (8) over every edge's endpoints
+    "repair_diagram": lambda n, rec: 20 * n + 16 * rec,  # read f (4) + read T (8) + write T (8) + records
+    "finish_diagram": lambda n, rec: 0,
+}
+
+
+def run_mt(args, rank, world):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2301_10838_b200 import _lib
+
+    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
+    torch.cuda.set_device(dev)
+    f_np, dims, conn = field_for(args.config, args.scale, dev if args.config == "c5" else "cpu")
+    n = int(np.prod(dims))
+    f = torch.from_numpy(f_np).to(dev)
+    mt = _lib.MergeTree(dims, conn, device=dev.index)
+    T = torch.empty(n, dtype=torch.int64, device=dev)
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream()
+    flags = _lib.MT_FLAG_SPLIT_TREE if args.split else 0
+
+    def step():
+        _lib.mt_compute(mt.ctx, f.data_ptr(), T.data_ptr(), flags, stream)
+        st, npairs, ness = _lib.mt_diagram(mt.ctx, 0, 0, stream)
+        if st != _lib.MT_OK:
+            raise _lib.MTError(st, "mt_diagram")
+        return npairs, ness
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    _lib.mt_set_profiling(mt.ctx, True)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    kt = {}
+    launches = 0
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(dev.index) as clk:
+        for i in range(args.steps):
+            flush.fill_(i & 0xff)  # evict L2 between timed steps (outside the events)
+            ev[i][0].record(stream)
+            npairs, ness = step()
+            ev[i][1].record(stream)
+            launches += _lib.mt_last_launch_count(mt.ctx)
+            for name, ms in _lib.mt_kernel_times(mt.ctx):
+                kt.setdefault(name, []).append(ms)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+    _lib.mt_set_profiling(mt.ctx, False)
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    my_ms = sum(step_ms)
+    if world > 1:
+        t = torch.tensor([my_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        max_ms = float(t.item())
+    else:
+        max_ms = my_ms
+    ms_per_step = max_ms / args.steps
+    value = world * n / (ms_per_step * 1e-3) / 1e6
+
+    # roofline of the dominant kernel
+    peak, peak_kind = peaks()
+    recs = npairs + ness
+    avg = {k: statistics.mean(v) for k, v in kt.items()}
+    dom = max((k for k in avg if k in ALG_BYTES), key=lambda k: avg[k])
+    alg = ALG_BYTES[dom](n, recs)
+    achieved = alg / (avg[dom] * 1e-3) / 1e9
+    traffic = None
+    prof_path = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(prof_path):
+        try:
+            traffic = json.load(open(prof_path)).get(args.config, {}).get(dom)
+        except Exception:
+            traffic = None
+    roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
+                "alg_bytes_per_launch": alg, "kernel_ms": avg[dom],
+                "kernel_share_of_step": avg[dom] / ms_per_step,
+                "kernels_ms": avg,
+                "step_alg_bytes_per_vertex": 12 + 16 * recs / n,
+                "step_frac": (12 * n + 16 * recs) / (ms_per_step * 1e-3) / 1e9 / peak}
+
+    # end to end through the public API with pinned host buffers
+    e2e = None
+    if not args.no_e2e:
+        f_host = torch.from_numpy(f_np).pin_memory()
+        T_host = torch.empty(n, dtype=torch.int64).pin_memory()
+        rec_dev = torch.empty(((n + 1) // 2 + 1, 4), dtype=torch.int32, device=dev)
+        rec_host = torch.empty_like(rec_dev, device="cpu").pin_memory()
+        f_dev = torch.empty_like(f)
+        e2e_steps = max(2, min(args.steps, 5))
+        h2d = d2h = 0
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0.record(stream)
+        for _ in range(e2e_steps):
+            f_dev.copy_(f_host, non_blocking=True)
+            _lib.mt_compute(mt.ctx, f_dev.data_ptr(), T.data_ptr(), flags, stream)
+            st, a, b = _lib.mt_diagram(mt.ctx, rec_dev.data_ptr(), rec_dev.shape[0], stream)
+            T_host.copy_(T, non_blocking=True)
+            rec_host[: a + b].copy_(rec_dev[: a + b], non_blocking=True)
+            h2d = 4 * n
+            d2h = 8 * n + 16 * (a + b)
+        t1.record(stream)
+        torch.cuda.synchronize()
+        e_ms = t0.elapsed_time(t1)
+        if world > 1:
+            t = torch.tensor([e_ms], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e_ms = float(t.item())
+        e2e = {"value": world * n * e2e_steps / (e_ms * 1e-3) / 1e6, "unit": "Mvertices/s",
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": e2e_steps}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        planes = cpu_sample_planes(args.config, 15.0)
+        r, nv, dt, sub = oracle_rate(f_np, dims, conn, planes, args.split)
+        cpu = {"value": r, "unit": "Mvertices/s", "cores": 1, "kind": "oracle",
+               "sample": f"O1 (serial C union-find + elder rule) on the first {sub} sub-grid "
+                         f"({nv} vertices, {dt:.1f} s) of the same field, 1 of {os.cpu_count()} host cores"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "Mvertices/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (seeded generator, paper_2301_10838_b200/fields.py)",
+            "config": _config(args, dims, conn),
+            "pairs": npairs, "essential": ness,
+            "step_ms": {"median": statistics.median(step_ms), "min": min(step_ms), "max": max(step_ms)},
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
+        dist.init_process_group("nccl")
+    try:
+        run_mt(args, rank, world)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

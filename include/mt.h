@@ -1,0 +1,137 @@
+/*
+ * mt.h -- C ABI of the B200-native triplet merge tree + 0-dimensional
+ * persistence diagram library (libmt_b200.so).  arXiv 2301.10838.
+ *
+ * Problem (PAPER.md = the paper's text):
+ *   f : V -> R on the vertices of a grid graph G = (V, E) ("we connect
+ *   neighboring grid points, obtaining a graph with the function defined on
+ *   its vertices"; "f : V -> R").
+ *   Output 1 -- the merge tree as the normalized, minimal triplet map
+ *   T[u] = (s, v): one triplet (u, s, v) per vertex u with
+ *   f(v) < f(u) <= f(s), u and v in one component of G_{f(s)}, v the deepest
+ *   vertex of that component; (u, u, u) for the minimum of a component.
+ *   Output 2 -- the 0-dimensional persistence diagram, "one point per branch
+ *   (a, b) of the merge tree": a pair (f(u), f(s)) for every
+ *   triplet with s != u, and one essential class (f(m), +inf) per component.
+ *
+ * Readings fixed for both this library and the oracle:
+ *   R1 ties in f are broken by vertex id (lexicographic (value, id) order);
+ *   R2 -0.0 and +0.0 are equal values;  R3 NaN/+-Inf are rejected;
+ *   R9/R10 grid: 4-connectivity in 2D (nz = 1), 6-connectivity in 3D, no
+ *   periodic faces, ids x fastest: id = x + nx * (y + ny * z);
+ *   R11 packed cell = (uint64)s << 32 | v ("a pair can be packed into a 64-bit
+ *   integer"; s in the high half);
+ *   R14 diagram values are copied from the input f (also for the split tree);
+ *   R16 split tree = merge tree of -f with the id tie break unchanged.
+ *
+ * Conventions: every data pointer is a DEVICE pointer unless marked (host).
+ * The caller owns all memory (static, pre-sized device
+ * buffers; the library never allocates on the hot path).  No call throws;
+ * every call returns mt_status.  Data errors found on the device (non-finite
+ * input, output capacity) are sticky and reported by the next syncing call
+ * (mt_diagram, mt_last_error).  A context is bound to one device and is not
+ * thread-safe; calls on one context must be issued from one host thread.
+ */
+#ifndef MT_B200_H
+#define MT_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct mt_ctx mt_ctx; /* opaque */
+typedef void *mt_stream_t;    /* a cudaStream_t (0 = legacy default stream) */
+
+typedef enum {
+    MT_OK = 0,
+    MT_ERR_INVALID_ARG = 1, /* NULL pointer, conn not in {4,6}, conn 4 with nz != 1, bad rank */
+    MT_ERR_TOO_LARGE = 2,   /* nx*ny*nz > 2^32 - 1: 32-bit vertex ids */
+    MT_ERR_NONFINITE = 3,   /* NaN or +-Inf in f (reading R3); sticky */
+    MT_ERR_CUDA = 4,        /* a CUDA runtime call failed */
+    MT_ERR_NCCL = 5,        /* reserved for the multi-GPU exchange */
+    MT_ERR_STATE = 6,       /* call out of order, e.g. mt_diagram before mt_compute */
+    MT_ERR_CAPACITY = 7,    /* output buffer too small; required count returned */
+    MT_ERR_WORKSPACE = 8    /* workspace NULL, too small or misaligned (needs 256 B) */
+} mt_status;
+
+enum { MT_FLAG_SPLIT_TREE = 1u }; /* merge tree of -f (split tree) */
+
+/* One diagram point, 16 bytes.  Finite pair: birth_v = the minimum u,
+ * death_v = the saddle s, birth = f[u], death = f[s].  Essential class:
+ * death_v = birth_v = the component minimum, death = +INFINITY. */
+typedef struct {
+    uint32_t birth_v, death_v;
+    float birth, death;
+} mt_pair;
+
+/* Bytes of device workspace mt_create needs for grid dims[3] = {nx,ny,nz}
+ * (host array) and connectivity conn.  0 on invalid arguments. */
+size_t mt_workspace_bytes(const uint32_t dims[3], int conn);
+
+/* Create a context for an nx*ny*nz grid (host dims; 2D: nz = 1) on CUDA
+ * device `cuda_device`.  `workspace` (device, >= mt_workspace_bytes, 256-B
+ * aligned) stays owned by the caller and must outlive the context.
+ * n = 0 is allowed (every compute is empty).  On error *out is set to NULL. */
+mt_status mt_create(mt_ctx **out, const uint32_t dims[3], int conn, int cuda_device,
+                    void *workspace, size_t workspace_bytes);
+
+/* Compute the merge tree of f (device, n float32, x fastest; borrowed until
+ * the stream reaches the end of this call's work) into `triplets` (device,
+ * n uint64, written: the normalized minimal store T[u] = s << 32 | v), and the
+ * persistence diagram into the context (see mt_diagram).  Asynchronous on
+ * `stream`: kernels only, no host synchronisation, no allocation.
+ * flags: 0 or MT_FLAG_SPLIT_TREE.
+ * Steps: keys (value, id) -> steepest-descent init with
+ * tile-local descent -> concurrent CAS edge merge (Alg. 3) -> repair by
+ * representatives (Alg. 4/5) fused with the ordered diagram compaction. */
+mt_status mt_compute(mt_ctx *ctx, const float *f, uint64_t *triplets, uint32_t flags,
+                     mt_stream_t stream);
+
+/* Register a caller-owned device buffer that later mt_compute calls write
+ * the diagram into directly (zero-copy); capacity in records.  NULL detaches.
+ * Without a registered buffer the diagram is kept in the workspace. */
+mt_status mt_set_diagram_output(mt_ctx *ctx, mt_pair *buf, uint64_t capacity);
+
+/* Wait for the last mt_compute on `stream`, then report the diagram:
+ * *n_pairs (host) finite pairs ordered by ascending birth_v, followed by
+ * *n_essential (host) essential classes ordered by ascending vertex.
+ * If `out` (device) is non-NULL and is not the registered buffer, the
+ * n_pairs + n_essential records are copied there (capacity in records;
+ * MT_ERR_CAPACITY if too small, counts still returned).  `out` may be NULL
+ * to query counts only.  Returns the sticky data error if any (e.g.
+ * MT_ERR_NONFINITE; the triplets are then unspecified). */
+mt_status mt_diagram(mt_ctx *ctx, mt_pair *out, uint64_t capacity, uint64_t *n_pairs,
+                     uint64_t *n_essential, mt_stream_t stream);
+
+/* Device pointer to the diagram records of the last compute (registered
+ * buffer or workspace); valid until the next mt_compute.  Syncs like
+ * mt_diagram. */
+mt_status mt_diagram_view(mt_ctx *ctx, const mt_pair **records, uint64_t *n_pairs,
+                          uint64_t *n_essential, mt_stream_t stream);
+
+/* Synchronise `stream` and return the sticky error state of the context. */
+mt_status mt_last_error(mt_ctx *ctx, mt_stream_t stream);
+
+/* Kernel launches issued by the most recent mt_compute (host counter). */
+uint32_t mt_last_launch_count(const mt_ctx *ctx);
+
+/* Per-kernel device time (ms) of the most recent mt_compute, measured with
+ * CUDA events recorded on `stream` when profiling is enabled with
+ * mt_set_profiling(ctx, 1).  names[i] are static strings.  Returns the
+ * number of entries written (<= max). */
+mt_status mt_set_profiling(mt_ctx *ctx, int enable);
+int mt_kernel_times(mt_ctx *ctx, const char **names, float *ms, int max);
+
+const char *mt_status_string(mt_status s);
+void mt_destroy(mt_ctx *ctx);
+
+/* Version of this ABI (bumped on any signature change). */
+int mt_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MT_B200_H */

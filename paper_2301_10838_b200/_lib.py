@@ -1,0 +1,234 @@
+"""Thin ctypes binding of libmt_b200.so (include/mt.h) -- argument marshalling only.
+
+Every step of the hot path runs in the library's sm_100a kernels; this module
+only passes device pointers (torch tensors' ``data_ptr()``), sizes and the
+current CUDA stream.  There is no CPU fallback: if the shared library is
+missing or a call fails, an exception is raised.
+
+Functions carry the C names (``mt_create``, ``mt_compute``, ``mt_diagram``,
+...); ``MergeTree`` is a convenience owner of a context + its workspace.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+SO_PATH = os.path.join(_PKG, "libmt_b200.so")
+
+MT_OK, MT_ERR_INVALID_ARG, MT_ERR_TOO_LARGE, MT_ERR_NONFINITE, MT_ERR_CUDA = 0, 1, 2, 3, 4
+MT_ERR_NCCL, MT_ERR_STATE, MT_ERR_CAPACITY, MT_ERR_WORKSPACE = 5, 6, 7, 8
+MT_FLAG_SPLIT_TREE = 1
+
+PAIR_DTYPE = np.dtype([("birth_v", "<u4"), ("death_v", "<u4"), ("birth", "<f4"), ("death", "<f4")])
+
+# every symbol include/mt.h declares (checked by tests/test_abi_cpu.py)
+EXPORTS = ["mt_workspace_bytes", "mt_create", "mt_compute", "mt_set_diagram_output", "mt_diagram",
+           "mt_diagram_view", "mt_last_error", "mt_last_launch_count", "mt_set_profiling", "mt_kernel_times",
+           "mt_status_string", "mt_destroy", "mt_abi_version"]
+
+
+class MTError(RuntimeError):
+    def __init__(self, status: int, where: str):
+        self.status = status
+        super().__init__(f"{where}: {status_string(status)} (status {status})")
+
+
+_lib = None
+
+
+def load(build_if_missing: bool = False):
+    """Load the in-tree libmt_b200.so (fails loudly if absent)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(SO_PATH):
+        if build_if_missing:
+            from . import build
+            build.build()
+        else:
+            raise ImportError(f"{SO_PATH} is missing: run `python -m paper_2301_10838_b200.build` "
+                              "(there is no CPU fallback)")
+    lib = ctypes.CDLL(SO_PATH)
+    u32p = ctypes.POINTER(ctypes.c_uint32)
+    u64p = ctypes.POINTER(ctypes.c_uint64)
+    vp = ctypes.c_void_p
+    sig = {
+        "mt_workspace_bytes": (ctypes.c_size_t, [u32p, ctypes.c_int]),
+        "mt_create": (ctypes.c_int, [ctypes.POINTER(vp), u32p, ctypes.c_int, ctypes.c_int, vp, ctypes.c_size_t]),
+        "mt_compute": (ctypes.c_int, [vp, vp, vp, ctypes.c_uint32, vp]),
+        "mt_set_diagram_output": (ctypes.c_int, [vp, vp, ctypes.c_uint64]),
+        "mt_diagram": (ctypes.c_int, [vp, vp, ctypes.c_uint64, u64p, u64p, vp]),
+        "mt_diagram_view": (ctypes.c_int, [vp, ctypes.POINTER(vp), u64p, u64p, vp]),
+        "mt_last_error": (ctypes.c_int, [vp, vp]),
+        "mt_last_launch_count": (ctypes.c_uint32, [vp]),
+        "mt_set_profiling": (ctypes.c_int, [vp, ctypes.c_int]),
+        "mt_kernel_times": (ctypes.c_int, [vp, ctypes.POINTER(ctypes.c_char_p), ctypes.POINTER(ctypes.c_float),
+                                           ctypes.c_int]),
+        "mt_status_string": (ctypes.c_char_p, [ctypes.c_int]),
+        "mt_destroy": (None, [vp]),
+        "mt_abi_version": (ctypes.c_int, []),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+def status_string(st: int) -> str:
+    try:
+        return load().mt_status_string(st).decode()
+    except ImportError:
+        return f"status {st}"
+
+
+def _dims(dims):
+    return (ctypes.c_uint32 * 3)(*[int(d) for d in dims])
+
+
+def _stream_handle(stream):
+    import torch
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+def _check(st, where):
+    if st != MT_OK:
+        raise MTError(st, where)
+
+
+# ---- C-named wrappers -------------------------------------------------------
+
+def mt_workspace_bytes(dims, conn: int) -> int:
+    return int(load().mt_workspace_bytes(_dims(dims), int(conn)))
+
+
+def mt_create(dims, conn: int, device: int, workspace_ptr: int, workspace_bytes: int):
+    h = ctypes.c_void_p()
+    _check(load().mt_create(ctypes.byref(h), _dims(dims), int(conn), int(device), ctypes.c_void_p(workspace_ptr),
+                            ctypes.c_size_t(workspace_bytes)), "mt_create")
+    return h
+
+
+def mt_compute(ctx, f_ptr: int, triplets_ptr: int, flags: int = 0, stream=None):
+    _check(load().mt_compute(ctx, ctypes.c_void_p(f_ptr), ctypes.c_void_p(triplets_ptr), int(flags),
+                             _stream_handle(stream)), "mt_compute")
+
+
+def mt_set_diagram_output(ctx, buf_ptr: int, capacity: int):
+    _check(load().mt_set_diagram_output(ctx, ctypes.c_void_p(buf_ptr), ctypes.c_uint64(capacity)),
+           "mt_set_diagram_output")
+
+
+def mt_diagram(ctx, out_ptr: int = 0, capacity: int = 0, stream=None):
+    """Returns (status, n_pairs, n_essential); raises only on CUDA/state errors."""
+    npairs, ness = ctypes.c_uint64(0), ctypes.c_uint64(0)
+    st = load().mt_diagram(ctx, ctypes.c_void_p(out_ptr or None), ctypes.c_uint64(capacity), ctypes.byref(npairs),
+                           ctypes.byref(ness), _stream_handle(stream))
+    if st in (MT_ERR_CUDA, MT_ERR_STATE, MT_ERR_INVALID_ARG):
+        raise MTError(st, "mt_diagram")
+    return st, npairs.value, ness.value
+
+
+def mt_diagram_view(ctx, stream=None):
+    ptr, npairs, ness = ctypes.c_void_p(), ctypes.c_uint64(0), ctypes.c_uint64(0)
+    st = load().mt_diagram_view(ctx, ctypes.byref(ptr), ctypes.byref(npairs), ctypes.byref(ness),
+                                _stream_handle(stream))
+    if st in (MT_ERR_CUDA, MT_ERR_STATE, MT_ERR_INVALID_ARG):
+        raise MTError(st, "mt_diagram_view")
+    return st, ptr.value, npairs.value, ness.value
+
+
+def mt_last_error(ctx, stream=None) -> int:
+    return int(load().mt_last_error(ctx, _stream_handle(stream)))
+
+
+def mt_last_launch_count(ctx) -> int:
+    return int(load().mt_last_launch_count(ctx))
+
+
+def mt_set_profiling(ctx, enable: bool):
+    _check(load().mt_set_profiling(ctx, int(bool(enable))), "mt_set_profiling")
+
+
+def mt_kernel_times(ctx, max_entries: int = 8):
+    names = (ctypes.c_char_p * max_entries)()
+    ms = (ctypes.c_float * max_entries)()
+    k = load().mt_kernel_times(ctx, names, ms, max_entries)
+    return [(names[i].decode(), float(ms[i])) for i in range(k)]
+
+
+def mt_destroy(ctx):
+    load().mt_destroy(ctx)
+
+
+# ---- convenience owner --------------------------------------------------------
+
+class MergeTree:
+    """A context for one grid shape on one device, owning its workspace (a torch tensor)."""
+
+    def __init__(self, dims, conn: int = 6, device=None):
+        import torch
+        self.dims = tuple(int(d) for d in dims)
+        self.conn = int(conn)
+        self.n = self.dims[0] * self.dims[1] * self.dims[2]
+        dev = torch.device("cuda", torch.cuda.current_device() if device is None else int(device)) \
+            if not isinstance(device, torch.device) else device
+        self.device = dev
+        nbytes = mt_workspace_bytes(self.dims, self.conn)
+        if nbytes == 0:
+            raise MTError(MT_ERR_INVALID_ARG, "mt_workspace_bytes")
+        self.workspace = torch.empty(nbytes + 256, dtype=torch.uint8, device=dev)
+        ptr = self.workspace.data_ptr()
+        self._ws_ptr = (ptr + 255) // 256 * 256
+        self.ctx = mt_create(self.dims, self.conn, dev.index, self._ws_ptr, nbytes)
+        self._out = None
+
+    def __del__(self):
+        ctx = getattr(self, "ctx", None)
+        if ctx is not None and _lib is not None:
+            _lib.mt_destroy(ctx)
+            self.ctx = None
+
+    def set_diagram_output(self, buf):
+        """Register a (k, 4) int32 CUDA tensor as the zero-copy diagram target (None detaches)."""
+        self._out = buf
+        mt_set_diagram_output(self.ctx, buf.data_ptr() if buf is not None else 0, buf.shape[0] if buf is not None else 0)
+
+    def compute(self, f, triplets=None, split: bool = False, stream=None):
+        """f: float32 CUDA tensor with n elements (x fastest).  Returns the int64 tensor
+        holding the uint64 cells s << 32 | v (asynchronous)."""
+        import torch
+        if f.dtype != torch.float32 or not f.is_cuda or not f.is_contiguous() or f.numel() != self.n:
+            raise ValueError("f must be a contiguous float32 CUDA tensor with nx*ny*nz elements")
+        if triplets is None:
+            triplets = torch.empty(self.n, dtype=torch.int64, device=f.device)
+        mt_compute(self.ctx, f.data_ptr(), triplets.data_ptr(), MT_FLAG_SPLIT_TREE if split else 0, stream)
+        return triplets
+
+    def diagram(self, stream=None, copy: bool = True):
+        """Synchronises; returns (records (k,4) int32 CUDA tensor, n_pairs, n_essential)."""
+        import torch
+        st, ptr, npairs, ness = mt_diagram_view(self.ctx, stream)
+        if st != MT_OK:
+            raise MTError(st, "mt_diagram")
+        k = npairs + ness
+        out = torch.empty((k, 4), dtype=torch.int32, device=self.device)
+        if k:
+            st, a, b = mt_diagram(self.ctx, out.data_ptr(), k, stream)
+            _check(st, "mt_diagram")
+        return out, npairs, ness
+
+    def last_launch_count(self):
+        return mt_last_launch_count(self.ctx)
+
+
+def pairs_to_numpy(records) -> np.ndarray:
+    """(k, 4) int32 tensor -> structured numpy array with PAIR_DTYPE."""
+    a = records.detach().cpu().contiguous().numpy()
+    return a.view(PAIR_DTYPE).reshape(-1)

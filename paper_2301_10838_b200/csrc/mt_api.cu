@@ -1,0 +1,317 @@
+// mt_api.cu -- the C ABI of libmt_b200 (declared and documented in
+// include/mt.h): context, caller-owned workspace layout, sticky errors, stream
+// plumbing and the launch sequence of the hot path:
+//   zero counters -> K1+K2 init_descent -> K3 merge_edges
+//   -> K4+K5 repair_diagram -> finish_diagram
+// All launches are asynchronous on the caller's stream; only mt_diagram /
+// mt_diagram_view / mt_last_error synchronise.
+#include <cstdio>
+#include <cstring>
+#include <new>
+
+#include "common.cuh"
+#include "kernels.cuh"
+#include "mt.h"
+
+namespace {
+
+constexpr size_t ALIGN = 256;
+constexpr uint32_t ESS_CAP = 64;  // essential classes = connected components (1 per grid)
+constexpr int MAX_EVENTS = 8;
+
+size_t align_up(size_t x) { return (x + ALIGN - 1) / ALIGN * ALIGN; }
+
+struct Layout {
+    size_t counters, status, ess, pairs, total;
+    uint64_t ntiles, pairs_cap;
+};
+
+bool valid_dims(const uint32_t dims[3], int conn) {
+    if (!dims) return false;
+    if (conn != 4 && conn != 6) return false;
+    if (conn == 4 && dims[2] > 1) return false;
+    return true;
+}
+
+Layout layout_for(uint64_t n) {
+    Layout L{};
+    L.ntiles = n ? mt::repair_tiles(n) : 0;
+    // finite pairs <= #minima - 1 and strict minima form an independent set of
+    // the grid graph, so at most ceil(n/2) records in total (+1 slack).
+    L.pairs_cap = n ? (n + 1) / 2 + 1 : 0;
+    size_t off = 0;
+    L.counters = off;
+    off += align_up(mt::CTR_COUNT * sizeof(uint64_t));
+    L.status = off;  // contiguous with counters: one memset zeroes both
+    off += align_up(L.ntiles * sizeof(uint64_t));
+    L.ess = off;
+    off += align_up(ESS_CAP * sizeof(mt_pair));
+    L.pairs = off;
+    off += align_up(L.pairs_cap * sizeof(mt_pair));
+    L.total = off;
+    return L;
+}
+
+}  // namespace
+
+struct mt_ctx {
+    uint32_t nx, ny, nz;
+    uint64_t n;
+    int conn;
+    int device;
+    int num_sms;
+    char* ws;
+    size_t ws_bytes;
+    Layout L;
+    mt_pair* reg_out = nullptr;
+    uint64_t reg_cap = 0;
+    bool computed = false;
+    mt_status sticky = MT_OK;
+    uint64_t* host_ctr = nullptr;  // pinned
+    uint32_t launches = 0;
+    bool profiling = false;
+    cudaEvent_t ev[MAX_EVENTS + 1] = {};
+    const char* ev_name[MAX_EVENTS] = {};
+    int nev = 0;
+};
+
+namespace {
+
+struct DeviceGuard {
+    int prev = -1;
+    bool ok = true;
+    explicit DeviceGuard(int dev) {
+        if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+        if (prev != dev) ok = cudaSetDevice(dev) == cudaSuccess;
+    }
+    ~DeviceGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
+
+unsigned long long* counters_of(mt_ctx* c) { return reinterpret_cast<unsigned long long*>(c->ws + c->L.counters); }
+mt_pair* target_of(mt_ctx* c, uint64_t* cap) {
+    if (c->reg_out) {
+        *cap = c->reg_cap;
+        return c->reg_out;
+    }
+    *cap = c->L.pairs_cap;
+    return reinterpret_cast<mt_pair*>(c->ws + c->L.pairs);
+}
+
+void mark(mt_ctx* c, const char* name, cudaStream_t s) {
+    if (!c->profiling || c->nev >= MAX_EVENTS) return;
+    c->ev_name[c->nev] = name;
+    cudaEventRecord(c->ev[c->nev], s);
+    c->nev++;
+}
+
+// Sync the stream, read the device counters, fold device error bits into the
+// sticky status.
+mt_status sync_counters(mt_ctx* c, cudaStream_t s) {
+    if (!c->computed) return MT_ERR_STATE;
+    if (c->n == 0) {
+        c->host_ctr[mt::CTR_FIN] = 0;
+        c->host_ctr[mt::CTR_ESS] = 0;
+        c->host_ctr[mt::CTR_ERR] = 0;
+        return c->sticky;
+    }
+    if (cudaMemcpyAsync(c->host_ctr, counters_of(c), mt::CTR_COUNT * sizeof(uint64_t), cudaMemcpyDeviceToHost, s) !=
+            cudaSuccess ||
+        cudaStreamSynchronize(s) != cudaSuccess)
+        return c->sticky = MT_ERR_CUDA;
+    const uint64_t err = c->host_ctr[mt::CTR_ERR];
+    if (err & mt::ERR_NONFINITE) c->sticky = MT_ERR_NONFINITE;
+    else if (err & (mt::ERR_CAPACITY | mt::ERR_ESS_CAPACITY)) c->sticky = MT_ERR_CAPACITY;
+    return c->sticky;
+}
+
+}  // namespace
+
+extern "C" {
+
+int mt_abi_version(void) { return 1; }
+
+const char* mt_status_string(mt_status s) {
+    switch (s) {
+        case MT_OK: return "ok";
+        case MT_ERR_INVALID_ARG: return "invalid argument";
+        case MT_ERR_TOO_LARGE: return "grid too large for 32-bit vertex ids";
+        case MT_ERR_NONFINITE: return "non-finite value in f";
+        case MT_ERR_CUDA: return "CUDA error";
+        case MT_ERR_NCCL: return "NCCL error";
+        case MT_ERR_STATE: return "call out of order";
+        case MT_ERR_CAPACITY: return "output capacity too small";
+        case MT_ERR_WORKSPACE: return "workspace missing, too small or misaligned";
+    }
+    return "unknown status";
+}
+
+size_t mt_workspace_bytes(const uint32_t dims[3], int conn) {
+    if (!valid_dims(dims, conn)) return 0;
+    const uint64_t n = uint64_t(dims[0]) * dims[1] * dims[2];
+    if (n > 0xffffffffull) return 0;
+    return layout_for(n).total;
+}
+
+mt_status mt_create(mt_ctx** out, const uint32_t dims[3], int conn, int cuda_device, void* workspace,
+                    size_t workspace_bytes) {
+    if (!out) return MT_ERR_INVALID_ARG;
+    *out = nullptr;
+    if (!valid_dims(dims, conn)) return MT_ERR_INVALID_ARG;
+    const uint64_t n = uint64_t(dims[0]) * dims[1] * dims[2];
+    if (n > 0xffffffffull) return MT_ERR_TOO_LARGE;
+    const Layout L = layout_for(n);
+    if (!workspace || workspace_bytes < L.total || (reinterpret_cast<uintptr_t>(workspace) % ALIGN))
+        return MT_ERR_WORKSPACE;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess) return MT_ERR_CUDA;
+    if (cuda_device < 0 || cuda_device >= ndev) return MT_ERR_INVALID_ARG;
+    DeviceGuard g(cuda_device);
+    if (!g.ok) return MT_ERR_CUDA;
+    mt_ctx* c = new (std::nothrow) mt_ctx();
+    if (!c) return MT_ERR_CUDA;
+    c->nx = dims[0];
+    c->ny = dims[1];
+    c->nz = dims[2];
+    c->n = n;
+    c->conn = conn;
+    c->device = cuda_device;
+    c->ws = static_cast<char*>(workspace);
+    c->ws_bytes = workspace_bytes;
+    c->L = L;
+    if (cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, cuda_device) != cudaSuccess ||
+        cudaMallocHost(&c->host_ctr, mt::CTR_COUNT * sizeof(uint64_t)) != cudaSuccess) {
+        delete c;
+        return MT_ERR_CUDA;
+    }
+    for (int i = 0; i <= MAX_EVENTS; ++i)
+        if (cudaEventCreate(&c->ev[i]) != cudaSuccess) {
+            mt_destroy(c);
+            return MT_ERR_CUDA;
+        }
+    *out = c;
+    return MT_OK;
+}
+
+mt_status mt_set_diagram_output(mt_ctx* c, mt_pair* buf, uint64_t capacity) {
+    if (!c) return MT_ERR_INVALID_ARG;
+    c->reg_out = buf;
+    c->reg_cap = buf ? capacity : 0;
+    return MT_OK;
+}
+
+mt_status mt_compute(mt_ctx* c, const float* f, uint64_t* T, uint32_t flags, mt_stream_t stream) {
+    if (!c) return MT_ERR_INVALID_ARG;
+    if (flags & ~uint32_t(MT_FLAG_SPLIT_TREE)) return MT_ERR_INVALID_ARG;
+    c->launches = 0;
+    c->nev = 0;
+    c->sticky = MT_OK;
+    c->computed = true;
+    if (c->n == 0) return MT_OK;
+    if (!f || !T) return MT_ERR_INVALID_ARG;
+    DeviceGuard g(c->device);
+    if (!g.ok) return MT_ERR_CUDA;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const uint32_t flip = (flags & MT_FLAG_SPLIT_TREE) ? 0xffffffffu : 0u;
+    unsigned long long* ctr = counters_of(c);
+    uint64_t cap = 0;
+    mt_pair* out = target_of(c, &cap);
+    mt_pair* ess = reinterpret_cast<mt_pair*>(c->ws + c->L.ess);
+    uint64_t* status = reinterpret_cast<uint64_t*>(c->ws + c->L.status);
+
+    mark(c, "zero", s);
+    if (cudaMemsetAsync(c->ws + c->L.counters, 0, c->L.status - c->L.counters + c->L.ntiles * sizeof(uint64_t),
+                        s) != cudaSuccess)
+        return c->sticky = MT_ERR_CUDA;
+    // the kernels read the capacity from their arguments; keep it visible for debugging
+    mark(c, "init_descent", s);
+    mt::launch_init_descent(f, T, c->nx, c->ny, c->nz, flip, ctr, s);
+    mark(c, "merge_edges", s);
+    mt::launch_merge_edges(T, f, c->nx, c->ny, c->nz, flip, c->num_sms, s);
+    mark(c, "repair_diagram", s);
+    mt::launch_repair_diagram(T, f, c->n, flip, ctr, status, out, cap, ess, ESS_CAP, s);
+    mark(c, "finish_diagram", s);
+    mt::launch_finish_diagram(ctr, out, cap, ess, ESS_CAP, s);
+    if (c->profiling) cudaEventRecord(c->ev[c->nev], s);
+    c->launches = 4;
+    if (cudaGetLastError() != cudaSuccess) return c->sticky = MT_ERR_CUDA;
+    return MT_OK;
+}
+
+mt_status mt_diagram(mt_ctx* c, mt_pair* out, uint64_t capacity, uint64_t* n_pairs, uint64_t* n_essential,
+                     mt_stream_t stream) {
+    if (!c) return MT_ERR_INVALID_ARG;
+    DeviceGuard g(c->device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const mt_status st = sync_counters(c, s);
+    if (st == MT_ERR_STATE || st == MT_ERR_CUDA) return st;
+    const uint64_t nfin = c->host_ctr[mt::CTR_FIN], ness = c->host_ctr[mt::CTR_ESS];
+    if (n_pairs) *n_pairs = nfin;
+    if (n_essential) *n_essential = ness;
+    if (st != MT_OK) return st;
+    uint64_t cap = 0;
+    mt_pair* src = target_of(c, &cap);
+    if (out && out != src && nfin + ness) {
+        if (capacity < nfin + ness) return MT_ERR_CAPACITY;
+        if (cudaMemcpyAsync(out, src, (nfin + ness) * sizeof(mt_pair), cudaMemcpyDeviceToDevice, s) != cudaSuccess ||
+            cudaStreamSynchronize(s) != cudaSuccess)
+            return c->sticky = MT_ERR_CUDA;
+    } else if (out == src && out && capacity < nfin + ness) {
+        return MT_ERR_CAPACITY;
+    }
+    return MT_OK;
+}
+
+mt_status mt_diagram_view(mt_ctx* c, const mt_pair** records, uint64_t* n_pairs, uint64_t* n_essential,
+                          mt_stream_t stream) {
+    if (!c) return MT_ERR_INVALID_ARG;
+    DeviceGuard g(c->device);
+    const mt_status st = sync_counters(c, static_cast<cudaStream_t>(stream));
+    if (st == MT_ERR_STATE || st == MT_ERR_CUDA) return st;
+    if (n_pairs) *n_pairs = c->host_ctr[mt::CTR_FIN];
+    if (n_essential) *n_essential = c->host_ctr[mt::CTR_ESS];
+    uint64_t cap = 0;
+    if (records) *records = target_of(c, &cap);
+    return st;
+}
+
+mt_status mt_last_error(mt_ctx* c, mt_stream_t stream) {
+    if (!c) return MT_ERR_INVALID_ARG;
+    if (!c->computed) return MT_OK;
+    DeviceGuard g(c->device);
+    return sync_counters(c, static_cast<cudaStream_t>(stream));
+}
+
+uint32_t mt_last_launch_count(const mt_ctx* c) { return c ? c->launches : 0; }
+
+mt_status mt_set_profiling(mt_ctx* c, int enable) {
+    if (!c) return MT_ERR_INVALID_ARG;
+    c->profiling = enable != 0;
+    return MT_OK;
+}
+
+int mt_kernel_times(mt_ctx* c, const char** names, float* ms, int max) {
+    if (!c || !c->profiling || c->nev == 0) return 0;
+    DeviceGuard g(c->device);
+    if (cudaEventSynchronize(c->ev[c->nev]) != cudaSuccess) return 0;
+    int k = 0;
+    for (int i = 0; i < c->nev && k < max; ++i, ++k) {
+        float t = 0.f;
+        cudaEventElapsedTime(&t, c->ev[i], c->ev[i + 1]);
+        if (names) names[k] = c->ev_name[i];
+        if (ms) ms[k] = t;
+    }
+    return k;
+}
+
+void mt_destroy(mt_ctx* c) {
+    if (!c) return;
+    DeviceGuard g(c->device);
+    for (int i = 0; i <= MAX_EVENTS; ++i)
+        if (c->ev[i]) cudaEventDestroy(c->ev[i]);
+    if (c->host_ctr) cudaFreeHost(c->host_ctr);
+    delete c;
+}
+
+}  // extern "C"

@@ -1,0 +1,187 @@
+// repair_diagram.cu -- K4 + K5: the repair phase of Alg. 1 (lines 9-11,
+// PAPER.md:255-257; Alg. 5 "Repair", with Alg. 4
+// "Representative") fused with the ordered extraction of the
+// 0-dimensional persistence diagram (one point (f(a), f(b))
+// per branch).
+//
+// Repair: T[u] = (s, v) becomes (s, Rep(u, key(s))), Rep following cells while
+// key(s') <= key(s) and the cell is not a root.  Reading R20: the walk returns
+// the vertex it stopped at (Alg. 4 as printed returns the next, too-deep v).
+// The walk runs in place while other threads rewrite their own cells; every
+// value a cell ever holds is a valid pointer at that cell's own level, so the
+// result does not depend on the interleaving (DESIGN.md derivation E).
+//
+// Diagram: after the merge phase the s fields are final (repair only rewrites
+// v), so a cell with s != u is the branch born at u dying at saddle s (finite
+// pair), and a root (u, u, u) is an essential class.  The
+// finite pairs are written in ascending u with a single-pass ordered
+// compaction: warp ballots + a CTA scan give each tile's count, published
+// BEFORE the tile does its repair walks, and a decoupled look-back over the
+// predecessors' published counts gives the tile's output offset.  Tiles take
+// dynamic ticket numbers so every predecessor is already resident.
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace mt {
+
+namespace {
+
+constexpr int THREADS = 256;
+constexpr int ITEMS = 4;
+constexpr int TILE = THREADS * ITEMS;  // 1024 vertices per ticket
+constexpr uint64_t ST_AGG = 1ull << 62, ST_PRE = 2ull << 62, ST_VAL = (1ull << 62) - 1;
+
+__global__ void __launch_bounds__(THREADS)
+repair_diagram_kernel(uint64_t* T, const float* __restrict__ f, uint64_t n, uint32_t flip,
+                      unsigned long long* __restrict__ counters, uint64_t* __restrict__ status,
+                      mt_pair* __restrict__ out, uint64_t out_cap, mt_pair* __restrict__ ess, uint32_t ess_cap,
+                      uint64_t ntiles) {
+    __shared__ uint64_t s_tile;
+    __shared__ uint32_t s_cnt[ITEMS * 8];
+    __shared__ uint64_t s_prefix;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (threadIdx.x == 0) s_tile = atomicAdd(counters + CTR_TICKET, 1ull);
+    __syncthreads();
+    const uint64_t tile = s_tile;
+    const uint64_t base = tile * TILE;
+
+    uint64_t cell[ITEMS];
+    bool fin[ITEMS];
+    uint32_t mask[ITEMS];
+#pragma unroll
+    for (int k = 0; k < ITEMS; ++k) {
+        const uint64_t u = base + uint64_t(k) * THREADS + threadIdx.x;
+        cell[k] = u < n ? ld_relaxed(T + u) : 0;
+        fin[k] = u < n && cell_s(cell[k]) != uint32_t(u);
+        mask[k] = __ballot_sync(FULL_MASK, fin[k]);
+        if (lane == 0) s_cnt[k * 8 + warp] = __popc(mask[k]);
+    }
+    __syncthreads();
+    // exclusive scan of the 32 (k, warp) counts in u order, by warp 0
+    if (warp == 0) {
+        const uint32_t c = s_cnt[lane];
+        uint32_t incl = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t t = __shfl_up_sync(FULL_MASK, incl, o);
+            if (lane >= o) incl += t;
+        }
+        s_cnt[lane] = incl - c;
+        const uint32_t agg = __shfl_sync(FULL_MASK, incl, 31);
+        if (lane == 0) {
+            st_relaxed(status + tile, (tile == 0 ? ST_PRE : ST_AGG) | agg);  // publish before walking
+        }
+    }
+
+    // --- repair (Alg. 5 with Alg. 4's walk) ------------------------------
+#pragma unroll 1
+    for (int k = 0; k < ITEMS; ++k) {
+        const uint64_t u = base + uint64_t(k) * THREADS + threadIdx.x;
+        if (u >= n) continue;
+        const uint32_t s = cell_s(cell[k]), v = cell_v(cell[k]);
+        if (v == uint32_t(u)) {                       // root (u, u, u): essential class
+            const uint32_t i = atomicAdd(reinterpret_cast<unsigned int*>(counters + CTR_ESS), 1u);
+            if (i < ess_cap) ess[i] = mt_pair{uint32_t(u), uint32_t(u), __ldg(f + u), __int_as_float(0x7f800000)};
+            else atomicOr(counters + CTR_ERR, ERR_ESS_CAPACITY);
+            continue;
+        }
+        const uint64_t a = keyf(f, s, flip);
+        uint32_t x = v;
+        while (true) {
+            const uint64_t c = ld_relaxed(T + x);
+            const uint32_t sx = cell_s(c), vx = cell_v(c);
+            if (vx == x) break;                       // root
+            if (keyf(f, sx, flip) > a) break;         // key(s_x) > a: x is the representative
+            x = vx;
+        }
+        if (x != v) st_relaxed(T + u, pack(s, x));
+    }
+
+    // --- decoupled look-back for the tile's output offset ----------------
+    __syncthreads();
+    if (warp == 0) {
+        uint64_t prefix = 0;
+        int64_t j = int64_t(tile) - 1;
+        while (j >= 0) {
+            const int64_t idx = j - lane;
+            const uint64_t st = idx >= 0 ? ld_relaxed(status + idx) : ST_PRE;
+            const uint64_t flag = st >> 62;
+            const uint32_t pmask = __ballot_sync(FULL_MASK, flag == 2);
+            const uint32_t xmask = __ballot_sync(FULL_MASK, flag == 0);
+            const int first_p = pmask ? __ffs(pmask) - 1 : 31;
+            const uint32_t upto = first_p == 31 ? FULL_MASK : ((2u << first_p) - 1u);
+            if (xmask & upto) continue;               // a needed predecessor has not published
+            uint64_t val = lane <= first_p ? (st & ST_VAL) : 0;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) val += __shfl_xor_sync(FULL_MASK, val, o);
+            prefix += val;
+            if (pmask) break;
+            j -= 32;
+        }
+        if (lane == 0) s_prefix = prefix;
+    }
+    __syncthreads();
+    const uint64_t prefix = s_prefix;
+    // inclusive prefix = prefix + this tile's aggregate; s_cnt holds exclusive
+    // offsets, so the aggregate is the last offset + the last (k, warp) count,
+    // which the last thread's own ballot holds.
+    if (threadIdx.x == THREADS - 1) {
+        const uint64_t total = prefix + s_cnt[(ITEMS - 1) * 8 + 7] + __popc(mask[ITEMS - 1]);
+        if (tile != 0) st_relaxed(status + tile, ST_PRE | total);
+        if (tile == ntiles - 1) counters[CTR_FIN] = total;
+    }
+
+    // --- write this tile's finite pairs in ascending u --------------------
+#pragma unroll
+    for (int k = 0; k < ITEMS; ++k) {
+        if (!fin[k]) continue;
+        const uint64_t u = base + uint64_t(k) * THREADS + threadIdx.x;
+        const uint64_t pos = prefix + s_cnt[k * 8 + warp] + __popc(mask[k] & ((1u << lane) - 1u));
+        const uint32_t s = cell_s(cell[k]);
+        if (pos < out_cap) out[pos] = mt_pair{uint32_t(u), s, __ldg(f + u), __ldg(f + s)};
+        else atomicOr(counters + CTR_ERR, ERR_CAPACITY);
+    }
+}
+
+// Appends the essential classes (ascending vertex) after the finite pairs and
+// checks the capacity.  One CTA; the number of essential classes is the number
+// of connected components (one for a non-empty grid).
+__global__ void finish_diagram_kernel(unsigned long long* __restrict__ counters, mt_pair* __restrict__ out,
+                                      uint64_t out_cap, mt_pair* __restrict__ ess, uint32_t ess_cap) {
+    const uint64_t nfin = counters[CTR_FIN];
+    uint32_t ness = uint32_t(counters[CTR_ESS]);
+    if (ness > ess_cap) ness = ess_cap;
+    if (threadIdx.x == 0) {
+        // insertion sort by vertex (ness is tiny)
+        for (uint32_t i = 1; i < ness; ++i) {
+            mt_pair p = ess[i];
+            uint32_t j = i;
+            while (j > 0 && ess[j - 1].birth_v > p.birth_v) { ess[j] = ess[j - 1]; --j; }
+            ess[j] = p;
+        }
+    }
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < ness; i += blockDim.x) {
+        if (nfin + i < out_cap) out[nfin + i] = ess[i];
+        else atomicOr(counters + CTR_ERR, ERR_CAPACITY);
+    }
+}
+
+}  // namespace
+
+uint64_t repair_tiles(uint64_t n) { return (n + TILE - 1) / TILE; }
+
+void launch_repair_diagram(uint64_t* T, const float* f, uint64_t n, uint32_t flip, unsigned long long* counters,
+                           uint64_t* status, mt_pair* out, uint64_t out_cap, mt_pair* ess, uint32_t ess_cap,
+                           cudaStream_t stream) {
+    const uint64_t ntiles = repair_tiles(n);
+    repair_diagram_kernel<<<uint32_t(ntiles), THREADS, 0, stream>>>(T, f, n, flip, counters, status, out, out_cap,
+                                                                     ess, ess_cap, ntiles);
+}
+
+void launch_finish_diagram(unsigned long long* counters, mt_pair* out, uint64_t out_cap, mt_pair* ess,
+                           uint32_t ess_cap, cudaStream_t stream) {
+    finish_diagram_kernel<<<1, 128, 0, stream>>>(counters, out, out_cap, ess, ess_cap);
+}
+
+}  // namespace mt

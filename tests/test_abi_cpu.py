@@ -1,0 +1,66 @@
+"""CPU-side checks of the C ABI: the in-tree library builds/loads and exports every symbol
+include/mt.h declares; host-only entry points behave (no compute without a GPU)."""
+import ctypes
+import os
+import re
+
+import pytest
+
+from paper_2301_10838_b200 import _lib, build
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def header_functions():
+    src = open(os.path.join(ROOT, "include", "mt.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(mt_[a-z_]+)\s*\(", src)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    build.build()
+    return _lib.load()
+
+
+def test_exports_every_declared_symbol(lib):
+    declared = header_functions()
+    assert len(declared) >= 12
+    for name in declared:
+        assert hasattr(lib, name), name
+    assert sorted(_lib.EXPORTS) == declared
+
+
+def test_abi_version_and_status_strings(lib):
+    assert lib.mt_abi_version() == 1
+    for st in range(9):
+        assert lib.mt_status_string(st)
+    assert b"non-finite" in lib.mt_status_string(3)
+
+
+def test_workspace_bytes(lib):
+    assert _lib.mt_workspace_bytes((16, 16, 16), 6) > 4096 * 8
+    assert _lib.mt_workspace_bytes((16, 16, 16), 5) == 0          # bad connectivity
+    assert _lib.mt_workspace_bytes((16, 16, 2), 4) == 0           # conn 4 needs nz == 1
+    assert _lib.mt_workspace_bytes((0, 16, 16), 6) > 0            # empty grid is valid
+    assert _lib.mt_workspace_bytes((1 << 16, 1 << 16, 2), 6) == 0  # > 2^32 vertices
+    a = _lib.mt_workspace_bytes((512, 512, 512), 6)
+    assert a % 256 == 0 and a < 512 ** 3 * 16
+
+
+def test_create_rejects_bad_args_without_gpu(lib):
+    h = ctypes.c_void_p()
+    dims = (ctypes.c_uint32 * 3)(4, 4, 4)
+    assert lib.mt_create(ctypes.byref(h), dims, 5, 0, None, 0) == _lib.MT_ERR_INVALID_ARG
+    assert lib.mt_create(ctypes.byref(h), dims, 6, 0, None, 0) == _lib.MT_ERR_WORKSPACE
+    assert lib.mt_compute(None, None, None, 0, None) == _lib.MT_ERR_INVALID_ARG
+    assert lib.mt_diagram(None, None, 0, None, None, None) == _lib.MT_ERR_INVALID_ARG
+    lib.mt_destroy(None)
+
+
+def test_sass_is_sm100a():
+    """The library carries sm_100a SASS for every kernel (cuobjdump)."""
+    import subprocess
+    so = build.build()
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", so], capture_output=True, text=True).stdout
+    assert "sm_100a" in out

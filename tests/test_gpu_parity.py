@@ -1,0 +1,171 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the oracle O1, bit-exact.
+
+The triplet store is unique for the (value, id) order, so the
+uint64 cells and the ordered diagram records (birth_v, death_v, f bits) are
+compared with memcmp semantics.  Sizes: golden fixtures, 100 seeds of the c1
+config, ragged shapes that span several tiles with partial tails, every
+BASELINE config scaled down, closed-form stress families, and the full-size
+configs c2/c3/c4 in the launch configuration bench.py times.
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+import oracle  # noqa: E402
+from oracle import invariants  # noqa: E402
+from paper_2301_10838_b200 import _lib, fields  # noqa: E402
+from golden_io import all_cases  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+_CTX = {}
+
+
+def ctx_for(dims, conn):
+    key = (tuple(dims), conn)
+    if key not in _CTX:
+        if len(_CTX) > 8:
+            _CTX.clear()
+        _CTX[key] = _lib.MergeTree(dims, conn, device=0)
+    return _CTX[key]
+
+
+def gpu_tree(f, dims, conn, split=False):
+    mt = ctx_for(dims, conn)
+    fd = torch.from_numpy(np.ascontiguousarray(f, dtype=np.float32)).cuda()
+    T = mt.compute(fd, split=split)
+    rec, npairs, ness = mt.diagram()
+    return T.cpu().numpy().view(np.uint64), _lib.pairs_to_numpy(rec), npairs, ness
+
+
+def assert_parity(f, dims, conn, split=False, check_invariants=False):
+    T, pairs, npairs, ness = gpu_tree(f, dims, conn, split)
+    To, po, npo, neo = oracle.merge_tree(f, dims, conn=conn, split=split)
+    if not np.array_equal(T, To):
+        bad = np.nonzero(T != To)[0]
+        u = int(bad[0])
+        raise AssertionError(f"{bad.size} cells differ; first u={u}: gpu (s={T[u] >> 32}, v={T[u] & 0xffffffff}) "
+                             f"oracle (s={To[u] >> 32}, v={To[u] & 0xffffffff})")
+    assert (npairs, ness) == (npo, neo)
+    assert pairs.tobytes() == po.tobytes()
+    if check_invariants:
+        invariants.check(T, f, dims, split=split, n_pairs=npairs, n_ess=ness)
+    return npairs
+
+
+@pytest.mark.parametrize("case", all_cases(), ids=lambda c: c["name"])
+def test_golden_on_gpu(case):
+    assert_parity(case["f"], case["dims"], case["conn"], case["split"])
+
+
+def test_c1_hundred_seeds():
+    """c1 recipe (16^3 u24 white noise, 6-conn), parity seeds 0-99."""
+    for seed in range(100):
+        f = fields.white_noise((16, 16, 16), seed)
+        assert_parity(f, (16, 16, 16), 6, split=bool(seed % 2))
+
+
+@pytest.mark.parametrize("dims", [(33, 9, 17), (1, 1, 1000), (1000, 1, 1), (7, 300, 1), (65, 66, 3),
+                                  (2, 2, 2), (31, 1, 9), (100, 100, 1), (45, 37, 29)])
+def test_ragged_shapes(dims):
+    rng = np.random.default_rng(sum(dims))
+    n = int(np.prod(dims))
+    conn = 4 if dims[2] == 1 else 6
+    for kind in range(3):
+        if kind == 0:
+            f = rng.random(n).astype(np.float32)
+        elif kind == 1:
+            f = rng.integers(0, 5, n).astype(np.float32)          # heavy ties
+        else:
+            f = np.where(rng.random(n) < 0.5, -0.0, 0.0).astype(np.float32)  # all-equal values, +-0
+        assert_parity(f, dims, conn, split=bool(kind == 1), check_invariants=True)
+
+
+@pytest.mark.parametrize("cfg,scale", [("c2", 512), ("c3", 64), ("c4", 96), ("c1", 40), ("c2", 97)])
+def test_scaled_configs(cfg, scale):
+    f, dims, conn = fields.make(cfg, scale=scale)
+    assert_parity(f, dims, conn, check_invariants=True)
+    assert_parity(f, dims, conn, split=True)
+
+
+@pytest.mark.parametrize("dims", [(64, 64, 64), (256, 256, 1)])
+def test_closed_form_stress(dims):
+    nx, ny, nz = dims
+    conn = 4 if nz == 1 else 6
+    z, y, x = np.meshgrid(np.arange(nz), np.arange(ny), np.arange(nx), indexing="ij")
+    checker = ((x + y + z) % 2).astype(np.float32).reshape(-1)   # 50% minima: CAS contention
+    npairs = assert_parity(checker, dims, conn)
+    assert npairs == int((checker == 0).sum()) - 1
+    const = np.full(nx * ny * nz, 3.0, np.float32)               # id order only
+    assert assert_parity(const, dims, conn) == 0
+    ramp = (x + y + z).astype(np.float32).reshape(-1)
+    assert assert_parity(-ramp, dims, conn) == 0
+
+
+def test_empty_and_single():
+    for dims in [(0, 5, 5), (5, 0, 1)]:
+        mt = _lib.MergeTree(dims, 6 if dims[2] > 1 else 4, device=0)
+        f = torch.empty(0, dtype=torch.float32, device="cuda")
+        T = mt.compute(f)
+        rec, npairs, ness = mt.diagram()
+        assert T.numel() == 0 and npairs == 0 and ness == 0
+    assert_parity(np.array([4.0], np.float32), (1, 1, 1), 6)
+
+
+def test_nonfinite_is_reported():
+    f = fields.white_noise((20, 20, 20), 3)
+    for bad in (np.nan, np.inf, -np.inf):
+        g = f.copy()
+        g[4321] = bad
+        mt = ctx_for((20, 20, 20), 6)
+        mt.compute(torch.from_numpy(g).cuda())
+        st, _, _ = _lib.mt_diagram(mt.ctx)
+        assert st == _lib.MT_ERR_NONFINITE
+    # the context recovers on the next valid input
+    assert_parity(f, (20, 20, 20), 6)
+
+
+def test_registered_output_and_capacity():
+    f, dims, conn = fields.make("c4", scale=40)
+    To, po, npo, neo = oracle.merge_tree(f, dims, conn)
+    mt = _lib.MergeTree(dims, conn, device=0)
+    fd = torch.from_numpy(f).cuda()
+    buf = torch.zeros((npo + neo, 4), dtype=torch.int32, device="cuda")
+    mt.set_diagram_output(buf)
+    mt.compute(fd)
+    st, a, b = _lib.mt_diagram(mt.ctx, buf.data_ptr(), buf.shape[0])
+    assert st == _lib.MT_OK and (a, b) == (npo, neo)
+    assert _lib.pairs_to_numpy(buf).tobytes() == po.tobytes()
+    small = torch.zeros((npo // 2, 4), dtype=torch.int32, device="cuda")
+    mt.set_diagram_output(small)
+    mt.compute(fd)
+    st, a, b = _lib.mt_diagram(mt.ctx)
+    assert st == _lib.MT_ERR_CAPACITY and (a, b) == (npo, neo)   # required counts still reported
+
+
+def test_repeat_runs_identical():
+    f, dims, conn = fields.make("c4", scale=128)
+    mt = ctx_for(dims, conn)
+    fd = torch.from_numpy(f).cuda()
+    first = mt.compute(fd).clone()
+    rec0, _, _ = mt.diagram()
+    for _ in range(5):
+        assert torch.equal(mt.compute(fd), first)
+        rec, _, _ = mt.diagram()
+        assert torch.equal(rec, rec0)
+
+
+def test_launches_are_library_kernels():
+    f, dims, conn = fields.make("c1")
+    mt = ctx_for(dims, conn)
+    mt.compute(torch.from_numpy(f).cuda())
+    mt.diagram()
+    assert mt.last_launch_count() == 4
+
+
+@pytest.mark.parametrize("cfg", ["c2", "c3", "c4"])
+def test_full_size_configs(cfg):
+    """BASELINE configs at full size, same launch configuration as bench.py, bit-exact vs O1."""
+    f, dims, conn = fields.make(cfg)
+    assert_parity(f, dims, conn, check_invariants=(cfg != "c4"))
