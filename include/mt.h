@@ -125,6 +125,15 @@ uint32_t mt_last_launch_count(const mt_ctx *ctx);
 mt_status mt_set_profiling(mt_ctx *ctx, int enable);
 int mt_kernel_times(mt_ctx *ctx, const char **names, float *ms, int max);
 
+/* Diagnostics: while enabled, mt_compute counts events of the merge and
+ * repair kernels: [0] edges examined, [1] edges skipped as redundant,
+ * [2] cells followed by the pre-filter walks, [3] Alg. 3 loop iterations,
+ * [4] failed CAS, [5] cells followed by the repair walks.  mt_stats syncs
+ * `stream` and copies up to `max` counters to out (host); returns the
+ * number written (0 if disabled). */
+mt_status mt_set_stats(mt_ctx *ctx, int enable);
+int mt_stats(mt_ctx *ctx, uint64_t *out, int max, mt_stream_t stream);
+
 const char *mt_status_string(mt_status s);
 void mt_destroy(mt_ctx *ctx);
 

@@ -27,7 +27,7 @@ PAIR_DTYPE = np.dtype([("birth_v", "<u4"), ("death_v", "<u4"), ("birth", "<f4"),
 # every symbol include/mt.h declares (checked by tests/test_abi_cpu.py)
 EXPORTS = ["mt_workspace_bytes", "mt_create", "mt_compute", "mt_set_diagram_output", "mt_diagram",
            "mt_diagram_view", "mt_last_error", "mt_last_launch_count", "mt_set_profiling", "mt_kernel_times",
-           "mt_status_string", "mt_destroy", "mt_abi_version"]
+           "mt_status_string", "mt_destroy", "mt_abi_version", "mt_set_stats", "mt_stats"]
 
 
 class MTError(RuntimeError):
@@ -68,6 +68,8 @@ def load(build_if_missing: bool = False):
         "mt_kernel_times": (ctypes.c_int, [vp, ctypes.POINTER(ctypes.c_char_p), ctypes.POINTER(ctypes.c_float),
                                            ctypes.c_int]),
         "mt_status_string": (ctypes.c_char_p, [ctypes.c_int]),
+        "mt_set_stats": (ctypes.c_int, [vp, ctypes.c_int]),
+        "mt_stats": (ctypes.c_int, [vp, u64p, ctypes.c_int, vp]),
         "mt_destroy": (None, [vp]),
         "mt_abi_version": (ctypes.c_int, []),
     }
@@ -161,6 +163,19 @@ def mt_kernel_times(ctx, max_entries: int = 8):
     ms = (ctypes.c_float * max_entries)()
     k = load().mt_kernel_times(ctx, names, ms, max_entries)
     return [(names[i].decode(), float(ms[i])) for i in range(k)]
+
+
+STAT_NAMES = ["edges", "skipped", "pre_hops", "merge_iters", "cas_fail", "repair_hops"]
+
+
+def mt_set_stats(ctx, enable: bool):
+    _check(load().mt_set_stats(ctx, int(bool(enable))), "mt_set_stats")
+
+
+def mt_stats(ctx, stream=None):
+    out = (ctypes.c_uint64 * 8)()
+    k = load().mt_stats(ctx, out, 8, _stream_handle(stream))
+    return {name: int(out[i]) for i, name in enumerate(STAT_NAMES) if i < k}
 
 
 def mt_destroy(ctx):

@@ -60,6 +60,53 @@ __device__ __forceinline__ uint64_t cas64(uint64_t* p, uint64_t expected, uint64
     return atomicCAS(reinterpret_cast<unsigned long long*>(p), expected, desired);
 }
 
+// ---- 16-byte working cells of the merge phase --------------------------
+// During the merge the store lives in the workspace as 16-byte cells
+//   lo = key(s) = ord(f[s]) << 32 | s        (the packed (s, v) of the paper,
+//   hi = ord(f[u]) << 32 | v                  widened by the two order keys)
+// so that a climb step (Alg. 3 l.2-8, Alg. 4 l.3) needs ONE dependent load:
+// the saddle's key and the owner's key travel with the cell instead of being
+// gathered from f.  Updates are single 128-bit CAS (atom.cas.b128, sm_90+);
+// loads are single-copy-atomic ld.relaxed.gpu.b128.  The output store T[u] =
+// s << 32 | v (reading R11) is written from these cells by the repair kernel.
+struct Cell {
+    uint64_t lo, hi;
+};
+__device__ __forceinline__ Cell make_cell(uint64_t key_s, uint32_t ord_u, uint32_t v) {
+    return Cell{key_s, (static_cast<uint64_t>(ord_u) << 32) | v};
+}
+__device__ __forceinline__ uint32_t cv_of(const Cell& c) { return static_cast<uint32_t>(c.hi); }
+__device__ __forceinline__ uint32_t cs_of(const Cell& c) { return static_cast<uint32_t>(c.lo); }
+__device__ __forceinline__ uint64_t self_key(const Cell& c, uint32_t u) {
+    return (c.hi & 0xffffffff00000000ull) | u;
+}
+__device__ __forceinline__ Cell ld_cell(const Cell* p) {
+    Cell c;
+    asm volatile("{\n\t.reg .b128 d;\n\tld.relaxed.gpu.global.b128 d, [%2];\n\tmov.b128 {%0, %1}, d;\n\t}"
+                 : "=l"(c.lo), "=l"(c.hi) : "l"(p) : "memory");
+    return c;
+}
+__device__ __forceinline__ void st_cell(Cell* p, const Cell& c) {
+    asm volatile("{\n\t.reg .b128 d;\n\tmov.b128 d, {%1, %2};\n\tst.relaxed.gpu.global.b128 [%0], d;\n\t}"
+                 ::"l"(p), "l"(c.lo), "l"(c.hi) : "memory");
+}
+// v field alone (single-copy atomic 32-bit store; a concurrent 128-bit load
+// sees either the old or the new v with the unchanged key fields)
+__device__ __forceinline__ void st_cell_v(Cell* p, uint32_t v) {
+    asm volatile("st.relaxed.gpu.global.b32 [%0], %1;" ::"l"(reinterpret_cast<char*>(p) + 8), "r"(v) : "memory");
+}
+// 128-bit compare-and-swap; returns the previous value.
+__device__ __forceinline__ Cell cas_cell(Cell* p, const Cell& expected, const Cell& desired) {
+    Cell old;
+    asm volatile(
+        "{\n\t.reg .b128 d, c, v;\n\tmov.b128 c, {%2, %3};\n\tmov.b128 v, {%4, %5};\n\t"
+        "atom.relaxed.gpu.global.cas.b128 d, [%6], c, v;\n\tmov.b128 {%0, %1}, d;\n\t}"
+        : "=l"(old.lo), "=l"(old.hi)
+        : "l"(expected.lo), "l"(expected.hi), "l"(desired.lo), "l"(desired.hi), "l"(p)
+        : "memory");
+    return old;
+}
+
 // Error bits (sticky, in the workspace counters).
 constexpr uint32_t ERR_NONFINITE = 1u;
 constexpr uint32_t ERR_CAPACITY = 2u;
@@ -73,6 +120,17 @@ enum CounterSlot : int {
     CTR_FIN = 3,        // number of finite pairs (written by the last tile)
     CTR_CAP = 4,        // capacity (records) of the diagram target buffer
     CTR_COUNT = 8
+};
+
+// Optional diagnostics (mt_set_stats): event counters in the workspace.
+enum StatSlot : int {
+    ST_EDGES = 0,        // edges examined by the merge kernel
+    ST_SKIPPED = 1,      // edges removed by the redundant-edge pre-filter
+    ST_PRE_HOPS = 2,     // cells followed by the pre-filter walks
+    ST_MERGE_ITERS = 3,  // iterations of the Alg. 3 loop
+    ST_CAS_FAIL = 4,     // failed CAS (Alg. 3 l.17 restarts)
+    ST_REPAIR_HOPS = 5,  // cells followed by the repair walks
+    ST_COUNT = 8
 };
 
 }  // namespace mt

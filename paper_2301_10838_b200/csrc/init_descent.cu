@@ -14,11 +14,12 @@
 // are joined below key(u) along the path), so every later climb through the
 // forest takes one hop per tile instead of one per vertex.
 //
-// Layout: f float32[n] x-fastest (reading R10); T uint64[n] (reading R11).
+// Layout: f float32[n] x-fastest (reading R10); C = 16-byte working cells
+// (common.cuh: key(s), owner key, v), written once.
 // One CTA of 256 threads = 8 warps owns a 32 x TY x TZ tile (TY*TZ = 64
 // rows, 2048 vertices); its f halo (+-1 in x, y, z) is staged in shared
 // memory as uint32 order keys (4 B/vertex read once from HBM, coalesced
-// 128-B rows), and T is written once with coalesced 256-B row stores.
+// 128-B rows), and the cells are written once with coalesced 512-B row stores.
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -32,7 +33,7 @@ constexpr uint8_t DIR_MIN = 6;
 
 template <int TY, int TZ>
 __global__ void __launch_bounds__(256)
-init_descent_kernel(const float* __restrict__ f, uint64_t* __restrict__ T, uint32_t nx, uint32_t ny,
+init_descent_kernel(const float* __restrict__ f, Cell* __restrict__ C, uint32_t nx, uint32_t ny,
                     uint32_t nz, uint32_t tiles_x, uint32_t tiles_y, uint32_t flip,
                     unsigned long long* __restrict__ counters) {
     constexpr int HX = TX + 2, HY = TY + 2, HZ = TZ + 2;
@@ -108,22 +109,56 @@ init_descent_kernel(const float* __restrict__ f, uint64_t* __restrict__ T, uint3
             d = s_dir[(cz * TY + cy) * TX + cx];
         }
         const uint64_t p = uint64_t(z0 + cz) * sxy + uint64_t(y0 + cy) * nx + uint64_t(x0 + cx);
-        T[u] = pack(uint32_t(u), uint32_t(p));  // (u, u, p(u)); p(u) = u at a minimum: root (u,u,u)
+        // (u, u, p(u)); p(u) = u at a minimum: root (u, u, u).  16-B cell:
+        // key(s) = key(u), owner order key, v.
+        const uint32_t o = s_ord[(lz + 1) * HX * HY + (ly + 1) * HX + (lx + 1)];
+        C[u] = make_cell(key_of(o, uint32_t(u)), o, uint32_t(p));
+    }
+}
+
+// Compress the steepest-descent forest: every regular cell (u, u, p) is
+// re-pointed at the root of its descent tree, the basin minimum m(u).
+// (u, u, m(u)) is a valid triplet (the descent path from u to m(u) lies below
+// key(u)) and is the representative Alg. 4 returns at level key(u) in the
+// forest, so this is Alg. 5 applied to the start state (DESIGN.md
+// derivation F).  Walks run in place; concurrent shortcuts only ever point
+// further down the same tree, and each thread writes only its own v field.
+__global__ void __launch_bounds__(256) compress_kernel(Cell* C, uint64_t n) {
+    for (uint64_t u = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; u < n;
+         u += uint64_t(gridDim.x) * blockDim.x) {
+        const Cell c = ld_cell(C + u);
+        const uint32_t v = cv_of(c);
+        if (v == uint32_t(u)) continue;           // basin minimum (root)
+        uint32_t x = v;
+        while (true) {
+            const Cell cx = ld_cell(C + x);
+            const uint32_t nx = cv_of(cx);
+            if (nx == x) break;
+            x = nx;
+        }
+        if (x != v) st_cell_v(C + u, x);
     }
 }
 
 }  // namespace
 
-void launch_init_descent(const float* f, uint64_t* T, uint32_t nx, uint32_t ny, uint32_t nz, uint32_t flip,
+void launch_compress(Cell* C, uint64_t n, int num_sms, cudaStream_t stream) {
+    uint64_t blocks = (n + 255) / 256;
+    const uint64_t cap = uint64_t(num_sms) * 8 * 32;
+    if (blocks > cap) blocks = cap;
+    compress_kernel<<<uint32_t(blocks), 256, 0, stream>>>(C, n);
+}
+
+void launch_init_descent(const float* f, Cell* C, uint32_t nx, uint32_t ny, uint32_t nz, uint32_t flip,
                          unsigned long long* counters, cudaStream_t stream) {
     if (nz == 1) {
         constexpr int TY = 64, TZ = 1;
         const uint32_t tx = (nx + TX - 1) / TX, ty = (ny + TY - 1) / TY, tz = 1;
-        init_descent_kernel<TY, TZ><<<tx * ty * tz, 256, 0, stream>>>(f, T, nx, ny, nz, tx, ty, flip, counters);
+        init_descent_kernel<TY, TZ><<<tx * ty * tz, 256, 0, stream>>>(f, C, nx, ny, nz, tx, ty, flip, counters);
     } else {
         constexpr int TY = 8, TZ = 8;
         const uint32_t tx = (nx + TX - 1) / TX, ty = (ny + TY - 1) / TY, tz = (nz + TZ - 1) / TZ;
-        init_descent_kernel<TY, TZ><<<tx * ty * tz, 256, 0, stream>>>(f, T, nx, ny, nz, tx, ty, flip, counters);
+        init_descent_kernel<TY, TZ><<<tx * ty * tz, 256, 0, stream>>>(f, C, nx, ny, nz, tx, ty, flip, counters);
     }
 }
 

@@ -1,7 +1,7 @@
 // mt_api.cu -- the C ABI of libmt_b200 (declared and documented in
 // include/mt.h): context, caller-owned workspace layout, sticky errors, stream
 // plumbing and the launch sequence of the hot path:
-//   zero counters -> K1+K2 init_descent -> K3 merge_edges
+//   zero counters -> K1+K2 init_descent -> K4 compress -> K3 merge_edges
 //   -> K4+K5 repair_diagram -> finish_diagram
 // All launches are asynchronous on the caller's stream; only mt_diagram /
 // mt_diagram_view / mt_last_error synchronise.
@@ -22,7 +22,7 @@ constexpr int MAX_EVENTS = 8;
 size_t align_up(size_t x) { return (x + ALIGN - 1) / ALIGN * ALIGN; }
 
 struct Layout {
-    size_t counters, status, ess, pairs, total;
+    size_t counters, status, stats, ess, cells, pairs, total;
     uint64_t ntiles, pairs_cap;
 };
 
@@ -44,8 +44,12 @@ Layout layout_for(uint64_t n) {
     off += align_up(mt::CTR_COUNT * sizeof(uint64_t));
     L.status = off;  // contiguous with counters: one memset zeroes both
     off += align_up(L.ntiles * sizeof(uint64_t));
+    L.stats = off;
+    off += align_up(mt::ST_COUNT * sizeof(uint64_t));
     L.ess = off;
     off += align_up(ESS_CAP * sizeof(mt_pair));
+    L.cells = off;  // 16-byte working cells of the merge phase
+    off += align_up(n * sizeof(mt::Cell));
     L.pairs = off;
     off += align_up(L.pairs_cap * sizeof(mt_pair));
     L.total = off;
@@ -70,6 +74,7 @@ struct mt_ctx {
     uint64_t* host_ctr = nullptr;  // pinned
     uint32_t launches = 0;
     bool profiling = false;
+    bool stats = false;
     cudaEvent_t ev[MAX_EVENTS + 1] = {};
     const char* ev_name[MAX_EVENTS] = {};
     int nev = 0;
@@ -219,22 +224,27 @@ mt_status mt_compute(mt_ctx* c, const float* f, uint64_t* T, uint32_t flags, mt_
     mt_pair* out = target_of(c, &cap);
     mt_pair* ess = reinterpret_cast<mt_pair*>(c->ws + c->L.ess);
     uint64_t* status = reinterpret_cast<uint64_t*>(c->ws + c->L.status);
+    mt::Cell* cells = reinterpret_cast<mt::Cell*>(c->ws + c->L.cells);
+    unsigned long long* stats = c->stats ? reinterpret_cast<unsigned long long*>(c->ws + c->L.stats) : nullptr;
+    if (stats && cudaMemsetAsync(stats, 0, mt::ST_COUNT * sizeof(uint64_t), s) != cudaSuccess)
+        return c->sticky = MT_ERR_CUDA;
 
     mark(c, "zero", s);
     if (cudaMemsetAsync(c->ws + c->L.counters, 0, c->L.status - c->L.counters + c->L.ntiles * sizeof(uint64_t),
                         s) != cudaSuccess)
         return c->sticky = MT_ERR_CUDA;
-    // the kernels read the capacity from their arguments; keep it visible for debugging
     mark(c, "init_descent", s);
-    mt::launch_init_descent(f, T, c->nx, c->ny, c->nz, flip, ctr, s);
+    mt::launch_init_descent(f, cells, c->nx, c->ny, c->nz, flip, ctr, s);
+    mark(c, "compress", s);
+    mt::launch_compress(cells, c->n, c->num_sms, s);
     mark(c, "merge_edges", s);
-    mt::launch_merge_edges(T, f, c->nx, c->ny, c->nz, flip, c->num_sms, s);
+    mt::launch_merge_edges(cells, c->nx, c->ny, c->nz, c->num_sms, stats, s);
     mark(c, "repair_diagram", s);
-    mt::launch_repair_diagram(T, f, c->n, flip, ctr, status, out, cap, ess, ESS_CAP, s);
+    mt::launch_repair_diagram(cells, T, f, c->n, ctr, status, out, cap, ess, ESS_CAP, stats, s);
     mark(c, "finish_diagram", s);
     mt::launch_finish_diagram(ctr, out, cap, ess, ESS_CAP, s);
     if (c->profiling) cudaEventRecord(c->ev[c->nev], s);
-    c->launches = 4;
+    c->launches = 5;
     if (cudaGetLastError() != cudaSuccess) return c->sticky = MT_ERR_CUDA;
     return MT_OK;
 }
@@ -302,6 +312,23 @@ int mt_kernel_times(mt_ctx* c, const char** names, float* ms, int max) {
         if (names) names[k] = c->ev_name[i];
         if (ms) ms[k] = t;
     }
+    return k;
+}
+
+mt_status mt_set_stats(mt_ctx* c, int enable) {
+    if (!c) return MT_ERR_INVALID_ARG;
+    c->stats = enable != 0;
+    return MT_OK;
+}
+
+int mt_stats(mt_ctx* c, uint64_t* out, int max, mt_stream_t stream) {
+    if (!c || !out || !c->stats || !c->computed || c->n == 0) return 0;
+    DeviceGuard g(c->device);
+    const int k = max < mt::ST_COUNT ? max : mt::ST_COUNT;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (cudaMemcpyAsync(out, c->ws + c->L.stats, k * sizeof(uint64_t), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+        cudaStreamSynchronize(s) != cudaSuccess)
+        return 0;
     return k;
 }
 

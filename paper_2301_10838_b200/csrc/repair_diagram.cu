@@ -32,10 +32,10 @@ constexpr int TILE = THREADS * ITEMS;  // 1024 vertices per ticket
 constexpr uint64_t ST_AGG = 1ull << 62, ST_PRE = 2ull << 62, ST_VAL = (1ull << 62) - 1;
 
 __global__ void __launch_bounds__(THREADS)
-repair_diagram_kernel(uint64_t* T, const float* __restrict__ f, uint64_t n, uint32_t flip,
+repair_diagram_kernel(Cell* C, uint64_t* __restrict__ T, const float* __restrict__ f, uint64_t n,
                       unsigned long long* __restrict__ counters, uint64_t* __restrict__ status,
                       mt_pair* __restrict__ out, uint64_t out_cap, mt_pair* __restrict__ ess, uint32_t ess_cap,
-                      uint64_t ntiles) {
+                      uint64_t ntiles, unsigned long long* __restrict__ stats) {
     __shared__ uint64_t s_tile;
     __shared__ uint32_t s_cnt[ITEMS * 8];
     __shared__ uint64_t s_prefix;
@@ -45,14 +45,14 @@ repair_diagram_kernel(uint64_t* T, const float* __restrict__ f, uint64_t n, uint
     const uint64_t tile = s_tile;
     const uint64_t base = tile * TILE;
 
-    uint64_t cell[ITEMS];
+    Cell cell[ITEMS];
     bool fin[ITEMS];
     uint32_t mask[ITEMS];
 #pragma unroll
     for (int k = 0; k < ITEMS; ++k) {
         const uint64_t u = base + uint64_t(k) * THREADS + threadIdx.x;
-        cell[k] = u < n ? ld_relaxed(T + u) : 0;
-        fin[k] = u < n && cell_s(cell[k]) != uint32_t(u);
+        cell[k] = u < n ? ld_cell(C + u) : Cell{0, 0};
+        fin[k] = u < n && cs_of(cell[k]) != uint32_t(u);
         mask[k] = __ballot_sync(FULL_MASK, fin[k]);
         if (lane == 0) s_cnt[k * 8 + warp] = __popc(mask[k]);
     }
@@ -74,28 +74,31 @@ repair_diagram_kernel(uint64_t* T, const float* __restrict__ f, uint64_t n, uint
     }
 
     // --- repair (Alg. 5 with Alg. 4's walk) ------------------------------
-#pragma unroll 1
+    unsigned long long hops = 0;
+#pragma unroll
     for (int k = 0; k < ITEMS; ++k) {
         const uint64_t u = base + uint64_t(k) * THREADS + threadIdx.x;
         if (u >= n) continue;
-        const uint32_t s = cell_s(cell[k]), v = cell_v(cell[k]);
+        const uint32_t s = cs_of(cell[k]), v = cv_of(cell[k]);
         if (v == uint32_t(u)) {                       // root (u, u, u): essential class
             const uint32_t i = atomicAdd(reinterpret_cast<unsigned int*>(counters + CTR_ESS), 1u);
             if (i < ess_cap) ess[i] = mt_pair{uint32_t(u), uint32_t(u), __ldg(f + u), __int_as_float(0x7f800000)};
             else atomicOr(counters + CTR_ERR, ERR_ESS_CAPACITY);
+            T[u] = pack(uint32_t(u), uint32_t(u));
             continue;
         }
-        const uint64_t a = keyf(f, s, flip);
+        const uint64_t a = cell[k].lo;                // key(s)
         uint32_t x = v;
         while (true) {
-            const uint64_t c = ld_relaxed(T + x);
-            const uint32_t sx = cell_s(c), vx = cell_v(c);
-            if (vx == x) break;                       // root
-            if (keyf(f, sx, flip) > a) break;         // key(s_x) > a: x is the representative
-            x = vx;
+            const Cell c = ld_cell(C + x);
+            if (cv_of(c) == x || c.lo > a) break;     // root, or key(s_x) > a: x is Rep(u, a)
+            x = cv_of(c);
+            ++hops;
         }
-        if (x != v) st_relaxed(T + u, pack(s, x));
+        if (x != v) st_cell_v(C + u, x);              // in-place shortcut for later walkers (derivation E)
+        T[u] = pack(s, x);
     }
+    if (stats) atomicAdd(stats + ST_REPAIR_HOPS, hops);
 
     // --- decoupled look-back for the tile's output offset ----------------
     __syncthreads();
@@ -137,7 +140,7 @@ repair_diagram_kernel(uint64_t* T, const float* __restrict__ f, uint64_t n, uint
         if (!fin[k]) continue;
         const uint64_t u = base + uint64_t(k) * THREADS + threadIdx.x;
         const uint64_t pos = prefix + s_cnt[k * 8 + warp] + __popc(mask[k] & ((1u << lane) - 1u));
-        const uint32_t s = cell_s(cell[k]);
+        const uint32_t s = cs_of(cell[k]);
         if (pos < out_cap) out[pos] = mt_pair{uint32_t(u), s, __ldg(f + u), __ldg(f + s)};
         else atomicOr(counters + CTR_ERR, ERR_CAPACITY);
     }
@@ -171,12 +174,12 @@ __global__ void finish_diagram_kernel(unsigned long long* __restrict__ counters,
 
 uint64_t repair_tiles(uint64_t n) { return (n + TILE - 1) / TILE; }
 
-void launch_repair_diagram(uint64_t* T, const float* f, uint64_t n, uint32_t flip, unsigned long long* counters,
+void launch_repair_diagram(Cell* C, uint64_t* T, const float* f, uint64_t n, unsigned long long* counters,
                            uint64_t* status, mt_pair* out, uint64_t out_cap, mt_pair* ess, uint32_t ess_cap,
-                           cudaStream_t stream) {
+                           unsigned long long* stats, cudaStream_t stream) {
     const uint64_t ntiles = repair_tiles(n);
-    repair_diagram_kernel<<<uint32_t(ntiles), THREADS, 0, stream>>>(T, f, n, flip, counters, status, out, out_cap,
-                                                                     ess, ess_cap, ntiles);
+    repair_diagram_kernel<<<uint32_t(ntiles), THREADS, 0, stream>>>(C, T, f, n, counters, status, out, out_cap,
+                                                                     ess, ess_cap, ntiles, stats);
 }
 
 void launch_finish_diagram(unsigned long long* counters, mt_pair* out, uint64_t out_cap, mt_pair* ess,

@@ -161,7 +161,7 @@ def test_launches_are_library_kernels():
     mt = ctx_for(dims, conn)
     mt.compute(torch.from_numpy(f).cuda())
     mt.diagram()
-    assert mt.last_launch_count() == 4
+    assert mt.last_launch_count() == 5
 
 
 @pytest.mark.parametrize("cfg", ["c2", "c3", "c4"])
@@ -169,3 +169,11 @@ def test_full_size_configs(cfg):
     """BASELINE configs at full size, same launch configuration as bench.py, bit-exact vs O1."""
     f, dims, conn = fields.make(cfg)
     assert_parity(f, dims, conn, check_invariants=(cfg != "c4"))
+
+
+@pytest.mark.parametrize("cfg", ["c4", "c5", "c3"])
+def test_medium_many_seeds(cfg):
+    """Concurrency stress at 128^3: many seeds of the noise / GRF / smooth recipes."""
+    for seed in range(6):
+        f, dims, conn = fields.make(cfg, seed=100 + seed, scale=128)
+        assert_parity(f, dims, conn, split=bool(seed % 2))
