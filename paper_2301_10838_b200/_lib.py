@@ -165,7 +165,7 @@ def mt_kernel_times(ctx, max_entries: int = 8):
     return [(names[i].decode(), float(ms[i])) for i in range(k)]
 
 
-STAT_NAMES = ["edges", "skipped", "pre_hops", "merge_iters", "cas_fail", "repair_hops"]
+STAT_NAMES = ["edges", "skipped", "pre_hops", "merge_iters", "cas_fail", "repair_hops", "queued"]
 
 
 def mt_set_stats(ctx, enable: bool):

@@ -119,6 +119,8 @@ enum CounterSlot : int {
     CTR_ESS = 2,        // number of essential classes found
     CTR_FIN = 3,        // number of finite pairs (written by the last tile)
     CTR_CAP = 4,        // capacity (records) of the diagram target buffer
+    CTR_QLEN = 5,       // inter-basin edges found by the filter (may exceed the queue)
+    CTR_QFETCH = 6,     // next queue entry to hand out (merge_queue)
     CTR_COUNT = 8
 };
 
@@ -130,6 +132,7 @@ enum StatSlot : int {
     ST_MERGE_ITERS = 3,  // iterations of the Alg. 3 loop
     ST_CAS_FAIL = 4,     // failed CAS (Alg. 3 l.17 restarts)
     ST_REPAIR_HOPS = 5,  // cells followed by the repair walks
+    ST_QUEUED = 6,       // inter-basin edges queued by the filter
     ST_COUNT = 8
 };
 

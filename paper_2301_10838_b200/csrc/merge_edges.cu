@@ -135,7 +135,10 @@ __device__ __forceinline__ void merge_edge(Cell* C, uint32_t a, const Cell& ca, 
 
 template <bool STATS>
 __global__ void __launch_bounds__(256)
-merge_edges_kernel(Cell* C, uint32_t nx, uint32_t ny, uint32_t nz, uint64_t n, unsigned long long* stats) {
+merge_edges_kernel(Cell* C, uint32_t nx, uint32_t ny, uint32_t nz, uint64_t n, unsigned long long* stats,
+                   const unsigned long long* guard, uint64_t guard_cap) {
+    // fallback mode: run only if the edge queue overflowed (guard = queue length)
+    if (guard && *reinterpret_cast<const volatile unsigned long long*>(guard) <= guard_cap) return;
     const uint64_t sxy = uint64_t(nx) * ny;
     Stats st;
     for (uint64_t u = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; u < n;
@@ -160,15 +163,18 @@ merge_edges_kernel(Cell* C, uint32_t nx, uint32_t ny, uint32_t nz, uint64_t n, u
 }  // namespace
 
 void launch_merge_edges(Cell* C, uint32_t nx, uint32_t ny, uint32_t nz, int num_sms,
-                        unsigned long long* stats, cudaStream_t stream) {
+                        unsigned long long* stats, const unsigned long long* guard, uint64_t guard_cap,
+                        cudaStream_t stream) {
     const uint64_t n = uint64_t(nx) * ny * nz;
     uint64_t blocks = (n + 255) / 256;
-    const uint64_t cap = uint64_t(num_sms) * 8 * 64;  // grid-stride beyond this
+    // grid-stride beyond this; as the overflow fallback (guard) keep the grid small so the
+    // common early exit costs one short launch
+    const uint64_t cap = uint64_t(num_sms) * 8 * (guard ? 1 : 64);
     if (blocks > cap) blocks = cap;
     if (stats)
-        merge_edges_kernel<true><<<uint32_t(blocks), 256, 0, stream>>>(C, nx, ny, nz, n, stats);
+        merge_edges_kernel<true><<<uint32_t(blocks), 256, 0, stream>>>(C, nx, ny, nz, n, stats, guard, guard_cap);
     else
-        merge_edges_kernel<false><<<uint32_t(blocks), 256, 0, stream>>>(C, nx, ny, nz, n, stats);
+        merge_edges_kernel<false><<<uint32_t(blocks), 256, 0, stream>>>(C, nx, ny, nz, n, stats, guard, guard_cap);
 }
 
 }  // namespace mt

@@ -1,7 +1,8 @@
 // mt_api.cu -- the C ABI of libmt_b200 (declared and documented in
 // include/mt.h): context, caller-owned workspace layout, sticky errors, stream
 // plumbing and the launch sequence of the hot path:
-//   zero counters -> K1+K2 init_descent -> K4 compress -> K3 merge_edges
+//   zero counters -> K1+K2 init_descent -> K4 compress -> K3 filter_edges + merge_queue
+//   (+ merge_edges over all edges only if the queue overflowed)
 //   -> K4+K5 repair_diagram -> finish_diagram
 // All launches are asynchronous on the caller's stream; only mt_diagram /
 // mt_diagram_view / mt_last_error synchronise.
@@ -17,13 +18,13 @@ namespace {
 
 constexpr size_t ALIGN = 256;
 constexpr uint32_t ESS_CAP = 64;  // essential classes = connected components (1 per grid)
-constexpr int MAX_EVENTS = 8;
+constexpr int MAX_EVENTS = 12;
 
 size_t align_up(size_t x) { return (x + ALIGN - 1) / ALIGN * ALIGN; }
 
 struct Layout {
-    size_t counters, status, stats, ess, cells, pairs, total;
-    uint64_t ntiles, pairs_cap;
+    size_t counters, status, stats, ess, cells, queue, pairs, total;
+    uint64_t ntiles, pairs_cap, queue_cap;
 };
 
 bool valid_dims(const uint32_t dims[3], int conn) {
@@ -50,6 +51,9 @@ Layout layout_for(uint64_t n) {
     off += align_up(ESS_CAP * sizeof(mt_pair));
     L.cells = off;  // 16-byte working cells of the merge phase
     off += align_up(n * sizeof(mt::Cell));
+    L.queue = off;  // inter-basin edges (2 per vertex; more falls back to the all-edge merge)
+    L.queue_cap = 2 * n;
+    off += align_up(L.queue_cap * mt::queue_entry_bytes());
     L.pairs = off;
     off += align_up(L.pairs_cap * sizeof(mt_pair));
     L.total = off;
@@ -237,14 +241,19 @@ mt_status mt_compute(mt_ctx* c, const float* f, uint64_t* T, uint32_t flags, mt_
     mt::launch_init_descent(f, cells, c->nx, c->ny, c->nz, flip, ctr, s);
     mark(c, "compress", s);
     mt::launch_compress(cells, c->n, c->num_sms, s);
-    mark(c, "merge_edges", s);
-    mt::launch_merge_edges(cells, c->nx, c->ny, c->nz, c->num_sms, stats, s);
+    void* queue = c->ws + c->L.queue;
+    mark(c, "filter_edges", s);
+    mt::launch_filter_edges(cells, c->nx, c->ny, c->nz, queue, c->L.queue_cap, ctr + mt::CTR_QLEN, c->num_sms, s);
+    mark(c, "merge_queue", s);
+    mt::launch_merge_queue(cells, queue, c->L.queue_cap, ctr + mt::CTR_QLEN, stats, c->num_sms, s);
+    mark(c, "merge_fallback", s);
+    mt::launch_merge_edges(cells, c->nx, c->ny, c->nz, c->num_sms, stats, ctr + mt::CTR_QLEN, c->L.queue_cap, s);
     mark(c, "repair_diagram", s);
     mt::launch_repair_diagram(cells, T, f, c->n, ctr, status, out, cap, ess, ESS_CAP, stats, s);
     mark(c, "finish_diagram", s);
     mt::launch_finish_diagram(ctr, out, cap, ess, ESS_CAP, s);
     if (c->profiling) cudaEventRecord(c->ev[c->nev], s);
-    c->launches = 5;
+    c->launches = 8;
     if (cudaGetLastError() != cudaSuccess) return c->sticky = MT_ERR_CUDA;
     return MT_OK;
 }

@@ -1,0 +1,41 @@
+"""Summarise ncu reports (raw page) into a compact per-kernel table (markdown)."""
+import csv
+import io
+import subprocess
+import sys
+
+METRICS = [
+    ("gpu__time_duration.sum", "time"),
+    ("dram__bytes_read.sum", "dram rd"),
+    ("dram__bytes_write.sum", "dram wr"),
+    ("dram__throughput.avg.pct_of_peak_sustained_elapsed", "dram %pk"),
+    ("lts__t_sector_hit_rate.pct", "L2 hit %"),
+    ("sm__throughput.avg.pct_of_peak_sustained_elapsed", "SM %pk"),
+    ("smsp__thread_inst_executed_per_inst_executed.ratio", "thr/inst"),
+    ("sm__warps_active.avg.pct_of_peak_sustained_active", "occ %"),
+    ("launch__registers_per_thread", "regs"),
+    ("launch__grid_size", "grid"),
+]
+
+
+def rows_of(rep):
+    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    hdr, units = rows[0], rows[1]
+    return hdr, units, rows[2:]
+
+
+print("| kernel | " + " | ".join(m[1] for m in METRICS) + " |")
+print("|---" * (len(METRICS) + 1) + "|")
+for rep in sys.argv[1:]:
+    hdr, units, rows = rows_of(rep)
+    for r in rows:
+        name = r[hdr.index("Kernel Name")].split("(")[0].replace("void ", "").replace("unnamed>::", "")
+        cells = []
+        for m, _ in METRICS:
+            if m in hdr:
+                i = hdr.index(m)
+                cells.append(f"{r[i]} {units[i]}".strip())
+            else:
+                cells.append("-")
+        print(f"| {name} | " + " | ".join(cells) + " |")

@@ -45,7 +45,7 @@ def test_workspace_bytes(lib):
     assert _lib.mt_workspace_bytes((0, 16, 16), 6) > 0            # empty grid is valid
     assert _lib.mt_workspace_bytes((1 << 16, 1 << 16, 2), 6) == 0  # > 2^32 vertices
     a = _lib.mt_workspace_bytes((512, 512, 512), 6)
-    assert a % 256 == 0 and a < 512 ** 3 * 25  # 16-B cells + <= n/2 records
+    assert a % 256 == 0 and a < 512 ** 3 * 57  # 16-B cells + 2n queue entries + <= n/2 records
 
 
 def test_create_rejects_bad_args_without_gpu(lib):
