@@ -185,12 +185,20 @@ def _config(args, dims, conn):
             "parallelism": f"replicas{args.gpus}" if args.gpus > 1 else "single"}
 
 
-# algorithmic bytes per vertex / per record of each kernel
+# algorithmic bytes of each kernel: n vertices, rec diagram
+# records, ecross tile-crossing edges; the store is counted at the paper's 8 B per vertex
+def _ecross(dims):
+    nx, ny, nz = dims
+    ty, tz = (128, 1) if nz == 1 else (16, 8)
+    kx, ky, kz = -(-nx // 32) - 1, -(-ny // ty) - 1, -(-nz // tz) - 1
+    return kx * ny * nz + ky * nx * nz + kz * nx * ny
+
+
 ALG_BYTES = {
-    "init_descent": lambda n, rec: 12 * n,          # read f (4) + write T (8)
-    "merge_edges": lambda n, rec: 12 * n,           # read f (4) + read T (8) over every edge's endpoints
-    "repair_diagram": lambda n, rec: 20 * n + 16 * rec,  # read f (4) + read T (8) + write T (8) + records
-    "finish_diagram": lambda n, rec: 0,
+    "tile_tmt": lambda n, rec, ec: 12 * n,                 # read f (4) + write the store (8)
+    "merge_cross": lambda n, rec, ec: 2 * 8 * ec,          # read both end cells of every crossing edge
+    "repair_diagram": lambda n, rec, ec: 20 * n + 16 * rec,  # read f (4) + read store (8) + write T (8) + records
+    "finish_diagram": lambda n, rec, ec: 0,
 }
 
 
@@ -256,7 +264,7 @@ def run_mt(args, rank, world):
     recs = npairs + ness
     avg = {k: statistics.mean(v) for k, v in kt.items()}
     dom = max((k for k in avg if k in ALG_BYTES), key=lambda k: avg[k])
-    alg = ALG_BYTES[dom](n, recs)
+    alg = ALG_BYTES[dom](n, recs, _ecross(dims))
     achieved = alg / (avg[dom] * 1e-3) / 1e9
     traffic = None
     prof_path = os.path.join(ROOT, "profiles", "traffic.json")

@@ -128,7 +128,10 @@ int mt_kernel_times(mt_ctx *ctx, const char **names, float *ms, int max);
 /* Diagnostics: while enabled, mt_compute counts events of the merge and
  * repair kernels: [0] edges examined, [1] edges skipped as redundant,
  * [2] cells followed by the pre-filter walks, [3] Alg. 3 loop iterations,
- * [4] failed CAS, [5] cells followed by the repair walks.  mt_stats syncs
+ * [4] failed CAS, [5] cells followed by the repair walks, [6..10] the
+ * same for the in-tile phase (edges, walk hops, merge iterations, repair
+ * hops, compress hops), [11..16] SM cycles of the tile phases (load,
+ * descent, compress, merge, repair, write; summed over tiles).  mt_stats syncs
  * `stream` and copies up to `max` counters to out (host); returns the
  * number written (0 if disabled). */
 mt_status mt_set_stats(mt_ctx *ctx, int enable);

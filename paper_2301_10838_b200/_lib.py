@@ -165,7 +165,9 @@ def mt_kernel_times(ctx, max_entries: int = 8):
     return [(names[i].decode(), float(ms[i])) for i in range(k)]
 
 
-STAT_NAMES = ["edges", "skipped", "pre_hops", "merge_iters", "cas_fail", "repair_hops", "queued"]
+STAT_NAMES = ["edges", "skipped", "pre_hops", "merge_iters", "cas_fail", "repair_hops", "tile_edges",
+              "tile_hops", "tile_iters", "tile_repair_hops", "tile_compress_hops", "cyc_load", "cyc_descent",
+              "cyc_compress", "cyc_merge", "cyc_repair", "cyc_write", "cyc_list", "tile_steps", "tile_active", "tile_maxiter", "tile_long"]
 
 
 def mt_set_stats(ctx, enable: bool):
@@ -173,8 +175,8 @@ def mt_set_stats(ctx, enable: bool):
 
 
 def mt_stats(ctx, stream=None):
-    out = (ctypes.c_uint64 * 8)()
-    k = load().mt_stats(ctx, out, 8, _stream_handle(stream))
+    out = (ctypes.c_uint64 * 24)()
+    k = load().mt_stats(ctx, out, 24, _stream_handle(stream))
     return {name: int(out[i]) for i, name in enumerate(STAT_NAMES) if i < k}
 
 

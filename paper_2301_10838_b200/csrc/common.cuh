@@ -119,21 +119,35 @@ enum CounterSlot : int {
     CTR_ESS = 2,        // number of essential classes found
     CTR_FIN = 3,        // number of finite pairs (written by the last tile)
     CTR_CAP = 4,        // capacity (records) of the diagram target buffer
-    CTR_QLEN = 5,       // inter-basin edges found by the filter (may exceed the queue)
-    CTR_QFETCH = 6,     // next queue entry to hand out (merge_queue)
+    CTR_QFETCH = 6,     // next crossing edge to hand out (merge_cross)
     CTR_COUNT = 8
 };
 
 // Optional diagnostics (mt_set_stats): event counters in the workspace.
 enum StatSlot : int {
-    ST_EDGES = 0,        // edges examined by the merge kernel
-    ST_SKIPPED = 1,      // edges removed by the redundant-edge pre-filter
-    ST_PRE_HOPS = 2,     // cells followed by the pre-filter walks
+    ST_EDGES = 0,        // tile-crossing edges examined by the global merge kernel
+    ST_SKIPPED = 1,      // of those, edges whose walks met (nothing to join)
+    ST_PRE_HOPS = 2,     // cells followed by the walks at the edge level
     ST_MERGE_ITERS = 3,  // iterations of the Alg. 3 loop
     ST_CAS_FAIL = 4,     // failed CAS (Alg. 3 l.17 restarts)
     ST_REPAIR_HOPS = 5,  // cells followed by the repair walks
-    ST_QUEUED = 6,       // inter-basin edges queued by the filter
-    ST_COUNT = 8
+    ST_TILE_EDGES = 6,   // in-tile edges between two basins (tile kernel)
+    ST_TILE_HOPS = 7,    // cells followed by the in-tile walks
+    ST_TILE_ITERS = 8,   // in-tile Alg. 3 loop iterations
+    ST_TILE_REPAIR = 9,  // cells followed by the in-tile repair
+    ST_TILE_COMPRESS = 10,  // cells followed by the in-tile compress
+    ST_CYC_LOAD = 11,    // SM cycles (summed over tiles) of each tile phase
+    ST_CYC_DESCENT = 12,
+    ST_CYC_COMPRESS = 13,
+    ST_CYC_MERGE = 14,
+    ST_CYC_REPAIR = 15,
+    ST_CYC_WRITE = 16,
+    ST_CYC_LIST = 17,
+    ST_TILE_STEPS = 18,  // warp steps of the in-tile merge state machine
+    ST_TILE_ACTIVE = 19, // busy lanes summed over those steps
+    ST_TILE_MAXITER = 20,  // longest single in-tile merge (Alg. 3 iterations)
+    ST_TILE_LONG = 21,     // in-tile merges with more than 32 iterations
+    ST_COUNT = 24
 };
 
 }  // namespace mt

@@ -1,0 +1,225 @@
+// merge_cross.cu -- K3 on the global store: merge every grid edge that
+// crosses a tile face (the in-tile edges were merged by tile_tmt.cu) with
+// Alg. 3 "Parallel Merge" over 128-bit CAS cells.
+//
+// Work: the crossing edges are enumerated directly (no queue): e in
+// [0, Ex + Ey + Ez) decodes to an x-, y- or z-face edge; consecutive e are
+// neighbours on one face.  Persistent warps take batches of 256 edge ids per
+// global atomic.
+//
+// Each lane runs its edge as a state machine advanced by ONE memory
+// round-trip per step (a cell load, a pair of independent cell loads, or a
+// CAS), and idle lanes are refilled at every step, so a warp stays converged
+// and keeps up to 32 independent loads in flight (a per-thread nested-loop
+// version left 2.5 active lanes per instruction, ncu profiles/r1_c4_ncu_v1.md).
+//
+// Per edge (a, b): L = max(key(a), key(b)) (Alg. 1 l.5-8); both ends are
+// walked through cells with key(s) <= L (Alg. 4's walk at level L, with path
+// splitting by 128-bit CAS, derivation E'); if the walks meet, the edge joins
+// nothing new (derivation C'); otherwise Merge(T, r_hi, hi, r_lo) runs: climbs
+// with the root guard R4, the swap of l.11-12, the CAS of l.14, the
+// re-merge of a displaced non-root pair (l.15, guard R5), restarts (l.17)
+// that re-read both cells.
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace mt {
+
+namespace {
+
+struct CrossGeom {
+    uint32_t nx, ny, nz, tx, ty, tz;   // grid and tile shape
+    uint64_t ex, ey, ez;               // number of crossing edges on x-, y-, z-faces
+};
+
+__device__ __forceinline__ void decode_edge(const CrossGeom& g, uint64_t e, uint32_t* a, uint32_t* b) {
+    const uint64_t sxy = uint64_t(g.nx) * g.ny;
+    uint64_t u, step;
+    if (e < g.ex) {                               // x-face k: x = (k+1) tx - 1 -> +1
+        const uint64_t per = uint64_t(g.ny) * g.nz;
+        const uint64_t k = e / per, r = e % per;
+        const uint64_t y = r % g.ny, z = r / g.ny;
+        u = z * sxy + y * g.nx + (k + 1) * g.tx - 1;
+        step = 1;
+    } else if ((e -= g.ex) < g.ey) {              // y-face k: y = (k+1) ty - 1 -> +nx
+        const uint64_t per = uint64_t(g.nx) * g.nz;
+        const uint64_t k = e / per, r = e % per;
+        const uint64_t x = r % g.nx, z = r / g.nx;
+        u = z * sxy + ((k + 1) * g.ty - 1) * g.nx + x;
+        step = g.nx;
+    } else {                                      // z-face k: z = (k+1) tz - 1 -> +nx ny
+        e -= g.ey;
+        const uint64_t k = e / sxy, r = e % sxy;
+        u = ((k + 1) * g.tz - 1) * sxy + r;
+        step = sxy;
+    }
+    *a = uint32_t(u);
+    *b = uint32_t(u + step);
+}
+
+enum Phase : int { IDLE = 0, LOAD_AB = 1, CLIMB_HI = 2, CLIMB_LO = 3, MERGE_LD = 4, MERGE_CAS = 5, DONE = 6 };
+
+template <bool STATS>
+__global__ void __launch_bounds__(256)
+merge_cross_kernel(Cell* C, CrossGeom g, unsigned long long* __restrict__ fetch,
+                   unsigned long long* __restrict__ stats) {
+    constexpr uint64_t BATCH = 256;
+    const int lane = threadIdx.x & 31;
+    const uint64_t total = g.ex + g.ey + g.ez;
+    uint64_t pool_next = 0, pool_end = 0;  // warp-uniform
+    bool exhausted = false;                // warp-uniform
+
+    int phase = IDLE;
+    uint64_t L = 0, ks = 0;
+    uint32_t x = 0, xp = 0, lo = 0, rh = 0, u = 0, v = 0;
+    bool has_prev = false, have_c = false;
+    Cell c{0, 0}, cp{0, 0}, clo{0, 0}, cu{0, 0}, cv{0, 0}, desired{0, 0}, got{0, 0};
+    unsigned long long n_edges = 0, n_hops = 0, n_iters = 0, n_fail = 0, n_skip = 0;
+
+    while (true) {
+        const uint32_t need = __ballot_sync(FULL_MASK, phase == IDLE);
+        if (need) {
+            if (pool_next == pool_end && !exhausted) {
+                unsigned long long b0 = 0;
+                if (lane == 0) b0 = atomicAdd(fetch, (unsigned long long)BATCH);
+                b0 = __shfl_sync(FULL_MASK, b0, 0);
+                pool_next = b0 < total ? b0 : total;
+                pool_end = b0 + BATCH < total ? b0 + BATCH : total;
+                exhausted = pool_next == pool_end;
+            }
+            const uint32_t rank = __popc(need & ((1u << lane) - 1u));
+            const uint64_t avail = pool_end - pool_next;
+            if (phase == IDLE) {
+                if (rank < avail) {
+                    decode_edge(g, pool_next + rank, &u, &v);   // u, v hold the edge ends a, b
+                    phase = LOAD_AB;
+                    if (STATS) n_edges++;
+                } else if (exhausted) {
+                    phase = DONE;
+                }
+            }
+            pool_next += avail < __popc(need) ? avail : __popc(need);
+        }
+        if (__ballot_sync(FULL_MASK, phase != DONE) == 0) break;
+
+        // ---- one memory round-trip ----
+        if (phase == LOAD_AB || phase == MERGE_LD) {
+            cu = ld_cell(C + u);
+            cv = ld_cell(C + v);
+        } else if ((phase == CLIMB_HI || phase == CLIMB_LO) && !have_c) {
+            c = ld_cell(C + x);
+        } else if (phase == MERGE_CAS) {
+            got = cas_cell(C + v, cv, desired);
+        }
+        have_c = false;
+
+        // ---- advance ----
+        if (phase == LOAD_AB) {
+            const uint64_t ka = self_key(cu, u), kb = self_key(cv, v);
+            L = ka > kb ? ka : kb;
+            x = ka > kb ? u : v;                     // walk the upper end first
+            c = ka > kb ? cu : cv;
+            lo = ka > kb ? v : u;
+            clo = ka > kb ? cv : cu;
+            has_prev = false;
+            phase = CLIMB_HI;
+        }
+        if (phase == CLIMB_HI || phase == CLIMB_LO) {
+            if (cv_of(c) != x && c.lo <= L) {          // followable at level L
+                if (STATS) n_hops++;
+                if (has_prev && c.lo <= cp.lo)         // path splitting: prev skips x
+                    cas_cell(C + xp, cp, Cell{cp.lo, (cp.hi & 0xffffffff00000000ull) | cv_of(c)});
+                xp = x;
+                cp = c;
+                has_prev = true;
+                x = cv_of(c);
+            } else if (phase == CLIMB_HI) {
+                rh = x;
+                x = lo;
+                c = clo;                               // already loaded
+                have_c = true;
+                has_prev = false;
+                phase = CLIMB_LO;
+            } else if (x == rh) {                      // walks met: nothing to join
+                if (STATS) n_skip++;
+                phase = IDLE;
+            } else {
+                u = rh;                                // Merge(T, r_hi, hi, r_lo) at level L
+                v = x;
+                ks = L;
+                phase = MERGE_LD;
+            }
+        } else if (phase == MERGE_LD) {
+            if (STATS) n_iters++;
+            if (cv_of(cu) != u && cu.lo < ks) {        // l.2-4 (+ R4): climb u, restart
+                u = cv_of(cu);
+            } else if (cv_of(cv) != v && cv.lo < ks) { // l.5-8 (+ R4): climb v, restart
+                v = cv_of(cv);
+            } else if (u == v) {                       // l.9-10
+                phase = IDLE;
+            } else {
+                if (self_key(cv, v) < self_key(cu, u)) {   // l.11-12: swap
+                    const uint32_t t = u; u = v; v = t;
+                    const Cell tc = cu; cu = cv; cv = tc;
+                }
+                desired = Cell{ks, (cv.hi & 0xffffffff00000000ull) | u};  // l.14: (s, u) into T[v]
+                phase = MERGE_CAS;
+            }
+        } else if (phase == MERGE_CAS) {
+            if (got.lo == cv.lo && got.hi == cv.hi) {
+                const uint32_t vp = cv_of(cv);
+                if (vp == v) {
+                    phase = IDLE;                      // displaced a root (R5)
+                } else {
+                    ks = cv.lo;                        // l.15: Merge(T, u, s_v, v')
+                    v = vp;
+                    phase = MERGE_LD;
+                }
+            } else {
+                if (STATS) n_fail++;
+                phase = MERGE_LD;                      // l.17: restart
+            }
+        }
+    }
+    if (STATS) {
+        atomicAdd(stats + ST_EDGES, n_edges);
+        atomicAdd(stats + ST_PRE_HOPS, n_hops);
+        atomicAdd(stats + ST_MERGE_ITERS, n_iters);
+        atomicAdd(stats + ST_CAS_FAIL, n_fail);
+        atomicAdd(stats + ST_SKIPPED, n_skip);
+    }
+}
+
+}  // namespace
+
+void launch_merge_cross(Cell* C, uint32_t nx, uint32_t ny, uint32_t nz, unsigned long long* fetch,
+                        unsigned long long* stats, int num_sms, cudaStream_t stream) {
+    CrossGeom g{};
+    g.nx = nx;
+    g.ny = ny;
+    g.nz = nz;
+    g.tx = 32;
+    tile_shape(nz, &g.ty, &g.tz);
+    const uint64_t kx = (nx + g.tx - 1) / g.tx - 1, ky = (ny + g.ty - 1) / g.ty - 1,
+                   kz = (nz + g.tz - 1) / g.tz - 1;
+    g.ex = kx * ny * nz;
+    g.ey = ky * nx * nz;
+    g.ez = kz * uint64_t(nx) * ny;
+    if (g.ex + g.ey + g.ez == 0) return;
+    static int per_sm[2] = {0, 0};  // persistent grid: as many CTAs as fit on every SM
+    const int t = stats ? 1 : 0;
+    if (!per_sm[t]) {
+        if (stats)
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[t], merge_cross_kernel<true>, 256, 0);
+        else
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[t], merge_cross_kernel<false>, 256, 0);
+        if (per_sm[t] < 1) per_sm[t] = 1;
+    }
+    const uint32_t blocks = uint32_t(num_sms) * per_sm[t];
+    if (stats)
+        merge_cross_kernel<true><<<blocks, 256, 0, stream>>>(C, g, fetch, stats);
+    else
+        merge_cross_kernel<false><<<blocks, 256, 0, stream>>>(C, g, fetch, stats);
+}
+
+}  // namespace mt

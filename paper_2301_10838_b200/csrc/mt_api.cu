@@ -1,8 +1,8 @@
 // mt_api.cu -- the C ABI of libmt_b200 (declared and documented in
 // include/mt.h): context, caller-owned workspace layout, sticky errors, stream
 // plumbing and the launch sequence of the hot path:
-//   zero counters -> K1+K2 init_descent -> K4 compress -> K3 filter_edges + merge_queue
-//   (+ merge_edges over all edges only if the queue overflowed)
+//   zero counters -> tile_tmt (K1, K2, in-tile K3/K4) -> merge_cross (K3 on
+//   the tile-crossing edges) -> repair_diagram (K4 + K5) -> finish_diagram
 //   -> K4+K5 repair_diagram -> finish_diagram
 // All launches are asynchronous on the caller's stream; only mt_diagram /
 // mt_diagram_view / mt_last_error synchronise.
@@ -23,8 +23,8 @@ constexpr int MAX_EVENTS = 12;
 size_t align_up(size_t x) { return (x + ALIGN - 1) / ALIGN * ALIGN; }
 
 struct Layout {
-    size_t counters, status, stats, ess, cells, queue, pairs, total;
-    uint64_t ntiles, pairs_cap, queue_cap;
+    size_t counters, status, stats, ess, cells, pairs, total;
+    uint64_t ntiles, pairs_cap;
 };
 
 bool valid_dims(const uint32_t dims[3], int conn) {
@@ -51,9 +51,6 @@ Layout layout_for(uint64_t n) {
     off += align_up(ESS_CAP * sizeof(mt_pair));
     L.cells = off;  // 16-byte working cells of the merge phase
     off += align_up(n * sizeof(mt::Cell));
-    L.queue = off;  // inter-basin edges (2 per vertex; more falls back to the all-edge merge)
-    L.queue_cap = 2 * n;
-    off += align_up(L.queue_cap * mt::queue_entry_bytes());
     L.pairs = off;
     off += align_up(L.pairs_cap * sizeof(mt_pair));
     L.total = off;
@@ -237,23 +234,16 @@ mt_status mt_compute(mt_ctx* c, const float* f, uint64_t* T, uint32_t flags, mt_
     if (cudaMemsetAsync(c->ws + c->L.counters, 0, c->L.status - c->L.counters + c->L.ntiles * sizeof(uint64_t),
                         s) != cudaSuccess)
         return c->sticky = MT_ERR_CUDA;
-    mark(c, "init_descent", s);
-    mt::launch_init_descent(f, cells, c->nx, c->ny, c->nz, flip, ctr, s);
-    mark(c, "compress", s);
-    mt::launch_compress(cells, c->n, c->num_sms, s);
-    void* queue = c->ws + c->L.queue;
-    mark(c, "filter_edges", s);
-    mt::launch_filter_edges(cells, c->nx, c->ny, c->nz, queue, c->L.queue_cap, ctr + mt::CTR_QLEN, c->num_sms, s);
-    mark(c, "merge_queue", s);
-    mt::launch_merge_queue(cells, queue, c->L.queue_cap, ctr + mt::CTR_QLEN, stats, c->num_sms, s);
-    mark(c, "merge_fallback", s);
-    mt::launch_merge_edges(cells, c->nx, c->ny, c->nz, c->num_sms, stats, ctr + mt::CTR_QLEN, c->L.queue_cap, s);
+    mark(c, "tile_tmt", s);
+    mt::launch_tile_tmt(f, cells, c->nx, c->ny, c->nz, flip, ctr, stats, s);
+    mark(c, "merge_cross", s);
+    mt::launch_merge_cross(cells, c->nx, c->ny, c->nz, ctr + mt::CTR_QFETCH, stats, c->num_sms, s);
     mark(c, "repair_diagram", s);
     mt::launch_repair_diagram(cells, T, f, c->n, ctr, status, out, cap, ess, ESS_CAP, stats, s);
     mark(c, "finish_diagram", s);
     mt::launch_finish_diagram(ctr, out, cap, ess, ESS_CAP, s);
     if (c->profiling) cudaEventRecord(c->ev[c->nev], s);
-    c->launches = 8;
+    c->launches = 4;
     if (cudaGetLastError() != cudaSuccess) return c->sticky = MT_ERR_CUDA;
     return MT_OK;
 }
@@ -333,7 +323,7 @@ mt_status mt_set_stats(mt_ctx* c, int enable) {
 int mt_stats(mt_ctx* c, uint64_t* out, int max, mt_stream_t stream) {
     if (!c || !out || !c->stats || !c->computed || c->n == 0) return 0;
     DeviceGuard g(c->device);
-    const int k = max < mt::ST_COUNT ? max : mt::ST_COUNT;
+    const int k = max < int(mt::ST_COUNT) ? max : int(mt::ST_COUNT);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     if (cudaMemcpyAsync(out, c->ws + c->L.stats, k * sizeof(uint64_t), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
         cudaStreamSynchronize(s) != cudaSuccess)
