@@ -15,8 +15,10 @@ oracle O1 (serial C, 1 core) on a bounded sub-block of the same field.
 
 --impl reference times the oracle itself (the only "reference" this paper-only
 build has) on bounded samples of the same workload.
-Under torchrun (N > 1) every rank runs its own replica of the workload (the
-slab decomposition of SURVEY.md 8e is not built yet), reported as weak scaling.
+Under torchrun (N > 1) the grid is split into z-slabs, one per rank
+(paper_2301_10838_b200/dist.py): local merge tree, NCCL all-gather of the
+boundary forests, global merge + repair; the same total grid on every N
+(strong scaling), time = max over ranks.
 """
 from __future__ import annotations
 
@@ -172,17 +174,23 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+def _device_index():
+    # MT_FORCE_DEVICE puts every rank on one GPU (with MT_DIST_BACKEND=gloo) to test the
+    # multi-rank path on a single-GPU box; normally LOCAL_RANK picks the GPU
+    return int(os.environ.get("MT_FORCE_DEVICE", os.environ.get("LOCAL_RANK", 0)))
+
+
 def _has_cuda():
     import torch
     return torch.cuda.is_available()
 
 
-def _config(args, dims, conn):
+def _config(args, dims, conn, world=1):
     from paper_2301_10838_b200.fields import CONFIGS
     return {"workload": f"{args.config}: {CONFIGS[args.config]['name']}" + (" (split tree)" if args.split else ""),
             "dims": list(dims), "connectivity": conn, "vertices": int(np.prod(dims)),
             "l2_policy": "inputs larger than L2 + 512 MiB L2 flush before every timed step",
-            "parallelism": f"replicas{args.gpus}" if args.gpus > 1 else "single"}
+            "parallelism": f"zslab{world} (NCCL all-gather of boundary forests)" if world > 1 else "single"}
 
 
 # algorithmic bytes of each kernel: n vertices, rec diagram
@@ -202,33 +210,87 @@ ALG_BYTES = {
 }
 
 
+class SingleRunner:
+    """One GPU, the whole grid: mt_compute + mt_diagram through the C ABI."""
+
+    def __init__(self, dims, conn, f, dev, flags):
+        from paper_2301_10838_b200 import _lib
+        self.lib = _lib
+        self.mt = _lib.MergeTree(dims, conn, device=dev.index)
+        self.ctx = self.mt.ctx
+        self.n = int(np.prod(dims))
+        self.f = f
+        self.T = torch_empty(self.n, dev)
+        self.flags = flags
+
+    def step(self, f=None, rec_dev=None):
+        lib = self.lib
+        lib.mt_compute(self.ctx, (self.f if f is None else f).data_ptr(), self.T.data_ptr(), self.flags)
+        st, npairs, ness = lib.mt_diagram(self.ctx, rec_dev.data_ptr() if rec_dev is not None else 0,
+                                          rec_dev.shape[0] if rec_dev is not None else 0)
+        if st != lib.MT_OK:
+            raise lib.MTError(st, "mt_diagram")
+        return npairs, ness
+
+
+class SlabRunner:
+    """Rank r of a z-slab decomposition (paper_2301_10838_b200.dist): local merge tree, NCCL all-gather
+    of the boundary forests, global merge + repair of the slab."""
+
+    def __init__(self, dims, f_slab, dev, flags):
+        from paper_2301_10838_b200 import _lib
+        from paper_2301_10838_b200.dist import DistMergeTree
+        self.lib = _lib
+        self.d = DistMergeTree(dims, device=dev)
+        self.ctx = self.d.slab.ctx
+        self.n = self.d.slab.n
+        self.f = f_slab
+        self.T = torch_empty(self.n, dev)
+        self.split = bool(flags)
+
+    def step(self, f=None, rec_dev=None):
+        lib = self.lib
+        self.d.compute(self.f if f is None else f, self.split, self.T)
+        st, npairs, ness = lib.mt_diagram(self.ctx, rec_dev.data_ptr() if rec_dev is not None else 0,
+                                          rec_dev.shape[0] if rec_dev is not None else 0)
+        if st != lib.MT_OK:
+            raise lib.MTError(st, "mt_diagram")
+        return npairs, ness
+
+
+def torch_empty(n, dev):
+    import torch
+    return torch.empty(n, dtype=torch.int64, device=dev)
+
+
 def run_mt(args, rank, world):
     import torch
     import torch.distributed as dist
 
     from paper_2301_10838_b200 import _lib
 
-    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
+    dev = torch.device("cuda", _device_index())
     torch.cuda.set_device(dev)
     f_np, dims, conn = field_for(args.config, args.scale, dev if args.config == "c5" else "cpu")
-    n = int(np.prod(dims))
-    f = torch.from_numpy(f_np).to(dev)
-    mt = _lib.MergeTree(dims, conn, device=dev.index)
-    T = torch.empty(n, dtype=torch.int64, device=dev)
+    n_global = int(np.prod(dims))
+    flags = _lib.MT_FLAG_SPLIT_TREE if args.split else 0
+    if world > 1:
+        from paper_2301_10838_b200.dist import slab_bounds
+        if dims[2] < world or conn != 6:
+            raise SystemExit("multi-GPU runs need a 3D grid with at least one plane per rank")
+        zb = slab_bounds(dims[2], world)
+        plane = dims[0] * dims[1]
+        f_np = np.ascontiguousarray(f_np[zb[rank] * plane: zb[rank + 1] * plane])
+        runner = SlabRunner(dims, torch.from_numpy(f_np).to(dev), dev, flags)
+    else:
+        runner = SingleRunner(dims, conn, torch.from_numpy(f_np).to(dev), dev, flags)
+    n_local = runner.n
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream()
-    flags = _lib.MT_FLAG_SPLIT_TREE if args.split else 0
-
-    def step():
-        _lib.mt_compute(mt.ctx, f.data_ptr(), T.data_ptr(), flags, stream)
-        st, npairs, ness = _lib.mt_diagram(mt.ctx, 0, 0, stream)
-        if st != _lib.MT_OK:
-            raise _lib.MTError(st, "mt_diagram")
-        return npairs, ness
 
     for _ in range(max(3, args.warmup)):
-        step()
-    _lib.mt_set_profiling(mt.ctx, True)
+        runner.step()
+    _lib.mt_set_profiling(runner.ctx, True)
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     kt = {}
     launches = 0
@@ -239,32 +301,36 @@ def run_mt(args, rank, world):
         for i in range(args.steps):
             flush.fill_(i & 0xff)  # evict L2 between timed steps (outside the events)
             ev[i][0].record(stream)
-            npairs, ness = step()
+            npairs, ness = runner.step()
             ev[i][1].record(stream)
-            launches += _lib.mt_last_launch_count(mt.ctx)
-            for name, ms in _lib.mt_kernel_times(mt.ctx):
+            launches += _lib.mt_last_launch_count(runner.ctx)
+            for name, ms in _lib.mt_kernel_times(runner.ctx, 16):
                 kt.setdefault(name, []).append(ms)
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
-    _lib.mt_set_profiling(mt.ctx, False)
+    _lib.mt_set_profiling(runner.ctx, False)
     step_ms = [a.elapsed_time(b) for a, b in ev]
     my_ms = sum(step_ms)
     if world > 1:
-        t = torch.tensor([my_ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        max_ms = float(t.item())
+        t = torch.tensor([my_ms, float(npairs), float(ness), float(launches)], dtype=torch.float64, device=dev)
+        tm = t.clone()
+        dist.all_reduce(tm, op=dist.ReduceOp.MAX)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        max_ms = float(tm[0].item())
+        npairs, ness, launches = int(t[1].item()), int(t[2].item()), int(t[3].item())
     else:
         max_ms = my_ms
     ms_per_step = max_ms / args.steps
-    value = world * n / (ms_per_step * 1e-3) / 1e6
+    value = n_global / (ms_per_step * 1e-3) / 1e6
 
-    # roofline of the dominant kernel
+    # roofline of the dominant kernel (rank 0's kernels; per launch, its own slab)
     peak, peak_kind = peaks()
     recs = npairs + ness
     avg = {k: statistics.mean(v) for k, v in kt.items()}
     dom = max((k for k in avg if k in ALG_BYTES), key=lambda k: avg[k])
-    alg = ALG_BYTES[dom](n, recs, _ecross(dims))
+    local_dims = (dims[0], dims[1], n_local // (dims[0] * dims[1]))
+    alg = ALG_BYTES[dom](n_local, recs * n_local // n_global, _ecross(local_dims))
     achieved = alg / (avg[dom] * 1e-3) / 1e9
     traffic = None
     prof_path = os.path.join(ROOT, "profiles", "traffic.json")
@@ -278,17 +344,17 @@ def run_mt(args, rank, world):
                 "alg_bytes_per_launch": alg, "kernel_ms": avg[dom],
                 "kernel_share_of_step": avg[dom] / ms_per_step,
                 "kernels_ms": avg,
-                "step_alg_bytes_per_vertex": 12 + 16 * recs / n,
-                "step_frac": (12 * n + 16 * recs) / (ms_per_step * 1e-3) / 1e9 / peak}
+                "step_alg_bytes_per_vertex": 12 + 16 * recs / n_global,
+                "step_frac": (12 * n_global + 16 * recs) / (ms_per_step * 1e-3) / 1e9 / (peak * world)}
 
     # end to end through the public API with pinned host buffers
     e2e = None
     if not args.no_e2e:
         f_host = torch.from_numpy(f_np).pin_memory()
-        T_host = torch.empty(n, dtype=torch.int64).pin_memory()
-        rec_dev = torch.empty(((n + 1) // 2 + 1, 4), dtype=torch.int32, device=dev)
-        rec_host = torch.empty_like(rec_dev, device="cpu").pin_memory()
-        f_dev = torch.empty_like(f)
+        T_host = torch.empty(n_local, dtype=torch.int64).pin_memory()
+        rec_dev = torch.empty(((n_local + 1) // 2 + 2, 4), dtype=torch.int32, device=dev)
+        rec_host = torch.empty(rec_dev.shape, dtype=torch.int32).pin_memory()
+        f_dev = torch.empty(n_local, dtype=torch.float32, device=dev)
         e2e_steps = max(2, min(args.steps, 5))
         h2d = d2h = 0
         if world > 1:
@@ -298,20 +364,21 @@ def run_mt(args, rank, world):
         t0.record(stream)
         for _ in range(e2e_steps):
             f_dev.copy_(f_host, non_blocking=True)
-            _lib.mt_compute(mt.ctx, f_dev.data_ptr(), T.data_ptr(), flags, stream)
-            st, a, b = _lib.mt_diagram(mt.ctx, rec_dev.data_ptr(), rec_dev.shape[0], stream)
-            T_host.copy_(T, non_blocking=True)
+            a, b = runner.step(f_dev, rec_dev)
+            T_host.copy_(runner.T, non_blocking=True)
             rec_host[: a + b].copy_(rec_dev[: a + b], non_blocking=True)
-            h2d = 4 * n
-            d2h = 8 * n + 16 * (a + b)
+            h2d = 4 * n_local
+            d2h = 8 * n_local + 16 * (a + b)
         t1.record(stream)
         torch.cuda.synchronize()
         e_ms = t0.elapsed_time(t1)
         if world > 1:
-            t = torch.tensor([e_ms], dtype=torch.float64, device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            e_ms = float(t.item())
-        e2e = {"value": world * n * e2e_steps / (e_ms * 1e-3) / 1e6, "unit": "Mvertices/s",
+            t = torch.tensor([e_ms, float(h2d), float(d2h)], dtype=torch.float64, device=dev)
+            tm = t.clone()
+            dist.all_reduce(tm, op=dist.ReduceOp.MAX)
+            dist.all_reduce(t, op=dist.ReduceOp.SUM)
+            e_ms, h2d, d2h = float(tm[0].item()), int(t[1].item()), int(t[2].item())
+        e2e = {"value": n_global * e2e_steps / (e_ms * 1e-3) / 1e6, "unit": "Mvertices/s",
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": e2e_steps}
 
     cpu = None
@@ -326,14 +393,16 @@ def run_mt(args, rank, world):
         line = {
             "metric": METRIC, "value": value, "unit": "Mvertices/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (seeded generator, paper_2301_10838_b200/fields.py)",
-            "config": _config(args, dims, conn),
+            "config": _config(args, dims, conn, world),
             "pairs": npairs, "essential": ness,
             "step_ms": {"median": statistics.median(step_ms), "min": min(step_ms), "max": max(step_ms)},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clk.summary(),
         }
+        if world > 1:
+            line["forest_records"] = runner.d.forest_records
         print(json.dumps(line), flush=True)
 
 
@@ -347,8 +416,12 @@ def main():
     if world > 1:
         import torch
         import torch.distributed as dist
-        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
-        dist.init_process_group("nccl")
+        torch.cuda.set_device(_device_index())
+        backend = os.environ.get("MT_DIST_BACKEND", "nccl")  # gloo: multi-rank test on one GPU
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", _device_index()))
+        else:
+            dist.init_process_group(backend)
     try:
         run_mt(args, rank, world)
     finally:

@@ -125,6 +125,52 @@ uint32_t mt_last_launch_count(const mt_ctx *ctx);
 mt_status mt_set_profiling(mt_ctx *ctx, int enable);
 int mt_kernel_times(mt_ctx *ctx, const char **names, float *ms, int max);
 
+/* ---- Multi-GPU: z-slab decomposition (distribution is the
+ * paper's future work) --------------------------------
+ * Rank r of P owns planes [z_begin, z_end) of the global grid; vertex ids stay
+ * GLOBAL everywhere (triplets and diagram records hold global ids).  3D grids
+ * only (conn 6), at most 64 slabs.  Per step:
+ *   1. mt_compute_local  -- merge tree of the slab subgraph + its boundary
+ *      forest (the cells reachable from the slab's inter-slab faces);
+ *   2. mt_forest_view    -- the forest records (the caller all-gathers them,
+ *      e.g. with NCCL, concatenating every rank's records in any order);
+ *   3. mt_compute_global -- merges every inter-slab edge on the union of the
+ *      forests, then repairs the slab and extracts its diagram: the slab's
+ *      finite pairs (births in the slab, ascending) and, on the rank owning
+ *      the global minimum, the essential class; mt_diagram as usual.
+ * The result equals the single-GPU result (the store is unique, PAPER.md:
+ * 196-200).  Forest record: the vertex id, its cell, and the f bits of the
+ * vertex and of its saddle s (a saddle travels with displaced pairs across
+ * slabs, and diagram values are copied from the input f, reading R14). */
+typedef struct {
+    uint32_t id;       /* global vertex id */
+    uint32_t f_bits;   /* bits of f[id] */
+    uint64_t key_s;    /* order key of s: ord(f[s]) << 32 | s */
+    uint64_t hi;       /* ord(f[id]) << 32 | v */
+    uint32_t s_f_bits; /* bits of f[s] (diagram values of saddles owned by other ranks) */
+    uint32_t reserved;
+} mt_forest_record;    /* 32 bytes */
+
+size_t mt_slab_workspace_bytes(const uint32_t global_dims[3], int conn, uint32_t z_begin, uint32_t z_end);
+mt_status mt_create_slab(mt_ctx **out, const uint32_t global_dims[3], int conn, uint32_t z_begin,
+                         uint32_t z_end, int cuda_device, void *workspace, size_t workspace_bytes);
+/* f_slab (device): the slab's nx*ny*(z_end-z_begin) values, borrowed until
+ * mt_compute_global's work completes.  Asynchronous. */
+mt_status mt_compute_local(mt_ctx *ctx, const float *f_slab, uint32_t flags, mt_stream_t stream);
+/* Syncs; device pointer to the slab's forest records (valid until the next
+ * mt_compute_local) and their number. */
+mt_status mt_forest_view(mt_ctx *ctx, const mt_forest_record **records, uint64_t *n_records,
+                         mt_stream_t stream);
+/* Device scratch bytes mt_compute_global needs for n_all gathered records. */
+size_t mt_forest_scratch_bytes(uint64_t n_all);
+/* all (device): the records of every slab, n_all of them; z_bounds (host):
+ * the P+1 plane boundaries of all slabs (z_bounds[0] = 0, z_bounds[P] = nz);
+ * scratch (device, >= mt_forest_scratch_bytes(n_all), 256-B aligned);
+ * triplets_slab (device, out): the slab's n_local cells.  Asynchronous. */
+mt_status mt_compute_global(mt_ctx *ctx, const mt_forest_record *all, uint64_t n_all,
+                            const uint32_t *z_bounds, uint32_t nslabs, void *scratch,
+                            size_t scratch_bytes, uint64_t *triplets_slab, mt_stream_t stream);
+
 /* Diagnostics: while enabled, mt_compute counts events of the merge and
  * repair kernels: [0] edges examined, [1] edges skipped as redundant,
  * [2] cells followed by the pre-filter walks, [3] Alg. 3 loop iterations,

@@ -23,11 +23,13 @@ MT_ERR_NCCL, MT_ERR_STATE, MT_ERR_CAPACITY, MT_ERR_WORKSPACE = 5, 6, 7, 8
 MT_FLAG_SPLIT_TREE = 1
 
 PAIR_DTYPE = np.dtype([("birth_v", "<u4"), ("death_v", "<u4"), ("birth", "<f4"), ("death", "<f4")])
+FOREST_RECORD_BYTES = 32  # mt_forest_record
 
 # every symbol include/mt.h declares (checked by tests/test_abi_cpu.py)
 EXPORTS = ["mt_workspace_bytes", "mt_create", "mt_compute", "mt_set_diagram_output", "mt_diagram",
            "mt_diagram_view", "mt_last_error", "mt_last_launch_count", "mt_set_profiling", "mt_kernel_times",
-           "mt_status_string", "mt_destroy", "mt_abi_version", "mt_set_stats", "mt_stats"]
+           "mt_status_string", "mt_destroy", "mt_abi_version", "mt_set_stats", "mt_stats", "mt_slab_workspace_bytes",
+           "mt_create_slab", "mt_compute_local", "mt_forest_view", "mt_forest_scratch_bytes", "mt_compute_global"]
 
 
 class MTError(RuntimeError):
@@ -71,6 +73,14 @@ def load(build_if_missing: bool = False):
         "mt_set_stats": (ctypes.c_int, [vp, ctypes.c_int]),
         "mt_stats": (ctypes.c_int, [vp, u64p, ctypes.c_int, vp]),
         "mt_destroy": (None, [vp]),
+        "mt_slab_workspace_bytes": (ctypes.c_size_t, [u32p, ctypes.c_int, ctypes.c_uint32, ctypes.c_uint32]),
+        "mt_create_slab": (ctypes.c_int, [ctypes.POINTER(vp), u32p, ctypes.c_int, ctypes.c_uint32, ctypes.c_uint32,
+                                          ctypes.c_int, vp, ctypes.c_size_t]),
+        "mt_compute_local": (ctypes.c_int, [vp, vp, ctypes.c_uint32, vp]),
+        "mt_forest_view": (ctypes.c_int, [vp, ctypes.POINTER(vp), u64p, vp]),
+        "mt_forest_scratch_bytes": (ctypes.c_size_t, [ctypes.c_uint64]),
+        "mt_compute_global": (ctypes.c_int, [vp, vp, ctypes.c_uint64, u32p, ctypes.c_uint32, vp, ctypes.c_size_t,
+                                             vp, vp]),
         "mt_abi_version": (ctypes.c_int, []),
     }
     for name, (res, args) in sig.items():
@@ -182,6 +192,42 @@ def mt_stats(ctx, stream=None):
 
 def mt_destroy(ctx):
     load().mt_destroy(ctx)
+
+
+# ---- multi-GPU z-slab entry points (include/mt.h) ---------------------------
+
+def mt_slab_workspace_bytes(dims, conn: int, z_begin: int, z_end: int) -> int:
+    return int(load().mt_slab_workspace_bytes(_dims(dims), int(conn), int(z_begin), int(z_end)))
+
+
+def mt_create_slab(dims, conn: int, z_begin: int, z_end: int, device: int, workspace_ptr: int, workspace_bytes: int):
+    h = ctypes.c_void_p()
+    _check(load().mt_create_slab(ctypes.byref(h), _dims(dims), int(conn), int(z_begin), int(z_end), int(device),
+                                 ctypes.c_void_p(workspace_ptr), ctypes.c_size_t(workspace_bytes)), "mt_create_slab")
+    return h
+
+
+def mt_compute_local(ctx, f_ptr: int, flags: int = 0, stream=None):
+    _check(load().mt_compute_local(ctx, ctypes.c_void_p(f_ptr), int(flags), _stream_handle(stream)),
+           "mt_compute_local")
+
+
+def mt_forest_view(ctx, stream=None):
+    ptr, n = ctypes.c_void_p(), ctypes.c_uint64(0)
+    _check(load().mt_forest_view(ctx, ctypes.byref(ptr), ctypes.byref(n), _stream_handle(stream)), "mt_forest_view")
+    return ptr.value, n.value
+
+
+def mt_forest_scratch_bytes(n_all: int) -> int:
+    return int(load().mt_forest_scratch_bytes(ctypes.c_uint64(n_all)))
+
+
+def mt_compute_global(ctx, all_ptr: int, n_all: int, z_bounds, scratch_ptr: int, scratch_bytes: int,
+                      triplets_ptr: int, stream=None):
+    zb = (ctypes.c_uint32 * len(z_bounds))(*[int(z) for z in z_bounds])
+    _check(load().mt_compute_global(ctx, ctypes.c_void_p(all_ptr or None), ctypes.c_uint64(n_all), zb,
+                                    len(z_bounds) - 1, ctypes.c_void_p(scratch_ptr), ctypes.c_size_t(scratch_bytes),
+                                    ctypes.c_void_p(triplets_ptr), _stream_handle(stream)), "mt_compute_global")
 
 
 # ---- convenience owner --------------------------------------------------------

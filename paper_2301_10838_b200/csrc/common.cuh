@@ -111,6 +111,7 @@ __device__ __forceinline__ Cell cas_cell(Cell* p, const Cell& expected, const Ce
 constexpr uint32_t ERR_NONFINITE = 1u;
 constexpr uint32_t ERR_CAPACITY = 2u;
 constexpr uint32_t ERR_ESS_CAPACITY = 4u;
+constexpr uint32_t ERR_FOREST = 8u;   // a vertex missing from the gathered boundary forest
 
 // Workspace counter slots (uint64 each).
 enum CounterSlot : int {
@@ -118,8 +119,9 @@ enum CounterSlot : int {
     CTR_ERR = 1,        // error bits
     CTR_ESS = 2,        // number of essential classes found
     CTR_FIN = 3,        // number of finite pairs (written by the last tile)
-    CTR_CAP = 4,        // capacity (records) of the diagram target buffer
+    CTR_FFETCH = 4,     // next inter-slab edge to hand out (forest_merge)
     CTR_QFETCH = 6,     // next crossing edge to hand out (merge_cross)
+    CTR_FCOUNT = 7,     // boundary-forest records of this slab
     CTR_COUNT = 8
 };
 

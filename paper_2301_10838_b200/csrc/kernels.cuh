@@ -8,23 +8,98 @@
 
 namespace mt {
 
+// The part of the global grid one context computes: planes [z_begin, z_end) of an
+// nx x ny x nz grid (the whole grid on one GPU; a z-slab per rank on several).
+// Vertex ids are global; device pointers handed to the launchers are shifted by
+// -base so that they are indexed by global id.
+struct Slab {
+    uint32_t nx, ny, nz;        // global grid
+    uint32_t z_begin, z_end;    // owned planes
+    uint64_t base;              // global id of the first owned vertex = nx ny z_begin
+    uint64_t n;                 // owned vertices
+};
+
+// Boundary forest of all slabs (multi-GPU, slab.cu): records of every rank in one
+// array, an open-addressing table global id -> record index, 16-B cells with global
+// ids after the forest merge, and the f bits of each record's vertex.
+struct ForestRef {
+    const uint64_t* table;      // (id << 32 | index) or ~0 (empty); size mask + 1
+    const uint64_t* vtable;     // (id << 32 | f bits) of every record's vertex and saddle; same size
+    uint32_t mask;
+    Cell* cells;                // merged cells, global ids
+    const mt_forest_record* recs;
+    unsigned long long* err;    // error bits (ERR_FOREST on a missing id)
+};
+
+__device__ __forceinline__ uint32_t forest_hash(uint32_t id, uint32_t mask) {
+    uint32_t h = id ^ (id >> 16);   // integer mixer: consecutive face ids spread over the table
+    h *= 0x7feb352du;
+    h ^= h >> 15;
+    h *= 0x846ca68bu;
+    h ^= h >> 16;
+    return h & mask;
+}
+constexpr uint32_t FOREST_MISS = 0xffffffffu;
+// index of id's record, or FOREST_MISS (an empty slot ends the probe)
+__device__ __forceinline__ uint32_t forest_lookup(const ForestRef& F, uint32_t id) {
+    uint32_t h = forest_hash(id, F.mask);
+    for (uint32_t probe = 0; probe <= F.mask; ++probe) {
+        const uint64_t e = F.table[h];
+        if (e == ~0ull) return FOREST_MISS;
+        if (uint32_t(e >> 32) == id) return uint32_t(e);
+        h = (h + 1) & F.mask;
+    }
+    return FOREST_MISS;
+}
+
+__device__ __forceinline__ bool forest_value(const ForestRef& F, uint32_t id, uint32_t* bits) {
+    uint32_t h = forest_hash(id, F.mask);
+    for (uint32_t probe = 0; probe <= F.mask; ++probe) {
+        const uint64_t e = F.vtable[h];
+        if (e == ~0ull) return false;
+        if (uint32_t(e >> 32) == id) {
+            *bits = uint32_t(e);
+            return true;
+        }
+        h = (h + 1) & F.mask;
+    }
+    return false;
+}
+
 // tile shape (32 x ty x tz, 4096 vertices) for a grid with nz planes
-void tile_shape(uint32_t nz, uint32_t* ty, uint32_t* tz);
+void tile_shape(uint32_t nz_global, uint32_t* ty, uint32_t* tz);
 
 // K1 + K2 + in-tile K3/K4: keys, steepest descent, tile-local merge tree (tile_tmt.cu)
-void launch_tile_tmt(const float* f, Cell* C, uint32_t nx, uint32_t ny, uint32_t nz, uint32_t flip,
-                     unsigned long long* counters, unsigned long long* stats, cudaStream_t stream);
+void launch_tile_tmt(const float* f, Cell* C, const Slab& sl, uint32_t flip, unsigned long long* counters,
+                     unsigned long long* stats, cudaStream_t stream);
 
 // K3: merge of the tile-crossing grid edges on the global store (merge_cross.cu)
-void launch_merge_cross(Cell* C, uint32_t nx, uint32_t ny, uint32_t nz, unsigned long long* fetch,
-                        unsigned long long* stats, int num_sms, cudaStream_t stream);
+void launch_merge_cross(Cell* C, const Slab& sl, unsigned long long* fetch, unsigned long long* stats, int num_sms,
+                        cudaStream_t stream);
 
 // K4+K5: repair fused with the ordered diagram compaction (repair_diagram.cu)
 uint64_t repair_tiles(uint64_t n);
-void launch_repair_diagram(Cell* C, uint64_t* T, const float* f, uint64_t n, unsigned long long* counters,
+void launch_repair_diagram(Cell* C, uint64_t* T, const float* f, uint64_t base, uint64_t n, unsigned long long* counters,
                            uint64_t* status, mt_pair* out, uint64_t out_cap, mt_pair* ess, uint32_t ess_cap,
-                           unsigned long long* stats, cudaStream_t stream);
+                           unsigned long long* stats, const ForestRef* forest, cudaStream_t stream);
 void launch_finish_diagram(unsigned long long* counters, mt_pair* out, uint64_t out_cap, mt_pair* ess,
                            uint32_t ess_cap, cudaStream_t stream);
+
+// multi-GPU boundary forest (slab.cu)
+constexpr int MAX_SLABS = 64;
+struct SlabBounds {
+    uint32_t z[MAX_SLABS + 1];
+    uint32_t count;             // number of slabs
+};
+void launch_forest_mark(const Cell* C, const Slab& sl, uint8_t* flag, cudaStream_t stream);
+void launch_forest_compact(const Cell* C, const float* f, const Slab& sl, const uint8_t* flag, mt_forest_record* recs,
+                           uint64_t cap, unsigned long long* count, int num_sms, cudaStream_t stream);
+uint32_t forest_table_size(uint64_t n_all);
+void launch_forest_build(const mt_forest_record* all, uint64_t n_all, uint64_t* table, uint64_t* vtable,
+                         uint32_t mask, Cell* cells, int num_sms, cudaStream_t stream);
+void launch_forest_merge(const ForestRef& F, const Slab& sl, const SlabBounds& b, unsigned long long* fetch,
+                         int num_sms, cudaStream_t stream);
+void launch_forest_writeback(const ForestRef& F, uint64_t n_all, Cell* C, const Slab& sl, int num_sms,
+                             cudaStream_t stream);
 
 }  // namespace mt

@@ -28,7 +28,8 @@ namespace mt {
 namespace {
 
 struct CrossGeom {
-    uint32_t nx, ny, nz, tx, ty, tz;   // grid and tile shape
+    uint32_t nx, ny, nz, tx, ty, tz;   // slab (nz = local planes) and tile shape
+    uint64_t base;                     // global id of the slab's first vertex
     uint64_t ex, ey, ez;               // number of crossing edges on x-, y-, z-faces
 };
 
@@ -53,8 +54,8 @@ __device__ __forceinline__ void decode_edge(const CrossGeom& g, uint64_t e, uint
         u = ((k + 1) * g.tz - 1) * sxy + r;
         step = sxy;
     }
-    *a = uint32_t(u);
-    *b = uint32_t(u + step);
+    *a = uint32_t(g.base + u);        // global ids
+    *b = uint32_t(g.base + u + step);
 }
 
 enum Phase : int { IDLE = 0, LOAD_AB = 1, CLIMB_HI = 2, CLIMB_LO = 3, MERGE_LD = 4, MERGE_CAS = 5, DONE = 6 };
@@ -192,19 +193,20 @@ merge_cross_kernel(Cell* C, CrossGeom g, unsigned long long* __restrict__ fetch,
 
 }  // namespace
 
-void launch_merge_cross(Cell* C, uint32_t nx, uint32_t ny, uint32_t nz, unsigned long long* fetch,
-                        unsigned long long* stats, int num_sms, cudaStream_t stream) {
+void launch_merge_cross(Cell* C, const Slab& sl, unsigned long long* fetch, unsigned long long* stats, int num_sms,
+                        cudaStream_t stream) {
     CrossGeom g{};
-    g.nx = nx;
-    g.ny = ny;
-    g.nz = nz;
+    g.nx = sl.nx;
+    g.ny = sl.ny;
+    g.nz = sl.z_end - sl.z_begin;
+    g.base = sl.base;
     g.tx = 32;
-    tile_shape(nz, &g.ty, &g.tz);
-    const uint64_t kx = (nx + g.tx - 1) / g.tx - 1, ky = (ny + g.ty - 1) / g.ty - 1,
-                   kz = (nz + g.tz - 1) / g.tz - 1;
-    g.ex = kx * ny * nz;
-    g.ey = ky * nx * nz;
-    g.ez = kz * uint64_t(nx) * ny;
+    tile_shape(sl.nz, &g.ty, &g.tz);
+    const uint64_t kx = (g.nx + g.tx - 1) / g.tx - 1, ky = (g.ny + g.ty - 1) / g.ty - 1,
+                   kz = g.nz ? (g.nz + g.tz - 1) / g.tz - 1 : 0;
+    g.ex = g.nz ? kx * g.ny * g.nz : 0;
+    g.ey = g.nz ? ky * g.nx * g.nz : 0;
+    g.ez = kz * uint64_t(g.nx) * g.ny;
     if (g.ex + g.ey + g.ez == 0) return;
     static int per_sm[2] = {0, 0};  // persistent grid: as many CTAs as fit on every SM
     const int t = stats ? 1 : 0;

@@ -23,8 +23,8 @@ constexpr int MAX_EVENTS = 12;
 size_t align_up(size_t x) { return (x + ALIGN - 1) / ALIGN * ALIGN; }
 
 struct Layout {
-    size_t counters, status, stats, ess, cells, pairs, total;
-    uint64_t ntiles, pairs_cap;
+    size_t counters, status, stats, ess, cells, pairs, flags, recs, total;
+    uint64_t ntiles, pairs_cap, recs_cap;
 };
 
 bool valid_dims(const uint32_t dims[3], int conn) {
@@ -34,7 +34,7 @@ bool valid_dims(const uint32_t dims[3], int conn) {
     return true;
 }
 
-Layout layout_for(uint64_t n) {
+Layout layout_for(uint64_t n, bool slab = false) {
     Layout L{};
     L.ntiles = n ? mt::repair_tiles(n) : 0;
     // finite pairs <= #minima - 1 and strict minima form an independent set of
@@ -53,6 +53,13 @@ Layout layout_for(uint64_t n) {
     off += align_up(n * sizeof(mt::Cell));
     L.pairs = off;
     off += align_up(L.pairs_cap * sizeof(mt_pair));
+    if (slab) {  // boundary forest of the slab: a flag per vertex, at most n records
+        L.flags = off;
+        off += align_up(n);
+        L.recs = off;
+        L.recs_cap = n;
+        off += align_up(n * sizeof(mt_forest_record));
+    }
     L.total = off;
     return L;
 }
@@ -61,7 +68,12 @@ Layout layout_for(uint64_t n) {
 
 struct mt_ctx {
     uint32_t nx, ny, nz;
-    uint64_t n;
+    uint64_t n;              // vertices this context owns
+    mt::Slab slab;           // owned planes of the global grid (all of them for mt_create)
+    bool multi = false;      // created by mt_create_slab
+    bool local_done = false; // mt_compute_local ran, mt_compute_global pending
+    const float* f = nullptr;
+    uint32_t flip = 0;
     int conn;
     int device;
     int num_sms;
@@ -96,6 +108,10 @@ struct DeviceGuard {
 };
 
 unsigned long long* counters_of(mt_ctx* c) { return reinterpret_cast<unsigned long long*>(c->ws + c->L.counters); }
+mt::Cell* cells_of(mt_ctx* c) { return reinterpret_cast<mt::Cell*>(c->ws + c->L.cells) - c->slab.base; }
+unsigned long long* stats_of(mt_ctx* c) {
+    return c->stats ? reinterpret_cast<unsigned long long*>(c->ws + c->L.stats) : nullptr;
+}
 mt_pair* target_of(mt_ctx* c, uint64_t* cap) {
     if (c->reg_out) {
         *cap = c->reg_cap;
@@ -117,6 +133,7 @@ void mark(mt_ctx* c, const char* name, cudaStream_t s) {
 mt_status sync_counters(mt_ctx* c, cudaStream_t s) {
     if (!c->computed) return MT_ERR_STATE;
     if (c->n == 0) {
+        c->host_ctr[mt::CTR_FCOUNT] = 0;
         c->host_ctr[mt::CTR_FIN] = 0;
         c->host_ctr[mt::CTR_ESS] = 0;
         c->host_ctr[mt::CTR_ERR] = 0;
@@ -128,8 +145,101 @@ mt_status sync_counters(mt_ctx* c, cudaStream_t s) {
         return c->sticky = MT_ERR_CUDA;
     const uint64_t err = c->host_ctr[mt::CTR_ERR];
     if (err & mt::ERR_NONFINITE) c->sticky = MT_ERR_NONFINITE;
+    else if (err & mt::ERR_FOREST) c->sticky = MT_ERR_INVALID_ARG;
     else if (err & (mt::ERR_CAPACITY | mt::ERR_ESS_CAPACITY)) c->sticky = MT_ERR_CAPACITY;
     return c->sticky;
+}
+
+
+}  // namespace
+extern "C" void mt_destroy(mt_ctx* c);
+namespace {
+
+mt_status create_ctx(mt_ctx** out, const uint32_t dims[3], int conn, uint32_t z_begin, uint32_t z_end, bool multi,
+                     int cuda_device, void* workspace, size_t workspace_bytes) {
+    if (!out) return MT_ERR_INVALID_ARG;
+    *out = nullptr;
+    if (!valid_dims(dims, conn)) return MT_ERR_INVALID_ARG;
+    if (uint64_t(dims[0]) * dims[1] * dims[2] > 0xffffffffull) return MT_ERR_TOO_LARGE;
+    const uint64_t n = uint64_t(dims[0]) * dims[1] * (z_end - z_begin);
+    const Layout L = layout_for(n, multi);
+    if (!workspace || workspace_bytes < L.total || (reinterpret_cast<uintptr_t>(workspace) % ALIGN))
+        return MT_ERR_WORKSPACE;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess) return MT_ERR_CUDA;
+    if (cuda_device < 0 || cuda_device >= ndev) return MT_ERR_INVALID_ARG;
+    DeviceGuard g(cuda_device);
+    if (!g.ok) return MT_ERR_CUDA;
+    mt_ctx* c = new (std::nothrow) mt_ctx();
+    if (!c) return MT_ERR_CUDA;
+    c->nx = dims[0];
+    c->ny = dims[1];
+    c->nz = dims[2];
+    c->n = n;
+    c->slab = mt::Slab{dims[0], dims[1], dims[2], z_begin, z_end, uint64_t(dims[0]) * dims[1] * z_begin, n};
+    c->multi = multi;
+    c->conn = conn;
+    c->device = cuda_device;
+    c->ws = static_cast<char*>(workspace);
+    c->ws_bytes = workspace_bytes;
+    c->L = L;
+    if (cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, cuda_device) != cudaSuccess ||
+        cudaMallocHost(&c->host_ctr, mt::CTR_COUNT * sizeof(uint64_t)) != cudaSuccess) {
+        delete c;
+        return MT_ERR_CUDA;
+    }
+    for (int i = 0; i <= MAX_EVENTS; ++i)
+        if (cudaEventCreate(&c->ev[i]) != cudaSuccess) {
+            mt_destroy(c);
+            return MT_ERR_CUDA;
+        }
+    *out = c;
+    return MT_OK;
+}
+
+// shared by mt_compute and mt_compute_local: reset, then the slab's own merge tree
+mt_status start_compute(mt_ctx* c, const float* f, uint32_t flags, cudaStream_t s) {
+    c->launches = 0;
+    c->nev = 0;
+    c->sticky = MT_OK;
+    c->computed = true;
+    c->f = f;
+    c->flip = (flags & MT_FLAG_SPLIT_TREE) ? 0xffffffffu : 0u;
+    unsigned long long* ctr = counters_of(c);
+    mt::Cell* cells = cells_of(c);
+    unsigned long long* stats = stats_of(c);
+    const float* fs = f - c->slab.base;  // every kernel indexes f, T and the cells by global id
+    if (stats && cudaMemsetAsync(stats, 0, mt::ST_COUNT * sizeof(uint64_t), s) != cudaSuccess)
+        return c->sticky = MT_ERR_CUDA;
+    mark(c, "zero", s);
+    if (cudaMemsetAsync(c->ws + c->L.counters, 0, c->L.status - c->L.counters + c->L.ntiles * sizeof(uint64_t),
+                        s) != cudaSuccess)
+        return c->sticky = MT_ERR_CUDA;
+    mark(c, "tile_tmt", s);
+    mt::launch_tile_tmt(fs, cells, c->slab, c->flip, ctr, stats, s);
+    mark(c, "merge_cross", s);
+    mt::launch_merge_cross(cells, c->slab, ctr + mt::CTR_QFETCH, stats, c->num_sms, s);
+    c->launches = 2;
+    return MT_OK;
+}
+
+// repair (with the merged forest on multi-GPU) + diagram into the target buffer
+mt_status finish_compute(mt_ctx* c, uint64_t* T, const mt::ForestRef* forest, cudaStream_t s) {
+    unsigned long long* ctr = counters_of(c);
+    uint64_t cap = 0;
+    mt_pair* out = target_of(c, &cap);
+    mt_pair* ess = reinterpret_cast<mt_pair*>(c->ws + c->L.ess);
+    uint64_t* status = reinterpret_cast<uint64_t*>(c->ws + c->L.status);
+    const uint64_t base = c->slab.base;
+    mark(c, "repair_diagram", s);
+    mt::launch_repair_diagram(cells_of(c), T - base, c->f - base, base, c->n, ctr, status, out, cap, ess, ESS_CAP,
+                              stats_of(c), forest, s);
+    mark(c, "finish_diagram", s);
+    mt::launch_finish_diagram(ctr, out, cap, ess, ESS_CAP, s);
+    if (c->profiling) cudaEventRecord(c->ev[c->nev], s);
+    c->launches += 2;
+    if (cudaGetLastError() != cudaSuccess) return c->sticky = MT_ERR_CUDA;
+    return MT_OK;
 }
 
 }  // namespace
@@ -162,42 +272,22 @@ size_t mt_workspace_bytes(const uint32_t dims[3], int conn) {
 
 mt_status mt_create(mt_ctx** out, const uint32_t dims[3], int conn, int cuda_device, void* workspace,
                     size_t workspace_bytes) {
+    if (!dims) return MT_ERR_INVALID_ARG;
+    return create_ctx(out, dims, conn, 0, dims[2], false, cuda_device, workspace, workspace_bytes);
+}
+
+size_t mt_slab_workspace_bytes(const uint32_t dims[3], int conn, uint32_t z_begin, uint32_t z_end) {
+    if (!valid_dims(dims, conn) || dims[2] < 2 || z_begin >= z_end || z_end > dims[2]) return 0;
+    if (uint64_t(dims[0]) * dims[1] * dims[2] > 0xffffffffull) return 0;
+    return layout_for(uint64_t(dims[0]) * dims[1] * (z_end - z_begin), true).total;
+}
+
+mt_status mt_create_slab(mt_ctx** out, const uint32_t dims[3], int conn, uint32_t z_begin, uint32_t z_end,
+                         int cuda_device, void* workspace, size_t workspace_bytes) {
     if (!out) return MT_ERR_INVALID_ARG;
     *out = nullptr;
-    if (!valid_dims(dims, conn)) return MT_ERR_INVALID_ARG;
-    const uint64_t n = uint64_t(dims[0]) * dims[1] * dims[2];
-    if (n > 0xffffffffull) return MT_ERR_TOO_LARGE;
-    const Layout L = layout_for(n);
-    if (!workspace || workspace_bytes < L.total || (reinterpret_cast<uintptr_t>(workspace) % ALIGN))
-        return MT_ERR_WORKSPACE;
-    int ndev = 0;
-    if (cudaGetDeviceCount(&ndev) != cudaSuccess) return MT_ERR_CUDA;
-    if (cuda_device < 0 || cuda_device >= ndev) return MT_ERR_INVALID_ARG;
-    DeviceGuard g(cuda_device);
-    if (!g.ok) return MT_ERR_CUDA;
-    mt_ctx* c = new (std::nothrow) mt_ctx();
-    if (!c) return MT_ERR_CUDA;
-    c->nx = dims[0];
-    c->ny = dims[1];
-    c->nz = dims[2];
-    c->n = n;
-    c->conn = conn;
-    c->device = cuda_device;
-    c->ws = static_cast<char*>(workspace);
-    c->ws_bytes = workspace_bytes;
-    c->L = L;
-    if (cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, cuda_device) != cudaSuccess ||
-        cudaMallocHost(&c->host_ctr, mt::CTR_COUNT * sizeof(uint64_t)) != cudaSuccess) {
-        delete c;
-        return MT_ERR_CUDA;
-    }
-    for (int i = 0; i <= MAX_EVENTS; ++i)
-        if (cudaEventCreate(&c->ev[i]) != cudaSuccess) {
-            mt_destroy(c);
-            return MT_ERR_CUDA;
-        }
-    *out = c;
-    return MT_OK;
+    if (!dims || dims[2] < 2 || conn != 6 || z_begin >= z_end || z_end > dims[2]) return MT_ERR_INVALID_ARG;
+    return create_ctx(out, dims, conn, z_begin, z_end, true, cuda_device, workspace, workspace_bytes);
 }
 
 mt_status mt_set_diagram_output(mt_ctx* c, mt_pair* buf, uint64_t capacity) {
@@ -210,42 +300,100 @@ mt_status mt_set_diagram_output(mt_ctx* c, mt_pair* buf, uint64_t capacity) {
 mt_status mt_compute(mt_ctx* c, const float* f, uint64_t* T, uint32_t flags, mt_stream_t stream) {
     if (!c) return MT_ERR_INVALID_ARG;
     if (flags & ~uint32_t(MT_FLAG_SPLIT_TREE)) return MT_ERR_INVALID_ARG;
-    c->launches = 0;
-    c->nev = 0;
-    c->sticky = MT_OK;
-    c->computed = true;
-    if (c->n == 0) return MT_OK;
+    if (c->multi) return MT_ERR_STATE;  // slab contexts use mt_compute_local / mt_compute_global
+    if (c->n == 0) {
+        c->computed = true;
+        c->sticky = MT_OK;
+        c->launches = 0;
+        return MT_OK;
+    }
     if (!f || !T) return MT_ERR_INVALID_ARG;
     DeviceGuard g(c->device);
     if (!g.ok) return MT_ERR_CUDA;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    const uint32_t flip = (flags & MT_FLAG_SPLIT_TREE) ? 0xffffffffu : 0u;
-    unsigned long long* ctr = counters_of(c);
-    uint64_t cap = 0;
-    mt_pair* out = target_of(c, &cap);
-    mt_pair* ess = reinterpret_cast<mt_pair*>(c->ws + c->L.ess);
-    uint64_t* status = reinterpret_cast<uint64_t*>(c->ws + c->L.status);
-    mt::Cell* cells = reinterpret_cast<mt::Cell*>(c->ws + c->L.cells);
-    unsigned long long* stats = c->stats ? reinterpret_cast<unsigned long long*>(c->ws + c->L.stats) : nullptr;
-    if (stats && cudaMemsetAsync(stats, 0, mt::ST_COUNT * sizeof(uint64_t), s) != cudaSuccess)
-        return c->sticky = MT_ERR_CUDA;
+    const mt_status st = start_compute(c, f, flags, s);
+    if (st != MT_OK) return st;
+    return finish_compute(c, T, nullptr, s);
+}
 
-    mark(c, "zero", s);
-    if (cudaMemsetAsync(c->ws + c->L.counters, 0, c->L.status - c->L.counters + c->L.ntiles * sizeof(uint64_t),
-                        s) != cudaSuccess)
-        return c->sticky = MT_ERR_CUDA;
-    mark(c, "tile_tmt", s);
-    mt::launch_tile_tmt(f, cells, c->nx, c->ny, c->nz, flip, ctr, stats, s);
-    mark(c, "merge_cross", s);
-    mt::launch_merge_cross(cells, c->nx, c->ny, c->nz, ctr + mt::CTR_QFETCH, stats, c->num_sms, s);
-    mark(c, "repair_diagram", s);
-    mt::launch_repair_diagram(cells, T, f, c->n, ctr, status, out, cap, ess, ESS_CAP, stats, s);
-    mark(c, "finish_diagram", s);
-    mt::launch_finish_diagram(ctr, out, cap, ess, ESS_CAP, s);
-    if (c->profiling) cudaEventRecord(c->ev[c->nev], s);
-    c->launches = 4;
+mt_status mt_compute_local(mt_ctx* c, const float* f, uint32_t flags, mt_stream_t stream) {
+    if (!c || !f) return MT_ERR_INVALID_ARG;
+    if (flags & ~uint32_t(MT_FLAG_SPLIT_TREE)) return MT_ERR_INVALID_ARG;
+    if (!c->multi) return MT_ERR_STATE;
+    DeviceGuard g(c->device);
+    if (!g.ok) return MT_ERR_CUDA;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    uint8_t* flag = reinterpret_cast<uint8_t*>(c->ws + c->L.flags);
+    if (cudaMemsetAsync(flag, 0, c->n, s) != cudaSuccess) return c->sticky = MT_ERR_CUDA;
+    mt_status st = start_compute(c, f, flags, s);
+    if (st != MT_OK) return st;
+    mark(c, "forest_mark", s);
+    mt::launch_forest_mark(cells_of(c), c->slab, flag, s);
+    mark(c, "forest_compact", s);
+    mt::launch_forest_compact(cells_of(c), f - c->slab.base, c->slab, flag,
+                              reinterpret_cast<mt_forest_record*>(c->ws + c->L.recs), c->L.recs_cap,
+                              counters_of(c) + mt::CTR_FCOUNT, c->num_sms, s);
+    mark(c, "exchange", s);  // closes at mt_compute_global's first mark: host sync + all-gather
+    c->launches += 2;
+    c->local_done = true;
     if (cudaGetLastError() != cudaSuccess) return c->sticky = MT_ERR_CUDA;
     return MT_OK;
+}
+
+mt_status mt_forest_view(mt_ctx* c, const mt_forest_record** records, uint64_t* n_records, mt_stream_t stream) {
+    if (!c) return MT_ERR_INVALID_ARG;
+    if (!c->multi || !c->local_done) return MT_ERR_STATE;
+    DeviceGuard g(c->device);
+    const mt_status st = sync_counters(c, static_cast<cudaStream_t>(stream));
+    if (st == MT_ERR_CUDA || st == MT_ERR_STATE) return st;
+    const uint64_t n = c->host_ctr[mt::CTR_FCOUNT];
+    if (n_records) *n_records = n;
+    if (records) *records = reinterpret_cast<const mt_forest_record*>(c->ws + c->L.recs);
+    if (n > c->L.recs_cap) return MT_ERR_CAPACITY;
+    return st;
+}
+
+size_t mt_forest_scratch_bytes(uint64_t n_all) {
+    return 2 * align_up(size_t(mt::forest_table_size(n_all)) * sizeof(uint64_t)) + align_up(n_all * sizeof(mt::Cell));
+}
+
+mt_status mt_compute_global(mt_ctx* c, const mt_forest_record* all, uint64_t n_all, const uint32_t* z_bounds,
+                            uint32_t nslabs, void* scratch, size_t scratch_bytes, uint64_t* T, mt_stream_t stream) {
+    if (!c || !z_bounds || !T || (n_all && !all)) return MT_ERR_INVALID_ARG;
+    if (!c->multi || !c->local_done) return MT_ERR_STATE;
+    if (nslabs < 1 || nslabs > uint32_t(mt::MAX_SLABS) || z_bounds[0] != 0 || z_bounds[nslabs] != c->nz)
+        return MT_ERR_INVALID_ARG;
+    bool found = false;
+    for (uint32_t k = 0; k < nslabs; ++k) {
+        if (z_bounds[k] >= z_bounds[k + 1]) return MT_ERR_INVALID_ARG;
+        found |= z_bounds[k] == c->slab.z_begin && z_bounds[k + 1] == c->slab.z_end;
+    }
+    if (!found) return MT_ERR_INVALID_ARG;
+    if (n_all > 0xffffffffull) return MT_ERR_TOO_LARGE;
+    if (!scratch || scratch_bytes < mt_forest_scratch_bytes(n_all) || reinterpret_cast<uintptr_t>(scratch) % ALIGN)
+        return MT_ERR_WORKSPACE;
+    DeviceGuard g(c->device);
+    if (!g.ok) return MT_ERR_CUDA;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const uint32_t tsize = mt::forest_table_size(n_all);
+    uint64_t* table = static_cast<uint64_t*>(scratch);
+    uint64_t* vtable = reinterpret_cast<uint64_t*>(static_cast<char*>(scratch) + align_up(size_t(tsize) * 8));
+    mt::Cell* fcells = reinterpret_cast<mt::Cell*>(static_cast<char*>(scratch) + 2 * align_up(size_t(tsize) * 8));
+    mt::ForestRef F{table, vtable, tsize - 1, fcells, all, counters_of(c) + mt::CTR_ERR};
+    mt::SlabBounds b{};
+    b.count = nslabs;
+    for (uint32_t k = 0; k <= nslabs; ++k) b.z[k] = z_bounds[k];
+    mark(c, "forest_build", s);
+    if (cudaMemsetAsync(table, 0xff, 2 * align_up(size_t(tsize) * 8), s) != cudaSuccess)
+        return c->sticky = MT_ERR_CUDA;
+    mt::launch_forest_build(all, n_all, table, vtable, tsize - 1, fcells, c->num_sms, s);
+    mark(c, "forest_merge", s);
+    mt::launch_forest_merge(F, c->slab, b, counters_of(c) + mt::CTR_FFETCH, c->num_sms, s);
+    mark(c, "forest_writeback", s);
+    mt::launch_forest_writeback(F, n_all, cells_of(c), c->slab, c->num_sms, s);
+    c->launches += 3;
+    c->local_done = false;
+    return finish_compute(c, T, &F, s);
 }
 
 mt_status mt_diagram(mt_ctx* c, mt_pair* out, uint64_t capacity, uint64_t* n_pairs, uint64_t* n_essential,

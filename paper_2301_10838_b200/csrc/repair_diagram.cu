@@ -26,13 +26,42 @@ namespace mt {
 
 namespace {
 
+// cell / value access for the repair walk: everything local (one GPU), or local
+// cells plus the merged boundary forest of all slabs (multi-GPU, slab.cu)
+struct LocalView {
+    __device__ __forceinline__ Cell cell(const Cell* C, uint32_t x) const { return ld_cell(C + x); }
+    __device__ __forceinline__ float value(const float* f, uint32_t x) const { return __ldg(f + x); }
+};
+
+struct ForestView {
+    ForestRef F;
+    uint64_t base, n;  // owned global ids [base, base + n)
+    __device__ __forceinline__ bool mine(uint32_t x) const { return uint64_t(x) - base < n; }
+    __device__ __forceinline__ Cell cell(const Cell* C, uint32_t x) const {
+        if (mine(x)) return ld_cell(C + x);
+        const uint32_t i = forest_lookup(F, x);
+        if (i == FOREST_MISS) {            // incomplete records: report, stop the walk here
+            atomicOr(F.err, ERR_FOREST);
+            return Cell{~0ull, x};
+        }
+        return Cell{F.cells[i].lo, F.cells[i].hi};
+    }
+    __device__ __forceinline__ float value(const float* f, uint32_t x) const {
+        if (mine(x)) return __ldg(f + x);
+        uint32_t bits = 0;
+        if (!forest_value(F, x, &bits)) atomicOr(F.err, ERR_FOREST);
+        return __uint_as_float(bits);
+    }
+};
+
 constexpr int THREADS = 256;
 constexpr int ITEMS = 4;
 constexpr int TILE = THREADS * ITEMS;  // 1024 vertices per ticket
 constexpr uint64_t ST_AGG = 1ull << 62, ST_PRE = 2ull << 62, ST_VAL = (1ull << 62) - 1;
 
+template <class View>
 __global__ void __launch_bounds__(THREADS)
-repair_diagram_kernel(Cell* C, uint64_t* __restrict__ T, const float* __restrict__ f, uint64_t n,
+repair_diagram_kernel(View view, Cell* C, uint64_t* __restrict__ T, const float* __restrict__ f, uint64_t base, uint64_t n,
                       unsigned long long* __restrict__ counters, uint64_t* __restrict__ status,
                       mt_pair* __restrict__ out, uint64_t out_cap, mt_pair* __restrict__ ess, uint32_t ess_cap,
                       uint64_t ntiles, unsigned long long* __restrict__ stats) {
@@ -43,16 +72,17 @@ repair_diagram_kernel(Cell* C, uint64_t* __restrict__ T, const float* __restrict
     if (threadIdx.x == 0) s_tile = atomicAdd(counters + CTR_TICKET, 1ull);
     __syncthreads();
     const uint64_t tile = s_tile;
-    const uint64_t base = tile * TILE;
+    const uint64_t first = tile * TILE;  // local index of the tile's first vertex
 
     Cell cell[ITEMS];
     bool fin[ITEMS];
     uint32_t mask[ITEMS];
 #pragma unroll
     for (int k = 0; k < ITEMS; ++k) {
-        const uint64_t u = base + uint64_t(k) * THREADS + threadIdx.x;
-        cell[k] = u < n ? ld_cell(C + u) : Cell{0, 0};
-        fin[k] = u < n && cs_of(cell[k]) != uint32_t(u);
+        const uint64_t l = first + uint64_t(k) * THREADS + threadIdx.x;
+        const uint64_t u = base + l;     // global id (C, T, f are indexed by global id)
+        cell[k] = l < n ? ld_cell(C + u) : Cell{0, 0};
+        fin[k] = l < n && cs_of(cell[k]) != uint32_t(u);
         mask[k] = __ballot_sync(FULL_MASK, fin[k]);
         if (lane == 0) s_cnt[k * 8 + warp] = __popc(mask[k]);
     }
@@ -77,8 +107,9 @@ repair_diagram_kernel(Cell* C, uint64_t* __restrict__ T, const float* __restrict
     unsigned long long hops = 0;
 #pragma unroll
     for (int k = 0; k < ITEMS; ++k) {
-        const uint64_t u = base + uint64_t(k) * THREADS + threadIdx.x;
-        if (u >= n) continue;
+        const uint64_t l = first + uint64_t(k) * THREADS + threadIdx.x;
+        const uint64_t u = base + l;
+        if (l >= n) continue;
         const uint32_t s = cs_of(cell[k]), v = cv_of(cell[k]);
         if (v == uint32_t(u)) {                       // root (u, u, u): essential class
             const uint32_t i = atomicAdd(reinterpret_cast<unsigned int*>(counters + CTR_ESS), 1u);
@@ -90,7 +121,7 @@ repair_diagram_kernel(Cell* C, uint64_t* __restrict__ T, const float* __restrict
         const uint64_t a = cell[k].lo;                // key(s)
         uint32_t x = v;
         while (true) {
-            const Cell c = ld_cell(C + x);
+            const Cell c = view.cell(C, x);
             if (cv_of(c) == x || c.lo > a) break;     // root, or key(s_x) > a: x is Rep(u, a)
             x = cv_of(c);
             ++hops;
@@ -138,10 +169,10 @@ repair_diagram_kernel(Cell* C, uint64_t* __restrict__ T, const float* __restrict
 #pragma unroll
     for (int k = 0; k < ITEMS; ++k) {
         if (!fin[k]) continue;
-        const uint64_t u = base + uint64_t(k) * THREADS + threadIdx.x;
+        const uint64_t u = base + first + uint64_t(k) * THREADS + threadIdx.x;
         const uint64_t pos = prefix + s_cnt[k * 8 + warp] + __popc(mask[k] & ((1u << lane) - 1u));
         const uint32_t s = cs_of(cell[k]);
-        if (pos < out_cap) out[pos] = mt_pair{uint32_t(u), s, __ldg(f + u), __ldg(f + s)};
+        if (pos < out_cap) out[pos] = mt_pair{uint32_t(u), s, __ldg(f + u), view.value(f, s)};
         else atomicOr(counters + CTR_ERR, ERR_CAPACITY);
     }
 }
@@ -174,12 +205,19 @@ __global__ void finish_diagram_kernel(unsigned long long* __restrict__ counters,
 
 uint64_t repair_tiles(uint64_t n) { return (n + TILE - 1) / TILE; }
 
-void launch_repair_diagram(Cell* C, uint64_t* T, const float* f, uint64_t n, unsigned long long* counters,
+void launch_repair_diagram(Cell* C, uint64_t* T, const float* f, uint64_t base, uint64_t n, unsigned long long* counters,
                            uint64_t* status, mt_pair* out, uint64_t out_cap, mt_pair* ess, uint32_t ess_cap,
-                           unsigned long long* stats, cudaStream_t stream) {
+                           unsigned long long* stats, const ForestRef* forest, cudaStream_t stream) {
     const uint64_t ntiles = repair_tiles(n);
-    repair_diagram_kernel<<<uint32_t(ntiles), THREADS, 0, stream>>>(C, T, f, n, counters, status, out, out_cap,
-                                                                     ess, ess_cap, ntiles, stats);
+    if (ntiles == 0) return;
+    if (forest)
+        repair_diagram_kernel<<<uint32_t(ntiles), THREADS, 0, stream>>>(ForestView{*forest, base, n}, C, T, f, base, n,
+                                                                         counters, status, out, out_cap, ess, ess_cap,
+                                                                         ntiles, stats);
+    else
+        repair_diagram_kernel<<<uint32_t(ntiles), THREADS, 0, stream>>>(LocalView{}, C, T, f, base, n, counters,
+                                                                         status, out, out_cap, ess, ess_cap, ntiles,
+                                                                         stats);
 }
 
 void launch_finish_diagram(unsigned long long* counters, mt_pair* out, uint64_t out_cap, mt_pair* ess,

@@ -1,0 +1,317 @@
+// slab.cu -- multi-GPU z-slab decomposition: the boundary forest of a slab,
+// its merge across all slabs, and the write-back (DESIGN.md
+// section 9; distribution is the paper's future work).
+//
+// After each rank computed the store of its slab subgraph (tile_tmt +
+// merge_cross), the global store is the union of the slab stores: a valid
+// normalized store of G minus the inter-slab edges.  Merging an inter-slab
+// edge (Alg. 3) only ever reads or writes cells reachable from the edge's two
+// endpoints by following v pointers (climbs, the CAS target, the displaced
+// pair, path splitting), and a displaced pair points into the same chain, so
+// the set of cells touched by ALL inter-slab merges is contained in the
+// closure of the face vertices under v (DESIGN.md derivation H).  Each rank
+//   1. marks that closure in its slab (forest_mark) and compacts it into
+//      records (forest_compact) -- the records of all ranks are all-gathered;
+//   2. builds an id -> record table over the union (forest_build) and merges
+//      every inter-slab edge on it (forest_merge; the same walks + Alg. 3 as
+//      merge_cross.cu, with cell access through the table);
+//   3. writes the merged cells of its own vertices back (forest_writeback);
+// then the repair walks local cells and, past a remote id, the merged forest
+// (repair_diagram.cu, ForestView).  Every rank merges the whole forest
+// redundantly; the post-repair store is unique, so the ranks agree.
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace mt {
+
+namespace {
+
+__global__ void __launch_bounds__(256)
+forest_mark_kernel(const Cell* C, uint32_t nx, uint32_t ny, uint64_t bottom, uint64_t top, bool has_bottom,
+                   bool has_top, uint64_t base, uint8_t* flag) {
+    const uint64_t sxy = uint64_t(nx) * ny;
+    const uint64_t nface = uint64_t(has_bottom) + uint64_t(has_top);
+    for (uint64_t t = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; t < nface * sxy;
+         t += uint64_t(gridDim.x) * blockDim.x) {
+        const bool first = t < sxy;
+        const uint64_t plane = (first && has_bottom) ? bottom : top;
+        uint32_t x = uint32_t(plane + (t % sxy));
+        // walk the chain, flagging each cell; stop at a flagged cell (its chain is taken)
+        while (true) {
+            uint8_t* fl = flag + (uint64_t(x) - base);
+            if (*reinterpret_cast<volatile uint8_t*>(fl)) break;
+            *reinterpret_cast<volatile uint8_t*>(fl) = 1;
+            const Cell c = ld_cell(C + x);
+            if (cv_of(c) == x) break;
+            x = cv_of(c);
+        }
+    }
+}
+
+__global__ void __launch_bounds__(256)
+forest_compact_kernel(const Cell* C, const float* f, uint64_t base, uint64_t n, const uint8_t* __restrict__ flag,
+                      mt_forest_record* __restrict__ recs, uint64_t cap, unsigned long long* count) {
+    const int lane = threadIdx.x & 31;
+    const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+    for (uint64_t l0 = uint64_t(blockIdx.x) * blockDim.x; l0 < n; l0 += stride) {
+        const uint64_t l = l0 + threadIdx.x;
+        const bool take = l < n && flag[l];
+        const uint32_t m = __ballot_sync(FULL_MASK, take);
+        unsigned long long b = 0;
+        if (lane == 0 && m) b = atomicAdd(count, (unsigned long long)__popc(m));
+        b = __shfl_sync(FULL_MASK, b, 0);
+        if (take) {
+            const uint64_t pos = b + __popc(m & ((1u << lane) - 1u));
+            const uint64_t u = base + l;
+            const Cell c = ld_cell(C + u);
+            if (pos < cap)
+                recs[pos] = mt_forest_record{uint32_t(u), __float_as_uint(f[u]), c.lo, c.hi,
+                                             __float_as_uint(f[cs_of(c)]), 0u};
+        }
+    }
+}
+
+// insert (id -> payload) unless id is present already
+__device__ __forceinline__ void table_put(unsigned long long* t, uint32_t mask, uint32_t id, uint32_t payload) {
+    const unsigned long long e = (static_cast<unsigned long long>(id) << 32) | payload;
+    uint32_t h = forest_hash(id, mask);
+    while (true) {
+        const unsigned long long old = atomicCAS(t + h, ~0ull, e);
+        if (old == ~0ull || uint32_t(old >> 32) == id) return;
+        h = (h + 1) & mask;
+    }
+}
+
+__global__ void __launch_bounds__(256)
+forest_build_kernel(const mt_forest_record* __restrict__ all, uint64_t n_all, unsigned long long* table,
+                    unsigned long long* vtable, uint32_t mask, Cell* cells) {
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n_all;
+         i += uint64_t(gridDim.x) * blockDim.x) {
+        const mt_forest_record r = all[i];
+        cells[i] = Cell{r.key_s, r.hi};
+        table_put(table, mask, r.id, uint32_t(i));
+        table_put(vtable, mask, r.id, r.f_bits);
+        table_put(vtable, mask, uint32_t(r.key_s), r.s_f_bits);
+    }
+}
+
+struct BoundaryGeom {
+    uint32_t nx, ny;
+    uint32_t nb;                   // inter-slab boundaries
+    uint32_t zb[MAX_SLABS];        // plane index of the upper side of boundary k
+};
+
+enum Phase : int { IDLE = 0, LOAD_AB = 1, CLIMB_HI = 2, CLIMB_LO = 3, MERGE_LD = 4, MERGE_CAS = 5, DONE = 6 };
+
+// merge_cross.cu's state machine on the forest: every cell access goes through the table
+__global__ void __launch_bounds__(256)
+forest_merge_kernel(ForestRef F, BoundaryGeom g, unsigned long long* __restrict__ fetch) {
+    constexpr uint64_t BATCH = 256;
+    const int lane = threadIdx.x & 31;
+    const uint64_t sxy = uint64_t(g.nx) * g.ny;
+    const uint64_t total = sxy * g.nb;
+    uint64_t pool_next = 0, pool_end = 0;
+    bool exhausted = false;
+    int phase = IDLE;
+    uint64_t L = 0, ks = 0;
+    uint32_t x = 0, lo = 0, rh = 0, u = 0, v = 0;
+    uint32_t ix = 0, ixp = 0, iu = 0, iv = 0, ilo = 0, irh = 0;   // table indices
+    bool has_prev = false, have_c = false;
+    Cell c{0, 0}, cp{0, 0}, clo{0, 0}, cu{0, 0}, cv{0, 0}, desired{0, 0}, got{0, 0};
+    auto at = [&](uint32_t i) { return F.cells + i; };
+    while (true) {
+        const uint32_t need = __ballot_sync(FULL_MASK, phase == IDLE);
+        if (need) {
+            if (pool_next == pool_end && !exhausted) {
+                unsigned long long b0 = 0;
+                if (lane == 0) b0 = atomicAdd(fetch, (unsigned long long)BATCH);
+                b0 = __shfl_sync(FULL_MASK, b0, 0);
+                pool_next = b0 < total ? b0 : total;
+                pool_end = b0 + BATCH < total ? b0 + BATCH : total;
+                exhausted = pool_next == pool_end;
+            }
+            const uint32_t rank = __popc(need & ((1u << lane) - 1u));
+            const uint64_t avail = pool_end - pool_next;
+            if (phase == IDLE) {
+                if (rank < avail) {
+                    const uint64_t e = pool_next + rank;
+                    const uint64_t k = e / sxy, r = e % sxy;
+                    u = uint32_t((uint64_t(g.zb[k]) - 1) * sxy + r);     // lower side of boundary k
+                    v = uint32_t(u + sxy);
+                    iu = forest_lookup(F, u);
+                    iv = forest_lookup(F, v);
+                    phase = LOAD_AB;
+                    if (iu == FOREST_MISS || iv == FOREST_MISS) {
+                        atomicOr(F.err, ERR_FOREST);
+                        phase = IDLE;
+                    }
+                } else if (exhausted) {
+                    phase = DONE;
+                }
+            }
+            pool_next += avail < __popc(need) ? avail : __popc(need);
+        }
+        if (__ballot_sync(FULL_MASK, phase != DONE) == 0) break;
+
+        if (phase == LOAD_AB || phase == MERGE_LD) {
+            cu = ld_cell(at(iu));
+            cv = ld_cell(at(iv));
+        } else if ((phase == CLIMB_HI || phase == CLIMB_LO) && !have_c) {
+            c = ld_cell(at(ix));
+        } else if (phase == MERGE_CAS) {
+            got = cas_cell(at(iv), cv, desired);
+        }
+        have_c = false;
+
+        if (phase == LOAD_AB) {
+            const uint64_t ka = self_key(cu, u), kb = self_key(cv, v);
+            L = ka > kb ? ka : kb;
+            x = ka > kb ? u : v;
+            ix = ka > kb ? iu : iv;
+            c = ka > kb ? cu : cv;
+            lo = ka > kb ? v : u;
+            ilo = ka > kb ? iv : iu;
+            clo = ka > kb ? cv : cu;
+            has_prev = false;
+            phase = CLIMB_HI;
+        }
+        if (phase == CLIMB_HI || phase == CLIMB_LO) {
+            if (cv_of(c) != x && c.lo <= L) {                       // followable at level L
+                if (has_prev && c.lo <= cp.lo)                      // path splitting
+                    cas_cell(at(ixp), cp, Cell{cp.lo, (cp.hi & 0xffffffff00000000ull) | cv_of(c)});
+                ixp = ix;
+                cp = c;
+                has_prev = true;
+                x = cv_of(c);
+                ix = forest_lookup(F, x);
+                if (ix == FOREST_MISS) {
+                    atomicOr(F.err, ERR_FOREST);
+                    phase = IDLE;
+                }
+            } else if (phase == CLIMB_HI) {
+                rh = x;
+                irh = ix;
+                x = lo;
+                ix = ilo;
+                c = clo;
+                have_c = true;
+                has_prev = false;
+                phase = CLIMB_LO;
+            } else if (x == rh) {
+                phase = IDLE;                                       // already joined below L
+            } else {
+                u = rh;                                             // Merge(T, r_hi, hi, r_lo) at level L
+                iu = irh;
+                v = x;
+                iv = ix;
+                ks = L;
+                phase = MERGE_LD;
+            }
+        } else if (phase == MERGE_LD) {
+            if (cv_of(cu) != u && cu.lo < ks) {                     // l.2-4 (+ R4)
+                u = cv_of(cu);
+                iu = forest_lookup(F, u);
+                if (iu == FOREST_MISS) { atomicOr(F.err, ERR_FOREST); phase = IDLE; }
+            } else if (cv_of(cv) != v && cv.lo < ks) {              // l.5-8 (+ R4)
+                v = cv_of(cv);
+                iv = forest_lookup(F, v);
+                if (iv == FOREST_MISS) { atomicOr(F.err, ERR_FOREST); phase = IDLE; }
+            } else if (u == v) {                                    // l.9-10
+                phase = IDLE;
+            } else {
+                if (self_key(cv, v) < self_key(cu, u)) {            // l.11-12
+                    uint32_t t = u; u = v; v = t;
+                    t = iu; iu = iv; iv = t;
+                    const Cell tc = cu; cu = cv; cv = tc;
+                }
+                desired = Cell{ks, (cv.hi & 0xffffffff00000000ull) | u};   // l.14
+                phase = MERGE_CAS;
+            }
+        } else if (phase == MERGE_CAS) {
+            if (got.lo == cv.lo && got.hi == cv.hi) {
+                const uint32_t vp = cv_of(cv);
+                if (vp == v) {
+                    phase = IDLE;                                   // displaced a root (R5)
+                } else {
+                    ks = cv.lo;                                     // l.15
+                    v = vp;
+                    iv = forest_lookup(F, vp);
+                    phase = MERGE_LD;
+                    if (iv == FOREST_MISS) { atomicOr(F.err, ERR_FOREST); phase = IDLE; }
+                }
+            } else {
+                phase = MERGE_LD;                                   // l.17
+            }
+        }
+    }
+}
+
+__global__ void __launch_bounds__(256)
+forest_writeback_kernel(ForestRef F, uint64_t n_all, Cell* C, uint64_t base, uint64_t n) {
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n_all;
+         i += uint64_t(gridDim.x) * blockDim.x) {
+        const uint32_t id = F.recs[i].id;
+        if (uint64_t(id) - base < n) {
+            const Cell c = F.cells[i];
+            st_cell(C + id, c);
+        }
+    }
+}
+
+uint32_t grid_for(uint64_t work, int num_sms) {
+    uint64_t b = (work + 255) / 256;
+    const uint64_t cap = uint64_t(num_sms) * 8 * 16;
+    if (b > cap) b = cap;
+    return uint32_t(b ? b : 1);
+}
+
+}  // namespace
+
+void launch_forest_mark(const Cell* C, const Slab& sl, uint8_t* flag, cudaStream_t stream) {
+    const bool has_bottom = sl.z_begin > 0, has_top = sl.z_end < sl.nz;
+    if (!has_bottom && !has_top) return;
+    const uint64_t sxy = uint64_t(sl.nx) * sl.ny;
+    const uint64_t work = sxy * (uint64_t(has_bottom) + uint64_t(has_top));
+    forest_mark_kernel<<<grid_for(work, 148), 256, 0, stream>>>(C, sl.nx, sl.ny, uint64_t(sl.z_begin) * sxy,
+                                                                uint64_t(sl.z_end - 1) * sxy, has_bottom, has_top,
+                                                                sl.base, flag);
+}
+
+void launch_forest_compact(const Cell* C, const float* f, const Slab& sl, const uint8_t* flag, mt_forest_record* recs,
+                           uint64_t cap, unsigned long long* count, int num_sms, cudaStream_t stream) {
+    if (sl.n == 0) return;
+    forest_compact_kernel<<<grid_for(sl.n, num_sms), 256, 0, stream>>>(C, f, sl.base, sl.n, flag, recs, cap, count);
+}
+
+uint32_t forest_table_size(uint64_t n_all) {
+    uint64_t s = 1024;
+    while (s < 4 * n_all) s <<= 1;   // the value table holds up to 2 entries per record
+    return uint32_t(s);
+}
+
+void launch_forest_build(const mt_forest_record* all, uint64_t n_all, uint64_t* table, uint64_t* vtable,
+                         uint32_t mask, Cell* cells, int num_sms, cudaStream_t stream) {
+    if (n_all == 0) return;
+    forest_build_kernel<<<grid_for(n_all, num_sms), 256, 0, stream>>>(
+        all, n_all, reinterpret_cast<unsigned long long*>(table), reinterpret_cast<unsigned long long*>(vtable), mask,
+        cells);
+}
+
+void launch_forest_merge(const ForestRef& F, const Slab& sl, const SlabBounds& b, unsigned long long* fetch,
+                         int num_sms, cudaStream_t stream) {
+    if (b.count < 2) return;
+    BoundaryGeom g{};
+    g.nx = sl.nx;
+    g.ny = sl.ny;
+    g.nb = b.count - 1;
+    for (uint32_t k = 0; k + 1 < b.count; ++k) g.zb[k] = b.z[k + 1];
+    forest_merge_kernel<<<uint32_t(num_sms) * 4, 256, 0, stream>>>(F, g, fetch);
+}
+
+void launch_forest_writeback(const ForestRef& F, uint64_t n_all, Cell* C, const Slab& sl, int num_sms,
+                             cudaStream_t stream) {
+    if (n_all == 0) return;
+    forest_writeback_kernel<<<grid_for(n_all, num_sms), 256, 0, stream>>>(F, n_all, C, sl.base, sl.n);
+}
+
+}  // namespace mt

@@ -67,8 +67,8 @@ __device__ __forceinline__ uint64_t scas64(uint64_t* p, uint64_t cmp, uint64_t v
 
 template <int TY, int TZ, int MODE>
 __global__ void __launch_bounds__(THREADS)
-tile_tmt_kernel(const float* __restrict__ f, Cell* __restrict__ C, uint32_t nx, uint32_t ny, uint32_t nz,
-                uint32_t tiles_x, uint32_t tiles_y, uint32_t flip, unsigned long long* __restrict__ counters,
+tile_tmt_kernel(const float* __restrict__ f, Cell* __restrict__ C, uint32_t nx, uint32_t ny, uint32_t z_begin,
+                uint32_t z_end, uint32_t tiles_x, uint32_t tiles_y, uint32_t flip, unsigned long long* __restrict__ counters,
                 unsigned long long* __restrict__ stats) {
     constexpr int ROWS = TY * TZ;               // 128 rows of 32
     static_assert(TX * ROWS == NV, "tile size");
@@ -93,7 +93,9 @@ tile_tmt_kernel(const float* __restrict__ f, Cell* __restrict__ C, uint32_t nx, 
 
     const uint32_t b = blockIdx.x;
     const uint32_t bx = b % tiles_x, by = (b / tiles_x) % tiles_y, bz = b / (tiles_x * tiles_y);
-    const uint32_t x0 = bx * TX, y0 = by * TY, z0 = bz * TZ;
+    // f and C are indexed by GLOBAL vertex id (the caller passes pointers shifted by the
+    // slab's first id); this CTA's tile starts at global plane z0
+    const uint32_t x0 = bx * TX, y0 = by * TY, z0 = z_begin + bz * TZ;
     const uint64_t sxy = uint64_t(nx) * ny;
     const int lx = threadIdx.x & (TX - 1);
     const int r0 = threadIdx.x / TX;
@@ -107,7 +109,7 @@ tile_tmt_kernel(const float* __restrict__ f, Cell* __restrict__ C, uint32_t nx, 
         const int ly = r % TY, lz = r / TY;
         const uint32_t gx = x0 + lx, gy = y0 + ly, gz = z0 + lz;
         uint32_t o = ABSENT;
-        if (gx < nx && gy < ny && gz < nz) {
+        if (gx < nx && gy < ny && gz < z_end) {
             const float val = __ldg(f + (uint64_t(gz) * sxy + uint64_t(gy) * nx + gx));
             bad |= nonfinite(val);
             o = ord32(val) ^ flip;
@@ -448,8 +450,8 @@ tile_tmt_kernel(const float* __restrict__ f, Cell* __restrict__ C, uint32_t nx, 
 
 }  // namespace
 
-void tile_shape(uint32_t nz, uint32_t* ty, uint32_t* tz) {
-    if (nz == 1) {
+void tile_shape(uint32_t nz_global, uint32_t* ty, uint32_t* tz) {
+    if (nz_global == 1) {
         *ty = 128;
         *tz = 1;
     } else {
@@ -458,8 +460,8 @@ void tile_shape(uint32_t nz, uint32_t* ty, uint32_t* tz) {
     }
 }
 
-void launch_tile_tmt(const float* f, Cell* C, uint32_t nx, uint32_t ny, uint32_t nz, uint32_t flip,
-                     unsigned long long* counters, unsigned long long* stats, cudaStream_t stream) {
+void launch_tile_tmt(const float* f, Cell* C, const Slab& sl, uint32_t flip, unsigned long long* counters,
+                     unsigned long long* stats, cudaStream_t stream) {
     static int mode = -1;
     if (mode < 0) {
         const char* e = getenv("MT_TILE_MODE");  // diagnostics: 0 state machine, 1 per-thread loops
@@ -470,17 +472,23 @@ void launch_tile_tmt(const float* f, Cell* C, uint32_t nx, uint32_t ny, uint32_t
         cudaFuncSetAttribute(tile_tmt_kernel<16, 8, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES));
     }
     uint32_t ty, tz;
-    tile_shape(nz, &ty, &tz);
-    const uint32_t tx = (nx + TX - 1) / TX, tyn = (ny + ty - 1) / ty, tzn = (nz + tz - 1) / tz;
+    tile_shape(sl.nz, &ty, &tz);
+    const uint32_t nzl = sl.z_end - sl.z_begin;
+    const uint32_t tx = (sl.nx + TX - 1) / TX, tyn = (sl.ny + ty - 1) / ty, tzn = (nzl + tz - 1) / tz;
     const uint32_t grid = tx * tyn * tzn;
-    if (nz == 1 && mode == 0)
-        tile_tmt_kernel<128, 1, 0><<<grid, THREADS, SMEM_BYTES, stream>>>(f, C, nx, ny, nz, tx, tyn, flip, counters, stats);
-    else if (nz == 1)
-        tile_tmt_kernel<128, 1, 1><<<grid, THREADS, SMEM_BYTES, stream>>>(f, C, nx, ny, nz, tx, tyn, flip, counters, stats);
+    if (grid == 0) return;
+#define MT_TILE_LAUNCH(TY_, TZ_, M_)                                                                     \
+    tile_tmt_kernel<TY_, TZ_, M_><<<grid, THREADS, SMEM_BYTES, stream>>>(f, C, sl.nx, sl.ny, sl.z_begin, \
+                                                                         sl.z_end, tx, tyn, flip, counters, stats)
+    if (sl.nz == 1 && mode == 0)
+        MT_TILE_LAUNCH(128, 1, 0);
+    else if (sl.nz == 1)
+        MT_TILE_LAUNCH(128, 1, 1);
     else if (mode == 0)
-        tile_tmt_kernel<16, 8, 0><<<grid, THREADS, SMEM_BYTES, stream>>>(f, C, nx, ny, nz, tx, tyn, flip, counters, stats);
+        MT_TILE_LAUNCH(16, 8, 0);
     else
-        tile_tmt_kernel<16, 8, 1><<<grid, THREADS, SMEM_BYTES, stream>>>(f, C, nx, ny, nz, tx, tyn, flip, counters, stats);
+        MT_TILE_LAUNCH(16, 8, 1);
+#undef MT_TILE_LAUNCH
 }
 
 }  // namespace mt

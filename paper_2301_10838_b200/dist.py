@@ -1,0 +1,165 @@
+"""Multi-GPU z-slab decomposition: one process per GPU, NCCL for the exchange.
+
+Rank r owns planes [z_bounds[r], z_bounds[r+1]) of the global grid (3D, 6-connectivity).
+Per step (include/mt.h, "Multi-GPU"):
+  1. ``mt_compute_local``   -- the slab's merge tree + its boundary forest (device kernels);
+  2. all-gather of the forest records over the process group (``torch.distributed``: NCCL
+     over NVLink on GPUs; gloo in the CPU tests of the exchange logic);
+  3. ``mt_compute_global``  -- every rank merges all inter-slab edges on the gathered forest,
+     writes back its cells, repairs its slab and extracts its part of the diagram.
+The triplets hold global ids; the finite pairs of rank r are the branches born in its slab
+(ascending), so concatenating the ranks in order gives the single-GPU diagram.
+This module is plumbing (argument marshalling + the collective); all computation runs in
+libmt_b200.so.
+"""
+from __future__ import annotations
+
+import torch
+
+from . import _lib
+
+RECORD_BYTES = _lib.FOREST_RECORD_BYTES
+
+
+def slab_bounds(nz: int, nranks: int, align: int = 8) -> list[int]:
+    """z boundaries of ``nranks`` slabs covering ``nz`` planes: as equal as possible, on
+    multiples of the tile depth ``align`` when the grid allows it."""
+    if nranks < 1 or nranks > nz:
+        raise ValueError("need 1 <= nranks <= nz")
+    b = [0]
+    for k in range(1, nranks):
+        z = round(k * nz / nranks / align) * align if nz >= nranks * align else round(k * nz / nranks)
+        z = max(z, b[-1] + 1)
+        z = min(z, nz - (nranks - k))
+        b.append(z)
+    b.append(nz)
+    return b
+
+
+def allgather_varsize(t: torch.Tensor, group=None) -> torch.Tensor:
+    """All-gather 1-D uint8 tensors of different lengths; returns the concatenation in rank order."""
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    n = torch.tensor([t.numel()], dtype=torch.int64, device=t.device)
+    sizes = [torch.zeros_like(n) for _ in range(world)]
+    dist.all_gather(sizes, n, group=group)
+    sizes = [int(s.item()) for s in sizes]
+    m = max(sizes)
+    padded = torch.zeros(m, dtype=t.dtype, device=t.device)
+    padded[: t.numel()] = t
+    outs = [torch.empty(m, dtype=t.dtype, device=t.device) for _ in range(world)]
+    dist.all_gather(outs, padded, group=group)
+    return torch.cat([o[:s] for o, s in zip(outs, sizes)])
+
+
+class SlabMergeTree:
+    """Context for planes [z_begin, z_end) of an nx x ny x nz grid on one device."""
+
+    def __init__(self, dims, z_begin: int, z_end: int, device=None):
+        self.dims = tuple(int(d) for d in dims)
+        self.z_begin, self.z_end = int(z_begin), int(z_end)
+        nx, ny, _ = self.dims
+        self.n = nx * ny * (self.z_end - self.z_begin)
+        dev = torch.device("cuda", torch.cuda.current_device() if device is None else int(device)) \
+            if not isinstance(device, torch.device) else device
+        self.device = dev
+        nbytes = _lib.mt_slab_workspace_bytes(self.dims, 6, self.z_begin, self.z_end)
+        if nbytes == 0:
+            raise _lib.MTError(_lib.MT_ERR_INVALID_ARG, "mt_slab_workspace_bytes")
+        self.workspace = torch.empty(nbytes + 256, dtype=torch.uint8, device=dev)
+        ptr = (self.workspace.data_ptr() + 255) // 256 * 256
+        self.ctx = _lib.mt_create_slab(self.dims, 6, self.z_begin, self.z_end, dev.index, ptr, nbytes)
+        self._scratch = None
+        self._f = None
+
+    def __del__(self):
+        ctx = getattr(self, "ctx", None)
+        if ctx is not None and _lib._lib is not None:
+            _lib._lib.mt_destroy(ctx)
+            self.ctx = None
+
+    def compute_local(self, f_slab: torch.Tensor, split: bool = False, stream=None):
+        if f_slab.dtype != torch.float32 or not f_slab.is_cuda or f_slab.numel() != self.n:
+            raise ValueError("f_slab must be a float32 CUDA tensor with the slab's nx*ny*(z_end-z_begin) values")
+        self._f = f_slab  # borrowed by the library until compute_global's work completes
+        _lib.mt_compute_local(self.ctx, f_slab.data_ptr(), _lib.MT_FLAG_SPLIT_TREE if split else 0, stream)
+
+    def forest(self, stream=None) -> torch.Tensor:
+        """The slab's boundary-forest records as a uint8 CUDA tensor (a view into the workspace)."""
+        ptr, n = _lib.mt_forest_view(self.ctx, stream)
+        if n == 0:
+            return torch.empty(0, dtype=torch.uint8, device=self.device)
+        off = ptr - self.workspace.data_ptr()
+        return self.workspace[off: off + n * RECORD_BYTES]
+
+    def compute_global(self, all_records: torch.Tensor, z_bounds, triplets=None, stream=None) -> torch.Tensor:
+        n_all = all_records.numel() // RECORD_BYTES
+        need = _lib.mt_forest_scratch_bytes(n_all)
+        if self._scratch is None or self._scratch.numel() < need + 256:
+            self._scratch = torch.empty(need + 256, dtype=torch.uint8, device=self.device)
+        sp = (self._scratch.data_ptr() + 255) // 256 * 256
+        if triplets is None:
+            triplets = torch.empty(self.n, dtype=torch.int64, device=self.device)
+        _lib.mt_compute_global(self.ctx, all_records.data_ptr() if n_all else 0, n_all, z_bounds, sp, need,
+                               triplets.data_ptr(), stream)
+        return triplets
+
+    def diagram(self, stream=None):
+        """Synchronises; (records (k,4) int32, n_pairs, n_essential) of this slab."""
+        st, ptr, npairs, ness = _lib.mt_diagram_view(self.ctx, stream)
+        if st != _lib.MT_OK:
+            raise _lib.MTError(st, "mt_diagram")
+        k = npairs + ness
+        out = torch.empty((k, 4), dtype=torch.int32, device=self.device)
+        if k:
+            st, a, b = _lib.mt_diagram(self.ctx, out.data_ptr(), k, stream)
+            if st != _lib.MT_OK:
+                raise _lib.MTError(st, "mt_diagram")
+        return out, npairs, ness
+
+
+class DistMergeTree:
+    """The global grid split into z-slabs over a torch.distributed group, one slab per rank."""
+
+    def __init__(self, dims, group=None, device=None):
+        import torch.distributed as dist
+
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        self.dims = tuple(int(d) for d in dims)
+        self.z_bounds = slab_bounds(self.dims[2], self.world)
+        zb, ze = self.z_bounds[self.rank], self.z_bounds[self.rank + 1]
+        self.slab = SlabMergeTree(self.dims, zb, ze, device)
+        self.forest_records = 0
+
+    def compute(self, f_slab: torch.Tensor, split: bool = False, triplets=None) -> torch.Tensor:
+        self.slab.compute_local(f_slab, split)
+        mine = self.slab.forest()
+        everything = allgather_varsize(mine, self.group)
+        self.forest_records = everything.numel() // RECORD_BYTES
+        return self.slab.compute_global(everything, self.z_bounds, triplets)
+
+    def diagram(self):
+        return self.slab.diagram()
+
+
+def virtual_compute(f: torch.Tensor, dims, nranks: int, split: bool = False):
+    """All slabs on ONE device, the all-gather replaced by a concatenation: the device code of
+    the multi-GPU path exercised without several GPUs (tests).  Returns (T, diagram records,
+    n_pairs, n_essential) assembled in the single-GPU order."""
+    nx, ny, nz = dims
+    zb = slab_bounds(nz, nranks)
+    slabs = [SlabMergeTree(dims, zb[r], zb[r + 1], f.device) for r in range(nranks)]
+    plane = nx * ny
+    for r, s in enumerate(slabs):
+        s.compute_local(f[zb[r] * plane: zb[r + 1] * plane].contiguous(), split)
+    everything = torch.cat([s.forest() for s in slabs])
+    Ts = [s.compute_global(everything, zb) for s in slabs]
+    diags = [s.diagram() for s in slabs]
+    fin = torch.cat([d[0][: d[1]] for d in diags])
+    ess = torch.cat([d[0][d[1]:] for d in diags])
+    npairs = sum(d[1] for d in diags)
+    ness = sum(d[2] for d in diags)
+    return torch.cat(Ts), torch.cat([fin, ess]), npairs, ness, everything.numel() // RECORD_BYTES
