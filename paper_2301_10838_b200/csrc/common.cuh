@@ -145,10 +145,7 @@ enum StatSlot : int {
     ST_CYC_REPAIR = 15,
     ST_CYC_WRITE = 16,
     ST_CYC_LIST = 17,
-    ST_TILE_STEPS = 18,  // warp steps of the in-tile merge state machine
-    ST_TILE_ACTIVE = 19, // busy lanes summed over those steps
-    ST_TILE_MAXITER = 20,  // longest single in-tile merge (Alg. 3 iterations)
-    ST_TILE_LONG = 21,     // in-tile merges with more than 32 iterations
+    ST_TILE_PAIRS = 18,  // adjacent basin pairs (one merged edge each)
     ST_COUNT = 24
 };
 

@@ -104,30 +104,49 @@ repair_diagram_kernel(View view, Cell* C, uint64_t* __restrict__ T, const float*
     }
 
     // --- repair (Alg. 5 with Alg. 4's walk) ------------------------------
+    // The ITEMS walks of a thread advance together, one hop each per round,
+    // so up to ITEMS independent cell loads are in flight per thread.
     unsigned long long hops = 0;
+    uint32_t x[ITEMS];
+    uint32_t active = 0;
 #pragma unroll
     for (int k = 0; k < ITEMS; ++k) {
         const uint64_t l = first + uint64_t(k) * THREADS + threadIdx.x;
         const uint64_t u = base + l;
+        x[k] = cv_of(cell[k]);
         if (l >= n) continue;
-        const uint32_t s = cs_of(cell[k]), v = cv_of(cell[k]);
-        if (v == uint32_t(u)) {                       // root (u, u, u): essential class
+        if (x[k] == uint32_t(u)) {                    // root (u, u, u): essential class
             const uint32_t i = atomicAdd(reinterpret_cast<unsigned int*>(counters + CTR_ESS), 1u);
             if (i < ess_cap) ess[i] = mt_pair{uint32_t(u), uint32_t(u), __ldg(f + u), __int_as_float(0x7f800000)};
             else atomicOr(counters + CTR_ERR, ERR_ESS_CAPACITY);
             T[u] = pack(uint32_t(u), uint32_t(u));
             continue;
         }
-        const uint64_t a = cell[k].lo;                // key(s)
-        uint32_t x = v;
-        while (true) {
-            const Cell c = view.cell(C, x);
-            if (cv_of(c) == x || c.lo > a) break;     // root, or key(s_x) > a: x is Rep(u, a)
-            x = cv_of(c);
-            ++hops;
+        active |= 1u << k;
+    }
+    const uint32_t todo = active;
+    while (active) {
+        Cell c[ITEMS];
+#pragma unroll
+        for (int k = 0; k < ITEMS; ++k)
+            if (active & (1u << k)) c[k] = view.cell(C, x[k]);
+#pragma unroll
+        for (int k = 0; k < ITEMS; ++k) {
+            if (!(active & (1u << k))) continue;
+            if (cv_of(c[k]) == x[k] || c[k].lo > cell[k].lo) {   // root, or key(s_x) > key(s): Rep(u, key(s))
+                active &= ~(1u << k);
+            } else {
+                x[k] = cv_of(c[k]);
+                ++hops;
+            }
         }
-        if (x != v) st_cell_v(C + u, x);              // in-place shortcut for later walkers (derivation E)
-        T[u] = pack(s, x);
+    }
+#pragma unroll
+    for (int k = 0; k < ITEMS; ++k) {
+        if (!(todo & (1u << k))) continue;
+        const uint64_t u = base + first + uint64_t(k) * THREADS + threadIdx.x;
+        if (x[k] != cv_of(cell[k])) st_cell_v(C + u, x[k]);   // in-place shortcut (derivation E)
+        T[u] = pack(cs_of(cell[k]), x[k]);
     }
     if (stats) atomicAdd(stats + ST_REPAIR_HOPS, hops);
 

@@ -41,10 +41,19 @@ namespace mt {
 namespace {
 
 constexpr int TX = 32;
-constexpr int THREADS = 512;
-constexpr int NV = 4096;                       // vertices per tile
 constexpr uint32_t ABSENT = 0xffffffffu;       // order key of a tile slot outside the grid
-constexpr size_t SMEM_BYTES = NV * 8 + NV * 4 + NV * 3 * 2 + 16;
+constexpr uint64_t EMPTY = ~0ull;
+// tile of NV vertices, NV / 8 threads (8 vertices each), basin-pair table of 2 NV slots
+template <int NV>
+constexpr size_t smem_bytes() { return size_t(NV) * 8 + size_t(NV) * 4 + size_t(2 * NV) * 8; }
+
+template <int TABLE>
+__device__ __forceinline__ uint32_t pair_hash(uint32_t p) {
+    p ^= p >> 13;
+    p *= 0x5bd1e995u;
+    p ^= p >> 15;
+    return p & (TABLE - 1);
+}
 
 __device__ __forceinline__ uint32_t c_v(uint64_t c) { return uint32_t(c) & 0xffffu; }
 __device__ __forceinline__ uint32_t c_s(uint64_t c) { return (uint32_t(c) >> 16) & 0xffffu; }
@@ -54,6 +63,9 @@ __device__ __forceinline__ uint64_t c_make(uint32_t ord_s, uint32_t s, uint32_t 
 }
 __device__ __forceinline__ uint64_t key48(const uint32_t* ord, uint32_t x) {
     return (uint64_t(ord[x]) << 16) | x;
+}
+__device__ __forceinline__ bool lkey_lt(const uint32_t* ord, uint32_t a, uint32_t b) {
+    return key48(ord, a) < key48(ord, b);
 }
 __device__ __forceinline__ uint64_t sld64(const uint64_t* p) {
     return *reinterpret_cast<const volatile uint64_t*>(p);
@@ -65,7 +77,7 @@ __device__ __forceinline__ uint64_t scas64(uint64_t* p, uint64_t cmp, uint64_t v
     return atomicCAS(reinterpret_cast<unsigned long long*>(p), cmp, val);
 }
 
-template <int TY, int TZ, int MODE>
+template <int TY, int TZ, int NV = TX * TY * TZ, int THREADS = NV / 8, int TABLE = 2 * NV>
 __global__ void __launch_bounds__(THREADS)
 tile_tmt_kernel(const float* __restrict__ f, Cell* __restrict__ C, uint32_t nx, uint32_t ny, uint32_t z_begin,
                 uint32_t z_end, uint32_t tiles_x, uint32_t tiles_y, uint32_t flip, unsigned long long* __restrict__ counters,
@@ -77,10 +89,11 @@ tile_tmt_kernel(const float* __restrict__ f, Cell* __restrict__ C, uint32_t nx, 
     extern __shared__ __align__(16) unsigned char smem[];
     uint64_t* cell = reinterpret_cast<uint64_t*>(smem);
     uint32_t* ord = reinterpret_cast<uint32_t*>(smem + NV * 8);
-    uint16_t* elist = reinterpret_cast<uint16_t*>(smem + NV * 12);
-    uint32_t* s_ctl = reinterpret_cast<uint32_t*>(smem + NV * 12 + NV * 6);   // [0] list length, [1] fetch
+    uint64_t* table = reinterpret_cast<uint64_t*>(smem + NV * 12);
+    __shared__ int s_overflow;
+    __shared__ uint32_t s_fetch;
 
-    unsigned long long n_edges = 0, n_hops = 0, n_iters = 0, n_rep = 0, n_cmp = 0, n_steps = 0, n_active = 0;
+    unsigned long long n_edges = 0, n_pairs = 0, n_hops = 0, n_iters = 0, n_rep = 0, n_cmp = 0;
     long long t_mark = clock64();
     // per-phase SM cycles (stats mode): thread 0 accumulates the time between barriers
     auto phase_time = [&](int slot) {
@@ -116,7 +129,11 @@ tile_tmt_kernel(const float* __restrict__ f, Cell* __restrict__ C, uint32_t nx, 
         }
         ord[r * TX + lx] = o;
     }
-    if (threadIdx.x < 2) s_ctl[threadIdx.x] = 0;
+    for (int i = threadIdx.x; i < TABLE; i += THREADS) table[i] = EMPTY;
+    if (threadIdx.x == 0) {
+        s_overflow = 0;
+        s_fetch = 0;
+    }
     if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(counters + CTR_ERR, ERR_NONFINITE);
     phase_time(ST_CYC_LOAD);
 
@@ -175,225 +192,145 @@ tile_tmt_kernel(const float* __restrict__ f, Cell* __restrict__ C, uint32_t nx, 
     __syncthreads();
     phase_time(ST_CYC_COMPRESS);
 
-    // ---- c. list the in-tile edges between two basins ----------------------------------
+    // ---- c. one edge per pair of adjacent basins: the lowest --------------------------------
+    // Between two basins A and B only the lowest edge matters: any other A-B edge at level
+    // L' joins vertices that are already connected at L' through their descent paths and
+    // that lowest edge (DESIGN.md derivation C'').  A shared-memory hash table keyed by the
+    // basin pair keeps, per pair, the edge's upper endpoint of lowest key.
 #pragma unroll 1
     for (int k = 0; k < PER; ++k) {
         const int r = r0 + k * RSTEP;
         const int ly = r % TY, lz = r / TY;
         const uint32_t u = r * TX + lx;
-        uint32_t mine = 0;                     // up to 3 entries, bit-packed
-        int cnt = 0;
-        if (ord[u] != ABSENT) {
-            const uint64_t cu = cell[u];
-            const uint32_t bu = c_v(cu);       // basin (a minimum points at itself)
+        if (ord[u] == ABSENT) continue;
+        const uint32_t bu = c_v(cell[u]);      // basin (a minimum points at itself)
+        const bool ok[3] = {lx + 1 < TX, ly + 1 < TY, lz + 1 < TZ};
+        const uint32_t off[3] = {1u, uint32_t(TX), uint32_t(TX * TY)};
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+            if (!ok[d]) continue;
+            const uint32_t w = u + off[d];
+            if (ord[w] == ABSENT) continue;
+            const uint32_t bw = c_v(cell[w]);
+            if (bw == bu) continue;
+            ++n_edges;
+            const uint32_t hi = lkey_lt(ord, w, u) ? u : w;
+            const uint32_t pair = bu < bw ? (bu << 12) | bw : (bw << 12) | bu;
+            const uint64_t entry = (uint64_t(pair) << 12) | hi;
+            uint32_t h = pair_hash<TABLE>(pair);
+            for (uint32_t probe = 0;;) {
+                const uint64_t cur = sld64(table + h);
+                if (cur == EMPTY) {
+                    if (scas64(table + h, EMPTY, entry) == EMPTY) break;
+                    continue;                                        // lost the slot: re-read it
+                }
+                if (uint32_t(cur >> 12) != pair) {
+                    h = (h + 1) & (TABLE - 1);
+                    if (++probe < TABLE) continue;
+                    // table full (e.g. a checkerboard: every vertex pair of basins is adjacent):
+                    // record the edge in the overflow flag; phase d' merges all edges then
+                    s_overflow = 1;
+                    break;
+                }
+                if (!lkey_lt(ord, hi, uint32_t(cur) & 0xfffu)) break;  // the stored edge is lower
+                if (scas64(table + h, cur, entry) == cur) break;
+            }
+        }
+    }
+    __syncthreads();
+    phase_time(ST_CYC_LIST);
+
+    // ---- d. merge one edge per basin pair ------------------------------------------------
+    // join basins bh (the one holding the edge's upper endpoint) and bl at level L
+    auto merge_at = [&](uint32_t bh, uint32_t bl, uint64_t L) {
+        uint32_t rr[2];
+#pragma unroll
+        for (int side = 0; side < 2; ++side) {           // walks at level L with path splitting
+            uint32_t x = side == 0 ? bh : bl;
+            uint64_t c = sld64(cell + x);
+            uint32_t xp = x;
+            uint64_t cp = 0;
+            bool has_prev = false;
+            while (c_v(c) != x && c_key(c) <= L) {
+                if (has_prev && c_key(c) <= c_key(cp)) scas64(cell + xp, cp, (cp & ~0xffffull) | c_v(c));
+                xp = x;
+                cp = c;
+                has_prev = true;
+                x = c_v(c);
+                c = sld64(cell + x);
+                ++n_hops;
+            }
+            rr[side] = x;
+        }
+        if (rr[0] == rr[1]) return;
+        uint32_t mu = rr[0], mv = rr[1];
+        uint64_t S = L;
+        while (true) {                                    // Alg. 3
+            ++n_iters;
+            const uint64_t cu = sld64(cell + mu), cv = sld64(cell + mv);
+            if (c_v(cu) != mu && c_key(cu) < S) { mu = c_v(cu); continue; }   // l.2-4 + R4
+            if (c_v(cv) != mv && c_key(cv) < S) { mv = c_v(cv); continue; }   // l.5-8 + R4
+            if (mu == mv) break;                                                // l.9-10
+            uint32_t uu = mu, vv = mv;
+            uint64_t cvv = cv;
+            if (key48(ord, mv) < key48(ord, mu)) { uu = mv; vv = mu; cvv = cu; }  // l.11-12
+            if (scas64(cell + vv, cvv, (S << 16) | uu) == cvv) {               // l.14
+                if (c_v(cvv) == vv) break;                                      // R5
+                mu = uu;                                                        // l.15
+                S = c_key(cvv);
+                mv = c_v(cvv);
+            } else {
+                mu = uu;                                                        // l.17
+                mv = vv;
+            }
+        }
+    };
+    // basin of x: a regular cell (s = x) is static and points at the minimum
+    auto basin = [&](uint32_t x) {
+        const uint64_t c = sld64(cell + x);
+        return c_s(c) == x ? c_v(c) : x;
+    };
+    // dynamic hand-out: a thread takes 4 table slots at a time from a CTA counter and skips
+    // the empty ones, so every lane of a warp works on a real pair (most slots are empty)
+    uint32_t chunk = 0, chunk_end = 0;
+#pragma unroll 1
+    while (true) {
+        uint64_t e = EMPTY;
+        while (e == EMPTY) {
+            if (chunk == chunk_end) {
+                chunk = atomicAdd(&s_fetch, 4u);
+                chunk_end = chunk + 4;
+                if (chunk >= uint32_t(TABLE)) break;
+            }
+            e = table[chunk++];
+        }
+        if (e == EMPTY) break;
+        ++n_pairs;
+        const uint32_t pair = uint32_t(e >> 12), hi = uint32_t(e) & 0xfffu;
+        const uint32_t ba = pair >> 12, bb = pair & 0xfffu;
+        const uint32_t bh = basin(hi);
+        merge_at(bh, bh == ba ? bb : ba, key48(ord, hi));
+    }
+    if (s_overflow) {  // (uniform: written before the last barrier) the table dropped edges
+#pragma unroll 1
+        for (int k = 0; k < PER; ++k) {
+            const int r = r0 + k * RSTEP;
+            const int ly = r % TY, lz = r / TY;
+            const uint32_t u = r * TX + lx;
+            if (ord[u] == ABSENT) continue;
             const bool ok[3] = {lx + 1 < TX, ly + 1 < TY, lz + 1 < TZ};
             const uint32_t off[3] = {1u, uint32_t(TX), uint32_t(TX * TY)};
-#pragma unroll
+#pragma unroll 1
             for (int d = 0; d < 3; ++d) {
                 if (!ok[d]) continue;
                 const uint32_t w = u + off[d];
                 if (ord[w] == ABSENT) continue;
-                if (c_v(cell[w]) != bu) {
-                    mine |= uint32_t(d) << (2 * cnt);
-                    ++cnt;
-                }
+                const uint32_t bu = basin(u), bw = basin(w);
+                if (bu == bw) continue;
+                const bool u_hi = lkey_lt(ord, w, u);
+                merge_at(u_hi ? bu : bw, u_hi ? bw : bu, key48(ord, u_hi ? u : w));
             }
         }
-        // warp-aggregated append
-        uint32_t incl = cnt;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t t = __shfl_up_sync(FULL_MASK, incl, o);
-            if (lane >= o) incl += t;
-        }
-        const uint32_t tot = __shfl_sync(FULL_MASK, incl, 31);
-        uint32_t base = 0;
-        if (lane == 31 && tot) base = atomicAdd(s_ctl, tot);
-        base = __shfl_sync(FULL_MASK, base, 31) + incl - cnt;
-        for (int i = 0; i < cnt; ++i) elist[base + i] = uint16_t((u << 2) | ((mine >> (2 * i)) & 3u));
-    }
-    __syncthreads();
-    phase_time(ST_CYC_LIST);
-    const uint32_t nlist = s_ctl[0];
-
-    // ---- d. merge the listed edges -------------------------------------------------------
-    if (MODE == 1) {
-        // per-thread loops: thread t takes entries t, t + 512, ...
-#pragma unroll 1
-        for (uint32_t i = threadIdx.x; i < nlist; i += THREADS) {
-            const uint32_t e = elist[i];
-            const uint32_t u = e >> 2, d = e & 3u;
-            const uint32_t w = u + (d == 0 ? 1u : (d == 1 ? uint32_t(TX) : uint32_t(TX * TY)));
-            const uint64_t ku = key48(ord, u), kw = key48(ord, w);
-            const uint64_t cu0 = sld64(cell + u), cw0 = sld64(cell + w);
-            const uint32_t bu = c_s(cu0) == u ? c_v(cu0) : u;
-            const uint32_t bw = c_s(cw0) == w ? c_v(cw0) : w;
-            const uint64_t L = ku > kw ? ku : kw;
-            ++n_edges;
-            uint32_t rr[2];
-#pragma unroll
-            for (int side = 0; side < 2; ++side) {       // walks at level L with path splitting
-                uint32_t x = (side == 0) == (ku > kw) ? bu : bw;
-                uint64_t c = sld64(cell + x);
-                uint32_t xp = x;
-                uint64_t cp = 0;
-                bool has_prev = false;
-                while (c_v(c) != x && c_key(c) <= L) {
-                    if (has_prev && c_key(c) <= c_key(cp)) scas64(cell + xp, cp, (cp & ~0xffffull) | c_v(c));
-                    xp = x;
-                    cp = c;
-                    has_prev = true;
-                    x = c_v(c);
-                    c = sld64(cell + x);
-                    ++n_hops;
-                }
-                rr[side] = x;
-            }
-            if (rr[0] == rr[1]) continue;
-            uint32_t mu = rr[0], mv = rr[1];
-            uint64_t S = L;
-            uint32_t my_iters = 0;
-            while (true) {                                // Alg. 3
-                ++n_iters;
-                ++my_iters;
-                const uint64_t cu = sld64(cell + mu), cv = sld64(cell + mv);
-                if (c_v(cu) != mu && c_key(cu) < S) { mu = c_v(cu); continue; }   // l.2-4 + R4
-                if (c_v(cv) != mv && c_key(cv) < S) { mv = c_v(cv); continue; }   // l.5-8 + R4
-                if (mu == mv) break;                                                // l.9-10
-                uint32_t uu = mu, vv = mv;
-                uint64_t cvv = cv;
-                if (key48(ord, mv) < key48(ord, mu)) { uu = mv; vv = mu; cvv = cu; }  // l.11-12
-                if (scas64(cell + vv, cvv, (S << 16) | uu) == cvv) {               // l.14
-                    if (c_v(cvv) == vv) break;                                      // R5
-                    mu = uu;                                                        // l.15
-                    S = c_key(cvv);
-                    mv = c_v(cvv);
-                } else {
-                    mu = uu;                                                        // l.17
-                    mv = vv;
-                }
-            }
-            if (stats) {
-                atomicMax(stats + ST_TILE_MAXITER, (unsigned long long)my_iters);
-                if (my_iters > 32) atomicAdd(stats + ST_TILE_LONG, 1ull);
-            }
-        }
-    } else {
-    {
-        uint32_t pool_next = 0, pool_end = 0;  // warp-uniform
-        bool exhausted = false;
-        int phase = 0;                          // 0 idle, 1 climb hi, 2 climb lo, 3 merge load, 4 cas, 5 done
-        uint32_t x = 0, xp = 0, mlo = 0, rh = 0, mu = 0, mv = 0;
-        uint64_t c = 0, cp = 0, cu = 0, cv = 0, L = 0, S = 0, desired = 0, got = 0;
-        bool has_prev = false;
-        while (true) {
-            const uint32_t need = __ballot_sync(FULL_MASK, phase == 0);
-            if (need) {
-                if (pool_next == pool_end && !exhausted) {
-                    uint32_t b0 = 0;
-                    if (lane == 0) b0 = atomicAdd(s_ctl + 1, 64u);
-                    b0 = __shfl_sync(FULL_MASK, b0, 0);
-                    pool_next = b0 < nlist ? b0 : nlist;
-                    pool_end = b0 + 64 < nlist ? b0 + 64 : nlist;
-                    exhausted = pool_next == pool_end;
-                }
-                const uint32_t rank = __popc(need & ((1u << lane) - 1u));
-                const uint32_t avail = pool_end - pool_next;
-                if (phase == 0) {
-                    if (rank < avail) {
-                        const uint32_t e = elist[pool_next + rank];
-                        const uint32_t u = e >> 2, d = e & 3u;
-                        const uint32_t w = u + (d == 0 ? 1u : (d == 1 ? uint32_t(TX) : uint32_t(TX * TY)));
-                        const uint64_t ku = key48(ord, u), kw = key48(ord, w);
-                        // basins: a regular cell (s = self) is static and points at its
-                        // minimum; a minimum (possibly merged already) is its own basin
-                        const uint64_t cu0 = sld64(cell + u), cw0 = sld64(cell + w);
-                        const uint32_t bu = c_s(cu0) == u ? c_v(cu0) : u;
-                        const uint32_t bw = c_s(cw0) == w ? c_v(cw0) : w;
-                        L = ku > kw ? ku : kw;
-                        x = ku > kw ? bu : bw;
-                        mlo = ku > kw ? bw : bu;
-                        has_prev = false;
-                        phase = 1;
-                        ++n_edges;
-                    } else if (exhausted) {
-                        phase = 5;
-                    }
-                }
-                pool_next += avail < uint32_t(__popc(need)) ? avail : uint32_t(__popc(need));
-            }
-            const uint32_t live = __ballot_sync(FULL_MASK, phase != 5);
-            if (live == 0) break;
-            if (stats) {
-                const uint32_t busy = __ballot_sync(FULL_MASK, phase != 0);   // lanes with an edge this step
-                if (lane == 0) {
-                    ++n_steps;
-                    n_active += __popc(busy & live);
-                }
-            }
-            // one shared-memory round-trip
-            if (phase == 1 || phase == 2) {
-                c = sld64(cell + x);
-            } else if (phase == 3) {
-                cu = sld64(cell + mu);
-                cv = sld64(cell + mv);
-            } else if (phase == 4) {
-                got = scas64(cell + mv, cv, desired);
-            }
-            // advance
-            if (phase == 1 || phase == 2) {
-                if (c_v(c) != x && c_key(c) <= L) {                         // followable at level L
-                    if (has_prev && c_key(c) <= c_key(cp))                   // path splitting
-                        scas64(cell + xp, cp, (cp & ~0xffffull) | c_v(c));
-                    xp = x;
-                    cp = c;
-                    has_prev = true;
-                    x = c_v(c);
-                    ++n_hops;
-                } else if (phase == 1) {
-                    rh = x;
-                    x = mlo;
-                    has_prev = false;
-                    phase = 2;
-                } else if (x == rh) {
-                    phase = 0;                                               // already joined
-                } else {
-                    mu = rh;                                                 // Merge(T, rh, hi, x)
-                    mv = x;
-                    S = L;
-                    phase = 3;
-                }
-            } else if (phase == 3) {
-                ++n_iters;
-                if (c_v(cu) != mu && c_key(cu) < S) {                        // l.2-4 + R4
-                    mu = c_v(cu);
-                } else if (c_v(cv) != mv && c_key(cv) < S) {                 // l.5-8 + R4
-                    mv = c_v(cv);
-                } else if (mu == mv) {                                       // l.9-10
-                    phase = 0;
-                } else {
-                    if (key48(ord, mv) < key48(ord, mu)) {                   // l.11-12
-                        const uint32_t t = mu; mu = mv; mv = t;
-                        const uint64_t tc = cu; cu = cv; cv = tc;
-                    }
-                    desired = (S << 16) | mu;                                // l.14: (s, u) into T[v]
-                    phase = 4;
-                }
-            } else if (phase == 4) {
-                if (got == cv) {
-                    if (c_v(cv) == mv) {
-                        phase = 0;                                           // displaced a root (R5)
-                    } else {
-                        S = c_key(cv);                                       // l.15
-                        mv = c_v(cv);
-                        phase = 3;
-                    }
-                } else {
-                    phase = 3;                                               // l.17
-                }
-            }
-        }
-    }
     }
     __syncthreads();
     phase_time(ST_CYC_MERGE);
@@ -443,52 +380,63 @@ tile_tmt_kernel(const float* __restrict__ f, Cell* __restrict__ C, uint32_t nx, 
         atomicAdd(stats + ST_TILE_ITERS, n_iters);
         atomicAdd(stats + ST_TILE_REPAIR, n_rep);
         atomicAdd(stats + ST_TILE_COMPRESS, n_cmp);
-        atomicAdd(stats + ST_TILE_STEPS, n_steps);
-        atomicAdd(stats + ST_TILE_ACTIVE, n_active);
+        atomicAdd(stats + ST_TILE_PAIRS, n_pairs);
     }
 }
 
 }  // namespace
 
+int tile_vertices() {
+    static int nv = 0;
+    if (!nv) {
+        const char* e = getenv("MT_TILE_NV");  // 4096 (default) or 2048; tile_shape follows it
+        nv = (e && atoi(e) == 2048) ? 2048 : 4096;
+    }
+    return nv;
+}
+
 void tile_shape(uint32_t nz_global, uint32_t* ty, uint32_t* tz) {
+    const int nv = tile_vertices();
     if (nz_global == 1) {
-        *ty = 128;
+        *ty = uint32_t(nv / TX);
         *tz = 1;
     } else {
-        *ty = 16;
+        *ty = nv == 4096 ? 16 : 8;
         *tz = 8;
     }
 }
 
+template <int TY, int TZ>
+void launch_tile(const float* f, Cell* C, const Slab& sl, uint32_t tx, uint32_t tyn, uint32_t grid, uint32_t flip,
+                 unsigned long long* counters, unsigned long long* stats, cudaStream_t stream) {
+    constexpr int NV = TX * TY * TZ;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(tile_tmt_kernel<TY, TZ>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             int(smem_bytes<NV>()));
+        attr = true;
+    }
+    tile_tmt_kernel<TY, TZ><<<grid, NV / 8, smem_bytes<NV>(), stream>>>(f, C, sl.nx, sl.ny, sl.z_begin, sl.z_end, tx,
+                                                                       tyn, flip, counters, stats);
+}
+
 void launch_tile_tmt(const float* f, Cell* C, const Slab& sl, uint32_t flip, unsigned long long* counters,
                      unsigned long long* stats, cudaStream_t stream) {
-    static int mode = -1;
-    if (mode < 0) {
-        const char* e = getenv("MT_TILE_MODE");  // diagnostics: 0 state machine, 1 per-thread loops
-        mode = e ? atoi(e) : 1;
-        cudaFuncSetAttribute(tile_tmt_kernel<128, 1, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES));
-        cudaFuncSetAttribute(tile_tmt_kernel<16, 8, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES));
-        cudaFuncSetAttribute(tile_tmt_kernel<128, 1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES));
-        cudaFuncSetAttribute(tile_tmt_kernel<16, 8, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES));
-    }
     uint32_t ty, tz;
     tile_shape(sl.nz, &ty, &tz);
     const uint32_t nzl = sl.z_end - sl.z_begin;
     const uint32_t tx = (sl.nx + TX - 1) / TX, tyn = (sl.ny + ty - 1) / ty, tzn = (nzl + tz - 1) / tz;
     const uint32_t grid = tx * tyn * tzn;
     if (grid == 0) return;
-#define MT_TILE_LAUNCH(TY_, TZ_, M_)                                                                     \
-    tile_tmt_kernel<TY_, TZ_, M_><<<grid, THREADS, SMEM_BYTES, stream>>>(f, C, sl.nx, sl.ny, sl.z_begin, \
-                                                                         sl.z_end, tx, tyn, flip, counters, stats)
-    if (sl.nz == 1 && mode == 0)
-        MT_TILE_LAUNCH(128, 1, 0);
+    const bool big = tile_vertices() == 4096;
+    if (sl.nz == 1 && big)
+        launch_tile<128, 1>(f, C, sl, tx, tyn, grid, flip, counters, stats, stream);
     else if (sl.nz == 1)
-        MT_TILE_LAUNCH(128, 1, 1);
-    else if (mode == 0)
-        MT_TILE_LAUNCH(16, 8, 0);
+        launch_tile<64, 1>(f, C, sl, tx, tyn, grid, flip, counters, stats, stream);
+    else if (big)
+        launch_tile<16, 8>(f, C, sl, tx, tyn, grid, flip, counters, stats, stream);
     else
-        MT_TILE_LAUNCH(16, 8, 1);
-#undef MT_TILE_LAUNCH
+        launch_tile<8, 8>(f, C, sl, tx, tyn, grid, flip, counters, stats, stream);
 }
 
 }  // namespace mt

@@ -29,8 +29,7 @@ for cfg in cfgs:
     _lib.mt_diagram(mt.ctx)
     stats = _lib.mt_stats(mt.ctx)
     _lib.mt_set_stats(mt.ctx, False)
-    per = {k: (v / n if not k.startswith("tile_maxiter") and not k.startswith("tile_long") else v)
-           for k, v in stats.items()}
+    per = {k: v / n for k, v in stats.items()}
     print(json.dumps({"cfg": cfg, "n": n, "pairs": npairs, "times_ms": times, "stats": stats,
                       "per_vertex": per}), flush=True)
     del mt, fd, T
