@@ -120,7 +120,8 @@ enum CounterSlot : int {
     CTR_ESS = 2,        // number of essential classes found
     CTR_FIN = 3,        // number of finite pairs (written by the last tile)
     CTR_FFETCH = 4,     // next inter-slab edge to hand out (forest_merge)
-    CTR_QFETCH = 6,     // next crossing edge to hand out (merge_cross)
+    CTR_QLEN = 5,       // crossing-edge queue length (dedupe_cross)
+    CTR_QFETCH = 6,     // next queue entry to hand out (merge_queue)
     CTR_FCOUNT = 7,     // boundary-forest records of this slab
     CTR_COUNT = 8
 };
@@ -146,6 +147,7 @@ enum StatSlot : int {
     ST_CYC_WRITE = 16,
     ST_CYC_LIST = 17,
     ST_TILE_PAIRS = 18,  // adjacent basin pairs (one merged edge each)
+    ST_QUEUED = 19,      // tile-crossing edges left after the warp-level basin-pair dedupe
     ST_COUNT = 24
 };
 

@@ -70,12 +70,15 @@ __device__ __forceinline__ bool forest_value(const ForestRef& F, uint32_t id, ui
 void tile_shape(uint32_t nz_global, uint32_t* ty, uint32_t* tz);
 
 // K1 + K2 + in-tile K3/K4: keys, steepest descent, tile-local merge tree (tile_tmt.cu)
-void launch_tile_tmt(const float* f, Cell* C, const Slab& sl, uint32_t flip, unsigned long long* counters,
-                     unsigned long long* stats, cudaStream_t stream);
+void launch_tile_tmt(const float* f, Cell* C, uint32_t* basin, const Slab& sl, uint32_t flip,
+                     unsigned long long* counters, unsigned long long* stats, cudaStream_t stream);
 
 // K3: merge of the tile-crossing grid edges on the global store (merge_cross.cu)
-void launch_merge_cross(Cell* C, const Slab& sl, unsigned long long* fetch, unsigned long long* stats, int num_sms,
-                        cudaStream_t stream);
+uint64_t cross_edges(const Slab& sl);
+size_t cross_queue_entry_bytes();
+void launch_merge_cross(Cell* C, const float* f, const uint32_t* basin, const Slab& sl, uint32_t flip, void* queue,
+                        uint64_t cap, unsigned long long* qlen, unsigned long long* fetch, unsigned long long* stats,
+                        int num_sms, cudaStream_t stream);
 
 // K4+K5: repair fused with the ordered diagram compaction (repair_diagram.cu)
 uint64_t repair_tiles(uint64_t n);

@@ -1,11 +1,21 @@
-// merge_cross.cu -- K3 on the global store: merge every grid edge that
-// crosses a tile face (the in-tile edges were merged by tile_tmt.cu) with
-// Alg. 3 "Parallel Merge" over 128-bit CAS cells.
+// merge_cross.cu -- K3 on the global store: merge the grid edges that cross a
+// tile face (the in-tile edges were merged by tile_tmt.cu) with Alg. 3
+// "Parallel Merge" over 128-bit CAS cells.  Two kernels:
 //
-// Work: the crossing edges are enumerated directly (no queue): e in
-// [0, Ex + Ey + Ez) decodes to an x-, y- or z-face edge; consecutive e are
-// neighbours on one face.  Persistent warps take batches of 256 edge ids per
-// global atomic.
+// dedupe_cross: the crossing edges are enumerated directly (e in
+// [0, Ex + Ey + Ez) decodes to an x-, y- or z-face edge; 32 consecutive e are
+// neighbours on one face, one per lane).  Each edge is reduced to the pair of
+// descent basins of its ends (tile_tmt's basin array) and its level L =
+// max(key(a), key(b)); lanes holding the same basin pair (__match_any_sync)
+// keep only the lowest edge (derivation C'': between two basins only the
+// lowest edge matters), and the survivors are queued as (L, basin_hi, basin_lo).
+//
+// merge_queue: persistent warps take batches of 256 queue entries per global
+// atomic; each lane runs its entry as a state machine advanced by ONE memory
+// round-trip per step (a cell load, a pair of independent cell loads, or a
+// CAS), and idle lanes are refilled at every step, so a warp stays converged
+// and keeps up to 32 independent loads in flight (a per-thread nested-loop
+// version left 2.5 active lanes per instruction, ncu profiles/r1_c4_ncu_v1.md).
 //
 // Each lane runs its edge as a state machine advanced by ONE memory
 // round-trip per step (a cell load, a pair of independent cell loads, or a
@@ -13,7 +23,7 @@
 // and keeps up to 32 independent loads in flight (a per-thread nested-loop
 // version left 2.5 active lanes per instruction, ncu profiles/r1_c4_ncu_v1.md).
 //
-// Per edge (a, b): L = max(key(a), key(b)) (Alg. 1 l.5-8); both ends are
+// Per entry: both basins (joined to the edge's ends below their own keys) are
 // walked through cells with key(s) <= L (Alg. 4's walk at level L, with path
 // splitting by 128-bit CAS, derivation E'); if the walks meet, the edge joins
 // nothing new (derivation C'); otherwise Merge(T, r_hi, hi, r_lo) runs: climbs
@@ -58,23 +68,82 @@ __device__ __forceinline__ void decode_edge(const CrossGeom& g, uint64_t e, uint
     *b = uint32_t(g.base + u + step);
 }
 
-enum Phase : int { IDLE = 0, LOAD_AB = 1, CLIMB_HI = 2, CLIMB_LO = 3, MERGE_LD = 4, MERGE_CAS = 5, DONE = 6 };
+struct QEntry {
+    uint64_t L;      // key of the edge's upper endpoint (the merge level)
+    uint32_t m_hi;   // descent basin of the upper endpoint
+    uint32_t m_lo;   // descent basin of the lower endpoint
+};
+
+__global__ void __launch_bounds__(256)
+dedupe_cross_kernel(const float* __restrict__ f, const uint32_t* __restrict__ basin, CrossGeom g, uint32_t flip,
+                    QEntry* __restrict__ q, uint64_t cap, unsigned long long* __restrict__ qlen,
+                    unsigned long long* __restrict__ stats) {
+    __shared__ uint32_t s_warp[8];
+    __shared__ unsigned long long s_base;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint64_t total = g.ex + g.ey + g.ez;
+    const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+    unsigned long long n_edges = 0;
+    for (uint64_t e0 = uint64_t(blockIdx.x) * blockDim.x; e0 < total; e0 += stride) {
+        const uint64_t e = e0 + threadIdx.x;
+        const bool valid = e < total;
+        QEntry en{0, 0, 0};
+        uint64_t pair = ~0ull;
+        if (valid) {
+            uint32_t a, b;
+            decode_edge(g, e, &a, &b);
+            const uint64_t ka = key_of(ord32(__ldg(f + a)) ^ flip, a), kb = key_of(ord32(__ldg(f + b)) ^ flip, b);
+            const uint32_t ba = __ldg(basin + a), bb = __ldg(basin + b);
+            en = ka > kb ? QEntry{ka, ba, bb} : QEntry{kb, bb, ba};
+            pair = ba < bb ? (uint64_t(ba) << 32 | bb) : (uint64_t(bb) << 32 | ba);
+            ++n_edges;
+        }
+        // lanes with the same basin pair keep the lowest edge only
+        const uint32_t group = __match_any_sync(FULL_MASK, pair);
+        bool keep = valid;
+#pragma unroll 4
+        for (int j = 0; j < 32; ++j) {
+            const uint64_t Lj = __shfl_sync(FULL_MASK, en.L, j);
+            if (((group >> j) & 1u) && Lj < en.L) keep = false;
+        }
+        const uint32_t km = __ballot_sync(FULL_MASK, keep);
+        if (lane == 0) s_warp[warp] = __popc(km);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            uint32_t tot = 0;
+            for (int w = 0; w < 8; ++w) {
+                const uint32_t t = s_warp[w];
+                s_warp[w] = tot;
+                tot += t;
+            }
+            s_base = tot ? atomicAdd(qlen, (unsigned long long)tot) : 0;
+        }
+        __syncthreads();
+        const uint64_t pos = s_base + s_warp[warp] + __popc(km & ((1u << lane) - 1u));
+        if (keep && pos < cap) q[pos] = en;
+        __syncthreads();  // s_warp / s_base are rewritten next iteration
+    }
+    if (stats) atomicAdd(stats + ST_EDGES, n_edges);
+}
+
+enum Phase : int { IDLE = 0, CLIMB_HI = 2, CLIMB_LO = 3, MERGE_LD = 4, MERGE_CAS = 5, DONE = 6 };
 
 template <bool STATS>
 __global__ void __launch_bounds__(256)
-merge_cross_kernel(Cell* C, CrossGeom g, unsigned long long* __restrict__ fetch,
-                   unsigned long long* __restrict__ stats) {
+merge_queue_kernel(Cell* C, const QEntry* __restrict__ q, uint64_t cap, const unsigned long long* __restrict__ qlen,
+                   unsigned long long* __restrict__ fetch, unsigned long long* __restrict__ stats) {
     constexpr uint64_t BATCH = 256;
     const int lane = threadIdx.x & 31;
-    const uint64_t total = g.ex + g.ey + g.ez;
+    const uint64_t qn = *reinterpret_cast<const volatile unsigned long long*>(qlen);
+    const uint64_t total = qn < cap ? qn : cap;
     uint64_t pool_next = 0, pool_end = 0;  // warp-uniform
     bool exhausted = false;                // warp-uniform
 
     int phase = IDLE;
     uint64_t L = 0, ks = 0;
     uint32_t x = 0, xp = 0, lo = 0, rh = 0, u = 0, v = 0;
-    bool has_prev = false, have_c = false;
-    Cell c{0, 0}, cp{0, 0}, clo{0, 0}, cu{0, 0}, cv{0, 0}, desired{0, 0}, got{0, 0};
+    bool has_prev = false;
+    Cell c{0, 0}, cp{0, 0}, cu{0, 0}, cv{0, 0}, desired{0, 0}, got{0, 0};
     unsigned long long n_edges = 0, n_hops = 0, n_iters = 0, n_fail = 0, n_skip = 0;
 
     while (true) {
@@ -92,8 +161,12 @@ merge_cross_kernel(Cell* C, CrossGeom g, unsigned long long* __restrict__ fetch,
             const uint64_t avail = pool_end - pool_next;
             if (phase == IDLE) {
                 if (rank < avail) {
-                    decode_edge(g, pool_next + rank, &u, &v);   // u, v hold the edge ends a, b
-                    phase = LOAD_AB;
+                    const QEntry en = q[pool_next + rank];
+                    L = en.L;
+                    x = en.m_hi;                      // walk the upper end's basin first
+                    lo = en.m_lo;
+                    has_prev = false;
+                    phase = CLIMB_HI;
                     if (STATS) n_edges++;
                 } else if (exhausted) {
                     phase = DONE;
@@ -104,27 +177,16 @@ merge_cross_kernel(Cell* C, CrossGeom g, unsigned long long* __restrict__ fetch,
         if (__ballot_sync(FULL_MASK, phase != DONE) == 0) break;
 
         // ---- one memory round-trip ----
-        if (phase == LOAD_AB || phase == MERGE_LD) {
+        if (phase == MERGE_LD) {
             cu = ld_cell(C + u);
             cv = ld_cell(C + v);
-        } else if ((phase == CLIMB_HI || phase == CLIMB_LO) && !have_c) {
+        } else if (phase == CLIMB_HI || phase == CLIMB_LO) {
             c = ld_cell(C + x);
         } else if (phase == MERGE_CAS) {
             got = cas_cell(C + v, cv, desired);
         }
-        have_c = false;
 
         // ---- advance ----
-        if (phase == LOAD_AB) {
-            const uint64_t ka = self_key(cu, u), kb = self_key(cv, v);
-            L = ka > kb ? ka : kb;
-            x = ka > kb ? u : v;                     // walk the upper end first
-            c = ka > kb ? cu : cv;
-            lo = ka > kb ? v : u;
-            clo = ka > kb ? cv : cu;
-            has_prev = false;
-            phase = CLIMB_HI;
-        }
         if (phase == CLIMB_HI || phase == CLIMB_LO) {
             if (cv_of(c) != x && c.lo <= L) {          // followable at level L
                 if (STATS) n_hops++;
@@ -137,8 +199,6 @@ merge_cross_kernel(Cell* C, CrossGeom g, unsigned long long* __restrict__ fetch,
             } else if (phase == CLIMB_HI) {
                 rh = x;
                 x = lo;
-                c = clo;                               // already loaded
-                have_c = true;
                 has_prev = false;
                 phase = CLIMB_LO;
             } else if (x == rh) {                      // walks met: nothing to join
@@ -183,7 +243,7 @@ merge_cross_kernel(Cell* C, CrossGeom g, unsigned long long* __restrict__ fetch,
         }
     }
     if (STATS) {
-        atomicAdd(stats + ST_EDGES, n_edges);
+        atomicAdd(stats + ST_QUEUED, n_edges);
         atomicAdd(stats + ST_PRE_HOPS, n_hops);
         atomicAdd(stats + ST_MERGE_ITERS, n_iters);
         atomicAdd(stats + ST_CAS_FAIL, n_fail);
@@ -193,8 +253,9 @@ merge_cross_kernel(Cell* C, CrossGeom g, unsigned long long* __restrict__ fetch,
 
 }  // namespace
 
-void launch_merge_cross(Cell* C, const Slab& sl, unsigned long long* fetch, unsigned long long* stats, int num_sms,
-                        cudaStream_t stream) {
+void launch_merge_cross(Cell* C, const float* f, const uint32_t* basin, const Slab& sl, uint32_t flip, void* queue,
+                        uint64_t cap, unsigned long long* qlen, unsigned long long* fetch, unsigned long long* stats,
+                        int num_sms, cudaStream_t stream) {
     CrossGeom g{};
     g.nx = sl.nx;
     g.ny = sl.ny;
@@ -207,21 +268,37 @@ void launch_merge_cross(Cell* C, const Slab& sl, unsigned long long* fetch, unsi
     g.ex = g.nz ? kx * g.ny * g.nz : 0;
     g.ey = g.nz ? ky * g.nx * g.nz : 0;
     g.ez = kz * uint64_t(g.nx) * g.ny;
-    if (g.ex + g.ey + g.ez == 0) return;
+    const uint64_t total = cross_edges(sl);
+    if (total == 0) return;
+    QEntry* q = static_cast<QEntry*>(queue);
+    uint64_t blocks = (total + 255) / 256;
+    if (blocks > uint64_t(num_sms) * 32) blocks = uint64_t(num_sms) * 32;
+    dedupe_cross_kernel<<<uint32_t(blocks), 256, 0, stream>>>(f, basin, g, flip, q, cap, qlen, stats);
     static int per_sm[2] = {0, 0};  // persistent grid: as many CTAs as fit on every SM
     const int t = stats ? 1 : 0;
     if (!per_sm[t]) {
         if (stats)
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[t], merge_cross_kernel<true>, 256, 0);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[t], merge_queue_kernel<true>, 256, 0);
         else
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[t], merge_cross_kernel<false>, 256, 0);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[t], merge_queue_kernel<false>, 256, 0);
         if (per_sm[t] < 1) per_sm[t] = 1;
     }
-    const uint32_t blocks = uint32_t(num_sms) * per_sm[t];
+    const uint32_t pblocks = uint32_t(num_sms) * per_sm[t];
     if (stats)
-        merge_cross_kernel<true><<<blocks, 256, 0, stream>>>(C, g, fetch, stats);
+        merge_queue_kernel<true><<<pblocks, 256, 0, stream>>>(C, q, cap, qlen, fetch, stats);
     else
-        merge_cross_kernel<false><<<blocks, 256, 0, stream>>>(C, g, fetch, stats);
+        merge_queue_kernel<false><<<pblocks, 256, 0, stream>>>(C, q, cap, qlen, fetch, stats);
 }
+
+uint64_t cross_edges(const Slab& sl) {
+    uint32_t ty, tz;
+    tile_shape(sl.nz, &ty, &tz);
+    const uint64_t nzl = sl.z_end - sl.z_begin;
+    if (!nzl || !sl.nx || !sl.ny) return 0;
+    const uint64_t kx = (sl.nx + 31) / 32 - 1, ky = (sl.ny + ty - 1) / ty - 1, kz = (nzl + tz - 1) / tz - 1;
+    return kx * sl.ny * nzl + ky * uint64_t(sl.nx) * nzl + kz * uint64_t(sl.nx) * sl.ny;
+}
+
+size_t cross_queue_entry_bytes() { return sizeof(QEntry); }
 
 }  // namespace mt

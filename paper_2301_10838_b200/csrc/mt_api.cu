@@ -23,8 +23,8 @@ constexpr int MAX_EVENTS = 12;
 size_t align_up(size_t x) { return (x + ALIGN - 1) / ALIGN * ALIGN; }
 
 struct Layout {
-    size_t counters, status, stats, ess, cells, pairs, flags, recs, total;
-    uint64_t ntiles, pairs_cap, recs_cap;
+    size_t counters, status, stats, ess, cells, basin, queue, pairs, flags, recs, total;
+    uint64_t ntiles, pairs_cap, recs_cap, queue_cap;
 };
 
 bool valid_dims(const uint32_t dims[3], int conn) {
@@ -34,7 +34,7 @@ bool valid_dims(const uint32_t dims[3], int conn) {
     return true;
 }
 
-Layout layout_for(uint64_t n, bool slab = false) {
+Layout layout_for(uint64_t n, uint64_t ncross, bool slab = false) {
     Layout L{};
     L.ntiles = n ? mt::repair_tiles(n) : 0;
     // finite pairs <= #minima - 1 and strict minima form an independent set of
@@ -51,6 +51,11 @@ Layout layout_for(uint64_t n, bool slab = false) {
     off += align_up(ESS_CAP * sizeof(mt_pair));
     L.cells = off;  // 16-byte working cells of the merge phase
     off += align_up(n * sizeof(mt::Cell));
+    L.basin = off;  // descent basin of every vertex (tile_tmt -> dedupe_cross)
+    off += align_up(n * sizeof(uint32_t));
+    L.queue = off;  // deduplicated tile-crossing edges
+    L.queue_cap = ncross;
+    off += align_up(ncross * mt::cross_queue_entry_bytes());
     L.pairs = off;
     off += align_up(L.pairs_cap * sizeof(mt_pair));
     if (slab) {  // boundary forest of the slab: a flag per vertex, at most n records
@@ -162,7 +167,9 @@ mt_status create_ctx(mt_ctx** out, const uint32_t dims[3], int conn, uint32_t z_
     if (!valid_dims(dims, conn)) return MT_ERR_INVALID_ARG;
     if (uint64_t(dims[0]) * dims[1] * dims[2] > 0xffffffffull) return MT_ERR_TOO_LARGE;
     const uint64_t n = uint64_t(dims[0]) * dims[1] * (z_end - z_begin);
-    const Layout L = layout_for(n, multi);
+    const Layout L = layout_for(
+        n, mt::cross_edges(mt::Slab{dims[0], dims[1], dims[2], z_begin, z_end, uint64_t(dims[0]) * dims[1] * z_begin, n}),
+        multi);
     if (!workspace || workspace_bytes < L.total || (reinterpret_cast<uintptr_t>(workspace) % ALIGN))
         return MT_ERR_WORKSPACE;
     int ndev = 0;
@@ -215,11 +222,13 @@ mt_status start_compute(mt_ctx* c, const float* f, uint32_t flags, cudaStream_t 
     if (cudaMemsetAsync(c->ws + c->L.counters, 0, c->L.status - c->L.counters + c->L.ntiles * sizeof(uint64_t),
                         s) != cudaSuccess)
         return c->sticky = MT_ERR_CUDA;
+    uint32_t* basin = reinterpret_cast<uint32_t*>(c->ws + c->L.basin) - c->slab.base;
     mark(c, "tile_tmt", s);
-    mt::launch_tile_tmt(fs, cells, c->slab, c->flip, ctr, stats, s);
+    mt::launch_tile_tmt(fs, cells, basin, c->slab, c->flip, ctr, stats, s);
     mark(c, "merge_cross", s);
-    mt::launch_merge_cross(cells, c->slab, ctr + mt::CTR_QFETCH, stats, c->num_sms, s);
-    c->launches = 2;
+    mt::launch_merge_cross(cells, fs, basin, c->slab, c->flip, c->ws + c->L.queue, c->L.queue_cap, ctr + mt::CTR_QLEN,
+                           ctr + mt::CTR_QFETCH, stats, c->num_sms, s);
+    c->launches = 3;
     return MT_OK;
 }
 
@@ -267,7 +276,7 @@ size_t mt_workspace_bytes(const uint32_t dims[3], int conn) {
     if (!valid_dims(dims, conn)) return 0;
     const uint64_t n = uint64_t(dims[0]) * dims[1] * dims[2];
     if (n > 0xffffffffull) return 0;
-    return layout_for(n).total;
+    return layout_for(n, mt::cross_edges(mt::Slab{dims[0], dims[1], dims[2], 0, dims[2], 0, n})).total;
 }
 
 mt_status mt_create(mt_ctx** out, const uint32_t dims[3], int conn, int cuda_device, void* workspace,
@@ -279,7 +288,8 @@ mt_status mt_create(mt_ctx** out, const uint32_t dims[3], int conn, int cuda_dev
 size_t mt_slab_workspace_bytes(const uint32_t dims[3], int conn, uint32_t z_begin, uint32_t z_end) {
     if (!valid_dims(dims, conn) || dims[2] < 2 || z_begin >= z_end || z_end > dims[2]) return 0;
     if (uint64_t(dims[0]) * dims[1] * dims[2] > 0xffffffffull) return 0;
-    return layout_for(uint64_t(dims[0]) * dims[1] * (z_end - z_begin), true).total;
+    const uint64_t n = uint64_t(dims[0]) * dims[1] * (z_end - z_begin);
+    return layout_for(n, mt::cross_edges(mt::Slab{dims[0], dims[1], dims[2], z_begin, z_end, 0, n}), true).total;
 }
 
 mt_status mt_create_slab(mt_ctx** out, const uint32_t dims[3], int conn, uint32_t z_begin, uint32_t z_end,

@@ -79,7 +79,8 @@ __device__ __forceinline__ uint64_t scas64(uint64_t* p, uint64_t cmp, uint64_t v
 
 template <int TY, int TZ, int NV = TX * TY * TZ, int THREADS = NV / 8, int TABLE = 2 * NV>
 __global__ void __launch_bounds__(THREADS)
-tile_tmt_kernel(const float* __restrict__ f, Cell* __restrict__ C, uint32_t nx, uint32_t ny, uint32_t z_begin,
+tile_tmt_kernel(const float* __restrict__ f, Cell* __restrict__ C, uint32_t* __restrict__ basin_out, uint32_t nx,
+                uint32_t ny, uint32_t z_begin,
                 uint32_t z_end, uint32_t tiles_x, uint32_t tiles_y, uint32_t flip, unsigned long long* __restrict__ counters,
                 unsigned long long* __restrict__ stats) {
     constexpr int ROWS = TY * TZ;               // 128 rows of 32
@@ -112,7 +113,6 @@ tile_tmt_kernel(const float* __restrict__ f, Cell* __restrict__ C, uint32_t nx, 
     const uint64_t sxy = uint64_t(nx) * ny;
     const int lx = threadIdx.x & (TX - 1);
     const int r0 = threadIdx.x / TX;
-    const int lane = threadIdx.x & 31;
 
     // ---- K1: load f once, order keys into shared memory ------------------------------
     bool bad = false;
@@ -190,6 +190,9 @@ tile_tmt_kernel(const float* __restrict__ f, Cell* __restrict__ C, uint32_t nx, 
         sst64(cell + u, (cell[u] & ~0xffffull) | x);
     }
     __syncthreads();
+    uint16_t bas[PER];  // descent basin of each owned vertex, for the crossing-edge dedupe
+#pragma unroll
+    for (int k = 0; k < PER; ++k) bas[k] = uint16_t(c_v(cell[(r0 + k * RSTEP) * TX + lx]));
     phase_time(ST_CYC_COMPRESS);
 
     // ---- c. one edge per pair of adjacent basins: the lowest --------------------------------
@@ -370,8 +373,9 @@ tile_tmt_kernel(const float* __restrict__ f, Cell* __restrict__ C, uint32_t nx, 
         if (ou == ABSENT) continue;
         const uint64_t cu = cell[u];
         const uint32_t s = c_s(cu), v = c_v(cu);
-        C[gbase + uint64_t(lz) * sxy + uint64_t(ly) * nx + lx] =
-            make_cell(key_of(uint32_t(cu >> 32), gid(s)), ou, gid(v));
+        const uint64_t g = gbase + uint64_t(lz) * sxy + uint64_t(ly) * nx + lx;
+        C[g] = make_cell(key_of(uint32_t(cu >> 32), gid(s)), ou, gid(v));
+        basin_out[g] = gid(bas[k]);
     }
     phase_time(ST_CYC_WRITE);
     if (stats) {
@@ -407,8 +411,8 @@ void tile_shape(uint32_t nz_global, uint32_t* ty, uint32_t* tz) {
 }
 
 template <int TY, int TZ>
-void launch_tile(const float* f, Cell* C, const Slab& sl, uint32_t tx, uint32_t tyn, uint32_t grid, uint32_t flip,
-                 unsigned long long* counters, unsigned long long* stats, cudaStream_t stream) {
+void launch_tile(const float* f, Cell* C, uint32_t* basin, const Slab& sl, uint32_t tx, uint32_t tyn, uint32_t grid,
+                 uint32_t flip, unsigned long long* counters, unsigned long long* stats, cudaStream_t stream) {
     constexpr int NV = TX * TY * TZ;
     static bool attr = false;
     if (!attr) {
@@ -416,12 +420,12 @@ void launch_tile(const float* f, Cell* C, const Slab& sl, uint32_t tx, uint32_t 
                              int(smem_bytes<NV>()));
         attr = true;
     }
-    tile_tmt_kernel<TY, TZ><<<grid, NV / 8, smem_bytes<NV>(), stream>>>(f, C, sl.nx, sl.ny, sl.z_begin, sl.z_end, tx,
+    tile_tmt_kernel<TY, TZ><<<grid, NV / 8, smem_bytes<NV>(), stream>>>(f, C, basin, sl.nx, sl.ny, sl.z_begin, sl.z_end, tx,
                                                                        tyn, flip, counters, stats);
 }
 
-void launch_tile_tmt(const float* f, Cell* C, const Slab& sl, uint32_t flip, unsigned long long* counters,
-                     unsigned long long* stats, cudaStream_t stream) {
+void launch_tile_tmt(const float* f, Cell* C, uint32_t* basin, const Slab& sl, uint32_t flip,
+                     unsigned long long* counters, unsigned long long* stats, cudaStream_t stream) {
     uint32_t ty, tz;
     tile_shape(sl.nz, &ty, &tz);
     const uint32_t nzl = sl.z_end - sl.z_begin;
@@ -430,13 +434,13 @@ void launch_tile_tmt(const float* f, Cell* C, const Slab& sl, uint32_t flip, uns
     if (grid == 0) return;
     const bool big = tile_vertices() == 4096;
     if (sl.nz == 1 && big)
-        launch_tile<128, 1>(f, C, sl, tx, tyn, grid, flip, counters, stats, stream);
+        launch_tile<128, 1>(f, C, basin, sl, tx, tyn, grid, flip, counters, stats, stream);
     else if (sl.nz == 1)
-        launch_tile<64, 1>(f, C, sl, tx, tyn, grid, flip, counters, stats, stream);
+        launch_tile<64, 1>(f, C, basin, sl, tx, tyn, grid, flip, counters, stats, stream);
     else if (big)
-        launch_tile<16, 8>(f, C, sl, tx, tyn, grid, flip, counters, stats, stream);
+        launch_tile<16, 8>(f, C, basin, sl, tx, tyn, grid, flip, counters, stats, stream);
     else
-        launch_tile<8, 8>(f, C, sl, tx, tyn, grid, flip, counters, stats, stream);
+        launch_tile<8, 8>(f, C, basin, sl, tx, tyn, grid, flip, counters, stats, stream);
 }
 
 }  // namespace mt
