@@ -112,6 +112,17 @@ mt_status mt_diagram(mt_ctx *ctx, mt_pair *out, uint64_t capacity, uint64_t *n_p
 mt_status mt_diagram_view(mt_ctx *ctx, const mt_pair **records, uint64_t *n_pairs,
                           uint64_t *n_essential, mt_stream_t stream);
 
+/* Persistence simplification ("short branches ... can
+ * be intuitively interpreted as topological noise"): copy to
+ * `out` (device, capacity records, must not be the diagram buffer itself) the
+ * finite pairs of the last compute with |death - birth| > eps (evaluated in
+ * float32, the precision of the values) followed by every essential class,
+ * in the order of mt_diagram.  eps >= 0.  Syncs; *n_pairs_kept and
+ * *n_essential (host) receive the counts; MT_ERR_CAPACITY if they exceed
+ * capacity (counts still returned). */
+mt_status mt_filter_diagram(mt_ctx *ctx, float eps, mt_pair *out, uint64_t capacity, uint64_t *n_pairs_kept,
+                            uint64_t *n_essential, mt_stream_t stream);
+
 /* Synchronise `stream` and return the sticky error state of the context. */
 mt_status mt_last_error(mt_ctx *ctx, mt_stream_t stream);
 

@@ -4,7 +4,7 @@ Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s
 ``cpu_baseline`` / ``--impl reference`` legs may import anything under
 ``oracle/``.  The product package ``paper_2301_10838_b200`` never imports it,
 and this package never imports the product (they share no code; the only
-common input is the seeded field generator module ``synthfields``, which
+common input is the seeded field generator module ``paper_2301_10838_b200/fields.py``, which
 holds none of the method's arithmetic).
 
 Contents
@@ -96,6 +96,15 @@ def merge_tree(f: np.ndarray, dims, conn: int = 6, split: bool = False, want_pai
         raise OracleError(st)
     k = npairs.value + ness.value
     return T, (pairs[:k] if want_pairs else None), npairs.value, ness.value
+
+
+def filter_by_persistence(pairs: np.ndarray, n_pairs: int, eps: float) -> np.ndarray:
+    """Finite pairs with persistence |f(b) - f(a)| > eps, then every essential class
+    (short branches as topological noise; SPEC.md "filter_by_persistence").
+    The persistence is computed in float32, the precision of the values."""
+    fin = pairs[:n_pairs]
+    pers = np.abs(fin["death"].astype(np.float32) - fin["birth"].astype(np.float32))
+    return np.concatenate([fin[pers > np.float32(eps)], pairs[n_pairs:]])
 
 
 def unpack(T: np.ndarray):

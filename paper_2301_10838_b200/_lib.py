@@ -29,7 +29,8 @@ FOREST_RECORD_BYTES = 32  # mt_forest_record
 EXPORTS = ["mt_workspace_bytes", "mt_create", "mt_compute", "mt_set_diagram_output", "mt_diagram",
            "mt_diagram_view", "mt_last_error", "mt_last_launch_count", "mt_set_profiling", "mt_kernel_times",
            "mt_status_string", "mt_destroy", "mt_abi_version", "mt_set_stats", "mt_stats", "mt_slab_workspace_bytes",
-           "mt_create_slab", "mt_compute_local", "mt_forest_view", "mt_forest_scratch_bytes", "mt_compute_global"]
+           "mt_create_slab", "mt_compute_local", "mt_forest_view", "mt_forest_scratch_bytes", "mt_compute_global",
+           "mt_filter_diagram"]
 
 
 class MTError(RuntimeError):
@@ -65,6 +66,7 @@ def load(build_if_missing: bool = False):
         "mt_diagram": (ctypes.c_int, [vp, vp, ctypes.c_uint64, u64p, u64p, vp]),
         "mt_diagram_view": (ctypes.c_int, [vp, ctypes.POINTER(vp), u64p, u64p, vp]),
         "mt_last_error": (ctypes.c_int, [vp, vp]),
+        "mt_filter_diagram": (ctypes.c_int, [vp, ctypes.c_float, vp, ctypes.c_uint64, u64p, u64p, vp]),
         "mt_last_launch_count": (ctypes.c_uint32, [vp]),
         "mt_set_profiling": (ctypes.c_int, [vp, ctypes.c_int]),
         "mt_kernel_times": (ctypes.c_int, [vp, ctypes.POINTER(ctypes.c_char_p), ctypes.POINTER(ctypes.c_float),
@@ -154,6 +156,16 @@ def mt_diagram_view(ctx, stream=None):
     if st in (MT_ERR_CUDA, MT_ERR_STATE, MT_ERR_INVALID_ARG):
         raise MTError(st, "mt_diagram_view")
     return st, ptr.value, npairs.value, ness.value
+
+
+def mt_filter_diagram(ctx, eps: float, out_ptr: int, capacity: int, stream=None):
+    """Returns (status, n_pairs_kept, n_essential)."""
+    a, b = ctypes.c_uint64(0), ctypes.c_uint64(0)
+    st = load().mt_filter_diagram(ctx, ctypes.c_float(eps), ctypes.c_void_p(out_ptr or None),
+                                  ctypes.c_uint64(capacity), ctypes.byref(a), ctypes.byref(b), _stream_handle(stream))
+    if st in (MT_ERR_CUDA, MT_ERR_STATE, MT_ERR_INVALID_ARG):
+        raise MTError(st, "mt_filter_diagram")
+    return st, a.value, b.value
 
 
 def mt_last_error(ctx, stream=None) -> int:
@@ -286,6 +298,16 @@ class MergeTree:
             st, a, b = mt_diagram(self.ctx, out.data_ptr(), k, stream)
             _check(st, "mt_diagram")
         return out, npairs, ness
+
+    def filter_diagram(self, eps: float, stream=None):
+        """Pairs with persistence > eps (+ essential classes): ((k,4) int32 CUDA tensor, n_pairs, n_ess)."""
+        import torch
+        st, ptr, npairs, ness = mt_diagram_view(self.ctx, stream)
+        cap = max(1, npairs + ness)
+        out = torch.empty((cap, 4), dtype=torch.int32, device=self.device)
+        st, a, b = mt_filter_diagram(self.ctx, eps, out.data_ptr(), cap, stream)
+        _check(st, "mt_filter_diagram")
+        return out[: a + b], a, b
 
     def last_launch_count(self):
         return mt_last_launch_count(self.ctx)

@@ -123,7 +123,9 @@ enum CounterSlot : int {
     CTR_QLEN = 5,       // crossing-edge queue length (dedupe_cross)
     CTR_QFETCH = 6,     // next queue entry to hand out (merge_queue)
     CTR_FCOUNT = 7,     // boundary-forest records of this slab
-    CTR_COUNT = 8
+    CTR_FILT_TICKET = 8,  // mt_filter_diagram: tile tickets
+    CTR_FILT_KEPT = 9,    // mt_filter_diagram: records kept
+    CTR_COUNT = 16
 };
 
 // Optional diagnostics (mt_set_stats): event counters in the workspace.

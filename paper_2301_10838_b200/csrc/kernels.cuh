@@ -88,6 +88,11 @@ void launch_repair_diagram(Cell* C, uint64_t* T, const float* f, uint64_t base, 
 void launch_finish_diagram(unsigned long long* counters, mt_pair* out, uint64_t out_cap, mt_pair* ess,
                            uint32_t ess_cap, cudaStream_t stream);
 
+// persistence simplification of the diagram (diagram_filter.cu)
+uint64_t filter_tiles(uint64_t n);
+void launch_filter_diagram(const mt_pair* in, uint64_t n_fin, uint64_t n_all, float eps, mt_pair* out, uint64_t cap,
+                           unsigned long long* ctl, uint64_t* status, cudaStream_t stream);
+
 // multi-GPU boundary forest (slab.cu)
 constexpr int MAX_SLABS = 64;
 struct SlabBounds {

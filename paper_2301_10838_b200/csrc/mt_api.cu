@@ -450,6 +450,39 @@ mt_status mt_last_error(mt_ctx* c, mt_stream_t stream) {
     return sync_counters(c, static_cast<cudaStream_t>(stream));
 }
 
+mt_status mt_filter_diagram(mt_ctx* c, float eps, mt_pair* out, uint64_t capacity, uint64_t* n_pairs_kept,
+                            uint64_t* n_essential, mt_stream_t stream) {
+    if (!c || !(eps >= 0.f)) return MT_ERR_INVALID_ARG;
+    DeviceGuard g(c->device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const mt_status st = sync_counters(c, s);
+    if (st != MT_OK) return st;
+    const uint64_t nfin = c->host_ctr[mt::CTR_FIN], ness = c->host_ctr[mt::CTR_ESS];
+    const uint64_t n_all = nfin + ness;
+    uint64_t kept = 0;
+    if (n_all) {
+        if (!out) return MT_ERR_INVALID_ARG;
+        uint64_t cap = 0;
+        const mt_pair* src = target_of(c, &cap);
+        if (out == src) return MT_ERR_INVALID_ARG;  // not in place
+        unsigned long long* ctl = counters_of(c) + mt::CTR_FILT_TICKET;
+        uint64_t* status = reinterpret_cast<uint64_t*>(c->ws + c->L.status);  // free after the repair
+        if (mt::filter_tiles(n_all) > c->L.ntiles) return MT_ERR_STATE;
+        if (cudaMemsetAsync(ctl, 0, 2 * sizeof(uint64_t), s) != cudaSuccess ||
+            cudaMemsetAsync(status, 0, mt::filter_tiles(n_all) * sizeof(uint64_t), s) != cudaSuccess)
+            return MT_ERR_CUDA;
+        mt::launch_filter_diagram(src, nfin, n_all, eps, out, capacity, ctl, status, s);
+        uint64_t host = 0;
+        if (cudaMemcpyAsync(&host, ctl + 1, sizeof(uint64_t), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+            cudaStreamSynchronize(s) != cudaSuccess)
+            return MT_ERR_CUDA;
+        kept = host;
+    }
+    if (n_pairs_kept) *n_pairs_kept = kept - ness;
+    if (n_essential) *n_essential = ness;
+    return kept > capacity ? MT_ERR_CAPACITY : MT_OK;
+}
+
 uint32_t mt_last_launch_count(const mt_ctx* c) { return c ? c->launches : 0; }
 
 mt_status mt_set_profiling(mt_ctx* c, int enable) {

@@ -177,3 +177,18 @@ def test_medium_many_seeds(cfg):
     for seed in range(6):
         f, dims, conn = fields.make(cfg, seed=100 + seed, scale=128)
         assert_parity(f, dims, conn, split=bool(seed % 2))
+
+
+@pytest.mark.parametrize("cfg,scale,split", [("c4", 64, False), ("c5", 64, True), ("c2", 256, False)])
+def test_persistence_filter(cfg, scale, split):
+    """mt_filter_diagram == the oracle's filter of the oracle diagram, order preserved."""
+    f, dims, conn = fields.make(cfg, scale=scale)
+    To, po, npo, neo = oracle.merge_tree(f, dims, conn=conn, split=split)
+    mt = ctx_for(dims, conn)
+    mt.compute(torch.from_numpy(f).cuda(), split=split)
+    pers = np.abs(po["death"][:npo] - po["birth"][:npo])
+    for eps in (0.0, float(np.quantile(pers, 0.5)) if npo else 0.1, float(pers.max()) if npo else 1.0, 1e30):
+        rec, a, b = mt.filter_diagram(eps)
+        want = oracle.filter_by_persistence(po, npo, eps)
+        assert a + b == want.size and b == neo
+        assert _lib.pairs_to_numpy(rec).tobytes() == want.tobytes()

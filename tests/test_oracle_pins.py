@@ -202,3 +202,17 @@ def test_field_generators_deterministic():
     assert np.all((a >= 0) & (a < 1))
     assert np.all(a * 2 ** 24 == np.round(a * 2 ** 24))  # exactly on the 2^-24 grid
     assert fields.field_hash(a) == fields.field_hash(b)
+
+
+def test_filter_by_persistence_definition():
+    """SPEC.md analysis examples: P3 diagram {(2,3)} ess {1}: eps 0.5 keeps the pair, eps 2 drops it,
+    eps 0 keeps every positive-persistence pair; essential classes always stay."""
+    f = np.array([1, 3, 2], np.float32)
+    T, pairs, npairs, ness = oracle.merge_tree(f, (3, 1, 1), 4)
+    assert oracle.filter_by_persistence(pairs, npairs, 0.5).tolist() == pairs.tolist()
+    kept = oracle.filter_by_persistence(pairs, npairs, 2.0)
+    assert kept.size == 1 and kept[0]["birth_v"] == 0 and np.isinf(kept[0]["death"])
+    f = np.array([0, 1, 0], np.float32)   # tie pair (0, 1) has persistence 1; zero-persistence pairs drop at eps 0
+    T, pairs, npairs, ness = oracle.merge_tree(np.array([1, 1, 0, 1], np.float32), (4, 1, 1), 4)
+    assert all(p["death"] - p["birth"] == 0 for p in pairs[:npairs])
+    assert oracle.filter_by_persistence(pairs, npairs, 0.0).size == ness
