@@ -7,9 +7,8 @@
 // Repair: T[u] = (s, v) becomes (s, Rep(u, key(s))), Rep following cells while
 // key(s') <= key(s) and the cell is not a root.  Reading R20: the walk returns
 // the vertex it stopped at (Alg. 4 as printed returns the next, too-deep v).
-// The walk runs in place while other threads rewrite their own cells; every
-// value a cell ever holds is a valid pointer at that cell's own level, so the
-// result does not depend on the interleaving (DESIGN.md derivation E).
+// The walks only read the working cells (the repaired pointer goes to T), so
+// they see the fixed post-merge store.
 //
 // Diagram: after the merge phase the s fields are final (repair only rewrites
 // v), so a cell with s != u is the branch born at u dying at saddle s (finite
@@ -145,7 +144,8 @@ repair_diagram_kernel(View view, Cell* C, uint64_t* __restrict__ T, const float*
     for (int k = 0; k < ITEMS; ++k) {
         if (!(todo & (1u << k))) continue;
         const uint64_t u = base + first + uint64_t(k) * THREADS + threadIdx.x;
-        if (x[k] != cv_of(cell[k])) st_cell_v(C + u, x[k]);   // in-place shortcut (derivation E)
+        // (no in-place shortcut of the working cell: the 4-B partial write would dirty a
+        // 32-B sector per vertex -- ~17 GB of write-back at 1024^3 for walks of ~2.5 hops)
         T[u] = pack(cs_of(cell[k]), x[k]);
     }
     if (stats) atomicAdd(stats + ST_REPAIR_HOPS, hops);
