@@ -77,7 +77,7 @@ __device__ __forceinline__ uint64_t scas64(uint64_t* p, uint64_t cmp, uint64_t v
     return atomicCAS(reinterpret_cast<unsigned long long*>(p), cmp, val);
 }
 
-template <int TY, int TZ, int NV = TX * TY * TZ, int THREADS = NV / 8, int TABLE = 2 * NV>
+template <int TY, int TZ, bool STATS, int NV = TX * TY * TZ, int THREADS = NV / 8, int TABLE = 2 * NV>
 __global__ void __launch_bounds__(THREADS)
 tile_tmt_kernel(const float* __restrict__ f, Cell* __restrict__ C, uint32_t* __restrict__ basin_out, uint32_t nx,
                 uint32_t ny, uint32_t z_begin,
@@ -98,7 +98,7 @@ tile_tmt_kernel(const float* __restrict__ f, Cell* __restrict__ C, uint32_t* __r
     long long t_mark = clock64();
     // per-phase SM cycles (stats mode): thread 0 accumulates the time between barriers
     auto phase_time = [&](int slot) {
-        if (stats && threadIdx.x == 0) {
+        if (STATS && threadIdx.x == 0) {
             const long long t = clock64();
             atomicAdd(stats + slot, (unsigned long long)(t - t_mark));
             t_mark = t;
@@ -177,7 +177,7 @@ tile_tmt_kernel(const float* __restrict__ f, Cell* __restrict__ C, uint32_t* __r
             const uint32_t y = c_v(sld64(cell + x));
             if (y == x) break;
             x = y;
-            ++n_cmp;
+            if (STATS) ++n_cmp;
         }
         // every regular cell on the path gets the root too (same tree, same basin)
         uint32_t y = v;
@@ -216,7 +216,7 @@ tile_tmt_kernel(const float* __restrict__ f, Cell* __restrict__ C, uint32_t* __r
             if (ord[w] == ABSENT) continue;
             const uint32_t bw = c_v(cell[w]);
             if (bw == bu) continue;
-            ++n_edges;
+            if (STATS) ++n_edges;
             const uint32_t hi = lkey_lt(ord, w, u) ? u : w;
             const uint32_t pair = bu < bw ? (bu << 12) | bw : (bw << 12) | bu;
             const uint64_t entry = (uint64_t(pair) << 12) | hi;
@@ -261,7 +261,7 @@ tile_tmt_kernel(const float* __restrict__ f, Cell* __restrict__ C, uint32_t* __r
                 has_prev = true;
                 x = c_v(c);
                 c = sld64(cell + x);
-                ++n_hops;
+                if (STATS) ++n_hops;
             }
             rr[side] = x;
         }
@@ -269,7 +269,7 @@ tile_tmt_kernel(const float* __restrict__ f, Cell* __restrict__ C, uint32_t* __r
         uint32_t mu = rr[0], mv = rr[1];
         uint64_t S = L;
         while (true) {                                    // Alg. 3
-            ++n_iters;
+            if (STATS) ++n_iters;
             const uint64_t cu = sld64(cell + mu), cv = sld64(cell + mv);
             if (c_v(cu) != mu && c_key(cu) < S) { mu = c_v(cu); continue; }   // l.2-4 + R4
             if (c_v(cv) != mv && c_key(cv) < S) { mv = c_v(cv); continue; }   // l.5-8 + R4
@@ -308,7 +308,7 @@ tile_tmt_kernel(const float* __restrict__ f, Cell* __restrict__ C, uint32_t* __r
             e = table[chunk++];
         }
         if (e == EMPTY) break;
-        ++n_pairs;
+        if (STATS) ++n_pairs;
         const uint32_t pair = uint32_t(e >> 12), hi = uint32_t(e) & 0xfffu;
         const uint32_t ba = pair >> 12, bb = pair & 0xfffu;
         const uint32_t bh = basin(hi);
@@ -351,7 +351,7 @@ tile_tmt_kernel(const float* __restrict__ f, Cell* __restrict__ C, uint32_t* __r
             const uint64_t cx = sld64(cell + x);
             if (c_v(cx) == x || c_key(cx) > a) break;
             x = c_v(cx);
-            ++n_rep;
+            if (STATS) ++n_rep;
         }
         if (x != v) sst64(cell + u, (cu & ~0xffffull) | x);
     }
@@ -378,7 +378,7 @@ tile_tmt_kernel(const float* __restrict__ f, Cell* __restrict__ C, uint32_t* __r
         basin_out[g] = gid(bas[k]);
     }
     phase_time(ST_CYC_WRITE);
-    if (stats) {
+    if (STATS) {
         atomicAdd(stats + ST_TILE_EDGES, n_edges);
         atomicAdd(stats + ST_TILE_HOPS, n_hops);
         atomicAdd(stats + ST_TILE_ITERS, n_iters);
@@ -416,11 +416,18 @@ void launch_tile(const float* f, Cell* C, uint32_t* basin, const Slab& sl, uint3
     constexpr int NV = TX * TY * TZ;
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(tile_tmt_kernel<TY, TZ>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(tile_tmt_kernel<TY, TZ, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             int(smem_bytes<NV>()));
+        cudaFuncSetAttribute(tile_tmt_kernel<TY, TZ, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              int(smem_bytes<NV>()));
         attr = true;
     }
-    tile_tmt_kernel<TY, TZ><<<grid, NV / 8, smem_bytes<NV>(), stream>>>(f, C, basin, sl.nx, sl.ny, sl.z_begin, sl.z_end, tx,
+    if (stats)
+        tile_tmt_kernel<TY, TZ, true><<<grid, NV / 8, smem_bytes<NV>(), stream>>>(f, C, basin, sl.nx, sl.ny,
+                                                                                 sl.z_begin, sl.z_end, tx, tyn,
+                                                                                 flip, counters, stats);
+    else
+        tile_tmt_kernel<TY, TZ, false><<<grid, NV / 8, smem_bytes<NV>(), stream>>>(f, C, basin, sl.nx, sl.ny, sl.z_begin, sl.z_end, tx,
                                                                        tyn, flip, counters, stats);
 }
 
