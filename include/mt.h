@@ -182,6 +182,23 @@ mt_status mt_compute_global(mt_ctx *ctx, const mt_forest_record *all, uint64_t n
                             const uint32_t *z_bounds, uint32_t nslabs, void *scratch,
                             size_t scratch_bytes, uint64_t *triplets_slab, mt_stream_t stream);
 
+/* ---- Explicit graphs ----------------------------------
+ * The same computation on an undirected graph G = (V, E) (PAPER.md:128-131:
+ * "the space is a graph G = (V, E), and the function is defined only on the
+ * vertices") given in CSR form: the neighbours of u are col[row[u] ..
+ * row[u+1]) (row: n+1 uint64, col: row[n] uint32 vertex ids, both device).
+ * Every undirected edge must be listed in both directions; self-loops and
+ * duplicate entries are allowed (they change nothing).  A graph may have
+ * several components: one essential class each, ascending.  n_adj bounds
+ * row[n] for the workspace size. */
+size_t mt_graph_workspace_bytes(uint32_t n, uint64_t n_adj);
+mt_status mt_create_graph(mt_ctx **out, uint32_t n, uint64_t n_adj, int cuda_device, void *workspace,
+                          size_t workspace_bytes);
+/* Asynchronous like mt_compute; f, row, col borrowed until the stream passes
+ * this call's work; triplets (device, n uint64) out.  mt_diagram as usual. */
+mt_status mt_compute_graph(mt_ctx *ctx, const float *f, const uint64_t *row, const uint32_t *col,
+                           uint64_t *triplets, uint32_t flags, mt_stream_t stream);
+
 /* Diagnostics: while enabled, mt_compute counts events of the merge and
  * repair kernels: [0] edges examined, [1] edges skipped as redundant,
  * [2] cells followed by the pre-filter walks, [3] Alg. 3 loop iterations,

@@ -68,6 +68,10 @@ def _load():
                 ctypes.c_void_p, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32,
                 ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p,
                 ctypes.POINTER(ctypes.c_uint64), ctypes.POINTER(ctypes.c_uint64)]
+            lib.oracle_merge_tree_graph.restype = ctypes.c_int
+            lib.oracle_merge_tree_graph.argtypes = [
+                ctypes.c_void_p, ctypes.c_uint32, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int,
+                ctypes.c_void_p, ctypes.c_void_p, ctypes.POINTER(ctypes.c_uint64), ctypes.POINTER(ctypes.c_uint64)]
             _lib = lib
     return _lib
 
@@ -96,6 +100,40 @@ def merge_tree(f: np.ndarray, dims, conn: int = 6, split: bool = False, want_pai
         raise OracleError(st)
     k = npairs.value + ness.value
     return T, (pairs[:k] if want_pairs else None), npairs.value, ness.value
+
+
+def merge_tree_graph(f: np.ndarray, row: np.ndarray, col: np.ndarray, split: bool = False):
+    """O1 on an explicit graph in CSR form (neighbours of u: col[row[u]:row[u+1]]); same outputs
+    as merge_tree.  Several components give several essential classes."""
+    lib = _load()
+    f = np.ascontiguousarray(f, dtype=np.float32).reshape(-1)
+    row = np.ascontiguousarray(row, dtype=np.uint64)
+    col = np.ascontiguousarray(col, dtype=np.uint32)
+    n = f.size
+    if row.size != n + 1:
+        raise ValueError("row must have n+1 entries")
+    T = np.empty(n, dtype=np.uint64)
+    pairs = np.empty(max(n, 1), dtype=PAIR_DTYPE)
+    npairs, ness = ctypes.c_uint64(0), ctypes.c_uint64(0)
+    st = lib.oracle_merge_tree_graph(f.ctypes.data if n else None, n, row.ctypes.data,
+                                     col.ctypes.data if col.size else None, int(bool(split)),
+                                     T.ctypes.data if n else None, pairs.ctypes.data, ctypes.byref(npairs),
+                                     ctypes.byref(ness))
+    if st != OK:
+        raise OracleError(st)
+    return T, pairs[: npairs.value + ness.value], npairs.value, ness.value
+
+
+def csr_from_edges(n: int, edges) -> tuple[np.ndarray, np.ndarray]:
+    """Symmetric CSR adjacency of an undirected edge list (each edge listed both ways)."""
+    e = np.asarray(list(edges), dtype=np.int64).reshape(-1, 2)
+    src = np.concatenate([e[:, 0], e[:, 1]])
+    dst = np.concatenate([e[:, 1], e[:, 0]])
+    order = np.lexsort((dst, src))
+    src, dst = src[order], dst[order]
+    row = np.zeros(n + 1, dtype=np.uint64)
+    np.add.at(row, src + 1, 1)
+    return np.cumsum(row).astype(np.uint64), dst.astype(np.uint32)
 
 
 def filter_by_persistence(pairs: np.ndarray, n_pairs: int, eps: float) -> np.ndarray:

@@ -33,6 +33,7 @@ def grid_edges(dims):
 
 
 def compute_merge_tree(f, dims, split=False, edge_order=None, seed=None, init=None):
+    """``edge_order`` may give any edge list (an explicit graph: dims = (n, 1, 1))."""
     """Alg. 1.  ``init`` optionally replaces line 2-3's (u, u) start state by
     any normalized triplet store of a subgraph (e.g. steepest descent)."""
     dims = tuple(int(d) for d in dims)

@@ -47,9 +47,10 @@ def keys(f, split=False):
     return [(g[i] + 0.0, i) for i in range(len(g))]
 
 
-def _components(member, dims):
-    """Label connected components of the vertex set ``member`` by BFS."""
+def _components(member, dims, adj=None):
+    """Label connected components of the vertex set ``member`` by BFS (grid, or adjacency lists)."""
     n = len(member)
+    nbrs = (lambda x: adj[x]) if adj is not None else (lambda x: grid_neighbours(x, dims))
     label = [-1] * n
     comps = []
     for s in range(n):
@@ -61,7 +62,7 @@ def _components(member, dims):
         comp = [s]
         while q:
             x = q.popleft()
-            for y in grid_neighbours(x, dims):
+            for y in nbrs(x):
                 if member[y] and label[y] < 0:
                     label[y] = cid
                     q.append(y)
@@ -70,8 +71,9 @@ def _components(member, dims):
     return label, comps
 
 
-def merge_tree(f, dims, split=False):
-    """Return (T as list of (u, s, v), finite pairs [(birth_v, death_v)], essential [u])."""
+def merge_tree(f, dims, split=False, adj=None):
+    """Return (T as list of (u, s, v), finite pairs [(birth_v, death_v)], essential [u]).
+    ``adj`` (lists of neighbours) replaces the grid for an explicit graph (dims = (n, 1, 1))."""
     dims = tuple(int(d) for d in dims)
     n = dims[0] * dims[1] * dims[2]
     K = keys(f, split)
@@ -81,7 +83,7 @@ def merge_tree(f, dims, split=False):
     for k, w in enumerate(order):
         # level = key(w): sublevel set {x : key(x) <= key(w)}
         member[w] = True
-        label, comps = _components(member, dims)
+        label, comps = _components(member, dims, adj)
         cmin = [min(c, key=lambda x: K[x]) for c in comps]
         for u in order[: k + 1]:
             if trip[u] is not None:

@@ -78,6 +78,14 @@ static uint32_t ds_find(uint32_t *parent, uint32_t x) {
     return x;
 }
 
+/* The graph: a grid (implicit 4/6-neighbour adjacency) or an explicit CSR
+ * adjacency list (row[n+1], col[]), SURVEY.md 8f f4 / PAPER.md:128-131. */
+typedef struct {
+    uint32_t nx, ny, nz;
+    const uint64_t *row;  /* NULL for a grid */
+    const uint32_t *col;
+} graph_t;
+
 /* Grid neighbours of u: +-x, +-y, +-z inside the box (reading R9, R10). */
 static int grid_neighbours(uint64_t u, uint32_t nx, uint32_t ny, uint32_t nz, uint32_t out[6]) {
     uint64_t x = u % nx, y = (u / nx) % ny, z = u / ((uint64_t)nx * ny);
@@ -103,12 +111,31 @@ static int grid_neighbours(uint64_t u, uint32_t nx, uint32_t ny, uint32_t nz, ui
  *              vertex (death_v = birth_v, death = +inf)
  *   n_pairs, n_ess : out counts
  */
+static int sweep(const float *f, uint64_t n, const graph_t *G, int split, uint64_t *T, oracle_pair *pairs,
+                 uint64_t *n_pairs, uint64_t *n_ess);
+
 int oracle_merge_tree(const float *f, uint32_t nx, uint32_t ny, uint32_t nz, int conn, int split,
                       uint64_t *T, oracle_pair *pairs, uint64_t *n_pairs, uint64_t *n_ess) {
-    if (!f && (uint64_t)nx * ny * nz) return OR_INVALID;
+    if (!f && (uint64_t)nx * ny * nz != 0) return OR_INVALID;
     if (conn != 4 && conn != 6) return OR_INVALID;
     if (conn == 4 && nz != 1) return OR_INVALID;
-    uint64_t n = (uint64_t)nx * ny * nz;
+    graph_t G = {nx, ny, nz, NULL, NULL};
+    return sweep(f, (uint64_t)nx * ny * nz, &G, split, T, pairs, n_pairs, n_ess);
+}
+
+/* Explicit graph: the neighbours of u are col[row[u] .. row[u+1]). */
+int oracle_merge_tree_graph(const float *f, uint32_t n, const uint64_t *row, const uint32_t *col, int split,
+                            uint64_t *T, oracle_pair *pairs, uint64_t *n_pairs, uint64_t *n_ess) {
+    if (n && (!f || !row)) return OR_INVALID;
+    for (uint32_t u = 0; u < n; u++)
+        for (uint64_t j = row[u]; j < row[u + 1]; j++)
+            if (col[j] >= n) return OR_INVALID;
+    graph_t G = {n, 1, 1, row, col};
+    return sweep(f, n, &G, split, T, pairs, n_pairs, n_ess);
+}
+
+static int sweep(const float *f, uint64_t n, const graph_t *G, int split, uint64_t *T, oracle_pair *pairs,
+                 uint64_t *n_pairs, uint64_t *n_ess) {
     if (n > 4294967295ull) return OR_TOO_LARGE; /* 32-bit ids */
     if (n_pairs) *n_pairs = 0;
     if (n_ess) *n_ess = 0;
@@ -140,18 +167,35 @@ int oracle_merge_tree(const float *f, uint32_t nx, uint32_t ny, uint32_t nz, int
     /* "First, one sorts the vertices by values of the function". */
     qsort(order, n, sizeof(vkey), cmp_vkey);
 
-    uint32_t nb[6], R[6];
+    uint32_t nb[6];
+    uint64_t rcap = 64;
+    uint32_t *R = (uint32_t *)malloc(rcap * sizeof(uint32_t));
+    if (!R) { free(order); free(parent); free(size); free(cmin); free(death); free(done); free(g); if (!T) free(Tl); return OR_NOMEM; }
     for (uint64_t k = 0; k < n; k++) {
         uint32_t u = order[k].id;
-        int deg = grid_neighbours(u, nx, ny, nz, nb);
+        const uint32_t *adj;
+        uint64_t deg;
+        if (G->row) {
+            adj = G->col + G->row[u];
+            deg = G->row[u + 1] - G->row[u];
+        } else {
+            deg = (uint64_t)grid_neighbours(u, G->nx, G->ny, G->nz, nb);
+            adj = nb;
+        }
+        if (deg > rcap) {
+            while (rcap < deg) rcap *= 2;
+            uint32_t *R2 = (uint32_t *)realloc(R, rcap * sizeof(uint32_t));
+            if (!R2) { free(R); free(order); free(parent); free(size); free(cmin); free(death); free(done); free(g); if (!T) free(Tl); return OR_NOMEM; }
+            R = R2;
+        }
         /* R = distinct components of the lower neighbours of u */
-        int nr = 0;
-        for (int j = 0; j < deg; j++) {
-            uint32_t w = nb[j];
-            if (!done[w]) continue; /* not yet in the sublevel set <=> !less(w,u) */
+        uint64_t nr = 0;
+        for (uint64_t j = 0; j < deg; j++) {
+            uint32_t w = adj[j];
+            if (!done[w]) continue; /* not yet in the sublevel set <=> !less(w,u) (self-loops: not done) */
             uint32_t r = ds_find(parent, w);
             int dup = 0;
-            for (int t = 0; t < nr; t++) dup |= (R[t] == r);
+            for (uint64_t t = 0; t < nr; t++) dup |= (R[t] == r);
             if (!dup) R[nr++] = r;
         }
         done[u] = 1;
@@ -164,13 +208,13 @@ int oracle_merge_tree(const float *f, uint32_t nx, uint32_t ny, uint32_t nz, int
         }
         /* m* = deepest vertex over the merged components (the oldest branch). */
         uint32_t mstar = cmin[R[0]];
-        for (int t = 1; t < nr; t++) {
+        for (uint64_t t = 1; t < nr; t++) {
             uint32_t m = cmin[R[t]];
             if (key_less(g[m], m, g[mstar], mstar)) mstar = m;
         }
         /* (3) merge: every younger minimum's branch ends at saddle u, merged
          * into the branch of m* (elder rule; triplet (m, u, m*)). */
-        for (int t = 0; t < nr; t++) {
+        for (uint64_t t = 0; t < nr; t++) {
             uint32_t m = cmin[R[t]];
             if (m != mstar) {
                 Tl[m] = ((uint64_t)u << 32) | mstar;
@@ -182,7 +226,7 @@ int oracle_merge_tree(const float *f, uint32_t nx, uint32_t ny, uint32_t nz, int
         Tl[u] = ((uint64_t)u << 32) | mstar;
         /* union u and all of R, the union's deepest vertex is m* */
         uint32_t root = R[0];
-        for (int t = 1; t < nr; t++) {
+        for (uint64_t t = 1; t < nr; t++) {
             uint32_t a = root, b = R[t];
             if (size[a] < size[b]) { uint32_t tmp = a; a = b; b = tmp; }
             parent[b] = a;
@@ -231,6 +275,7 @@ int oracle_merge_tree(const float *f, uint32_t nx, uint32_t ny, uint32_t nz, int
     if (n_pairs) *n_pairs = np;
     if (n_ess) *n_ess = ne;
 
+    free(R);
     free(order); free(parent); free(size); free(cmin); free(death); free(done); free(g);
     if (!T) free(Tl);
     return OR_OK;

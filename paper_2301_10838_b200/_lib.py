@@ -30,7 +30,7 @@ EXPORTS = ["mt_workspace_bytes", "mt_create", "mt_compute", "mt_set_diagram_outp
            "mt_diagram_view", "mt_last_error", "mt_last_launch_count", "mt_set_profiling", "mt_kernel_times",
            "mt_status_string", "mt_destroy", "mt_abi_version", "mt_set_stats", "mt_stats", "mt_slab_workspace_bytes",
            "mt_create_slab", "mt_compute_local", "mt_forest_view", "mt_forest_scratch_bytes", "mt_compute_global",
-           "mt_filter_diagram"]
+           "mt_filter_diagram", "mt_graph_workspace_bytes", "mt_create_graph", "mt_compute_graph"]
 
 
 class MTError(RuntimeError):
@@ -67,6 +67,10 @@ def load(build_if_missing: bool = False):
         "mt_diagram_view": (ctypes.c_int, [vp, ctypes.POINTER(vp), u64p, u64p, vp]),
         "mt_last_error": (ctypes.c_int, [vp, vp]),
         "mt_filter_diagram": (ctypes.c_int, [vp, ctypes.c_float, vp, ctypes.c_uint64, u64p, u64p, vp]),
+        "mt_graph_workspace_bytes": (ctypes.c_size_t, [ctypes.c_uint32, ctypes.c_uint64]),
+        "mt_create_graph": (ctypes.c_int, [ctypes.POINTER(vp), ctypes.c_uint32, ctypes.c_uint64, ctypes.c_int, vp,
+                                           ctypes.c_size_t]),
+        "mt_compute_graph": (ctypes.c_int, [vp, vp, vp, vp, vp, ctypes.c_uint32, vp]),
         "mt_last_launch_count": (ctypes.c_uint32, [vp]),
         "mt_set_profiling": (ctypes.c_int, [vp, ctypes.c_int]),
         "mt_kernel_times": (ctypes.c_int, [vp, ctypes.POINTER(ctypes.c_char_p), ctypes.POINTER(ctypes.c_float),
@@ -242,6 +246,59 @@ def mt_compute_global(ctx, all_ptr: int, n_all: int, z_bounds, scratch_ptr: int,
                                     ctypes.c_void_p(triplets_ptr), _stream_handle(stream)), "mt_compute_global")
 
 
+# ---- explicit graphs ------------------------------------------------------------
+
+def mt_graph_workspace_bytes(n: int, n_adj: int) -> int:
+    return int(load().mt_graph_workspace_bytes(int(n), ctypes.c_uint64(n_adj)))
+
+
+def mt_create_graph(n: int, n_adj: int, device: int, workspace_ptr: int, workspace_bytes: int):
+    h = ctypes.c_void_p()
+    _check(load().mt_create_graph(ctypes.byref(h), int(n), ctypes.c_uint64(n_adj), int(device),
+                                  ctypes.c_void_p(workspace_ptr), ctypes.c_size_t(workspace_bytes)), "mt_create_graph")
+    return h
+
+
+def mt_compute_graph(ctx, f_ptr: int, row_ptr: int, col_ptr: int, triplets_ptr: int, flags: int = 0, stream=None):
+    _check(load().mt_compute_graph(ctx, ctypes.c_void_p(f_ptr), ctypes.c_void_p(row_ptr),
+                                   ctypes.c_void_p(col_ptr or None), ctypes.c_void_p(triplets_ptr), int(flags),
+                                   _stream_handle(stream)), "mt_compute_graph")
+
+
+class GraphMergeTree:
+    """A context for an explicit graph (CSR adjacency, both directions listed) on one device."""
+
+    def __init__(self, n: int, n_adj: int, device=None):
+        import torch
+        self.n, self.n_adj = int(n), int(n_adj)
+        dev = torch.device("cuda", torch.cuda.current_device() if device is None else int(device)) \
+            if not isinstance(device, torch.device) else device
+        self.device = dev
+        nbytes = mt_graph_workspace_bytes(self.n, self.n_adj)
+        self.workspace = torch.empty(nbytes + 256, dtype=torch.uint8, device=dev)
+        ptr = (self.workspace.data_ptr() + 255) // 256 * 256
+        self.ctx = mt_create_graph(self.n, self.n_adj, dev.index, ptr, nbytes)
+
+    def __del__(self):
+        ctx = getattr(self, "ctx", None)
+        if ctx is not None and _lib is not None:
+            _lib.mt_destroy(ctx)
+            self.ctx = None
+
+    def compute(self, f, row, col, split: bool = False, triplets=None, stream=None):
+        """f float32[n], row int64[n+1], col int32[row[n]] CUDA tensors -> int64 triplets (async)."""
+        import torch
+        if f.numel() != self.n or row.numel() != self.n + 1 or col.numel() > self.n_adj:
+            raise ValueError("graph sizes do not match the context")
+        if triplets is None:
+            triplets = torch.empty(self.n, dtype=torch.int64, device=f.device)
+        mt_compute_graph(self.ctx, f.data_ptr(), row.data_ptr(), col.data_ptr() if col.numel() else 0,
+                         triplets.data_ptr(), MT_FLAG_SPLIT_TREE if split else 0, stream)
+        return triplets
+
+    diagram = None  # set below (shared with MergeTree)
+
+
 # ---- convenience owner --------------------------------------------------------
 
 class MergeTree:
@@ -311,6 +368,10 @@ class MergeTree:
 
     def last_launch_count(self):
         return mt_last_launch_count(self.ctx)
+
+
+GraphMergeTree.diagram = MergeTree.diagram
+GraphMergeTree.filter_diagram = MergeTree.filter_diagram
 
 
 def pairs_to_numpy(records) -> np.ndarray:

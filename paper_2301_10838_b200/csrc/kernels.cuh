@@ -80,13 +80,24 @@ void launch_merge_cross(Cell* C, const float* f, const uint32_t* basin, const Sl
                         uint64_t cap, unsigned long long* qlen, unsigned long long* fetch, unsigned long long* stats,
                         int num_sms, cudaStream_t stream);
 
+// the queue consumer alone (queue entries: {uint64 L, uint32 basin_hi, uint32 basin_lo})
+void launch_merge_queue(Cell* C, const void* queue, uint64_t cap, const unsigned long long* qlen,
+                        unsigned long long* fetch, unsigned long long* stats, int num_sms, cudaStream_t stream);
+
+// explicit graphs in CSR form (graph.cu)
+void launch_graph_init(const float* f, const uint64_t* row, const uint32_t* col, uint32_t n, uint32_t flip, Cell* C,
+                       unsigned long long* counters, int num_sms, cudaStream_t stream);
+void launch_graph_edges(const uint64_t* row, const uint32_t* col, uint32_t n, Cell* C, uint32_t* basin, void* queue,
+                        uint64_t cap, unsigned long long* qlen, int num_sms, cudaStream_t stream);
+
 // K4+K5: repair fused with the ordered diagram compaction (repair_diagram.cu)
 uint64_t repair_tiles(uint64_t n);
 void launch_repair_diagram(Cell* C, uint64_t* T, const float* f, uint64_t base, uint64_t n, unsigned long long* counters,
-                           uint64_t* status, mt_pair* out, uint64_t out_cap, mt_pair* ess, uint32_t ess_cap,
+                           uint64_t* status, uint64_t* status_ess, mt_pair* out, uint64_t out_cap, mt_pair* ess,
+                           uint64_t ess_cap,
                            unsigned long long* stats, const ForestRef* forest, cudaStream_t stream);
 void launch_finish_diagram(unsigned long long* counters, mt_pair* out, uint64_t out_cap, mt_pair* ess,
-                           uint32_t ess_cap, cudaStream_t stream);
+                           uint64_t ess_cap, cudaStream_t stream);
 
 // persistence simplification of the diagram (diagram_filter.cu)
 uint64_t filter_tiles(uint64_t n);

@@ -274,6 +274,12 @@ void launch_merge_cross(Cell* C, const float* f, const uint32_t* basin, const Sl
     uint64_t blocks = (total + 255) / 256;
     if (blocks > uint64_t(num_sms) * 32) blocks = uint64_t(num_sms) * 32;
     dedupe_cross_kernel<<<uint32_t(blocks), 256, 0, stream>>>(f, basin, g, flip, q, cap, qlen, stats);
+    launch_merge_queue(C, q, cap, qlen, fetch, stats, num_sms, stream);
+}
+
+void launch_merge_queue(Cell* C, const void* queue, uint64_t cap, const unsigned long long* qlen,
+                        unsigned long long* fetch, unsigned long long* stats, int num_sms, cudaStream_t stream) {
+    const QEntry* q = static_cast<const QEntry*>(queue);
     static int per_sm[2] = {0, 0};  // persistent grid: as many CTAs as fit on every SM
     const int t = stats ? 1 : 0;
     if (!per_sm[t]) {

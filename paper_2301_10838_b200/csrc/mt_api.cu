@@ -23,8 +23,8 @@ constexpr int MAX_EVENTS = 12;
 size_t align_up(size_t x) { return (x + ALIGN - 1) / ALIGN * ALIGN; }
 
 struct Layout {
-    size_t counters, status, stats, ess, cells, basin, queue, pairs, flags, recs, total;
-    uint64_t ntiles, pairs_cap, recs_cap, queue_cap;
+    size_t counters, status, status_ess, stats, ess, cells, basin, queue, pairs, flags, recs, total;
+    uint64_t ntiles, pairs_cap, recs_cap, queue_cap, ess_cap;
 };
 
 bool valid_dims(const uint32_t dims[3], int conn) {
@@ -34,21 +34,26 @@ bool valid_dims(const uint32_t dims[3], int conn) {
     return true;
 }
 
-Layout layout_for(uint64_t n, uint64_t ncross, bool slab = false) {
+// n vertices; ncross queue entries; ess_cap essential records (components);
+// slab: add the boundary-forest buffers
+Layout layout_for(uint64_t n, uint64_t ncross, bool slab = false, uint64_t ess_cap = ESS_CAP) {
     Layout L{};
     L.ntiles = n ? mt::repair_tiles(n) : 0;
-    // finite pairs <= #minima - 1 and strict minima form an independent set of
-    // the grid graph, so at most ceil(n/2) records in total (+1 slack).
-    L.pairs_cap = n ? (n + 1) / 2 + 1 : 0;
+    // records = #minima.  On a grid the strict minima form an independent set,
+    // so at most ceil(n/2) (+1 slack); a general graph (ess_cap = n) may have n.
+    L.pairs_cap = n ? (ess_cap >= n ? n : (n + 1) / 2 + 1) : 0;
     size_t off = 0;
     L.counters = off;
     off += align_up(mt::CTR_COUNT * sizeof(uint64_t));
-    L.status = off;  // contiguous with counters: one memset zeroes both
-    off += align_up(L.ntiles * sizeof(uint64_t));
+    L.status = off;  // contiguous with counters: one memset zeroes both status arrays too
+    off += L.ntiles * sizeof(uint64_t);
+    L.status_ess = off;
+    off = align_up(off + L.ntiles * sizeof(uint64_t));
     L.stats = off;
     off += align_up(mt::ST_COUNT * sizeof(uint64_t));
     L.ess = off;
-    off += align_up(ESS_CAP * sizeof(mt_pair));
+    L.ess_cap = ess_cap;
+    off += align_up(ess_cap * sizeof(mt_pair));
     L.cells = off;  // 16-byte working cells of the merge phase
     off += align_up(n * sizeof(mt::Cell));
     L.basin = off;  // descent basin of every vertex (tile_tmt -> dedupe_cross)
@@ -76,9 +81,11 @@ struct mt_ctx {
     uint64_t n;              // vertices this context owns
     mt::Slab slab;           // owned planes of the global grid (all of them for mt_create)
     bool multi = false;      // created by mt_create_slab
+    bool graph = false;      // created by mt_create_graph (CSR adjacency instead of a grid)
     bool local_done = false; // mt_compute_local ran, mt_compute_global pending
     const float* f = nullptr;
     uint32_t flip = 0;
+    uint64_t n_adj = 0;      // graph contexts: adjacency entries (the queue capacity)
     int conn;
     int device;
     int num_sms;
@@ -161,15 +168,17 @@ extern "C" void mt_destroy(mt_ctx* c);
 namespace {
 
 mt_status create_ctx(mt_ctx** out, const uint32_t dims[3], int conn, uint32_t z_begin, uint32_t z_end, bool multi,
-                     int cuda_device, void* workspace, size_t workspace_bytes) {
+                     int cuda_device, void* workspace, size_t workspace_bytes, const Layout* graph_layout = nullptr) {
     if (!out) return MT_ERR_INVALID_ARG;
     *out = nullptr;
-    if (!valid_dims(dims, conn)) return MT_ERR_INVALID_ARG;
+    if (!graph_layout && !valid_dims(dims, conn)) return MT_ERR_INVALID_ARG;
     if (uint64_t(dims[0]) * dims[1] * dims[2] > 0xffffffffull) return MT_ERR_TOO_LARGE;
     const uint64_t n = uint64_t(dims[0]) * dims[1] * (z_end - z_begin);
-    const Layout L = layout_for(
-        n, mt::cross_edges(mt::Slab{dims[0], dims[1], dims[2], z_begin, z_end, uint64_t(dims[0]) * dims[1] * z_begin, n}),
-        multi);
+    const Layout L = graph_layout ? *graph_layout
+                                  : layout_for(n,
+                                               mt::cross_edges(mt::Slab{dims[0], dims[1], dims[2], z_begin, z_end,
+                                                                        uint64_t(dims[0]) * dims[1] * z_begin, n}),
+                                               multi);
     if (!workspace || workspace_bytes < L.total || (reinterpret_cast<uintptr_t>(workspace) % ALIGN))
         return MT_ERR_WORKSPACE;
     int ndev = 0;
@@ -185,6 +194,7 @@ mt_status create_ctx(mt_ctx** out, const uint32_t dims[3], int conn, uint32_t z_
     c->n = n;
     c->slab = mt::Slab{dims[0], dims[1], dims[2], z_begin, z_end, uint64_t(dims[0]) * dims[1] * z_begin, n};
     c->multi = multi;
+    c->graph = graph_layout != nullptr;
     c->conn = conn;
     c->device = cuda_device;
     c->ws = static_cast<char*>(workspace);
@@ -219,7 +229,7 @@ mt_status start_compute(mt_ctx* c, const float* f, uint32_t flags, cudaStream_t 
     if (stats && cudaMemsetAsync(stats, 0, mt::ST_COUNT * sizeof(uint64_t), s) != cudaSuccess)
         return c->sticky = MT_ERR_CUDA;
     mark(c, "zero", s);
-    if (cudaMemsetAsync(c->ws + c->L.counters, 0, c->L.status - c->L.counters + c->L.ntiles * sizeof(uint64_t),
+    if (cudaMemsetAsync(c->ws + c->L.counters, 0, c->L.status_ess - c->L.counters + c->L.ntiles * sizeof(uint64_t),
                         s) != cudaSuccess)
         return c->sticky = MT_ERR_CUDA;
     uint32_t* basin = reinterpret_cast<uint32_t*>(c->ws + c->L.basin) - c->slab.base;
@@ -241,10 +251,11 @@ mt_status finish_compute(mt_ctx* c, uint64_t* T, const mt::ForestRef* forest, cu
     uint64_t* status = reinterpret_cast<uint64_t*>(c->ws + c->L.status);
     const uint64_t base = c->slab.base;
     mark(c, "repair_diagram", s);
-    mt::launch_repair_diagram(cells_of(c), T - base, c->f - base, base, c->n, ctr, status, out, cap, ess, ESS_CAP,
-                              stats_of(c), forest, s);
+    uint64_t* status_ess = reinterpret_cast<uint64_t*>(c->ws + c->L.status_ess);
+    mt::launch_repair_diagram(cells_of(c), T - base, c->f - base, base, c->n, ctr, status, status_ess, out, cap, ess,
+                              c->L.ess_cap, stats_of(c), forest, s);
     mark(c, "finish_diagram", s);
-    mt::launch_finish_diagram(ctr, out, cap, ess, ESS_CAP, s);
+    mt::launch_finish_diagram(ctr, out, cap, ess, c->L.ess_cap, s);
     if (c->profiling) cudaEventRecord(c->ev[c->nev], s);
     c->launches += 2;
     if (cudaGetLastError() != cudaSuccess) return c->sticky = MT_ERR_CUDA;
@@ -307,10 +318,62 @@ mt_status mt_set_diagram_output(mt_ctx* c, mt_pair* buf, uint64_t capacity) {
     return MT_OK;
 }
 
+// ---- explicit graphs -----------------------------------
+size_t mt_graph_workspace_bytes(uint32_t n, uint64_t n_adj) {
+    return layout_for(n, n_adj, false, n ? n : 1).total;
+}
+
+mt_status mt_create_graph(mt_ctx** out, uint32_t n, uint64_t n_adj, int cuda_device, void* workspace,
+                          size_t workspace_bytes) {
+    if (!out) return MT_ERR_INVALID_ARG;
+    const uint32_t dims[3] = {n, 1, 1};
+    const Layout L = layout_for(n, n_adj, false, n ? n : 1);
+    mt_status st = create_ctx(out, dims, 0, 0, 1, false, cuda_device, workspace, workspace_bytes, &L);
+    if (st == MT_OK) (*out)->n_adj = n_adj;
+    return st;
+}
+
+mt_status mt_compute_graph(mt_ctx* c, const float* f, const uint64_t* row, const uint32_t* col, uint64_t* T,
+                           uint32_t flags, mt_stream_t stream) {
+    if (!c) return MT_ERR_INVALID_ARG;
+    if (flags & ~uint32_t(MT_FLAG_SPLIT_TREE)) return MT_ERR_INVALID_ARG;
+    if (!c->graph) return MT_ERR_STATE;
+    c->launches = 0;
+    c->nev = 0;
+    c->sticky = MT_OK;
+    c->computed = true;
+    if (c->n == 0) return MT_OK;
+    if (!f || !row || !T) return MT_ERR_INVALID_ARG;  // col may be NULL for an edgeless graph
+    DeviceGuard g(c->device);
+    if (!g.ok) return MT_ERR_CUDA;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    c->f = f;
+    c->flip = (flags & MT_FLAG_SPLIT_TREE) ? 0xffffffffu : 0u;
+    unsigned long long* ctr = counters_of(c);
+    mt::Cell* cells = cells_of(c);
+    unsigned long long* stats = stats_of(c);
+    if (stats && cudaMemsetAsync(stats, 0, mt::ST_COUNT * sizeof(uint64_t), s) != cudaSuccess)
+        return c->sticky = MT_ERR_CUDA;
+    mark(c, "zero", s);
+    if (cudaMemsetAsync(c->ws + c->L.counters, 0, c->L.status_ess - c->L.counters + c->L.ntiles * sizeof(uint64_t),
+                        s) != cudaSuccess)
+        return c->sticky = MT_ERR_CUDA;
+    mark(c, "graph_init", s);
+    mt::launch_graph_init(f, row, col, uint32_t(c->n), c->flip, cells, ctr, c->num_sms, s);
+    mark(c, "graph_edges", s);
+    mt::launch_graph_edges(row, col, uint32_t(c->n), cells, nullptr, c->ws + c->L.queue, c->L.queue_cap,
+                           ctr + mt::CTR_QLEN, c->num_sms, s);
+    mark(c, "merge_queue", s);
+    mt::launch_merge_queue(cells, c->ws + c->L.queue, c->L.queue_cap, ctr + mt::CTR_QLEN, ctr + mt::CTR_QFETCH, stats,
+                           c->num_sms, s);
+    c->launches = 4;
+    return finish_compute(c, T, nullptr, s);
+}
+
 mt_status mt_compute(mt_ctx* c, const float* f, uint64_t* T, uint32_t flags, mt_stream_t stream) {
     if (!c) return MT_ERR_INVALID_ARG;
     if (flags & ~uint32_t(MT_FLAG_SPLIT_TREE)) return MT_ERR_INVALID_ARG;
-    if (c->multi) return MT_ERR_STATE;  // slab contexts use mt_compute_local / mt_compute_global
+    if (c->multi || c->graph) return MT_ERR_STATE;  // slab contexts use mt_compute_local / mt_compute_global
     if (c->n == 0) {
         c->computed = true;
         c->sticky = MT_OK;

@@ -62,11 +62,12 @@ template <class View>
 __global__ void __launch_bounds__(THREADS)
 repair_diagram_kernel(View view, Cell* C, uint64_t* __restrict__ T, const float* __restrict__ f, uint64_t base, uint64_t n,
                       unsigned long long* __restrict__ counters, uint64_t* __restrict__ status,
-                      mt_pair* __restrict__ out, uint64_t out_cap, mt_pair* __restrict__ ess, uint32_t ess_cap,
+                      uint64_t* __restrict__ status_ess,
+                      mt_pair* __restrict__ out, uint64_t out_cap, mt_pair* __restrict__ ess, uint64_t ess_cap,
                       uint64_t ntiles, unsigned long long* __restrict__ stats) {
     __shared__ uint64_t s_tile;
-    __shared__ uint32_t s_cnt[ITEMS * 8];
-    __shared__ uint64_t s_prefix;
+    __shared__ uint32_t s_cnt[ITEMS * 8], s_ecnt[ITEMS * 8];
+    __shared__ uint64_t s_prefix, s_eprefix;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     if (threadIdx.x == 0) s_tile = atomicAdd(counters + CTR_TICKET, 1ull);
     __syncthreads();
@@ -74,32 +75,39 @@ repair_diagram_kernel(View view, Cell* C, uint64_t* __restrict__ T, const float*
     const uint64_t first = tile * TILE;  // local index of the tile's first vertex
 
     Cell cell[ITEMS];
-    bool fin[ITEMS];
-    uint32_t mask[ITEMS];
+    bool fin[ITEMS], root[ITEMS];
+    uint32_t mask[ITEMS], emask[ITEMS];
 #pragma unroll
     for (int k = 0; k < ITEMS; ++k) {
         const uint64_t l = first + uint64_t(k) * THREADS + threadIdx.x;
         const uint64_t u = base + l;     // global id (C, T, f are indexed by global id)
         cell[k] = l < n ? ld_cell(C + u) : Cell{0, 0};
         fin[k] = l < n && cs_of(cell[k]) != uint32_t(u);
+        root[k] = l < n && cv_of(cell[k]) == uint32_t(u);   // (u, u, u): an essential class
         mask[k] = __ballot_sync(FULL_MASK, fin[k]);
-        if (lane == 0) s_cnt[k * 8 + warp] = __popc(mask[k]);
+        emask[k] = __ballot_sync(FULL_MASK, root[k]);
+        if (lane == 0) {
+            s_cnt[k * 8 + warp] = __popc(mask[k]);
+            s_ecnt[k * 8 + warp] = __popc(emask[k]);
+        }
     }
     __syncthreads();
-    // exclusive scan of the 32 (k, warp) counts in u order, by warp 0
-    if (warp == 0) {
-        const uint32_t c = s_cnt[lane];
+    // exclusive scans of the 32 (k, warp) counts in u order: finite pairs by
+    // warp 0, essential classes by warp 1; each publishes the tile's count
+    // before the walks
+    if (warp < 2) {
+        uint32_t* cnt = warp == 0 ? s_cnt : s_ecnt;
+        uint64_t* st = warp == 0 ? status : status_ess;
+        const uint32_t c = cnt[lane];
         uint32_t incl = c;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
             const uint32_t t = __shfl_up_sync(FULL_MASK, incl, o);
             if (lane >= o) incl += t;
         }
-        s_cnt[lane] = incl - c;
+        cnt[lane] = incl - c;
         const uint32_t agg = __shfl_sync(FULL_MASK, incl, 31);
-        if (lane == 0) {
-            st_relaxed(status + tile, (tile == 0 ? ST_PRE : ST_AGG) | agg);  // publish before walking
-        }
+        if (lane == 0) st_relaxed(st + tile, (tile == 0 ? ST_PRE : ST_AGG) | agg);
     }
 
     // --- repair (Alg. 5 with Alg. 4's walk) ------------------------------
@@ -114,10 +122,7 @@ repair_diagram_kernel(View view, Cell* C, uint64_t* __restrict__ T, const float*
         const uint64_t u = base + l;
         x[k] = cv_of(cell[k]);
         if (l >= n) continue;
-        if (x[k] == uint32_t(u)) {                    // root (u, u, u): essential class
-            const uint32_t i = atomicAdd(reinterpret_cast<unsigned int*>(counters + CTR_ESS), 1u);
-            if (i < ess_cap) ess[i] = mt_pair{uint32_t(u), uint32_t(u), __ldg(f + u), __int_as_float(0x7f800000)};
-            else atomicOr(counters + CTR_ERR, ERR_ESS_CAPACITY);
+        if (root[k]) {                                // root (u, u, u): written with the diagram below
             T[u] = pack(uint32_t(u), uint32_t(u));
             continue;
         }
@@ -150,14 +155,15 @@ repair_diagram_kernel(View view, Cell* C, uint64_t* __restrict__ T, const float*
     }
     if (stats) atomicAdd(stats + ST_REPAIR_HOPS, hops);
 
-    // --- decoupled look-back for the tile's output offset ----------------
+    // --- decoupled look-backs for the tile's output offsets --------------
     __syncthreads();
-    if (warp == 0) {
+    if (warp < 2) {
+        uint64_t* stat = warp == 0 ? status : status_ess;
         uint64_t prefix = 0;
         int64_t j = int64_t(tile) - 1;
         while (j >= 0) {
             const int64_t idx = j - lane;
-            const uint64_t st = idx >= 0 ? ld_relaxed(status + idx) : ST_PRE;
+            const uint64_t st = idx >= 0 ? ld_relaxed(stat + idx) : ST_PRE;
             const uint64_t flag = st >> 62;
             const uint32_t pmask = __ballot_sync(FULL_MASK, flag == 2);
             const uint32_t xmask = __ballot_sync(FULL_MASK, flag == 0);
@@ -171,17 +177,34 @@ repair_diagram_kernel(View view, Cell* C, uint64_t* __restrict__ T, const float*
             if (pmask) break;
             j -= 32;
         }
-        if (lane == 0) s_prefix = prefix;
+        if (lane == 0) (warp == 0 ? s_prefix : s_eprefix) = prefix;
     }
     __syncthreads();
-    const uint64_t prefix = s_prefix;
+    const uint64_t prefix = s_prefix, eprefix = s_eprefix;
     // inclusive prefix = prefix + this tile's aggregate; s_cnt holds exclusive
     // offsets, so the aggregate is the last offset + the last (k, warp) count,
     // which the last thread's own ballot holds.
     if (threadIdx.x == THREADS - 1) {
         const uint64_t total = prefix + s_cnt[(ITEMS - 1) * 8 + 7] + __popc(mask[ITEMS - 1]);
-        if (tile != 0) st_relaxed(status + tile, ST_PRE | total);
-        if (tile == ntiles - 1) counters[CTR_FIN] = total;
+        const uint64_t etotal = eprefix + s_ecnt[(ITEMS - 1) * 8 + 7] + __popc(emask[ITEMS - 1]);
+        if (tile != 0) {
+            st_relaxed(status + tile, ST_PRE | total);
+            st_relaxed(status_ess + tile, ST_PRE | etotal);
+        }
+        if (tile == ntiles - 1) {
+            counters[CTR_FIN] = total;
+            counters[CTR_ESS] = etotal;
+        }
+    }
+
+    // --- essential classes in ascending u (into the essential buffer) ------
+#pragma unroll
+    for (int k = 0; k < ITEMS; ++k) {
+        if (!root[k]) continue;
+        const uint64_t u = base + first + uint64_t(k) * THREADS + threadIdx.x;
+        const uint64_t pos = eprefix + s_ecnt[k * 8 + warp] + __popc(emask[k] & ((1u << lane) - 1u));
+        if (pos < ess_cap) ess[pos] = mt_pair{uint32_t(u), uint32_t(u), __ldg(f + u), __int_as_float(0x7f800000)};
+        else atomicOr(counters + CTR_ERR, ERR_ESS_CAPACITY);
     }
 
     // --- write this tile's finite pairs in ascending u --------------------
@@ -196,25 +219,14 @@ repair_diagram_kernel(View view, Cell* C, uint64_t* __restrict__ T, const float*
     }
 }
 
-// Appends the essential classes (ascending vertex) after the finite pairs and
-// checks the capacity.  One CTA; the number of essential classes is the number
-// of connected components (one for a non-empty grid).
+// Appends the essential classes (already in ascending vertex order) after the
+// finite pairs and checks the capacity.
 __global__ void finish_diagram_kernel(unsigned long long* __restrict__ counters, mt_pair* __restrict__ out,
-                                      uint64_t out_cap, mt_pair* __restrict__ ess, uint32_t ess_cap) {
+                                      uint64_t out_cap, mt_pair* __restrict__ ess, uint64_t ess_cap) {
     const uint64_t nfin = counters[CTR_FIN];
-    uint32_t ness = uint32_t(counters[CTR_ESS]);
+    uint64_t ness = counters[CTR_ESS];
     if (ness > ess_cap) ness = ess_cap;
-    if (threadIdx.x == 0) {
-        // insertion sort by vertex (ness is tiny)
-        for (uint32_t i = 1; i < ness; ++i) {
-            mt_pair p = ess[i];
-            uint32_t j = i;
-            while (j > 0 && ess[j - 1].birth_v > p.birth_v) { ess[j] = ess[j - 1]; --j; }
-            ess[j] = p;
-        }
-    }
-    __syncthreads();
-    for (uint32_t i = threadIdx.x; i < ness; i += blockDim.x) {
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < ness; i += uint64_t(gridDim.x) * blockDim.x) {
         if (nfin + i < out_cap) out[nfin + i] = ess[i];
         else atomicOr(counters + CTR_ERR, ERR_CAPACITY);
     }
@@ -225,23 +237,28 @@ __global__ void finish_diagram_kernel(unsigned long long* __restrict__ counters,
 uint64_t repair_tiles(uint64_t n) { return (n + TILE - 1) / TILE; }
 
 void launch_repair_diagram(Cell* C, uint64_t* T, const float* f, uint64_t base, uint64_t n, unsigned long long* counters,
-                           uint64_t* status, mt_pair* out, uint64_t out_cap, mt_pair* ess, uint32_t ess_cap,
+                           uint64_t* status, uint64_t* status_ess, mt_pair* out, uint64_t out_cap, mt_pair* ess,
+                           uint64_t ess_cap,
                            unsigned long long* stats, const ForestRef* forest, cudaStream_t stream) {
     const uint64_t ntiles = repair_tiles(n);
     if (ntiles == 0) return;
     if (forest)
         repair_diagram_kernel<<<uint32_t(ntiles), THREADS, 0, stream>>>(ForestView{*forest, base, n}, C, T, f, base, n,
-                                                                         counters, status, out, out_cap, ess, ess_cap,
+                                                                         counters, status, status_ess, out, out_cap,
+                                                                         ess, ess_cap,
                                                                          ntiles, stats);
     else
         repair_diagram_kernel<<<uint32_t(ntiles), THREADS, 0, stream>>>(LocalView{}, C, T, f, base, n, counters,
-                                                                         status, out, out_cap, ess, ess_cap, ntiles,
+                                                                         status, status_ess, out, out_cap, ess,
+                                                                         ess_cap, ntiles,
                                                                          stats);
 }
 
 void launch_finish_diagram(unsigned long long* counters, mt_pair* out, uint64_t out_cap, mt_pair* ess,
-                           uint32_t ess_cap, cudaStream_t stream) {
-    finish_diagram_kernel<<<1, 128, 0, stream>>>(counters, out, out_cap, ess, ess_cap);
+                           uint64_t ess_cap, cudaStream_t stream) {
+    uint64_t blocks = (ess_cap + 255) / 256;
+    if (blocks > 1184) blocks = 1184;
+    finish_diagram_kernel<<<uint32_t(blocks ? blocks : 1), 256, 0, stream>>>(counters, out, out_cap, ess, ess_cap);
 }
 
 }  // namespace mt
