@@ -126,10 +126,14 @@ dedupe_cross_kernel(const float* __restrict__ f, const uint32_t* __restrict__ ba
     if (stats) atomicAdd(stats + ST_EDGES, n_edges);
 }
 
+#ifndef MQ_MIN_BLOCKS
+#define MQ_MIN_BLOCKS 6   // 6 x 256 threads per SM: <= 42 registers, 48 warps of loads in flight
+#endif
+
 enum Phase : int { IDLE = 0, CLIMB_HI = 2, CLIMB_LO = 3, MERGE_LD = 4, MERGE_CAS = 5, DONE = 6 };
 
 template <bool STATS>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, MQ_MIN_BLOCKS)
 merge_queue_kernel(Cell* C, const QEntry* __restrict__ q, uint64_t cap, const unsigned long long* __restrict__ qlen,
                    unsigned long long* __restrict__ fetch, unsigned long long* __restrict__ stats) {
     constexpr uint64_t BATCH = 256;

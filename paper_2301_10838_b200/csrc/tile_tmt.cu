@@ -92,7 +92,7 @@ tile_tmt_kernel(const float* __restrict__ f, Cell* __restrict__ C, uint32_t* __r
     uint32_t* ord = reinterpret_cast<uint32_t*>(smem + NV * 8);
     uint64_t* table = reinterpret_cast<uint64_t*>(smem + NV * 12);
     __shared__ int s_overflow;
-    __shared__ uint32_t s_fetch;
+    __shared__ uint32_t s_fetch, s_row, s_row_b, s_row_e;
 
     unsigned long long n_edges = 0, n_pairs = 0, n_hops = 0, n_iters = 0, n_rep = 0, n_cmp = 0;
     long long t_mark = clock64();
@@ -133,6 +133,9 @@ tile_tmt_kernel(const float* __restrict__ f, Cell* __restrict__ C, uint32_t* __r
     if (threadIdx.x == 0) {
         s_overflow = 0;
         s_fetch = 0;
+        s_row = 0;
+        s_row_b = 0;
+        s_row_e = 0;
     }
     if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(counters + CTR_ERR, ERR_NONFINITE);
     phase_time(ST_CYC_LOAD);
@@ -167,9 +170,14 @@ tile_tmt_kernel(const float* __restrict__ f, Cell* __restrict__ C, uint32_t* __r
     phase_time(ST_CYC_DESCENT);
 
     // ---- b. compress with path compression ---------------------------------------------
+    // rows handed out dynamically, one warp per row (no warp waits on a long walk of another)
 #pragma unroll 1
-    for (int k = 0; k < PER; ++k) {
-        const uint32_t u = (r0 + k * RSTEP) * TX + lx;
+    while (true) {
+        int rr = 0;
+        if ((threadIdx.x & 31) == 0) rr = int(atomicAdd(&s_row_b, 1u));
+        rr = __shfl_sync(FULL_MASK, rr, 0);
+        if (rr >= ROWS) break;
+        const uint32_t u = rr * TX + lx;
         const uint32_t v = c_v(cell[u]);
         if (v == u) continue;
         uint32_t x = v;
@@ -200,9 +208,15 @@ tile_tmt_kernel(const float* __restrict__ f, Cell* __restrict__ C, uint32_t* __r
     // L' joins vertices that are already connected at L' through their descent paths and
     // that lowest edge (DESIGN.md derivation C'').  A shared-memory hash table keyed by the
     // basin pair keeps, per pair, the edge's upper endpoint of lowest key.
+    // rows of 32 vertices are handed out dynamically (a warp per row) so that warps with
+    // contended inserts do not hold the barrier for the others
+    const int lane_c = threadIdx.x & 31;
 #pragma unroll 1
-    for (int k = 0; k < PER; ++k) {
-        const int r = r0 + k * RSTEP;
+    while (true) {
+        int r = 0;
+        if (lane_c == 0) r = int(atomicAdd(&s_row, 1u));
+        r = __shfl_sync(FULL_MASK, r, 0);
+        if (r >= ROWS) break;
         const int ly = r % TY, lz = r / TY;
         const uint32_t u = r * TX + lx;
         if (ord[u] == ABSENT) continue;
@@ -340,8 +354,12 @@ tile_tmt_kernel(const float* __restrict__ f, Cell* __restrict__ C, uint32_t* __r
 
     // ---- e. repair: every cell points at its representative (minimal tile store) -------
 #pragma unroll 1
-    for (int k = 0; k < PER; ++k) {
-        const uint32_t u = (r0 + k * RSTEP) * TX + lx;
+    while (true) {
+        int rr = 0;
+        if ((threadIdx.x & 31) == 0) rr = int(atomicAdd(&s_row_e, 1u));
+        rr = __shfl_sync(FULL_MASK, rr, 0);
+        if (rr >= ROWS) break;
+        const uint32_t u = rr * TX + lx;
         const uint64_t cu = cell[u];
         const uint32_t v = c_v(cu);
         if (v == u) continue;
