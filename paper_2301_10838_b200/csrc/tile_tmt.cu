@@ -315,8 +315,8 @@ tile_tmt_kernel(const float* __restrict__ f, Cell* __restrict__ C, uint32_t* __r
         uint64_t e = EMPTY;
         while (e == EMPTY) {
             if (chunk == chunk_end) {
-                chunk = atomicAdd(&s_fetch, 4u);
-                chunk_end = chunk + 4;
+                chunk = atomicAdd(&s_fetch, 1u);
+                chunk_end = chunk + 1;
                 if (chunk >= uint32_t(TABLE)) break;
             }
             e = table[chunk++];
