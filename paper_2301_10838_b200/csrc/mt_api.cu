@@ -236,9 +236,9 @@ mt_status start_compute(mt_ctx* c, const float* f, uint32_t flags, cudaStream_t 
     mark(c, "tile_tmt", s);
     mt::launch_tile_tmt(fs, cells, basin, c->slab, c->flip, ctr, stats, s);
     mark(c, "merge_cross", s);
-    mt::launch_merge_cross(cells, fs, basin, c->slab, c->flip, c->ws + c->L.queue, c->L.queue_cap, ctr + mt::CTR_QLEN,
-                           ctr + mt::CTR_QFETCH, stats, c->num_sms, s);
-    c->launches = 3;
+    const int nl = mt::launch_merge_cross(cells, fs, basin, c->slab, c->flip, c->ws + c->L.queue, c->L.queue_cap,
+                                          ctr + mt::CTR_QLEN, ctr + mt::CTR_QFETCH, stats, c->num_sms, s);
+    c->launches = 1 + nl;
     return MT_OK;
 }
 
