@@ -92,7 +92,8 @@ void launch_graph_edges(const uint64_t* row, const uint32_t* col, uint32_t n, Ce
 
 // K4+K5: repair fused with the ordered diagram compaction (repair_diagram.cu)
 uint64_t repair_tiles(uint64_t n);
-void launch_repair_diagram(Cell* C, uint64_t* T, const float* f, uint64_t base, uint64_t n, unsigned long long* counters,
+void launch_repair_diagram(Cell* C, uint64_t* T, const float* f, uint64_t base, uint64_t n, uint32_t flip,
+                           unsigned long long* counters,
                            uint64_t* status, uint64_t* status_ess, mt_pair* out, uint64_t out_cap, mt_pair* ess,
                            uint64_t ess_cap,
                            unsigned long long* stats, const ForestRef* forest, cudaStream_t stream);

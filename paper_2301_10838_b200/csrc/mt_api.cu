@@ -252,7 +252,8 @@ mt_status finish_compute(mt_ctx* c, uint64_t* T, const mt::ForestRef* forest, cu
     const uint64_t base = c->slab.base;
     mark(c, "repair_diagram", s);
     uint64_t* status_ess = reinterpret_cast<uint64_t*>(c->ws + c->L.status_ess);
-    mt::launch_repair_diagram(cells_of(c), T - base, c->f - base, base, c->n, ctr, status, status_ess, out, cap, ess,
+    mt::launch_repair_diagram(cells_of(c), T - base, c->f - base, base, c->n, c->flip, ctr, status, status_ess, out,
+                              cap, ess,
                               c->L.ess_cap, stats_of(c), forest, s);
     mark(c, "finish_diagram", s);
     mt::launch_finish_diagram(ctr, out, cap, ess, c->L.ess_cap, s);

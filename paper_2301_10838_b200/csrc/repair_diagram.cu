@@ -61,6 +61,7 @@ constexpr uint64_t ST_AGG = 1ull << 62, ST_PRE = 2ull << 62, ST_VAL = (1ull << 6
 template <class View>
 __global__ void __launch_bounds__(THREADS)
 repair_diagram_kernel(View view, Cell* C, uint64_t* __restrict__ T, const float* __restrict__ f, uint64_t base, uint64_t n,
+                      uint32_t flip,
                       unsigned long long* __restrict__ counters, uint64_t* __restrict__ status,
                       uint64_t* __restrict__ status_ess,
                       mt_pair* __restrict__ out, uint64_t out_cap, mt_pair* __restrict__ ess, uint64_t ess_cap,
@@ -214,9 +215,16 @@ repair_diagram_kernel(View view, Cell* C, uint64_t* __restrict__ T, const float*
         const uint64_t u = base + first + uint64_t(k) * THREADS + threadIdx.x;
         const uint64_t pos = prefix + s_cnt[k * 8 + warp] + __popc(mask[k] & ((1u << lane) - 1u));
         const uint32_t s = cs_of(cell[k]);
-        if (pos < out_cap) out[pos] = mt_pair{uint32_t(u), s, __ldg(f + u), view.value(f, s)};
+        // death value f[s]: the cell carries ord(f[s]); invert it (exact for every value but
+        // zero, whose sign the canonicalisation -0 -> +0 dropped: gather those, reading R14)
+        const uint32_t o = uint32_t(cell[k].lo >> 32) ^ flip;
+        const uint32_t bits = (o & 0x80000000u) ? (o & 0x7fffffffu) : ~o;
+        const float death = bits == 0u ? view.value(f, s) : __uint_as_float(bits);
+        if (pos < out_cap) out[pos] = mt_pair{uint32_t(u), s, __ldg(f + u), death};
         else atomicOr(counters + CTR_ERR, ERR_CAPACITY);
     }
+
+
 }
 
 // Appends the essential classes (already in ascending vertex order) after the
@@ -236,19 +244,20 @@ __global__ void finish_diagram_kernel(unsigned long long* __restrict__ counters,
 
 uint64_t repair_tiles(uint64_t n) { return (n + TILE - 1) / TILE; }
 
-void launch_repair_diagram(Cell* C, uint64_t* T, const float* f, uint64_t base, uint64_t n, unsigned long long* counters,
+void launch_repair_diagram(Cell* C, uint64_t* T, const float* f, uint64_t base, uint64_t n, uint32_t flip,
+                           unsigned long long* counters,
                            uint64_t* status, uint64_t* status_ess, mt_pair* out, uint64_t out_cap, mt_pair* ess,
                            uint64_t ess_cap,
                            unsigned long long* stats, const ForestRef* forest, cudaStream_t stream) {
     const uint64_t ntiles = repair_tiles(n);
     if (ntiles == 0) return;
     if (forest)
-        repair_diagram_kernel<<<uint32_t(ntiles), THREADS, 0, stream>>>(ForestView{*forest, base, n}, C, T, f, base, n,
+        repair_diagram_kernel<<<uint32_t(ntiles), THREADS, 0, stream>>>(ForestView{*forest, base, n}, C, T, f, base, n, flip,
                                                                          counters, status, status_ess, out, out_cap,
                                                                          ess, ess_cap,
                                                                          ntiles, stats);
     else
-        repair_diagram_kernel<<<uint32_t(ntiles), THREADS, 0, stream>>>(LocalView{}, C, T, f, base, n, counters,
+        repair_diagram_kernel<<<uint32_t(ntiles), THREADS, 0, stream>>>(LocalView{}, C, T, f, base, n, flip, counters,
                                                                          status, status_ess, out, out_cap, ess,
                                                                          ess_cap, ntiles,
                                                                          stats);
