@@ -204,7 +204,8 @@ def _ecross(dims):
 
 ALG_BYTES = {
     "tile_tmt": lambda n, rec, ec: 12 * n,                 # read f (4) + write the store (8)
-    "merge_cross": lambda n, rec, ec: 2 * 8 * ec,          # read both end cells of every crossing edge
+    "dedupe_cross": lambda n, rec, ec: 16 * ec,            # read f + basin of both ends of every crossing edge
+    "merge_queue": lambda n, rec, ec: 2 * 8 * ec,          # (lower bound) both end cells of every crossing edge
     "repair_diagram": lambda n, rec, ec: 20 * n + 16 * rec,  # read f (4) + read store (8) + write T (8) + records
     "finish_diagram": lambda n, rec, ec: 0,
 }

@@ -76,9 +76,10 @@ void launch_tile_tmt(const float* f, Cell* C, uint32_t* basin, const Slab& sl, u
 // K3: merge of the tile-crossing grid edges on the global store (merge_cross.cu)
 uint64_t cross_edges(const Slab& sl);
 size_t cross_queue_entry_bytes();
-int launch_merge_cross(Cell* C, const float* f, const uint32_t* basin, const Slab& sl, uint32_t flip, void* queue,
-                       uint64_t cap, unsigned long long* qlen, unsigned long long* fetch, unsigned long long* stats,
-                       int num_sms, cudaStream_t stream);   // returns the kernels launched
+// returns 0 when the slab has a single tile (no crossing edges, no kernel launched)
+int launch_dedupe_cross(const float* f, const uint32_t* basin, const Slab& sl, uint32_t flip, void* queue,
+                        uint64_t cap, unsigned long long* qlen, unsigned long long* stats, int num_sms,
+                        cudaStream_t stream);
 
 // the queue consumer alone (queue entries: {uint64 L, uint32 basin_hi, uint32 basin_lo})
 void launch_merge_queue(Cell* C, const void* queue, uint64_t cap, const unsigned long long* qlen,

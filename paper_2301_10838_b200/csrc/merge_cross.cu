@@ -257,9 +257,9 @@ merge_queue_kernel(Cell* C, const QEntry* __restrict__ q, uint64_t cap, const un
 
 }  // namespace
 
-int launch_merge_cross(Cell* C, const float* f, const uint32_t* basin, const Slab& sl, uint32_t flip, void* queue,
-                       uint64_t cap, unsigned long long* qlen, unsigned long long* fetch, unsigned long long* stats,
-                       int num_sms, cudaStream_t stream) {
+int launch_dedupe_cross(const float* f, const uint32_t* basin, const Slab& sl, uint32_t flip, void* queue,
+                        uint64_t cap, unsigned long long* qlen, unsigned long long* stats, int num_sms,
+                        cudaStream_t stream) {
     CrossGeom g{};
     g.nx = sl.nx;
     g.ny = sl.ny;
@@ -278,8 +278,7 @@ int launch_merge_cross(Cell* C, const float* f, const uint32_t* basin, const Sla
     uint64_t blocks = (total + 255) / 256;
     if (blocks > uint64_t(num_sms) * 32) blocks = uint64_t(num_sms) * 32;
     dedupe_cross_kernel<<<uint32_t(blocks), 256, 0, stream>>>(f, basin, g, flip, q, cap, qlen, stats);
-    launch_merge_queue(C, q, cap, qlen, fetch, stats, num_sms, stream);
-    return 2;
+    return 1;
 }
 
 void launch_merge_queue(Cell* C, const void* queue, uint64_t cap, const unsigned long long* qlen,

@@ -235,9 +235,15 @@ mt_status start_compute(mt_ctx* c, const float* f, uint32_t flags, cudaStream_t 
     uint32_t* basin = reinterpret_cast<uint32_t*>(c->ws + c->L.basin) - c->slab.base;
     mark(c, "tile_tmt", s);
     mt::launch_tile_tmt(fs, cells, basin, c->slab, c->flip, ctr, stats, s);
-    mark(c, "merge_cross", s);
-    const int nl = mt::launch_merge_cross(cells, fs, basin, c->slab, c->flip, c->ws + c->L.queue, c->L.queue_cap,
-                                          ctr + mt::CTR_QLEN, ctr + mt::CTR_QFETCH, stats, c->num_sms, s);
+    mark(c, "dedupe_cross", s);
+    int nl = mt::launch_dedupe_cross(fs, basin, c->slab, c->flip, c->ws + c->L.queue, c->L.queue_cap,
+                                     ctr + mt::CTR_QLEN, stats, c->num_sms, s);
+    if (nl) {
+        mark(c, "merge_queue", s);
+        mt::launch_merge_queue(cells, c->ws + c->L.queue, c->L.queue_cap, ctr + mt::CTR_QLEN, ctr + mt::CTR_QFETCH,
+                               stats, c->num_sms, s);
+        ++nl;
+    }
     c->launches = 1 + nl;
     return MT_OK;
 }
