@@ -192,3 +192,22 @@ def test_persistence_filter(cfg, scale, split):
         want = oracle.filter_by_persistence(po, npo, eps)
         assert a + b == want.size and b == neo
         assert _lib.pairs_to_numpy(rec).tobytes() == want.tobytes()
+
+
+def test_host_pipeline_outputs():
+    """The overlapped host->host pipeline returns, for every field, exactly the oracle's store
+    and diagram (double buffers must not mix steps)."""
+    from paper_2301_10838_b200.pipeline import HostPipeline
+    dims = (48, 40, 36)
+    fs = [fields.white_noise(dims, 50 + i) for i in range(4)]
+    pipe = HostPipeline(dims, 6, device=0)
+    n = int(np.prod(dims))
+    f_hosts = [torch.from_numpy(f).pin_memory() for f in fs]
+    T_hosts = [torch.empty(n, dtype=torch.int64).pin_memory() for _ in fs]
+    rec_hosts = [torch.empty((n // 2 + 2, 4), dtype=torch.int32).pin_memory() for _ in fs]
+    counts = pipe.run(f_hosts, T_hosts, rec_hosts)
+    for f, T, rec, (a, b) in zip(fs, T_hosts, rec_hosts, counts):
+        To, po, npo, neo = oracle.merge_tree(f, dims, 6)
+        assert np.array_equal(T.numpy().view(np.uint64), To)
+        assert (a, b) == (npo, neo)
+        assert rec[: a + b].numpy().view(_lib.PAIR_DTYPE).reshape(-1).tobytes() == po.tobytes()
