@@ -206,7 +206,8 @@ ALG_BYTES = {
     "tile_tmt": lambda n, rec, ec: 12 * n,                 # read f (4) + write the store (8)
     "dedupe_cross": lambda n, rec, ec: 16 * ec,            # read f + basin of both ends of every crossing edge
     "merge_queue": lambda n, rec, ec: 2 * 8 * ec,          # (lower bound) both end cells of every crossing edge
-    "repair_diagram": lambda n, rec, ec: 20 * n + 16 * rec,  # read f (4) + read store (8) + write T (8) + records
+    "repair": lambda n, rec, ec: 16 * n,                   # read the store (8) + write T (8)
+    "diagram": lambda n, rec, ec: 4 * n + 16 * rec,        # one 4-B word per vertex to find the minima + records
     "finish_diagram": lambda n, rec, ec: 0,
 }
 

@@ -16,7 +16,8 @@ import os
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-SO_PATH = os.path.join(_PKG, "libmt_b200.so")
+# MT_LIBRARY: load another build of the same ABI (A/B experiments, scripts/ab_build.py)
+SO_PATH = os.environ.get("MT_LIBRARY") or os.path.join(_PKG, "libmt_b200.so")
 
 MT_OK, MT_ERR_INVALID_ARG, MT_ERR_TOO_LARGE, MT_ERR_NONFINITE, MT_ERR_CUDA = 0, 1, 2, 3, 4
 MT_ERR_NCCL, MT_ERR_STATE, MT_ERR_CAPACITY, MT_ERR_WORKSPACE = 5, 6, 7, 8

@@ -125,6 +125,7 @@ enum CounterSlot : int {
     CTR_FCOUNT = 7,     // boundary-forest records of this slab
     CTR_FILT_TICKET = 8,  // mt_filter_diagram: tile tickets
     CTR_FILT_KEPT = 9,    // mt_filter_diagram: records kept
+    CTR_STAGE = 10,       // diagram records staged by the repair bricks
     CTR_COUNT = 16
 };
 

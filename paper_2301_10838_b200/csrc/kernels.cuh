@@ -87,17 +87,26 @@ void launch_merge_queue(Cell* C, const void* queue, uint64_t cap, const unsigned
 
 // explicit graphs in CSR form (graph.cu)
 void launch_graph_init(const float* f, const uint64_t* row, const uint32_t* col, uint32_t n, uint32_t flip, Cell* C,
-                       unsigned long long* counters, int num_sms, cudaStream_t stream);
+                       uint32_t* basin, unsigned long long* counters, int num_sms, cudaStream_t stream);
 void launch_graph_edges(const uint64_t* row, const uint32_t* col, uint32_t n, Cell* C, uint32_t* basin, void* queue,
                         uint64_t cap, unsigned long long* qlen, int num_sms, cudaStream_t stream);
 
-// K4+K5: repair fused with the ordered diagram compaction (repair_diagram.cu)
-uint64_t repair_tiles(uint64_t n);
-void launch_repair_diagram(Cell* C, uint64_t* T, const float* f, uint64_t base, uint64_t n, uint32_t flip,
-                           unsigned long long* counters,
-                           uint64_t* status, uint64_t* status_ess, mt_pair* out, uint64_t out_cap, mt_pair* ess,
-                           uint64_t ess_cap,
-                           unsigned long long* stats, const ForestRef* forest, cudaStream_t stream);
+// K4: repair (memoised walks per brick, diagram records staged per segment)
+// and K5: the ordered diagram (repair_diagram.cu)
+struct RepairOut {
+    mt_pair* stage;                 // staging runs of the bricks' diagram records
+    uint64_t stage_cap;
+    uint16_t* seg_cnt;              // per segment (<= 32 consecutive ids): finite | essential << 8
+    uint32_t* seg_pos;              // per segment: first staged record
+    unsigned long long* counters;
+};
+uint64_t repair_segments(const Slab& sl);     // segments of the slab
+uint64_t repair_segments_bound(uint64_t n);   // >= repair_segments of any slab of n vertices
+uint64_t diagram_tiles(uint64_t nseg);        // diagram tiles; one 16-B status record each
+void launch_repair(const Cell* C, uint64_t* T, const float* f, const Slab& sl, uint32_t flip, const RepairOut& o,
+                   unsigned long long* stats, const ForestRef* forest, cudaStream_t stream);
+void launch_diagram(const Slab& sl, const RepairOut& o, void* status, mt_pair* out, uint64_t out_cap, mt_pair* ess,
+                    uint64_t ess_cap, cudaStream_t stream);
 void launch_finish_diagram(unsigned long long* counters, mt_pair* out, uint64_t out_cap, mt_pair* ess,
                            uint64_t ess_cap, cudaStream_t stream);
 

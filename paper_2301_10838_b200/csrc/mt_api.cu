@@ -6,6 +6,7 @@
 //   -> K4+K5 repair_diagram -> finish_diagram
 // All launches are asynchronous on the caller's stream; only mt_diagram /
 // mt_diagram_view / mt_last_error synchronise.
+#include <algorithm>
 #include <cstdio>
 #include <cstring>
 #include <new>
@@ -23,8 +24,9 @@ constexpr int MAX_EVENTS = 12;
 size_t align_up(size_t x) { return (x + ALIGN - 1) / ALIGN * ALIGN; }
 
 struct Layout {
-    size_t counters, status, status_ess, stats, ess, cells, basin, queue, pairs, flags, recs, total;
-    uint64_t ntiles, pairs_cap, recs_cap, queue_cap, ess_cap;
+    size_t counters, status, status_bytes, stats, ess, cells, basin, queue, pairs, stage, seg_cnt, seg_pos, flags, recs,
+        total;
+    uint64_t pairs_cap, recs_cap, queue_cap, ess_cap, seg_cap;
 };
 
 bool valid_dims(const uint32_t dims[3], int conn) {
@@ -38,17 +40,18 @@ bool valid_dims(const uint32_t dims[3], int conn) {
 // slab: add the boundary-forest buffers
 Layout layout_for(uint64_t n, uint64_t ncross, bool slab = false, uint64_t ess_cap = ESS_CAP) {
     Layout L{};
-    L.ntiles = n ? mt::repair_tiles(n) : 0;
     // records = #minima.  On a grid the strict minima form an independent set,
     // so at most ceil(n/2) (+1 slack); a general graph (ess_cap = n) may have n.
     L.pairs_cap = n ? (ess_cap >= n ? n : (n + 1) / 2 + 1) : 0;
+    L.seg_cap = n ? mt::repair_segments_bound(n) : 0;
+    // tile records of the diagram compaction (16 B) / of mt_filter_diagram (8 B)
+    L.status_bytes = std::max(mt::diagram_tiles(L.seg_cap) * sizeof(mt::Cell),
+                              mt::filter_tiles(L.pairs_cap + ess_cap) * sizeof(uint64_t));
     size_t off = 0;
     L.counters = off;
     off += align_up(mt::CTR_COUNT * sizeof(uint64_t));
-    L.status = off;  // contiguous with counters: one memset zeroes both status arrays too
-    off += L.ntiles * sizeof(uint64_t);
-    L.status_ess = off;
-    off = align_up(off + L.ntiles * sizeof(uint64_t));
+    L.status = off;  // contiguous with counters: one memset zeroes the chunk status records too
+    off = align_up(off + L.status_bytes);
     L.stats = off;
     off += align_up(mt::ST_COUNT * sizeof(uint64_t));
     L.ess = off;
@@ -63,6 +66,12 @@ Layout layout_for(uint64_t n, uint64_t ncross, bool slab = false, uint64_t ess_c
     off += align_up(ncross * mt::cross_queue_entry_bytes());
     L.pairs = off;
     off += align_up(L.pairs_cap * sizeof(mt_pair));
+    L.stage = off;    // diagram records staged by the repair (at most one per minimum)
+    off += align_up(L.pairs_cap * sizeof(mt_pair));
+    L.seg_cnt = off;
+    off += align_up(L.seg_cap * sizeof(uint16_t));
+    L.seg_pos = off;
+    off += align_up(L.seg_cap * sizeof(uint32_t));
     if (slab) {  // boundary forest of the slab: a flag per vertex, at most n records
         L.flags = off;
         off += align_up(n);
@@ -229,7 +238,7 @@ mt_status start_compute(mt_ctx* c, const float* f, uint32_t flags, cudaStream_t 
     if (stats && cudaMemsetAsync(stats, 0, mt::ST_COUNT * sizeof(uint64_t), s) != cudaSuccess)
         return c->sticky = MT_ERR_CUDA;
     mark(c, "zero", s);
-    if (cudaMemsetAsync(c->ws + c->L.counters, 0, c->L.status_ess - c->L.counters + c->L.ntiles * sizeof(uint64_t),
+    if (cudaMemsetAsync(c->ws + c->L.counters, 0, c->L.status - c->L.counters + c->L.status_bytes,
                         s) != cudaSuccess)
         return c->sticky = MT_ERR_CUDA;
     uint32_t* basin = reinterpret_cast<uint32_t*>(c->ws + c->L.basin) - c->slab.base;
@@ -254,17 +263,18 @@ mt_status finish_compute(mt_ctx* c, uint64_t* T, const mt::ForestRef* forest, cu
     uint64_t cap = 0;
     mt_pair* out = target_of(c, &cap);
     mt_pair* ess = reinterpret_cast<mt_pair*>(c->ws + c->L.ess);
-    uint64_t* status = reinterpret_cast<uint64_t*>(c->ws + c->L.status);
     const uint64_t base = c->slab.base;
-    mark(c, "repair_diagram", s);
-    uint64_t* status_ess = reinterpret_cast<uint64_t*>(c->ws + c->L.status_ess);
-    mt::launch_repair_diagram(cells_of(c), T - base, c->f - base, base, c->n, c->flip, ctr, status, status_ess, out,
-                              cap, ess,
-                              c->L.ess_cap, stats_of(c), forest, s);
+    const mt::RepairOut ro{reinterpret_cast<mt_pair*>(c->ws + c->L.stage), c->L.pairs_cap,
+                           reinterpret_cast<uint16_t*>(c->ws + c->L.seg_cnt),
+                           reinterpret_cast<uint32_t*>(c->ws + c->L.seg_pos), ctr};
+    mark(c, "repair", s);
+    mt::launch_repair(cells_of(c), T - base, c->f - base, c->slab, c->flip, ro, stats_of(c), forest, s);
+    mark(c, "diagram", s);
+    mt::launch_diagram(c->slab, ro, c->ws + c->L.status, out, cap, ess, c->L.ess_cap, s);
     mark(c, "finish_diagram", s);
     mt::launch_finish_diagram(ctr, out, cap, ess, c->L.ess_cap, s);
     if (c->profiling) cudaEventRecord(c->ev[c->nev], s);
-    c->launches += 2;
+    c->launches += 3;
     if (cudaGetLastError() != cudaSuccess) return c->sticky = MT_ERR_CUDA;
     return MT_OK;
 }
@@ -362,11 +372,12 @@ mt_status mt_compute_graph(mt_ctx* c, const float* f, const uint64_t* row, const
     if (stats && cudaMemsetAsync(stats, 0, mt::ST_COUNT * sizeof(uint64_t), s) != cudaSuccess)
         return c->sticky = MT_ERR_CUDA;
     mark(c, "zero", s);
-    if (cudaMemsetAsync(c->ws + c->L.counters, 0, c->L.status_ess - c->L.counters + c->L.ntiles * sizeof(uint64_t),
+    if (cudaMemsetAsync(c->ws + c->L.counters, 0, c->L.status - c->L.counters + c->L.status_bytes,
                         s) != cudaSuccess)
         return c->sticky = MT_ERR_CUDA;
     mark(c, "graph_init", s);
-    mt::launch_graph_init(f, row, col, uint32_t(c->n), c->flip, cells, ctr, c->num_sms, s);
+    mt::launch_graph_init(f, row, col, uint32_t(c->n), c->flip, cells, reinterpret_cast<uint32_t*>(c->ws + c->L.basin),
+                          ctr, c->num_sms, s);
     mark(c, "graph_edges", s);
     mt::launch_graph_edges(row, col, uint32_t(c->n), cells, nullptr, c->ws + c->L.queue, c->L.queue_cap,
                            ctr + mt::CTR_QLEN, c->num_sms, s);
@@ -537,7 +548,7 @@ mt_status mt_filter_diagram(mt_ctx* c, float eps, mt_pair* out, uint64_t capacit
         if (out == src) return MT_ERR_INVALID_ARG;  // not in place
         unsigned long long* ctl = counters_of(c) + mt::CTR_FILT_TICKET;
         uint64_t* status = reinterpret_cast<uint64_t*>(c->ws + c->L.status);  // free after the repair
-        if (mt::filter_tiles(n_all) > c->L.ntiles) return MT_ERR_STATE;
+        if (mt::filter_tiles(n_all) * sizeof(uint64_t) > c->L.status_bytes) return MT_ERR_STATE;
         if (cudaMemsetAsync(ctl, 0, 2 * sizeof(uint64_t), s) != cudaSuccess ||
             cudaMemsetAsync(status, 0, mt::filter_tiles(n_all) * sizeof(uint64_t), s) != cudaSuccess)
             return MT_ERR_CUDA;

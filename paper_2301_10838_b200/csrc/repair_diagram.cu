@@ -1,22 +1,30 @@
-// repair_diagram.cu -- K4 + K5: the repair phase of Alg. 1 (lines 9-11,
+// repair_diagram.cu -- K4: the repair phase of Alg. 1 (lines 9-11,
 // PAPER.md:255-257; Alg. 5 "Repair", with Alg. 4
-// "Representative") fused with the ordered extraction of the
+// "Representative") and K5: the ordered extraction of the
 // 0-dimensional persistence diagram (one point (f(a), f(b))
 // per branch).
 //
-// Repair: T[u] = (s, v) becomes (s, Rep(u, key(s))), Rep following cells while
-// key(s') <= key(s) and the cell is not a root.  Reading R20: the walk returns
-// the vertex it stopped at (Alg. 4 as printed returns the next, too-deep v).
-// The walks only read the working cells (the repaired pointer goes to T), so
-// they see the fixed post-merge store.
+// Repair (repair_brick_kernel): T[u] = (s, v) becomes (s, Rep(u, key(s))), Rep
+// following cells while key(s') <= key(s) and the cell is not a root.
+// Reading R20: the walk returns the vertex it stopped at (Alg. 4 as printed
+// returns the next, too-deep v).  The walks only read the working cells (the
+// repaired pointer goes to T), so they see the fixed post-merge store.
+//   Many vertices of a brick of the grid start their walk at the same v (the
+// tile-local representative): the brick collects its distinct start vertices
+// in a shared-memory hash set, walks each one's chain of cells ONCE -- up to
+// the largest threshold key(s) among the vertices that start there -- into a
+// shared-memory pool, and resolves every vertex's walk from that pool
+// (derivation I).  The memo changes which loads are issued, never what a walk
+// computes: a chain entry is exactly the cell the walk would have read.
 //
 // Diagram: after the merge phase the s fields are final (repair only rewrites
-// v), so a cell with s != u is the branch born at u dying at saddle s (finite
-// pair), and a root (u, u, u) is an essential class.  The
-// finite pairs are written in ascending u with a single-pass ordered
-// compaction: warp ballots + a CTA scan give each tile's count, published
-// BEFORE the tile does its repair walks, and a decoupled look-back over the
-// predecessors' published counts gives the tile's output offset.  Tiles take
+// v).  A cell with s != u is the branch born at u dying at saddle s (finite
+// pair) and a root (u, u, u) is an essential class.  The
+// repair bricks, which read every cell anyway, stage these records per
+// segment (a brick row: <= 32 consecutive ids) with the segment's counts;
+// diagram_kernel then walks the segments in id order and places the records
+// with a single-pass ordered compaction (CTA scan + decoupled look-back over
+// 16-B tile records), so the pairs come out in ascending u.  Tiles take
 // dynamic ticket numbers so every predecessor is already resident.
 #include "common.cuh"
 #include "kernels.cuh"
@@ -53,178 +61,390 @@ struct ForestView {
     }
 };
 
-constexpr int THREADS = 256;
-constexpr int ITEMS = 4;
-constexpr int TILE = THREADS * ITEMS;  // 1024 vertices per ticket
-constexpr uint64_t ST_AGG = 1ull << 62, ST_PRE = 2ull << 62, ST_VAL = (1ull << 62) - 1;
+// bit pattern of the float whose order key is o (inverse of ord32 for every value but -0)
+__device__ __forceinline__ uint32_t inv_ord(uint32_t o) { return (o & 0x80000000u) ? (o & 0x7fffffffu) : ~o; }
 
-template <class View>
-__global__ void __launch_bounds__(THREADS)
-repair_diagram_kernel(View view, Cell* C, uint64_t* __restrict__ T, const float* __restrict__ f, uint64_t base, uint64_t n,
-                      uint32_t flip,
-                      unsigned long long* __restrict__ counters, uint64_t* __restrict__ status,
-                      uint64_t* __restrict__ status_ess,
-                      mt_pair* __restrict__ out, uint64_t out_cap, mt_pair* __restrict__ ess, uint64_t ess_cap,
-                      uint64_t ntiles, unsigned long long* __restrict__ stats) {
-    __shared__ uint64_t s_tile;
-    __shared__ uint32_t s_cnt[ITEMS * 8], s_ecnt[ITEMS * 8];
-    __shared__ uint64_t s_prefix, s_eprefix;
+// ============================ K4: repair ====================================
+// Brick of 32 x BY x BZ vertices (BY * BZ = RB_ROWS rows of 32), one CTA of
+// RB_THREADS; each warp owns RB_ROWS / 16 rows (lane = x).  LINEAR bricks are
+// 4096 consecutive ids instead (graphs, thin grids).  A row of a brick is a
+// "segment" of at most 32 consecutive ids; segments are numbered in id order.
+constexpr int RB_THREADS = 512;
+constexpr int RB_ROWS = 128;
+constexpr int RB_PER = RB_ROWS / (RB_THREADS / 32);   // rows (vertices) per thread
+constexpr int RB_NV = RB_ROWS * 32;
+constexpr int RB_HASH = RB_NV;         // >= vertices per brick: an insertion always finds its slot
+constexpr int RB_POOL = 2048;          // chain entries per brick (overflow: plain walks)
+constexpr uint32_t RB_EMPTY = 0xffffffffu;
+constexpr uint16_t RB_NIL = 0xffffu;
+constexpr uint64_t KEY_ROOT = ~0ull;   // chain entry of a root: stops every walk
+
+struct RepairSmem {
+    unsigned long long pkey[RB_POOL];  // chain entry: key(s_x) of the cell of x (KEY_ROOT: root) ...
+    uint32_t hkey[RB_HASH];            // start vertex v (RB_EMPTY: free slot)
+    uint32_t hmax[RB_HASH];            // largest ord(f[s]) among the vertices starting there
+    uint32_t px[RB_POOL];              // ... and its v (the next vertex of the walk)
+    uint16_t hhead[RB_HASH];           // first chain entry of the slot
+    uint16_t plink[RB_POOL];           // next chain entry
+    uint16_t list[RB_HASH];            // occupied slots
+    uint32_t rowcnt[RB_ROWS];          // finite | essential << 16 records of each row
+    uint32_t rowoff[RB_ROWS];          // their offset in the brick's staging run
+    uint64_t rowbase[RB_ROWS];         // first id of each row
+    uint64_t rowseg[RB_ROWS];          // its segment number
+    uint32_t rowlim[RB_ROWS];          // lanes of the row inside the grid
+    uint32_t rowfm[RB_ROWS], rowem[RB_ROWS];   // lanes holding a finite pair / a root
+    uint16_t slot[RB_PER][RB_THREADS];  // per vertex: hash slot of its start vertex (RB_NIL: none)
+    uint32_t nslots, ptop, base;
+};
+
+__device__ __forceinline__ uint32_t rb_hash(uint32_t v) {
+    v ^= v >> 16;
+    v *= 0x7feb352du;
+    v ^= v >> 15;
+    return v & (RB_HASH - 1);
+}
+
+struct BrickGeom {
+    uint32_t by, bx_n, by_n;   // brick rows along y; bricks along x and y (brick mode)
+};
+
+template <class View, bool LINEAR>
+__global__ void __launch_bounds__(RB_THREADS, 2)
+repair_brick_kernel(View view, const Cell* C, uint64_t* __restrict__ T, const float* __restrict__ f, Slab sl,
+                    BrickGeom g, uint32_t flip, mt_pair* __restrict__ stage, uint64_t stage_cap,
+                    uint16_t* __restrict__ seg_cnt, uint32_t* __restrict__ seg_pos,
+                    unsigned long long* __restrict__ counters, unsigned long long* __restrict__ stats) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    RepairSmem& S = *reinterpret_cast<RepairSmem*>(smem_raw);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    if (threadIdx.x == 0) s_tile = atomicAdd(counters + CTR_TICKET, 1ull);
-    __syncthreads();
-    const uint64_t tile = s_tile;
-    const uint64_t first = tile * TILE;  // local index of the tile's first vertex
+    const uint32_t lt = (1u << lane) - 1u;
+    for (int i = threadIdx.x; i < RB_HASH; i += RB_THREADS) {
+        S.hkey[i] = RB_EMPTY;
+        S.hmax[i] = 0;
+        S.hhead[i] = RB_NIL;
+    }
+    if (threadIdx.x == 0) S.nslots = S.ptop = 0;
 
-    Cell cell[ITEMS];
-    bool fin[ITEMS], root[ITEMS];
-    uint32_t mask[ITEMS], emask[ITEMS];
+    // brick origin and the id-order number of its first segment
+    uint64_t u0 = 0, seg0 = 0;
+    uint32_t x0 = 0, y0 = 0, z0 = 0, bxi = 0;
+    if (LINEAR) {
+        u0 = uint64_t(blockIdx.x) * RB_NV;
+        seg0 = uint64_t(blockIdx.x) * RB_ROWS;
+    } else {
+        const uint32_t b = blockIdx.x;
+        bxi = b % g.bx_n;
+        x0 = bxi * 32;
+        y0 = ((b / g.bx_n) % g.by_n) * g.by;
+        z0 = sl.z_begin + (b / g.bx_n / g.by_n) * (RB_ROWS / g.by);
+    }
+    // the warp's rows (item k = row warp + 16 k): first id, valid lanes and segment number, computed
+    // once by lanes 0..RB_PER-1 (integer divisions) and read back from shared memory
+    if (lane < RB_PER) {
+        const uint32_t r = uint32_t(warp + 16 * lane);
+        uint64_t rb, seg;
+        uint32_t lim;
+        if (LINEAR) {
+            rb = sl.base + u0 + uint64_t(r) * 32;
+            const uint64_t left = u0 + uint64_t(r) * 32 < sl.n ? sl.n - (u0 + uint64_t(r) * 32) : 0;
+            lim = left > 32 ? 32u : uint32_t(left);
+            seg = seg0 + r;
+        } else {
+            const uint32_t y = y0 + r % g.by, z = z0 + r / g.by;
+            rb = (uint64_t(z) * sl.ny + y) * sl.nx + x0;
+            lim = (y < sl.ny && z < sl.z_end) ? min(32u, sl.nx - x0) : 0u;
+            seg = (uint64_t(z - sl.z_begin) * sl.ny + y) * g.bx_n + bxi;
+        }
+        S.rowbase[r] = rb;
+        S.rowseg[r] = seg;
+        S.rowlim[r] = lim;
+    }
+    __syncwarp();
+    uint32_t inb = 0;
 #pragma unroll
-    for (int k = 0; k < ITEMS; ++k) {
-        const uint64_t l = first + uint64_t(k) * THREADS + threadIdx.x;
-        const uint64_t u = base + l;     // global id (C, T, f are indexed by global id)
-        cell[k] = l < n ? ld_cell(C + u) : Cell{0, 0};
-        fin[k] = l < n && cs_of(cell[k]) != uint32_t(u);
-        root[k] = l < n && cv_of(cell[k]) == uint32_t(u);   // (u, u, u): an essential class
-        mask[k] = __ballot_sync(FULL_MASK, fin[k]);
-        emask[k] = __ballot_sync(FULL_MASK, root[k]);
+    for (int k = 0; k < RB_PER; ++k) inb |= uint32_t(uint32_t(lane) < S.rowlim[warp + 16 * k]) << k;
+#define UID(k) (S.rowbase[warp + 16 * (k)] + lane)
+#define INB(k) ((inb >> (k)) & 1u)
+    Cell cell[RB_PER];
+#pragma unroll
+    for (int k = 0; k < RB_PER; ++k) cell[k] = INB(k) ? ld_cell(C + UID(k)) : Cell{0, 0};
+    // diagram records of each row: finite pairs (s != u) and roots (v == u)
+#define FMASK(k) __ballot_sync(FULL_MASK, INB(k) && cs_of(cell[k]) != uint32_t(UID(k)))
+#define EMASK(k) __ballot_sync(FULL_MASK, INB(k) && cv_of(cell[k]) == uint32_t(UID(k)))
+#pragma unroll
+    for (int k = 0; k < RB_PER; ++k) {
+        const uint32_t fm = FMASK(k), em = EMASK(k);
         if (lane == 0) {
-            s_cnt[k * 8 + warp] = __popc(mask[k]);
-            s_ecnt[k * 8 + warp] = __popc(emask[k]);
+            S.rowcnt[warp + 16 * k] = __popc(fm) | (__popc(em) << 16);
+            S.rowfm[warp + 16 * k] = fm;
+            S.rowem[warp + 16 * k] = em;
         }
     }
-    __syncthreads();
-    // exclusive scans of the 32 (k, warp) counts in u order: finite pairs by
-    // warp 0, essential classes by warp 1; each publishes the tile's count
-    // before the walks
-    if (warp < 2) {
-        uint32_t* cnt = warp == 0 ? s_cnt : s_ecnt;
-        uint64_t* st = warp == 0 ? status : status_ess;
-        const uint32_t c = cnt[lane];
-        uint32_t incl = c;
+    __syncthreads();   // hash set initialised, row counts in
+
+    // warp 0: the brick's staging run (one global atomic) and each row's offset in it
+    if (warp == 0) {
+        uint32_t c[RB_ROWS / 32], tot = 0;
+#pragma unroll
+        for (int j = 0; j < RB_ROWS / 32; ++j) {
+            const uint32_t rc = S.rowcnt[lane * (RB_ROWS / 32) + j];
+            c[j] = (rc & 0xffffu) + (rc >> 16);
+            tot += c[j];
+        }
+        uint32_t incl = tot;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
             const uint32_t t = __shfl_up_sync(FULL_MASK, incl, o);
             if (lane >= o) incl += t;
         }
-        cnt[lane] = incl - c;
-        const uint32_t agg = __shfl_sync(FULL_MASK, incl, 31);
-        if (lane == 0) st_relaxed(st + tile, (tile == 0 ? ST_PRE : ST_AGG) | agg);
+        uint32_t off = incl - tot;
+#pragma unroll
+        for (int j = 0; j < RB_ROWS / 32; ++j) {
+            S.rowoff[lane * (RB_ROWS / 32) + j] = off;
+            off += c[j];
+        }
+        const uint32_t all = __shfl_sync(FULL_MASK, incl, 31);
+        uint32_t base = 0;
+        if (lane == 0 && all) base = uint32_t(atomicAdd(counters + CTR_STAGE, (unsigned long long)all));
+        if (lane == 0) S.base = base;
     }
 
-    // --- repair (Alg. 5 with Alg. 4's walk) ------------------------------
-    // The ITEMS walks of a thread advance together, one hop each per round,
-    // so up to ITEMS independent cell loads are in flight per thread.
-    unsigned long long hops = 0;
-    uint32_t x[ITEMS];
-    uint32_t active = 0;
+    // distinct start vertices: one insertion per group of lanes sharing v (warp-aggregated),
+    // threshold = the group's largest ord(f[s])
+    uint64_t key[RB_PER];     // threshold key(s)
+    uint32_t sv[RB_PER];      // s of the vertex
 #pragma unroll
-    for (int k = 0; k < ITEMS; ++k) {
-        const uint64_t l = first + uint64_t(k) * THREADS + threadIdx.x;
-        const uint64_t u = base + l;
-        x[k] = cv_of(cell[k]);
-        if (l >= n) continue;
-        if (root[k]) {                                // root (u, u, u): written with the diagram below
+    for (int k = 0; k < RB_PER; ++k) {
+        key[k] = cell[k].lo;
+        sv[k] = cs_of(cell[k]);
+        const uint32_t v = cv_of(cell[k]);
+        const bool walk = INB(k) && v != uint32_t(UID(k));
+        const uint32_t wv = walk ? v : RB_EMPTY;
+        const uint32_t peers = __match_any_sync(FULL_MASK, wv);
+        const int leader = __ffs(peers) - 1;
+        const uint32_t m = __reduce_max_sync(peers, uint32_t(key[k] >> 32));
+        uint32_t h = 0;
+        if (walk && lane == leader) {
+            h = rb_hash(v);
+            while (true) {
+                const uint32_t old = atomicCAS(&S.hkey[h], RB_EMPTY, v);
+                if (old == RB_EMPTY) {
+                    S.list[atomicAdd(&S.nslots, 1u)] = uint16_t(h);
+                    break;
+                }
+                if (old == v) break;
+                h = (h + 1) & (RB_HASH - 1);
+            }
+            atomicMax(&S.hmax[h], m);
+        }
+        h = __shfl_sync(FULL_MASK, h, leader);
+        S.slot[k][threadIdx.x] = walk ? uint16_t(h) : RB_NIL;   // hash slot of its start vertex
+    }
+    __syncthreads();
+
+    // staging records of every row, in id order within the row: finite pairs, then roots
+    const uint32_t sbase = S.base;
+#pragma unroll
+    for (int k = 0; k < RB_PER; ++k) {
+        const int r = warp + 16 * k;
+        const uint32_t fm = S.rowfm[r], em = S.rowem[r];
+        const bool isf = (fm >> lane) & 1u, ise = (em >> lane) & 1u;
+        if (lane == 0 && INB(k)) {
+            // every row holding a vertex of the grid is a segment (lane 0 is its first vertex)
+            const uint64_t seg = S.rowseg[r];
+            seg_cnt[seg] = uint16_t(S.rowcnt[r] & 0xffffu) | uint16_t((S.rowcnt[r] >> 16) << 8);
+            seg_pos[seg] = sbase + S.rowoff[r];
+        }
+        if (!(isf || ise)) continue;
+        const uint64_t u = UID(k);
+        const uint64_t pos = uint64_t(sbase) + S.rowoff[r] +
+                             (isf ? __popc(fm & lt) : __popc(fm) + __popc(em & lt));
+        mt_pair rec;
+        if (isf) {
+            const uint32_t s = cs_of(cell[k]);
+            // values f[u] and f[s]: the cell carries ord(f[u]) (hi) and ord(f[s]) (lo); invert
+            // them (exact for every value but zero, whose sign the canonicalisation -0 -> +0
+            // dropped: gather those, reading R14)
+            const uint32_t bb = inv_ord(uint32_t(cell[k].hi >> 32) ^ flip);
+            const uint32_t db = inv_ord(uint32_t(cell[k].lo >> 32) ^ flip);
+            rec = mt_pair{uint32_t(u), s, bb == 0u ? __ldg(f + u) : __uint_as_float(bb),
+                          db == 0u ? view.value(f, s) : __uint_as_float(db)};
+        } else {
+            rec = mt_pair{uint32_t(u), uint32_t(u), __ldg(f + u), __int_as_float(0x7f800000)};
+        }
+        if (pos < stage_cap) stage[pos] = rec;
+        else atomicOr(counters + CTR_ERR, ERR_CAPACITY);
+    }
+
+    // one walk per distinct start vertex, recorded up to its largest threshold
+    unsigned long long hops = 0;
+    const uint32_t nslots = S.nslots;
+    for (uint32_t i = threadIdx.x; i < nslots; i += RB_THREADS) {
+        const uint32_t h = S.list[i];
+        const uint32_t omax = S.hmax[h];
+        uint32_t x = S.hkey[h];
+        uint16_t prev = RB_NIL;
+        while (true) {
+            const Cell c = view.cell(C, x);
+            const uint32_t nx = cv_of(c);
+            const uint64_t k = nx == x ? KEY_ROOT : c.lo;
+            const uint32_t e = atomicAdd(&S.ptop, 1u);
+            if (e >= RB_POOL) break;              // pool full: the chain ends here, users walk on
+            S.pkey[e] = k;
+            S.px[e] = nx;
+            S.plink[e] = RB_NIL;
+            if (prev == RB_NIL) S.hhead[h] = uint16_t(e);
+            else S.plink[prev] = uint16_t(e);
+            prev = uint16_t(e);
+            if (uint32_t(k >> 32) > omax || k == KEY_ROOT) break;   // k > every threshold of the slot
+            x = nx;
+            ++hops;
+        }
+    }
+    __syncthreads();
+
+    // resolve each vertex's walk: Rep(u, key(s)) from the chain of its start vertex
+#pragma unroll
+    for (int k = 0; k < RB_PER; ++k) {
+        if (!INB(k)) continue;
+        const uint64_t u = UID(k);
+        const uint16_t slot = S.slot[k][threadIdx.x];
+        if (slot == RB_NIL) {
             T[u] = pack(uint32_t(u), uint32_t(u));
             continue;
         }
-        active |= 1u << k;
-    }
-    const uint32_t todo = active;
-    while (active) {
-        Cell c[ITEMS];
-#pragma unroll
-        for (int k = 0; k < ITEMS; ++k)
-            if (active & (1u << k)) c[k] = view.cell(C, x[k]);
-#pragma unroll
-        for (int k = 0; k < ITEMS; ++k) {
-            if (!(active & (1u << k))) continue;
-            if (cv_of(c[k]) == x[k] || c[k].lo > cell[k].lo) {   // root, or key(s_x) > key(s): Rep(u, key(s))
-                active &= ~(1u << k);
-            } else {
-                x[k] = cv_of(c[k]);
+        const uint64_t a = key[k];
+        uint32_t x = S.hkey[slot];
+        uint16_t e = S.hhead[slot];
+        bool done = false;
+        while (e != RB_NIL) {
+            if (S.pkey[e] > a) {
+                done = true;
+                break;
+            }
+            x = S.px[e];
+            e = S.plink[e];
+        }
+        if (!done) {                              // truncated chain: the plain walk from x
+            while (true) {
+                const Cell c = view.cell(C, x);
+                if (cv_of(c) == x || c.lo > a) break;
+                x = cv_of(c);
                 ++hops;
             }
         }
+        T[u] = pack(sv[k], x);
     }
-#pragma unroll
-    for (int k = 0; k < ITEMS; ++k) {
-        if (!(todo & (1u << k))) continue;
-        const uint64_t u = base + first + uint64_t(k) * THREADS + threadIdx.x;
-        // (no in-place shortcut of the working cell: the 4-B partial write would dirty a
-        // 32-B sector per vertex -- ~17 GB of write-back at 1024^3 for walks of ~2.5 hops)
-        T[u] = pack(cs_of(cell[k]), x[k]);
-    }
-    if (stats) atomicAdd(stats + ST_REPAIR_HOPS, hops);
+    if (stats && hops) atomicAdd(stats + ST_REPAIR_HOPS, hops);
+#undef UID
+#undef INB
+#undef FMASK
+#undef EMASK
+}
 
-    // --- decoupled look-backs for the tile's output offsets --------------
+// ============================ K5: diagram ===================================
+// One thread per segment, segments in id order: the counts give each record's
+// place in the diagram (ordered compaction: CTA scan + decoupled look-back);
+// the records are copied from the staging runs the repair wrote.
+constexpr int THREADS = 256;
+constexpr uint64_t ST_AGG = 1ull << 62, ST_PRE = 2ull << 62, ST_VAL = (1ull << 62) - 1;
+
+__global__ void __launch_bounds__(THREADS)
+diagram_kernel(const uint16_t* __restrict__ seg_cnt, const uint32_t* __restrict__ seg_pos, uint64_t nseg,
+               const mt_pair* __restrict__ stage, unsigned long long* __restrict__ counters, Cell* __restrict__ status,
+               mt_pair* __restrict__ out, uint64_t out_cap, mt_pair* __restrict__ ess, uint64_t ess_cap,
+               uint64_t ntiles) {
+    __shared__ uint64_t s_tile;
+    __shared__ uint32_t s_w[THREADS / 32], s_we[THREADS / 32];
+    __shared__ uint64_t s_prefix, s_eprefix;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (threadIdx.x == 0) s_tile = atomicAdd(counters + CTR_TICKET, 1ull);
     __syncthreads();
-    if (warp < 2) {
-        uint64_t* stat = warp == 0 ? status : status_ess;
-        uint64_t prefix = 0;
+    const uint64_t tile = s_tile;
+    const uint64_t seg = tile * THREADS + threadIdx.x;
+    const uint32_t cnt = seg < nseg ? seg_cnt[seg] : 0u;
+    const uint32_t cf = cnt & 0xffu, ce = cnt >> 8;
+    // block-wide exclusive scans (finite, essential)
+    uint32_t incl = cf, eincl = ce;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(FULL_MASK, incl, o);
+        const uint32_t te = __shfl_up_sync(FULL_MASK, eincl, o);
+        if (lane >= o) {
+            incl += t;
+            eincl += te;
+        }
+    }
+    if (lane == 31) {
+        s_w[warp] = incl;
+        s_we[warp] = eincl;
+    }
+    __syncthreads();
+    if (warp == 0) {
+        const uint32_t w = lane < THREADS / 32 ? s_w[lane] : 0u, we = lane < THREADS / 32 ? s_we[lane] : 0u;
+        uint32_t wi = w, wei = we;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t t = __shfl_up_sync(FULL_MASK, wi, o);
+            const uint32_t te = __shfl_up_sync(FULL_MASK, wei, o);
+            if (lane >= o) {
+                wi += t;
+                wei += te;
+            }
+        }
+        if (lane < THREADS / 32) {
+            s_w[lane] = wi - w;
+            s_we[lane] = wei - we;
+        }
+        const uint32_t agg = __shfl_sync(FULL_MASK, wi, 31), eagg = __shfl_sync(FULL_MASK, wei, 31);
+        const uint64_t fl = tile == 0 ? ST_PRE : ST_AGG;
+        if (lane == 0) st_cell(status + tile, Cell{fl | agg, fl | eagg});
+        uint64_t prefix = 0, eprefix = 0;
         int64_t j = int64_t(tile) - 1;
         while (j >= 0) {
             const int64_t idx = j - lane;
-            const uint64_t st = idx >= 0 ? ld_relaxed(stat + idx) : ST_PRE;
-            const uint64_t flag = st >> 62;
+            const Cell sv = idx >= 0 ? ld_cell(status + idx) : Cell{ST_PRE, ST_PRE};
+            const uint64_t flag = sv.lo >> 62;
             const uint32_t pmask = __ballot_sync(FULL_MASK, flag == 2);
             const uint32_t xmask = __ballot_sync(FULL_MASK, flag == 0);
             const int first_p = pmask ? __ffs(pmask) - 1 : 31;
             const uint32_t upto = first_p == 31 ? FULL_MASK : ((2u << first_p) - 1u);
             if (xmask & upto) continue;               // a needed predecessor has not published
-            uint64_t val = lane <= first_p ? (st & ST_VAL) : 0;
+            uint64_t val = lane <= first_p ? (sv.lo & ST_VAL) : 0;
+            uint64_t eval = lane <= first_p ? (sv.hi & ST_VAL) : 0;
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) val += __shfl_xor_sync(FULL_MASK, val, o);
+            for (int o = 16; o > 0; o >>= 1) {
+                val += __shfl_xor_sync(FULL_MASK, val, o);
+                eval += __shfl_xor_sync(FULL_MASK, eval, o);
+            }
             prefix += val;
+            eprefix += eval;
             if (pmask) break;
             j -= 32;
         }
-        if (lane == 0) (warp == 0 ? s_prefix : s_eprefix) = prefix;
+        if (lane == 0) {
+            s_prefix = prefix;
+            s_eprefix = eprefix;
+            if (tile != 0) st_cell(status + tile, Cell{ST_PRE | (prefix + agg), ST_PRE | (eprefix + eagg)});
+            if (tile == ntiles - 1) {
+                counters[CTR_FIN] = prefix + agg;
+                counters[CTR_ESS] = eprefix + eagg;
+            }
+        }
     }
     __syncthreads();
-    const uint64_t prefix = s_prefix, eprefix = s_eprefix;
-    // inclusive prefix = prefix + this tile's aggregate; s_cnt holds exclusive
-    // offsets, so the aggregate is the last offset + the last (k, warp) count,
-    // which the last thread's own ballot holds.
-    if (threadIdx.x == THREADS - 1) {
-        const uint64_t total = prefix + s_cnt[(ITEMS - 1) * 8 + 7] + __popc(mask[ITEMS - 1]);
-        const uint64_t etotal = eprefix + s_ecnt[(ITEMS - 1) * 8 + 7] + __popc(emask[ITEMS - 1]);
-        if (tile != 0) {
-            st_relaxed(status + tile, ST_PRE | total);
-            st_relaxed(status_ess + tile, ST_PRE | etotal);
-        }
-        if (tile == ntiles - 1) {
-            counters[CTR_FIN] = total;
-            counters[CTR_ESS] = etotal;
-        }
-    }
-
-    // --- essential classes in ascending u (into the essential buffer) ------
-#pragma unroll
-    for (int k = 0; k < ITEMS; ++k) {
-        if (!root[k]) continue;
-        const uint64_t u = base + first + uint64_t(k) * THREADS + threadIdx.x;
-        const uint64_t pos = eprefix + s_ecnt[k * 8 + warp] + __popc(emask[k] & ((1u << lane) - 1u));
-        if (pos < ess_cap) ess[pos] = mt_pair{uint32_t(u), uint32_t(u), __ldg(f + u), __int_as_float(0x7f800000)};
-        else atomicOr(counters + CTR_ERR, ERR_ESS_CAPACITY);
-    }
-
-    // --- write this tile's finite pairs in ascending u --------------------
-#pragma unroll
-    for (int k = 0; k < ITEMS; ++k) {
-        if (!fin[k]) continue;
-        const uint64_t u = base + first + uint64_t(k) * THREADS + threadIdx.x;
-        const uint64_t pos = prefix + s_cnt[k * 8 + warp] + __popc(mask[k] & ((1u << lane) - 1u));
-        const uint32_t s = cs_of(cell[k]);
-        // death value f[s]: the cell carries ord(f[s]); invert it (exact for every value but
-        // zero, whose sign the canonicalisation -0 -> +0 dropped: gather those, reading R14)
-        const uint32_t o = uint32_t(cell[k].lo >> 32) ^ flip;
-        const uint32_t bits = (o & 0x80000000u) ? (o & 0x7fffffffu) : ~o;
-        const float death = bits == 0u ? view.value(f, s) : __uint_as_float(bits);
-        if (pos < out_cap) out[pos] = mt_pair{uint32_t(u), s, __ldg(f + u), death};
+    if (!(cf | ce)) return;
+    const uint64_t pos = s_prefix + s_w[warp] + incl - cf;
+    const uint64_t epos = s_eprefix + s_we[warp] + eincl - ce;
+    const mt_pair* src = stage + seg_pos[seg];
+    for (uint32_t i = 0; i < cf; ++i) {
+        if (pos + i < out_cap) out[pos + i] = src[i];
         else atomicOr(counters + CTR_ERR, ERR_CAPACITY);
     }
-
-
+    for (uint32_t i = 0; i < ce; ++i) {
+        if (epos + i < ess_cap) ess[epos + i] = src[cf + i];
+        else atomicOr(counters + CTR_ERR, ERR_ESS_CAPACITY);
+    }
 }
 
 // Appends the essential classes (already in ascending vertex order) after the
@@ -240,27 +460,74 @@ __global__ void finish_diagram_kernel(unsigned long long* __restrict__ counters,
     }
 }
 
+template <class View, bool LINEAR>
+void launch_brick(const View& view, const Cell* C, uint64_t* T, const float* f, const Slab& sl, BrickGeom g,
+                  uint64_t nb, uint32_t flip, const RepairOut& o, unsigned long long* stats, cudaStream_t stream) {
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(repair_brick_kernel<View, LINEAR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             int(sizeof(RepairSmem)));
+        attr = true;
+    }
+    repair_brick_kernel<View, LINEAR><<<uint32_t(nb), RB_THREADS, sizeof(RepairSmem), stream>>>(
+        view, C, T, f, sl, g, flip, o.stage, o.stage_cap, o.seg_cnt, o.seg_pos, o.counters, stats);
+}
+
+// brick geometry: 3-D bricks 32 x 16 x 8 on volumes, 32 x 128 on images, id ranges otherwise
+bool brick_mode(const Slab& sl, BrickGeom* g, uint64_t* nb, uint64_t* nseg) {
+    const uint32_t nzl = sl.z_end - sl.z_begin;
+    uint32_t by = 0;
+    if (nzl >= 8 && sl.ny >= 16) by = 16;
+    else if (sl.nz == 1 && sl.ny >= 128) by = 128;
+    if (by && sl.nx >= 32) {
+        const uint32_t bz = RB_ROWS / by;
+        const uint32_t bx_n = (sl.nx + 31) / 32, by_n = (sl.ny + by - 1) / by, bz_n = (nzl + bz - 1) / bz;
+        *g = BrickGeom{by, bx_n, by_n};
+        *nb = uint64_t(bx_n) * by_n * bz_n;
+        *nseg = uint64_t(bx_n) * sl.ny * nzl;
+        return true;
+    }
+    *g = BrickGeom{1, 1, 1};
+    *nb = (sl.n + RB_NV - 1) / RB_NV;
+    *nseg = (sl.n + 31) / 32;
+    return false;
+}
+
+template <class View>
+void launch_repair_view(const View& view, const Cell* C, uint64_t* T, const float* f, const Slab& sl, uint32_t flip,
+                        const RepairOut& o, unsigned long long* stats, cudaStream_t stream) {
+    BrickGeom g;
+    uint64_t nb, nseg;
+    if (brick_mode(sl, &g, &nb, &nseg)) launch_brick<View, false>(view, C, T, f, sl, g, nb, flip, o, stats, stream);
+    else launch_brick<View, true>(view, C, T, f, sl, g, nb, flip, o, stats, stream);
+}
+
 }  // namespace
 
-uint64_t repair_tiles(uint64_t n) { return (n + TILE - 1) / TILE; }
+uint64_t repair_segments(const Slab& sl) {
+    BrickGeom g;
+    uint64_t nb, nseg;
+    brick_mode(sl, &g, &nb, &nseg);
+    return nseg;
+}
+uint64_t repair_segments_bound(uint64_t n) { return n / 16 + 2; }
+uint64_t diagram_tiles(uint64_t nseg) { return (nseg + THREADS - 1) / THREADS; }
 
-void launch_repair_diagram(Cell* C, uint64_t* T, const float* f, uint64_t base, uint64_t n, uint32_t flip,
-                           unsigned long long* counters,
-                           uint64_t* status, uint64_t* status_ess, mt_pair* out, uint64_t out_cap, mt_pair* ess,
-                           uint64_t ess_cap,
-                           unsigned long long* stats, const ForestRef* forest, cudaStream_t stream) {
-    const uint64_t ntiles = repair_tiles(n);
+void launch_repair(const Cell* C, uint64_t* T, const float* f, const Slab& sl, uint32_t flip, const RepairOut& o,
+                   unsigned long long* stats, const ForestRef* forest, cudaStream_t stream) {
+    if (sl.n == 0) return;
+    if (forest) launch_repair_view(ForestView{*forest, sl.base, sl.n}, C, T, f, sl, flip, o, stats, stream);
+    else launch_repair_view(LocalView{}, C, T, f, sl, flip, o, stats, stream);
+}
+
+void launch_diagram(const Slab& sl, const RepairOut& o, void* status, mt_pair* out, uint64_t out_cap, mt_pair* ess,
+                    uint64_t ess_cap, cudaStream_t stream) {
+    const uint64_t nseg = sl.n ? repair_segments(sl) : 0;
+    const uint64_t ntiles = diagram_tiles(nseg);
     if (ntiles == 0) return;
-    if (forest)
-        repair_diagram_kernel<<<uint32_t(ntiles), THREADS, 0, stream>>>(ForestView{*forest, base, n}, C, T, f, base, n, flip,
-                                                                         counters, status, status_ess, out, out_cap,
-                                                                         ess, ess_cap,
-                                                                         ntiles, stats);
-    else
-        repair_diagram_kernel<<<uint32_t(ntiles), THREADS, 0, stream>>>(LocalView{}, C, T, f, base, n, flip, counters,
-                                                                         status, status_ess, out, out_cap, ess,
-                                                                         ess_cap, ntiles,
-                                                                         stats);
+    diagram_kernel<<<uint32_t(ntiles), THREADS, 0, stream>>>(o.seg_cnt, o.seg_pos, nseg, o.stage, o.counters,
+                                                             static_cast<Cell*>(status), out, out_cap, ess, ess_cap,
+                                                             ntiles);
 }
 
 void launch_finish_diagram(unsigned long long* counters, mt_pair* out, uint64_t out_cap, mt_pair* ess,

@@ -7,5 +7,5 @@ timeout 600 python scripts/stats.py c2 c3 c4 c5 > gpurun_out/${T}_stats.log 2>&1
 timeout 300 python bench.py --config c4 --steps 5 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/${T}_bench_c4.log 2>&1
 timeout 600 python bench.py --config c5 --steps 5 --warmup 3 > gpurun_out/${T}_bench_c5.log 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:merge_cross -s 3 -c 1 -o gpurun_out/${T}_merge_c4 python bench.py --config c4 --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/${T}_ncu.log 2>&1
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:"tile_tmt|repair_diagram" -s 6 -c 2 -o gpurun_out/${T}_other_c4 python bench.py --config c4 --steps 1 --warmup 3 --no-e2e --no-cpu-baseline >> gpurun_out/${T}_ncu.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:"tile_tmt|repair_brick|diagram_kernel" -s 6 -c 2 -o gpurun_out/${T}_other_c4 python bench.py --config c4 --steps 1 --warmup 3 --no-e2e --no-cpu-baseline >> gpurun_out/${T}_ncu.log 2>&1
 tail -3 gpurun_out/${T}_*.log

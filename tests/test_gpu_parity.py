@@ -161,7 +161,7 @@ def test_launches_are_library_kernels():
     mt = ctx_for(dims, conn)
     mt.compute(torch.from_numpy(f).cuda())
     mt.diagram()
-    assert mt.last_launch_count() == 5
+    assert mt.last_launch_count() == 6
 
 
 @pytest.mark.parametrize("cfg", ["c2", "c3", "c4"])
