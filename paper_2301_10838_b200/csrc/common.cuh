@@ -151,6 +151,8 @@ enum StatSlot : int {
     ST_CYC_LIST = 17,
     ST_TILE_PAIRS = 18,  // adjacent basin pairs (one merged edge each)
     ST_QUEUED = 19,      // tile-crossing edges left after the warp-level basin-pair dedupe
+    ST_REPAIR_CHAINS = 20,    // distinct start vertices whose chain the repair bricks walked
+    ST_REPAIR_FALLBACK = 21,  // vertices whose memo chain was truncated (plain walk)
     ST_COUNT = 24
 };
 

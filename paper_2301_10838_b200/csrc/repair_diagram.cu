@@ -74,7 +74,10 @@ constexpr int RB_ROWS = 128;
 constexpr int RB_PER = RB_ROWS / (RB_THREADS / 32);   // rows (vertices) per thread
 constexpr int RB_NV = RB_ROWS * 32;
 constexpr int RB_HASH = RB_NV;         // >= vertices per brick: an insertion always finds its slot
-constexpr int RB_POOL = 2048;          // chain entries per brick (overflow: plain walks)
+#ifndef MT_REPAIR_POOL
+#define MT_REPAIR_POOL 2048            // (a test build shrinks it to exercise the overflow path)
+#endif
+constexpr int RB_POOL = MT_REPAIR_POOL;   // chain entries per brick (overflow: plain walks)
 constexpr uint32_t RB_EMPTY = 0xffffffffu;
 constexpr uint16_t RB_NIL = 0xffffu;
 constexpr uint64_t KEY_ROOT = ~0ull;   // chain entry of a root: stops every walk
@@ -277,7 +280,7 @@ repair_brick_kernel(View view, const Cell* C, uint64_t* __restrict__ T, const fl
     }
 
     // one walk per distinct start vertex, recorded up to its largest threshold
-    unsigned long long hops = 0;
+    unsigned long long hops = 0, fallback = 0;
     const uint32_t nslots = S.nslots;
     for (uint32_t i = threadIdx.x; i < nslots; i += RB_THREADS) {
         const uint32_t h = S.list[i];
@@ -326,6 +329,7 @@ repair_brick_kernel(View view, const Cell* C, uint64_t* __restrict__ T, const fl
             e = S.plink[e];
         }
         if (!done) {                              // truncated chain: the plain walk from x
+            ++fallback;
             while (true) {
                 const Cell c = view.cell(C, x);
                 if (cv_of(c) == x || c.lo > a) break;
@@ -335,7 +339,11 @@ repair_brick_kernel(View view, const Cell* C, uint64_t* __restrict__ T, const fl
         }
         T[u] = pack(sv[k], x);
     }
-    if (stats && hops) atomicAdd(stats + ST_REPAIR_HOPS, hops);
+    if (stats) {
+        if (hops) atomicAdd(stats + ST_REPAIR_HOPS, hops);
+        if (fallback) atomicAdd(stats + ST_REPAIR_FALLBACK, fallback);
+        if (threadIdx.x == 0) atomicAdd(stats + ST_REPAIR_CHAINS, (unsigned long long)nslots);
+    }
 #undef UID
 #undef INB
 #undef FMASK
