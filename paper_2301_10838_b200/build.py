@@ -50,6 +50,7 @@ def build(force: bool = False, verbose: bool = False, defines=(), out: str | Non
         subprocess.check_call(cmd)
         objs.append(obj)
     dst = SO if out is None else out
+    os.makedirs(os.path.dirname(os.path.abspath(dst)), exist_ok=True)
     tmp = dst + f".tmp{os.getpid()}"
     subprocess.check_call([NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-cudart", "static"])
     os.replace(tmp, dst)

@@ -40,6 +40,10 @@ namespace mt {
 
 namespace {
 
+#ifndef TILE_SPLIT
+#define TILE_SPLIT 1   // path splitting in the merge-phase walks (A/B knob)
+#endif
+
 constexpr int TX = 32;
 constexpr uint32_t ABSENT = 0xffffffffu;       // order key of a tile slot outside the grid
 constexpr uint64_t EMPTY = ~0ull;
@@ -93,6 +97,7 @@ tile_tmt_kernel(const float* __restrict__ f, Cell* __restrict__ C, uint32_t* __r
     uint64_t* table = reinterpret_cast<uint64_t*>(smem + NV * 12);
     __shared__ int s_overflow;
     __shared__ uint32_t s_fetch, s_row, s_row_b, s_row_e;
+    __shared__ uint32_t s_wcnt[THREADS / 32], s_wpre[THREADS / 32 + 1];
 
     unsigned long long n_edges = 0, n_pairs = 0, n_hops = 0, n_iters = 0, n_rep = 0, n_cmp = 0;
     long long t_mark = clock64();
@@ -269,7 +274,8 @@ tile_tmt_kernel(const float* __restrict__ f, Cell* __restrict__ C, uint32_t* __r
             uint64_t cp = 0;
             bool has_prev = false;
             while (c_v(c) != x && c_key(c) <= L) {
-                if (has_prev && c_key(c) <= c_key(cp)) scas64(cell + xp, cp, (cp & ~0xffffull) | c_v(c));
+                if (TILE_SPLIT && has_prev && c_key(c) <= c_key(cp))
+                    scas64(cell + xp, cp, (cp & ~0xffffull) | c_v(c));
                 xp = x;
                 cp = c;
                 has_prev = true;
@@ -307,21 +313,48 @@ tile_tmt_kernel(const float* __restrict__ f, Cell* __restrict__ C, uint32_t* __r
         const uint64_t c = sld64(cell + x);
         return c_s(c) == x ? c_v(c) : x;
     };
-    // dynamic hand-out: a thread takes 4 table slots at a time from a CTA counter and skips
-    // the empty ones, so every lane of a warp works on a real pair (most slots are empty)
-    uint32_t chunk = 0, chunk_end = 0;
+    // d0. most table slots are empty (c5: ~1200 pairs in 8192 slots): every warp compacts
+    // its 1/NW of the table in place (a chunk of 32 slots is read before any of its lanes
+    // writes, and a write never lands past the chunk being read), then the pairs are handed
+    // out one per fetch from a CTA counter over the concatenated runs, so that every
+    // fetch yields a pair and every lane of a warp works on one
+    constexpr int NW = THREADS / 32, REG = TABLE / NW;
+    {
+        const int warp = threadIdx.x >> 5;
+        uint64_t* reg = table + warp * REG;
+        uint32_t cnt = 0;
+#pragma unroll 4
+        for (int c = 0; c < REG; c += 32) {
+            const uint64_t e = reg[c + lane_c];
+            const uint32_t m = __ballot_sync(FULL_MASK, e != EMPTY);
+            __syncwarp();
+            if (e != EMPTY) reg[cnt + __popc(m & ((1u << lane_c) - 1u))] = e;
+            cnt += __popc(m);
+        }
+        if (lane_c == 0) s_wcnt[warp] = cnt;
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {     // exclusive prefix of the NW run lengths
+        const uint32_t c = threadIdx.x < NW ? s_wcnt[threadIdx.x] : 0u;
+        uint32_t incl = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t t = __shfl_up_sync(FULL_MASK, incl, o);
+            if (lane_c >= o) incl += t;
+        }
+        if (threadIdx.x <= NW) s_wpre[threadIdx.x] = incl - c;
+    }
+    __syncthreads();
+    const uint32_t n_listed = s_wpre[NW];
 #pragma unroll 1
     while (true) {
-        uint64_t e = EMPTY;
-        while (e == EMPTY) {
-            if (chunk == chunk_end) {
-                chunk = atomicAdd(&s_fetch, 1u);
-                chunk_end = chunk + 1;
-                if (chunk >= uint32_t(TABLE)) break;
-            }
-            e = table[chunk++];
-        }
-        if (e == EMPTY) break;
+        const uint32_t j = atomicAdd(&s_fetch, 1u);
+        if (j >= n_listed) break;
+        int w = 0;                                       // run holding pair j (binary search)
+#pragma unroll
+        for (int step = NW / 2; step > 0; step >>= 1)
+            if (s_wpre[w + step] <= j) w += step;
+        const uint64_t e = table[w * REG + (j - s_wpre[w])];
         if (STATS) ++n_pairs;
         const uint32_t pair = uint32_t(e >> 12), hi = uint32_t(e) & 0xfffu;
         const uint32_t ba = pair >> 12, bb = pair & 0xfffu;
