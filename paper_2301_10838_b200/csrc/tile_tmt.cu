@@ -43,6 +43,15 @@ namespace {
 #ifndef TILE_SPLIT
 #define TILE_SPLIT 1   // path splitting in the merge-phase walks (A/B knob)
 #endif
+#ifndef TILE_STOP
+#define TILE_STOP 0    // timing only (WRONG results): run phases < k: 1 load+descent, 2 +compress, 3 +list, 4 +merge
+#endif
+#ifndef LIST_DEDUPE
+#define LIST_DEDUPE 0  // drop y/z edges with a lower edge of the same basin pair in a neighbour lane
+#endif
+#ifndef TILE_SM
+#define TILE_SM 1      // merge phase as a per-lane state machine (A/B knob)
+#endif
 
 constexpr int TX = 32;
 constexpr uint32_t ABSENT = 0xffffffffu;       // order key of a tile slot outside the grid
@@ -177,7 +186,7 @@ tile_tmt_kernel(const float* __restrict__ f, Cell* __restrict__ C, uint32_t* __r
     // ---- b. compress with path compression ---------------------------------------------
     // rows handed out dynamically, one warp per row (no warp waits on a long walk of another)
 #pragma unroll 1
-    while (true) {
+    while (TILE_STOP == 0 || TILE_STOP > 1) {
         int rr = 0;
         if ((threadIdx.x & 31) == 0) rr = int(atomicAdd(&s_row_b, 1u));
         rr = __shfl_sync(FULL_MASK, rr, 0);
@@ -217,27 +226,46 @@ tile_tmt_kernel(const float* __restrict__ f, Cell* __restrict__ C, uint32_t* __r
     // contended inserts do not hold the barrier for the others
     const int lane_c = threadIdx.x & 31;
 #pragma unroll 1
-    while (true) {
+    while (TILE_STOP == 0 || TILE_STOP > 2) {
         int r = 0;
         if (lane_c == 0) r = int(atomicAdd(&s_row, 1u));
         r = __shfl_sync(FULL_MASK, r, 0);
         if (r >= ROWS) break;
         const int ly = r % TY, lz = r / TY;
         const uint32_t u = r * TX + lx;
-        if (ord[u] == ABSENT) continue;
+        const uint32_t ou = ord[u];
         const uint32_t bu = c_v(cell[u]);      // basin (a minimum points at itself)
         const bool ok[3] = {lx + 1 < TX, ly + 1 < TY, lz + 1 < TZ};
         const uint32_t off[3] = {1u, uint32_t(TX), uint32_t(TX * TY)};
 #pragma unroll
         for (int d = 0; d < 3; ++d) {
-            if (!ok[d]) continue;
-            const uint32_t w = u + off[d];
-            if (ord[w] == ABSENT) continue;
-            const uint32_t bw = c_v(cell[w]);
-            if (bw == bu) continue;
+            constexpr uint32_t NONE = 0xffffffffu;
+            uint32_t pair = NONE, hi = 0;
+            uint64_t kh = 0;                    // key of the edge's upper endpoint (its level)
+            if (ou != ABSENT && ok[d]) {
+                const uint32_t w = u + off[d];
+                const uint32_t ow = ord[w];
+                if (ow != ABSENT) {
+                    const uint32_t bw = c_v(cell[w]);
+                    if (bw != bu) {
+                        const uint64_t ku = (uint64_t(ou) << 16) | u, kw = (uint64_t(ow) << 16) | w;
+                        hi = kw < ku ? u : w;
+                        kh = kw < ku ? ku : kw;
+                        pair = bu < bw ? (bu << 12) | bw : (bw << 12) | bu;
+                    }
+                }
+            }
+            if (LIST_DEDUPE && d > 0) {
+                // y/z edges of neighbouring lanes often join the same two basins: an edge with
+                // a lower one of the same pair in the next or previous lane is dropped (the
+                // lowest edge of every run survives, and the table keeps the lowest per pair)
+                const uint32_t pu = __shfl_up_sync(FULL_MASK, pair, 1), pd = __shfl_down_sync(FULL_MASK, pair, 1);
+                const uint64_t ku = __shfl_up_sync(FULL_MASK, kh, 1), kd = __shfl_down_sync(FULL_MASK, kh, 1);
+                if (pair != NONE && ((lane_c > 0 && pu == pair && ku < kh) || (lane_c < 31 && pd == pair && kd < kh)))
+                    pair = NONE;
+            }
+            if (pair == NONE) continue;
             if (STATS) ++n_edges;
-            const uint32_t hi = lkey_lt(ord, w, u) ? u : w;
-            const uint32_t pair = bu < bw ? (bu << 12) | bw : (bw << 12) | bu;
             const uint64_t entry = (uint64_t(pair) << 12) | hi;
             uint32_t h = pair_hash<TABLE>(pair);
             for (uint32_t probe = 0;;) {
@@ -254,7 +282,7 @@ tile_tmt_kernel(const float* __restrict__ f, Cell* __restrict__ C, uint32_t* __r
                     s_overflow = 1;
                     break;
                 }
-                if (!lkey_lt(ord, hi, uint32_t(cur) & 0xfffu)) break;  // the stored edge is lower
+                if (kh >= key48(ord, uint32_t(cur) & 0xfffu)) break;  // the stored edge is lower
                 if (scas64(table + h, cur, entry) == cur) break;
             }
         }
@@ -345,22 +373,108 @@ tile_tmt_kernel(const float* __restrict__ f, Cell* __restrict__ C, uint32_t* __r
         if (threadIdx.x <= NW) s_wpre[threadIdx.x] = incl - c;
     }
     __syncthreads();
-    const uint32_t n_listed = s_wpre[NW];
+    const uint32_t n_listed = (TILE_STOP == 0 || TILE_STOP > 3) ? s_wpre[NW] : 0u;
+    auto listed = [&](uint32_t j) {                       // pair j of the concatenated runs
+        int w = 0;                                        // (binary search over the run starts)
+#pragma unroll
+        for (int step = NW / 2; step > 0; step >>= 1)
+            if (s_wpre[w + step] <= j) w += step;
+        return table[w * REG + (j - s_wpre[w])];
+    };
+#if TILE_SM
+    // d1. one state machine per lane, advanced by one shared-memory round trip per loop
+    // iteration (a walk step, the pair of Alg. 3 loads (+ CAS)); a lane whose pair is done
+    // takes the next listed pair at the top of the next iteration, so the lanes of a warp
+    // stay busy and converged instead of waiting for the longest merge of the warp
+    enum { P_IDLE = 0, P_W0 = 1, P_W1 = 2, P_A3 = 3, P_DONE = 4 };
+    int ph = P_IDLE;
+    uint64_t L = 0, S = 0, cp = 0;
+    uint32_t x = 0, xp = 0, lo = 0, r0v = 0, mu = 0, mv = 0;
+    bool has_prev = false;
+#pragma unroll 1
+    while (true) {
+        if (ph == P_IDLE) {
+            const uint32_t j = atomicAdd(&s_fetch, 1u);
+            if (j >= n_listed) {
+                ph = P_DONE;
+            } else {
+                const uint64_t e = listed(j);
+                if (STATS) ++n_pairs;
+                const uint32_t pair = uint32_t(e >> 12), hi = uint32_t(e) & 0xfffu;
+                const uint32_t ba = pair >> 12, bb = pair & 0xfffu;
+                const uint32_t bh = basin(hi);
+                L = key48(ord, hi);                       // join bh and the other basin at level L
+                x = bh;
+                lo = bh == ba ? bb : ba;
+                has_prev = false;
+                ph = P_W0;
+            }
+        }
+        if (__all_sync(FULL_MASK, ph == P_DONE)) break;
+        if (ph == P_W0 || ph == P_W1) {                   // walks at level L with path splitting
+            const uint64_t c = sld64(cell + x);
+            if (c_v(c) != x && c_key(c) <= L) {
+                if (TILE_SPLIT && has_prev && c_key(c) <= c_key(cp))
+                    scas64(cell + xp, cp, (cp & ~0xffffull) | c_v(c));
+                xp = x;
+                cp = c;
+                has_prev = true;
+                x = c_v(c);
+                if (STATS) ++n_hops;
+            } else if (ph == P_W0) {
+                r0v = x;
+                x = lo;
+                has_prev = false;
+                ph = P_W1;
+            } else if (x == r0v) {
+                ph = P_IDLE;                              // joined below L already
+            } else {
+                mu = r0v;
+                mv = x;
+                S = L;
+                ph = P_A3;
+            }
+        } else if (ph == P_A3) {                          // Alg. 3, one iteration
+            if (STATS) ++n_iters;
+            const uint64_t cu = sld64(cell + mu), cv = sld64(cell + mv);
+            if (c_v(cu) != mu && c_key(cu) < S) {         // l.2-4 + R4
+                mu = c_v(cu);
+            } else if (c_v(cv) != mv && c_key(cv) < S) {  // l.5-8 + R4
+                mv = c_v(cv);
+            } else if (mu == mv) {                        // l.9-10
+                ph = P_IDLE;
+            } else {
+                uint32_t uu = mu, vv = mv;
+                uint64_t cvv = cv;
+                if (key48(ord, mv) < key48(ord, mu)) { uu = mv; vv = mu; cvv = cu; }   // l.11-12
+                if (scas64(cell + vv, cvv, (S << 16) | uu) == cvv) {                  // l.14
+                    if (c_v(cvv) == vv) {
+                        ph = P_IDLE;                      // R5
+                    } else {
+                        mu = uu;                          // l.15
+                        S = c_key(cvv);
+                        mv = c_v(cvv);
+                    }
+                } else {
+                    mu = uu;                              // l.17
+                    mv = vv;
+                }
+            }
+        }
+    }
+#else
 #pragma unroll 1
     while (true) {
         const uint32_t j = atomicAdd(&s_fetch, 1u);
         if (j >= n_listed) break;
-        int w = 0;                                       // run holding pair j (binary search)
-#pragma unroll
-        for (int step = NW / 2; step > 0; step >>= 1)
-            if (s_wpre[w + step] <= j) w += step;
-        const uint64_t e = table[w * REG + (j - s_wpre[w])];
+        const uint64_t e = listed(j);
         if (STATS) ++n_pairs;
         const uint32_t pair = uint32_t(e >> 12), hi = uint32_t(e) & 0xfffu;
         const uint32_t ba = pair >> 12, bb = pair & 0xfffu;
         const uint32_t bh = basin(hi);
         merge_at(bh, bh == ba ? bb : ba, key48(ord, hi));
     }
+#endif
     if (s_overflow) {  // (uniform: written before the last barrier) the table dropped edges
 #pragma unroll 1
         for (int k = 0; k < PER; ++k) {
@@ -387,7 +501,7 @@ tile_tmt_kernel(const float* __restrict__ f, Cell* __restrict__ C, uint32_t* __r
 
     // ---- e. repair: every cell points at its representative (minimal tile store) -------
 #pragma unroll 1
-    while (true) {
+    while (TILE_STOP == 0 || TILE_STOP > 4) {
         int rr = 0;
         if ((threadIdx.x & 31) == 0) rr = int(atomicAdd(&s_row_e, 1u));
         rr = __shfl_sync(FULL_MASK, rr, 0);
