@@ -49,8 +49,14 @@ namespace {
 #ifndef LIST_DEDUPE
 #define LIST_DEDUPE 0  // drop y/z edges with a lower edge of the same basin pair in a neighbour lane
 #endif
-#ifndef TILE_SM
-#define TILE_SM 1      // merge phase as a per-lane state machine (A/B knob)
+#ifndef TILE_MINB
+#define TILE_MINB 2    // __launch_bounds__ min blocks per SM (register budget knob)
+#endif
+#ifndef TILE_REP
+#define TILE_REP 1     // crossing edges grouped by tile representative at own level (else descent basin)
+#endif
+#ifndef TILE_OWNRUN
+#define TILE_OWNRUN 1  // each warp merges the pairs of its own compacted run (no CTA counter)
 #endif
 
 constexpr int TX = 32;
@@ -91,7 +97,7 @@ __device__ __forceinline__ uint64_t scas64(uint64_t* p, uint64_t cmp, uint64_t v
 }
 
 template <int TY, int TZ, bool STATS, int NV = TX * TY * TZ, int THREADS = NV / 8, int TABLE = 2 * NV>
-__global__ void __launch_bounds__(THREADS)
+__global__ void __launch_bounds__(THREADS, TILE_MINB)
 tile_tmt_kernel(const float* __restrict__ f, Cell* __restrict__ C, uint32_t* __restrict__ basin_out, uint32_t nx,
                 uint32_t ny, uint32_t z_begin,
                 uint32_t z_end, uint32_t tiles_x, uint32_t tiles_y, uint32_t flip, unsigned long long* __restrict__ counters,
@@ -106,7 +112,9 @@ tile_tmt_kernel(const float* __restrict__ f, Cell* __restrict__ C, uint32_t* __r
     uint64_t* table = reinterpret_cast<uint64_t*>(smem + NV * 12);
     __shared__ int s_overflow;
     __shared__ uint32_t s_fetch, s_row, s_row_b, s_row_e;
+#if !TILE_OWNRUN
     __shared__ uint32_t s_wcnt[THREADS / 32], s_wpre[THREADS / 32 + 1];
+#endif
 
     unsigned long long n_edges = 0, n_pairs = 0, n_hops = 0, n_iters = 0, n_rep = 0, n_cmp = 0;
     long long t_mark = clock64();
@@ -212,9 +220,11 @@ tile_tmt_kernel(const float* __restrict__ f, Cell* __restrict__ C, uint32_t* __r
         sst64(cell + u, (cell[u] & ~0xffffull) | x);
     }
     __syncthreads();
+#if !TILE_REP
     uint16_t bas[PER];  // descent basin of each owned vertex, for the crossing-edge dedupe
 #pragma unroll
     for (int k = 0; k < PER; ++k) bas[k] = uint16_t(c_v(cell[(r0 + k * RSTEP) * TX + lx]));
+#endif
     phase_time(ST_CYC_COMPRESS);
 
     // ---- c. one edge per pair of adjacent basins: the lowest --------------------------------
@@ -347,20 +357,20 @@ tile_tmt_kernel(const float* __restrict__ f, Cell* __restrict__ C, uint32_t* __r
     // out one per fetch from a CTA counter over the concatenated runs, so that every
     // fetch yields a pair and every lane of a warp works on one
     constexpr int NW = THREADS / 32, REG = TABLE / NW;
-    {
-        const int warp = threadIdx.x >> 5;
-        uint64_t* reg = table + warp * REG;
-        uint32_t cnt = 0;
+    const int warp_d = threadIdx.x >> 5;
+    uint64_t* const run = table + warp_d * REG;          // this warp's run of pairs
+    uint32_t run_len = 0;
 #pragma unroll 4
-        for (int c = 0; c < REG; c += 32) {
-            const uint64_t e = reg[c + lane_c];
-            const uint32_t m = __ballot_sync(FULL_MASK, e != EMPTY);
-            __syncwarp();
-            if (e != EMPTY) reg[cnt + __popc(m & ((1u << lane_c) - 1u))] = e;
-            cnt += __popc(m);
-        }
-        if (lane_c == 0) s_wcnt[warp] = cnt;
+    for (int c = 0; c < REG; c += 32) {
+        const uint64_t e = run[c + lane_c];
+        const uint32_t m = __ballot_sync(FULL_MASK, e != EMPTY);
+        __syncwarp();
+        if (e != EMPTY) run[run_len + __popc(m & ((1u << lane_c) - 1u))] = e;
+        run_len += __popc(m);
     }
+    if (TILE_STOP != 0 && TILE_STOP <= 3) run_len = 0;
+#if !TILE_OWNRUN
+    if (lane_c == 0) s_wcnt[warp_d] = run_len;
     __syncthreads();
     if (threadIdx.x < 32) {     // exclusive prefix of the NW run lengths
         const uint32_t c = threadIdx.x < NW ? s_wcnt[threadIdx.x] : 0u;
@@ -373,7 +383,9 @@ tile_tmt_kernel(const float* __restrict__ f, Cell* __restrict__ C, uint32_t* __r
         if (threadIdx.x <= NW) s_wpre[threadIdx.x] = incl - c;
     }
     __syncthreads();
-    const uint32_t n_listed = (TILE_STOP == 0 || TILE_STOP > 3) ? s_wpre[NW] : 0u;
+#endif
+#if !TILE_OWNRUN
+    const uint32_t n_listed = s_wpre[NW];
     auto listed = [&](uint32_t j) {                       // pair j of the concatenated runs
         int w = 0;                                        // (binary search over the run starts)
 #pragma unroll
@@ -381,7 +393,7 @@ tile_tmt_kernel(const float* __restrict__ f, Cell* __restrict__ C, uint32_t* __r
             if (s_wpre[w + step] <= j) w += step;
         return table[w * REG + (j - s_wpre[w])];
     };
-#if TILE_SM
+#endif
     // d1. one state machine per lane, advanced by one shared-memory round trip per loop
     // iteration (a walk step, the pair of Alg. 3 loads (+ CAS)); a lane whose pair is done
     // takes the next listed pair at the top of the next iteration, so the lanes of a warp
@@ -391,24 +403,40 @@ tile_tmt_kernel(const float* __restrict__ f, Cell* __restrict__ C, uint32_t* __r
     uint64_t L = 0, S = 0, cp = 0;
     uint32_t x = 0, xp = 0, lo = 0, r0v = 0, mu = 0, mv = 0;
     bool has_prev = false;
+    uint32_t run_pos = 0;
 #pragma unroll 1
     while (true) {
+#if TILE_OWNRUN
+        // the warp's own run is its pool: idle lanes take the next pairs in lane order
+        const uint32_t need = __ballot_sync(FULL_MASK, ph == P_IDLE);
+        if (need) {
+            if (ph == P_IDLE) {
+                const uint32_t j = run_pos + __popc(need & ((1u << lane_c) - 1u));
+                if (j < run_len) {
+                    const uint64_t e = run[j];
+#else
         if (ph == P_IDLE) {
-            const uint32_t j = atomicAdd(&s_fetch, 1u);
-            if (j >= n_listed) {
-                ph = P_DONE;
-            } else {
-                const uint64_t e = listed(j);
-                if (STATS) ++n_pairs;
-                const uint32_t pair = uint32_t(e >> 12), hi = uint32_t(e) & 0xfffu;
-                const uint32_t ba = pair >> 12, bb = pair & 0xfffu;
-                const uint32_t bh = basin(hi);
-                L = key48(ord, hi);                       // join bh and the other basin at level L
-                x = bh;
-                lo = bh == ba ? bb : ba;
-                has_prev = false;
-                ph = P_W0;
+            {
+                const uint32_t j = atomicAdd(&s_fetch, 1u);
+                if (j < n_listed) {
+                    const uint64_t e = listed(j);
+#endif
+                    if (STATS) ++n_pairs;
+                    const uint32_t pair = uint32_t(e >> 12), hi = uint32_t(e) & 0xfffu;
+                    const uint32_t ba = pair >> 12, bb = pair & 0xfffu;
+                    const uint32_t bh = basin(hi);
+                    L = key48(ord, hi);                   // join bh and the other basin at level L
+                    x = bh;
+                    lo = bh == ba ? bb : ba;
+                    has_prev = false;
+                    ph = P_W0;
+                } else {
+                    ph = P_DONE;
+                }
             }
+#if TILE_OWNRUN
+            run_pos += __popc(need);
+#endif
         }
         if (__all_sync(FULL_MASK, ph == P_DONE)) break;
         if (ph == P_W0 || ph == P_W1) {                   // walks at level L with path splitting
@@ -462,19 +490,6 @@ tile_tmt_kernel(const float* __restrict__ f, Cell* __restrict__ C, uint32_t* __r
             }
         }
     }
-#else
-#pragma unroll 1
-    while (true) {
-        const uint32_t j = atomicAdd(&s_fetch, 1u);
-        if (j >= n_listed) break;
-        const uint64_t e = listed(j);
-        if (STATS) ++n_pairs;
-        const uint32_t pair = uint32_t(e >> 12), hi = uint32_t(e) & 0xfffu;
-        const uint32_t ba = pair >> 12, bb = pair & 0xfffu;
-        const uint32_t bh = basin(hi);
-        merge_at(bh, bh == ba ? bb : ba, key48(ord, hi));
-    }
-#endif
     if (s_overflow) {  // (uniform: written before the last barrier) the table dropped edges
 #pragma unroll 1
         for (int k = 0; k < PER; ++k) {
@@ -540,7 +555,14 @@ tile_tmt_kernel(const float* __restrict__ f, Cell* __restrict__ C, uint32_t* __r
         const uint32_t s = c_s(cu), v = c_v(cu);
         const uint64_t g = gbase + uint64_t(lz) * sxy + uint64_t(ly) * nx + lx;
         C[g] = make_cell(key_of(uint32_t(cu >> 32), gid(s)), ou, gid(v));
+#if TILE_REP
+        // the vertex the crossing-edge walks may start from: Rep_tile(u, key(u)), joined to u
+        // below key(u) -- the v of a regular cell of the minimal tile store, u itself for a
+        // minimum (DESIGN.md derivation C''')
+        basin_out[g] = gid(s == u ? v : u);
+#else
         basin_out[g] = gid(bas[k]);
+#endif
     }
     phase_time(ST_CYC_WRITE);
     if (STATS) {
