@@ -52,6 +52,9 @@ namespace {
 #ifndef TILE_MINB
 #define TILE_MINB 2    // __launch_bounds__ min blocks per SM (register budget knob)
 #endif
+#ifndef TILE_PJ
+#define TILE_PJ 1      // compress by synchronous pointer jumping (else walks + path compression)
+#endif
 #ifndef TILE_REP
 #define TILE_REP 1     // crossing edges grouped by tile representative at own level (else descent basin)
 #endif
@@ -163,6 +166,7 @@ tile_tmt_kernel(const float* __restrict__ f, Cell* __restrict__ C, uint32_t* __r
     phase_time(ST_CYC_LOAD);
 
     // ---- a. steepest descent over in-tile neighbours -----------------------------------
+    uint32_t par[PER];  // descent pointer of each owned vertex (then its basin, phase b)
 #pragma unroll
     for (int k = 0; k < PER; ++k) {
         const int r = r0 + k * RSTEP;
@@ -187,11 +191,34 @@ tile_tmt_kernel(const float* __restrict__ f, Cell* __restrict__ C, uint32_t* __r
             }
         }
         cell[u] = c_make(ou, u, best);
+        par[k] = best;
     }
     __syncthreads();
     phase_time(ST_CYC_DESCENT);
 
-    // ---- b. compress with path compression ---------------------------------------------
+    // ---- b. compress: every regular cell points at its basin minimum ----------------------
+#if TILE_PJ
+    // synchronous pointer jumping, par <- par(par), on the thread's own 8 vertices (8
+    // independent load chains per round), until every pointer is a root: ceil(log2 depth) + 1
+    // rounds.  Rounds run in place: a pointer read while its owner rewrites it is the old or
+    // the new ancestor, both in the same descent tree (derivation F), so the v fields (16-bit
+    // stores) only ever move up the tree.
+#pragma unroll 1
+    while (TILE_STOP == 0 || TILE_STOP > 1) {
+        bool changed = false;
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+            const uint32_t q = *reinterpret_cast<const volatile uint16_t*>(cell + par[k]);
+            if (q != par[k]) {
+                par[k] = q;
+                changed = true;
+                *reinterpret_cast<volatile uint16_t*>(cell + (r0 + k * RSTEP) * TX + lx) = uint16_t(q);
+                if (STATS) ++n_cmp;
+            }
+        }
+        if (!__syncthreads_or(changed)) break;
+    }
+#else
     // rows handed out dynamically, one warp per row (no warp waits on a long walk of another)
 #pragma unroll 1
     while (TILE_STOP == 0 || TILE_STOP > 1) {
@@ -219,6 +246,7 @@ tile_tmt_kernel(const float* __restrict__ f, Cell* __restrict__ C, uint32_t* __r
         }
         sst64(cell + u, (cell[u] & ~0xffffull) | x);
     }
+#endif
     __syncthreads();
 #if !TILE_REP
     uint16_t bas[PER];  // descent basin of each owned vertex, for the crossing-edge dedupe
