@@ -5,10 +5,10 @@
 // dedupe_cross: the crossing edges are enumerated directly (e in
 // [0, Ex + Ey + Ez) decodes to an x-, y- or z-face edge; 32 consecutive e are
 // neighbours on one face, one per lane).  Each edge is reduced to the pair of
-// descent basins of its ends (tile_tmt's basin array) and its level L =
-// max(key(a), key(b)); lanes holding the same basin pair (__match_any_sync)
-// keep only the lowest edge (derivation C'': between two basins only the
-// lowest edge matters), and the survivors are queued as (L, basin_hi, basin_lo).
+// tile representatives of its ends at their own levels (tile_tmt's R array,
+// DESIGN.md derivation C''') and its level L = max(key(a), key(b)); lanes
+// holding the same pair (__match_any_sync) keep only the lowest edge
+// (derivation C''), and the survivors are queued as (L, R_hi, R_lo).
 //
 // merge_queue: persistent warps take batches of 256 queue entries per global
 // atomic; each lane runs its entry as a state machine advanced by ONE memory

@@ -16,21 +16,24 @@
 // -- is compared straight from the cell, without a lookup:
 //   a. steepest descent over in-tile neighbours -> forest of (u, u, w) cells
 //      (derivation B);
-//   b. compress with path compression: every regular cell points at its
-//      basin minimum (derivation F);
+//   b. compress by synchronous pointer jumping: every regular cell points at
+//      its basin minimum (derivations F, F');
 //   c. compact the in-tile edges between two basins into a list;
 //   d. merge them: Alg. 4-style walks at the edge level with path splitting,
 //      then Alg. 3 with 64-bit shared-memory CAS and the root guards R4/R5
 //      (DESIGN.md), as a warp-converged state machine (one shared-memory
-//      round-trip per lane per step; idle lanes take the next listed edge);
+//      round-trip per lane per step; idle lanes take the next pair of the
+//      warp's compacted run);
 //   e. repair (Alg. 5 with Alg. 4's walk, reading R20): the tile store is
 //      minimal for G_t;
-//   f. write the 16-byte global cells (common.cuh) with global ids.
+//   f. write the 16-byte global cells (common.cuh) with global ids, and each
+//      vertex's tile representative at its own level for the crossing edges
+//      (derivation C''').
 // No halo is needed: only in-tile edges are used here.
 //
 // Layout: f float32[n] x fastest (reading R10) read once (coalesced 128-B
 // rows); 16-B cells written once (coalesced 512-B rows).  One CTA of 512
-// threads per tile; 72 KB of dynamic shared memory.
+// threads per tile; 112 KB of dynamic shared memory (2 CTAs per SM).
 #include <cstdlib>
 
 #include "common.cuh"
