@@ -207,8 +207,7 @@ mt_status mt_compute_graph(mt_ctx *ctx, const float *f, const uint64_t *row, con
  * hops, compress hops), [11..17] SM cycles of the tile phases (load,
  * descent, compress, merge, repair, write, edge list; summed over tiles),
  * [18] adjacent basin pairs in the tiles, [19] crossing edges queued,
- * [20] distinct start vertices whose chain the repair walked (memo),
- * [21] vertices whose memo chain was truncated (plain walk).  mt_stats syncs
+ * [20..21] unused (0).  mt_stats syncs
  * `stream` and copies up to `max` counters to out (host); returns the
  * number written (0 if disabled). */
 mt_status mt_set_stats(mt_ctx *ctx, int enable);

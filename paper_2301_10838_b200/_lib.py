@@ -194,8 +194,7 @@ def mt_kernel_times(ctx, max_entries: int = 8):
 
 STAT_NAMES = ["edges", "skipped", "pre_hops", "merge_iters", "cas_fail", "repair_hops", "tile_edges",
               "tile_hops", "tile_iters", "tile_repair_hops", "tile_compress_hops", "cyc_load", "cyc_descent",
-              "cyc_compress", "cyc_merge", "cyc_repair", "cyc_write", "cyc_list", "tile_pairs", "queued",
-              "repair_chains", "repair_fallback"]
+              "cyc_compress", "cyc_merge", "cyc_repair", "cyc_write", "cyc_list", "tile_pairs", "queued"]
 
 
 def mt_set_stats(ctx, enable: bool):

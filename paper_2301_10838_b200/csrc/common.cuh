@@ -86,6 +86,12 @@ __device__ __forceinline__ Cell ld_cell(const Cell* p) {
                  : "=l"(c.lo), "=l"(c.hi) : "l"(p) : "memory");
     return c;
 }
+// non-coherent (L1-cached) 16-byte load: only for cells no thread writes during the kernel
+__device__ __forceinline__ Cell ld_cell_nc(const Cell* p) {
+    Cell c;
+    asm("ld.global.nc.v2.u64 {%0, %1}, [%2];" : "=l"(c.lo), "=l"(c.hi) : "l"(p));
+    return c;
+}
 __device__ __forceinline__ void st_cell(Cell* p, const Cell& c) {
     asm volatile("{\n\t.reg .b128 d;\n\tmov.b128 d, {%1, %2};\n\tst.relaxed.gpu.global.b128 [%0], d;\n\t}"
                  ::"l"(p), "l"(c.lo), "l"(c.hi) : "memory");
@@ -151,8 +157,8 @@ enum StatSlot : int {
     ST_CYC_LIST = 17,
     ST_TILE_PAIRS = 18,  // adjacent basin pairs (one merged edge each)
     ST_QUEUED = 19,      // tile-crossing edges left after the warp-level basin-pair dedupe
-    ST_REPAIR_CHAINS = 20,    // distinct start vertices whose chain the repair bricks walked
-    ST_REPAIR_FALLBACK = 21,  // vertices whose memo chain was truncated (plain walk)
+    ST_UNUSED_20 = 20,        // (retired: repair memo statistics)
+    ST_UNUSED_21 = 21,
     ST_COUNT = 24
 };
 

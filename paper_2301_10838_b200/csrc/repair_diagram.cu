@@ -9,13 +9,11 @@
 // Reading R20: the walk returns the vertex it stopped at (Alg. 4 as printed
 // returns the next, too-deep v).  The walks only read the working cells (the
 // repaired pointer goes to T), so they see the fixed post-merge store.
-//   Many vertices of a brick of the grid start their walk at the same v (the
-// tile-local representative): the brick collects its distinct start vertices
-// in a shared-memory hash set, walks each one's chain of cells ONCE -- up to
-// the largest threshold key(s) among the vertices that start there -- into a
-// shared-memory pool, and resolves every vertex's walk from that pool
-// (derivation I).  The memo changes which loads are issued, never what a walk
-// computes: a chain entry is exactly the cell the walk would have read.
+//   The cells are read-only during the repair, so the walks use non-coherent
+// L1-cached loads: the vertices of a brick mostly walk the same few chains of
+// cells (their tile representatives and the minima these merged into), which
+// stay in L1.  (A shared-memory memo of the brick's distinct chains, one walk
+// per distinct start vertex, was measured slower: c5 19.0 vs 14.0 ms.)
 //
 // Diagram: after the merge phase the s fields are final (repair only rewrites
 // v).  A cell with s != u is the branch born at u dying at saddle s (finite
@@ -35,8 +33,16 @@ namespace {
 
 // cell / value access for the repair walk: everything local (one GPU), or local
 // cells plus the merged boundary forest of all slabs (multi-GPU, slab.cu)
+#ifndef MT_REPAIR_NC
+#define MT_REPAIR_NC 1      // the repair reads cells no thread writes: L1-cached non-coherent loads
+#endif
+#ifndef MT_REPAIR_MINB
+#define MT_REPAIR_MINB 3    // __launch_bounds__ min blocks per SM (register budget knob)
+#endif
+__device__ __forceinline__ Cell ld_cell_ro(const Cell* p) { return MT_REPAIR_NC ? ld_cell_nc(p) : ld_cell(p); }
+
 struct LocalView {
-    __device__ __forceinline__ Cell cell(const Cell* C, uint32_t x) const { return ld_cell(C + x); }
+    __device__ __forceinline__ Cell cell(const Cell* C, uint32_t x) const { return ld_cell_ro(C + x); }
     __device__ __forceinline__ float value(const float* f, uint32_t x) const { return __ldg(f + x); }
 };
 
@@ -45,7 +51,7 @@ struct ForestView {
     uint64_t base, n;  // owned global ids [base, base + n)
     __device__ __forceinline__ bool mine(uint32_t x) const { return uint64_t(x) - base < n; }
     __device__ __forceinline__ Cell cell(const Cell* C, uint32_t x) const {
-        if (mine(x)) return ld_cell(C + x);
+        if (mine(x)) return ld_cell_ro(C + x);
         const uint32_t i = forest_lookup(F, x);
         if (i == FOREST_MISS) {            // incomplete records: report, stop the walk here
             atomicOr(F.err, ERR_FOREST);
@@ -73,46 +79,23 @@ constexpr int RB_THREADS = 512;
 constexpr int RB_ROWS = 128;
 constexpr int RB_PER = RB_ROWS / (RB_THREADS / 32);   // rows (vertices) per thread
 constexpr int RB_NV = RB_ROWS * 32;
-constexpr int RB_HASH = RB_NV;         // >= vertices per brick: an insertion always finds its slot
-#ifndef MT_REPAIR_POOL
-#define MT_REPAIR_POOL 2048            // (a test build shrinks it to exercise the overflow path)
-#endif
-constexpr int RB_POOL = MT_REPAIR_POOL;   // chain entries per brick (overflow: plain walks)
-constexpr uint32_t RB_EMPTY = 0xffffffffu;
-constexpr uint16_t RB_NIL = 0xffffu;
-constexpr uint64_t KEY_ROOT = ~0ull;   // chain entry of a root: stops every walk
 
 struct RepairSmem {
-    unsigned long long pkey[RB_POOL];  // chain entry: key(s_x) of the cell of x (KEY_ROOT: root) ...
-    uint32_t hkey[RB_HASH];            // start vertex v (RB_EMPTY: free slot)
-    uint32_t hmax[RB_HASH];            // largest ord(f[s]) among the vertices starting there
-    uint32_t px[RB_POOL];              // ... and its v (the next vertex of the walk)
-    uint16_t hhead[RB_HASH];           // first chain entry of the slot
-    uint16_t plink[RB_POOL];           // next chain entry
-    uint16_t list[RB_HASH];            // occupied slots
     uint32_t rowcnt[RB_ROWS];          // finite | essential << 16 records of each row
     uint32_t rowoff[RB_ROWS];          // their offset in the brick's staging run
     uint64_t rowbase[RB_ROWS];         // first id of each row
     uint64_t rowseg[RB_ROWS];          // its segment number
     uint32_t rowlim[RB_ROWS];          // lanes of the row inside the grid
     uint32_t rowfm[RB_ROWS], rowem[RB_ROWS];   // lanes holding a finite pair / a root
-    uint16_t slot[RB_PER][RB_THREADS];  // per vertex: hash slot of its start vertex (RB_NIL: none)
-    uint32_t nslots, ptop, base;
+    uint32_t base;
 };
-
-__device__ __forceinline__ uint32_t rb_hash(uint32_t v) {
-    v ^= v >> 16;
-    v *= 0x7feb352du;
-    v ^= v >> 15;
-    return v & (RB_HASH - 1);
-}
 
 struct BrickGeom {
     uint32_t by, bx_n, by_n;   // brick rows along y; bricks along x and y (brick mode)
 };
 
 template <class View, bool LINEAR>
-__global__ void __launch_bounds__(RB_THREADS, 2)
+__global__ void __launch_bounds__(RB_THREADS, MT_REPAIR_MINB)
 repair_brick_kernel(View view, const Cell* C, uint64_t* __restrict__ T, const float* __restrict__ f, Slab sl,
                     BrickGeom g, uint32_t flip, mt_pair* __restrict__ stage, uint64_t stage_cap,
                     uint16_t* __restrict__ seg_cnt, uint32_t* __restrict__ seg_pos,
@@ -121,12 +104,6 @@ repair_brick_kernel(View view, const Cell* C, uint64_t* __restrict__ T, const fl
     RepairSmem& S = *reinterpret_cast<RepairSmem*>(smem_raw);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t lt = (1u << lane) - 1u;
-    for (int i = threadIdx.x; i < RB_HASH; i += RB_THREADS) {
-        S.hkey[i] = RB_EMPTY;
-        S.hmax[i] = 0;
-        S.hhead[i] = RB_NIL;
-    }
-    if (threadIdx.x == 0) S.nslots = S.ptop = 0;
 
     // brick origin and the id-order number of its first segment
     uint64_t u0 = 0, seg0 = 0;
@@ -170,7 +147,7 @@ repair_brick_kernel(View view, const Cell* C, uint64_t* __restrict__ T, const fl
 #define INB(k) ((inb >> (k)) & 1u)
     Cell cell[RB_PER];
 #pragma unroll
-    for (int k = 0; k < RB_PER; ++k) cell[k] = INB(k) ? ld_cell(C + UID(k)) : Cell{0, 0};
+    for (int k = 0; k < RB_PER; ++k) cell[k] = INB(k) ? ld_cell_ro(C + UID(k)) : Cell{0, 0};
     // diagram records of each row: finite pairs (s != u) and roots (v == u)
 #define FMASK(k) __ballot_sync(FULL_MASK, INB(k) && cs_of(cell[k]) != uint32_t(UID(k)))
 #define EMASK(k) __ballot_sync(FULL_MASK, INB(k) && cv_of(cell[k]) == uint32_t(UID(k)))
@@ -212,38 +189,14 @@ repair_brick_kernel(View view, const Cell* C, uint64_t* __restrict__ T, const fl
         if (lane == 0) S.base = base;
     }
 
-    // distinct start vertices: one insertion per group of lanes sharing v (warp-aggregated),
-    // threshold = the group's largest ord(f[s])
     uint64_t key[RB_PER];     // threshold key(s)
     uint32_t sv[RB_PER];      // s of the vertex
 #pragma unroll
     for (int k = 0; k < RB_PER; ++k) {
         key[k] = cell[k].lo;
         sv[k] = cs_of(cell[k]);
-        const uint32_t v = cv_of(cell[k]);
-        const bool walk = INB(k) && v != uint32_t(UID(k));
-        const uint32_t wv = walk ? v : RB_EMPTY;
-        const uint32_t peers = __match_any_sync(FULL_MASK, wv);
-        const int leader = __ffs(peers) - 1;
-        const uint32_t m = __reduce_max_sync(peers, uint32_t(key[k] >> 32));
-        uint32_t h = 0;
-        if (walk && lane == leader) {
-            h = rb_hash(v);
-            while (true) {
-                const uint32_t old = atomicCAS(&S.hkey[h], RB_EMPTY, v);
-                if (old == RB_EMPTY) {
-                    S.list[atomicAdd(&S.nslots, 1u)] = uint16_t(h);
-                    break;
-                }
-                if (old == v) break;
-                h = (h + 1) & (RB_HASH - 1);
-            }
-            atomicMax(&S.hmax[h], m);
-        }
-        h = __shfl_sync(FULL_MASK, h, leader);
-        S.slot[k][threadIdx.x] = walk ? uint16_t(h) : RB_NIL;   // hash slot of its start vertex
     }
-    __syncthreads();
+    __syncthreads();   // staging base and row offsets in
 
     // staging records of every row, in id order within the row: finite pairs, then roots
     const uint32_t sbase = S.base;
@@ -279,58 +232,16 @@ repair_brick_kernel(View view, const Cell* C, uint64_t* __restrict__ T, const fl
         else atomicOr(counters + CTR_ERR, ERR_CAPACITY);
     }
 
-    // one walk per distinct start vertex, recorded up to its largest threshold
-    unsigned long long hops = 0, fallback = 0;
-    const uint32_t nslots = S.nslots;
-    for (uint32_t i = threadIdx.x; i < nslots; i += RB_THREADS) {
-        const uint32_t h = S.list[i];
-        const uint32_t omax = S.hmax[h];
-        uint32_t x = S.hkey[h];
-        uint16_t prev = RB_NIL;
-        while (true) {
-            const Cell c = view.cell(C, x);
-            const uint32_t nx = cv_of(c);
-            const uint64_t k = nx == x ? KEY_ROOT : c.lo;
-            const uint32_t e = atomicAdd(&S.ptop, 1u);
-            if (e >= RB_POOL) break;              // pool full: the chain ends here, users walk on
-            S.pkey[e] = k;
-            S.px[e] = nx;
-            S.plink[e] = RB_NIL;
-            if (prev == RB_NIL) S.hhead[h] = uint16_t(e);
-            else S.plink[prev] = uint16_t(e);
-            prev = uint16_t(e);
-            if (uint32_t(k >> 32) > omax || k == KEY_ROOT) break;   // k > every threshold of the slot
-            x = nx;
-            ++hops;
-        }
-    }
-    __syncthreads();
-
-    // resolve each vertex's walk: Rep(u, key(s)) from the chain of its start vertex
+    // Rep(u, key(s)): walk from v through cells with key(s') <= key(s) that are not roots
+    unsigned long long hops = 0;
 #pragma unroll
     for (int k = 0; k < RB_PER; ++k) {
         if (!INB(k)) continue;
         const uint64_t u = UID(k);
-        const uint16_t slot = S.slot[k][threadIdx.x];
-        if (slot == RB_NIL) {
-            T[u] = pack(uint32_t(u), uint32_t(u));
-            continue;
-        }
-        const uint64_t a = key[k];
-        uint32_t x = S.hkey[slot];
-        uint16_t e = S.hhead[slot];
-        bool done = false;
-        while (e != RB_NIL) {
-            if (S.pkey[e] > a) {
-                done = true;
-                break;
-            }
-            x = S.px[e];
-            e = S.plink[e];
-        }
-        if (!done) {                              // truncated chain: the plain walk from x
-            ++fallback;
-            while (true) {
+        uint32_t x = cv_of(cell[k]);
+        if (x != uint32_t(u)) {
+            const uint64_t a = key[k];
+            while (true) {                        // Alg. 4, reading R20
                 const Cell c = view.cell(C, x);
                 if (cv_of(c) == x || c.lo > a) break;
                 x = cv_of(c);
@@ -339,11 +250,7 @@ repair_brick_kernel(View view, const Cell* C, uint64_t* __restrict__ T, const fl
         }
         T[u] = pack(sv[k], x);
     }
-    if (stats) {
-        if (hops) atomicAdd(stats + ST_REPAIR_HOPS, hops);
-        if (fallback) atomicAdd(stats + ST_REPAIR_FALLBACK, fallback);
-        if (threadIdx.x == 0) atomicAdd(stats + ST_REPAIR_CHAINS, (unsigned long long)nslots);
-    }
+    if (stats && hops) atomicAdd(stats + ST_REPAIR_HOPS, hops);
 #undef UID
 #undef INB
 #undef FMASK

@@ -104,8 +104,9 @@ def test_closed_form_stress(dims):
 
 
 @pytest.mark.parametrize("dims", [(64, 64, 64), (96, 40, 1), (40, 7, 3)])
-def test_repair_memo_stats(dims):
-    """Checkerboard + noise: parity, and the repair bricks walked memo chains."""
+def test_repair_long_walks(dims):
+    """Checkerboard + noise (every vertex pair of basins adjacent, long repair walks): parity,
+    and the repair walked cells."""
     nx, ny, nz = dims
     conn = 4 if nz == 1 else 6
     z, y, x = np.meshgrid(np.arange(nz), np.arange(ny), np.arange(nx), indexing="ij")
@@ -119,39 +120,7 @@ def test_repair_memo_stats(dims):
     To, po, npo, neo = oracle.merge_tree(checker, dims, conn=conn)
     assert np.array_equal(T.cpu().numpy().view(np.uint64), To)
     assert _lib.pairs_to_numpy(rec).tobytes() == po.tobytes()
-    assert st["repair_chains"] > 0
-
-
-def test_repair_memo_overflow_build():
-    """The same library built with an 8-entry chain pool per brick (MT_REPAIR_POOL=8): most
-    chains are truncated and their vertices finish with the plain walk -- still bit-exact."""
-    import os
-    import subprocess
-    import sys
-    from paper_2301_10838_b200 import build as B
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    lib = B.build(defines=["MT_REPAIR_POOL=8"], out=os.path.join(root, "ab", "libmt_pool8.so"))
-    code = r"""
-import sys, numpy as np, torch
-sys.path.insert(0, %r)
-import oracle
-from paper_2301_10838_b200 import _lib, fields
-for cfg, scale in [("c4", 64), ("c2", 200), ("c1", None)]:
-    f, dims, conn = fields.make(cfg, scale=scale)
-    mt = _lib.MergeTree(dims, conn, device=0)
-    _lib.mt_set_stats(mt.ctx, True)
-    T = mt.compute(torch.from_numpy(f).cuda())
-    rec, npairs, ness = mt.diagram()
-    st = _lib.mt_stats(mt.ctx)
-    To, po, npo, neo = oracle.merge_tree(f, dims, conn=conn)
-    assert np.array_equal(T.cpu().numpy().view(np.uint64), To), cfg
-    assert _lib.pairs_to_numpy(rec).tobytes() == po.tobytes(), cfg
-    assert st["repair_fallback"] > 0, (cfg, st)
-print("ok")
-""" % root
-    env = dict(os.environ, MT_LIBRARY=lib)
-    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
-    assert r.returncode == 0 and "ok" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
+    assert st["repair_hops"] > 0
 
 
 def test_empty_and_single():
