@@ -55,6 +55,9 @@ namespace {
 #ifndef TILE_MINB
 #define TILE_MINB 2    // __launch_bounds__ min blocks per SM (register budget knob)
 #endif
+#ifndef TILE_REP_ILP
+#define TILE_REP_ILP 1 // in-tile repair: own vertices in lock-step rounds, results in registers
+#endif
 #ifndef TILE_PJ
 #define TILE_PJ 1      // compress by synchronous pointer jumping (else walks + path compression)
 #endif
@@ -95,7 +98,7 @@ __device__ __forceinline__ bool lkey_lt(const uint32_t* ord, uint32_t a, uint32_
 __device__ __forceinline__ uint64_t sld64(const uint64_t* p) {
     return *reinterpret_cast<const volatile uint64_t*>(p);
 }
-__device__ __forceinline__ void sst64(uint64_t* p, uint64_t v) {
+[[maybe_unused]] __device__ __forceinline__ void sst64(uint64_t* p, uint64_t v) {
     *reinterpret_cast<volatile uint64_t*>(p) = v;
 }
 __device__ __forceinline__ uint64_t scas64(uint64_t* p, uint64_t cmp, uint64_t val) {
@@ -546,6 +549,34 @@ tile_tmt_kernel(const float* __restrict__ f, Cell* __restrict__ C, uint32_t* __r
     phase_time(ST_CYC_MERGE);
 
     // ---- e. repair: every cell points at its representative (minimal tile store) -------
+#if TILE_REP_ILP
+    // each thread walks its own 8 vertices in lock-step rounds (8 independent shared-memory
+    // load chains in flight); the cells are final after the merge barrier and this phase only
+    // reads them, so the representatives stay in registers and go straight to phase f
+    uint32_t rep[PER];
+    uint32_t act = 0;
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+        const uint32_t u = (r0 + k * RSTEP) * TX + lx;
+        rep[k] = c_v(cell[u]);
+        if (rep[k] != u && (TILE_STOP == 0 || TILE_STOP > 4)) act |= 1u << k;
+    }
+#pragma unroll 1
+    while (act) {
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+            if (!((act >> k) & 1u)) continue;
+            const uint64_t cx = cell[rep[k]];
+            const uint64_t a = c_key(cell[(r0 + k * RSTEP) * TX + lx]);
+            if (c_v(cx) == rep[k] || c_key(cx) > a) {
+                act &= ~(1u << k);
+            } else {
+                rep[k] = c_v(cx);
+                if (STATS) ++n_rep;
+            }
+        }
+    }
+#else
 #pragma unroll 1
     while (TILE_STOP == 0 || TILE_STOP > 4) {
         int rr = 0;
@@ -567,6 +598,7 @@ tile_tmt_kernel(const float* __restrict__ f, Cell* __restrict__ C, uint32_t* __r
         if (x != v) sst64(cell + u, (cu & ~0xffffull) | x);
     }
     __syncthreads();
+#endif
     phase_time(ST_CYC_REPAIR);
 
     // ---- f. write the global 16-byte cells ---------------------------------------------
@@ -583,7 +615,11 @@ tile_tmt_kernel(const float* __restrict__ f, Cell* __restrict__ C, uint32_t* __r
         const uint32_t ou = ord[u];
         if (ou == ABSENT) continue;
         const uint64_t cu = cell[u];
+#if TILE_REP_ILP
+        const uint32_t s = c_s(cu), v = rep[k];
+#else
         const uint32_t s = c_s(cu), v = c_v(cu);
+#endif
         const uint64_t g = gbase + uint64_t(lz) * sxy + uint64_t(ly) * nx + lx;
         C[g] = make_cell(key_of(uint32_t(cu >> 32), gid(s)), ou, gid(v));
 #if TILE_REP
