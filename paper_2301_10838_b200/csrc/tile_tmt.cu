@@ -49,8 +49,8 @@ namespace {
 #ifndef TILE_STOP
 #define TILE_STOP 0    // timing only (WRONG results): run phases < k: 1 load+descent, 2 +compress, 3 +list, 4 +merge
 #endif
-#ifndef LIST_DEDUPE
-#define LIST_DEDUPE 0  // drop y/z edges with a lower edge of the same basin pair in a neighbour lane
+#ifndef LIST_STAGE
+#define LIST_STAGE 1   // list phase: per-warp staging of the candidate edges, inserts 32 at a time
 #endif
 #ifndef TILE_MINB
 #define TILE_MINB 2    // __launch_bounds__ min blocks per SM (register budget knob)
@@ -71,16 +71,20 @@ namespace {
 constexpr int TX = 32;
 constexpr uint32_t ABSENT = 0xffffffffu;       // order key of a tile slot outside the grid
 constexpr uint64_t EMPTY = ~0ull;
-// tile of NV vertices, NV / 8 threads (8 vertices each), basin-pair table of 2 NV slots
+// tile of NV vertices, NV / 8 threads (8 vertices each), basin-pair table of 1.5 NV slots
+// (2 NV without the staging buffers), staging buffer of 128 entries per warp
+constexpr int table_slots(int nv) { return LIST_STAGE ? 3 * nv / 2 : 2 * nv; }
 template <int NV>
-constexpr size_t smem_bytes() { return size_t(NV) * 8 + size_t(NV) * 4 + size_t(2 * NV) * 8; }
+constexpr size_t smem_bytes() {
+    return size_t(NV) * 8 + size_t(NV) * 4 + size_t(table_slots(NV)) * 8 + (LIST_STAGE ? size_t(NV) * 4 : 0);
+}
 
 template <int TABLE>
 __device__ __forceinline__ uint32_t pair_hash(uint32_t p) {
     p ^= p >> 13;
     p *= 0x5bd1e995u;
     p ^= p >> 15;
-    return p & (TABLE - 1);
+    return uint32_t((uint64_t(p) * TABLE) >> 32);
 }
 
 __device__ __forceinline__ uint32_t c_v(uint64_t c) { return uint32_t(c) & 0xffffu; }
@@ -105,7 +109,7 @@ __device__ __forceinline__ uint64_t scas64(uint64_t* p, uint64_t cmp, uint64_t v
     return atomicCAS(reinterpret_cast<unsigned long long*>(p), cmp, val);
 }
 
-template <int TY, int TZ, bool STATS, int NV = TX * TY * TZ, int THREADS = NV / 8, int TABLE = 2 * NV>
+template <int TY, int TZ, bool STATS, int NV = TX * TY * TZ, int THREADS = NV / 8, int TABLE = table_slots(NV)>
 __global__ void __launch_bounds__(THREADS, TILE_MINB)
 tile_tmt_kernel(const float* __restrict__ f, Cell* __restrict__ C, uint32_t* __restrict__ basin_out, uint32_t nx,
                 uint32_t ny, uint32_t z_begin,
@@ -266,9 +270,82 @@ tile_tmt_kernel(const float* __restrict__ f, Cell* __restrict__ C, uint32_t* __r
     // L' joins vertices that are already connected at L' through their descent paths and
     // that lowest edge (DESIGN.md derivation C'').  A shared-memory hash table keyed by the
     // basin pair keeps, per pair, the edge's upper endpoint of lowest key.
+    const int lane_c = threadIdx.x & 31;
+    // keep, per basin pair, the edge of lowest level (entry = pair << 12 | upper endpoint)
+    auto insert_entry = [&](uint64_t entry) {
+        const uint32_t pair = uint32_t(entry >> 12);
+        const uint64_t kh = key48(ord, uint32_t(entry) & 0xfffu);
+        uint32_t h = pair_hash<TABLE>(pair);
+        for (uint32_t probe = 0;;) {
+            const uint64_t cur = sld64(table + h);
+            if (cur == EMPTY) {
+                if (scas64(table + h, EMPTY, entry) == EMPTY) break;
+                continue;                                        // lost the slot: re-read it
+            }
+            if (uint32_t(cur >> 12) != pair) {
+                h = h + 1 == uint32_t(TABLE) ? 0u : h + 1;
+                if (++probe < uint32_t(TABLE)) continue;
+                // table full (e.g. a checkerboard: every vertex pair of basins is adjacent):
+                // record the edge in the overflow flag; phase d' merges all edges then
+                s_overflow = 1;
+                break;
+            }
+            if (kh >= key48(ord, uint32_t(cur) & 0xfffu)) break;  // the stored edge is lower
+            if (scas64(table + h, cur, entry) == cur) break;
+        }
+    };
+    // the in-tile edge (u, w) in direction d (+x, +y, +z) if its ends lie in two basins
+    auto candidate = [&](uint32_t u, uint32_t ou, uint32_t bu, bool ok, uint32_t off, uint64_t* entry) {
+        if (ou == ABSENT || !ok) return false;
+        const uint32_t w = u + off;
+        const uint32_t ow = ord[w];
+        if (ow == ABSENT) return false;
+        const uint32_t bw = c_v(cell[w]);
+        if (bw == bu) return false;
+        const uint32_t hi = ((uint64_t(ow) << 16) | w) < ((uint64_t(ou) << 16) | u) ? u : w;
+        const uint32_t pair = bu < bw ? (bu << 12) | bw : (bw << 12) | bu;
+        *entry = (uint64_t(pair) << 12) | hi;
+        return true;
+    };
+#if LIST_STAGE
+    // each warp lists the edges of its own rows into a 128-entry staging buffer (ballot +
+    // popc) and inserts them 32 at a time, so the insert code runs with every lane busy
+    // (about 40 % of the in-tile edges join two basins)
+    if (TILE_STOP == 0 || TILE_STOP > 2) {
+        uint64_t* stage = reinterpret_cast<uint64_t*>(smem + NV * 12 + TABLE * 8) + (threadIdx.x >> 5) * 128;
+        const uint32_t lt = (1u << lane_c) - 1u;
+        uint32_t nst = 0;
+#pragma unroll 1
+        for (int k = 0; k < PER; ++k) {
+            const int r = r0 + k * RSTEP;
+            const int ly = r % TY, lz = r / TY;
+            const uint32_t u = r * TX + lx;
+            const uint32_t ou = ord[u];
+            const uint32_t bu = c_v(cell[u]);      // basin (a minimum points at itself)
+            const bool ok[3] = {lx + 1 < TX, ly + 1 < TY, lz + 1 < TZ};
+            const uint32_t off[3] = {1u, uint32_t(TX), uint32_t(TX * TY)};
+#pragma unroll
+            for (int d = 0; d < 3; ++d) {
+                uint64_t entry = 0;
+                const bool valid = candidate(u, ou, bu, ok[d], off[d], &entry);
+                const uint32_t m = __ballot_sync(FULL_MASK, valid);
+                if (valid) stage[nst + __popc(m & lt)] = entry;
+                nst += __popc(m);
+                if (STATS && valid) ++n_edges;
+            }
+            __syncwarp();
+            while (nst >= 32) {
+                const uint64_t e = stage[nst - 32 + lane_c];
+                __syncwarp();
+                nst -= 32;
+                insert_entry(e);
+            }
+        }
+        if (uint32_t(lane_c) < nst) insert_entry(stage[lane_c]);
+    }
+#else
     // rows of 32 vertices are handed out dynamically (a warp per row) so that warps with
     // contended inserts do not hold the barrier for the others
-    const int lane_c = threadIdx.x & 31;
 #pragma unroll 1
     while (TILE_STOP == 0 || TILE_STOP > 2) {
         int r = 0;
@@ -283,54 +360,13 @@ tile_tmt_kernel(const float* __restrict__ f, Cell* __restrict__ C, uint32_t* __r
         const uint32_t off[3] = {1u, uint32_t(TX), uint32_t(TX * TY)};
 #pragma unroll
         for (int d = 0; d < 3; ++d) {
-            constexpr uint32_t NONE = 0xffffffffu;
-            uint32_t pair = NONE, hi = 0;
-            uint64_t kh = 0;                    // key of the edge's upper endpoint (its level)
-            if (ou != ABSENT && ok[d]) {
-                const uint32_t w = u + off[d];
-                const uint32_t ow = ord[w];
-                if (ow != ABSENT) {
-                    const uint32_t bw = c_v(cell[w]);
-                    if (bw != bu) {
-                        const uint64_t ku = (uint64_t(ou) << 16) | u, kw = (uint64_t(ow) << 16) | w;
-                        hi = kw < ku ? u : w;
-                        kh = kw < ku ? ku : kw;
-                        pair = bu < bw ? (bu << 12) | bw : (bw << 12) | bu;
-                    }
-                }
-            }
-            if (LIST_DEDUPE && d > 0) {
-                // y/z edges of neighbouring lanes often join the same two basins: an edge with
-                // a lower one of the same pair in the next or previous lane is dropped (the
-                // lowest edge of every run survives, and the table keeps the lowest per pair)
-                const uint32_t pu = __shfl_up_sync(FULL_MASK, pair, 1), pd = __shfl_down_sync(FULL_MASK, pair, 1);
-                const uint64_t ku = __shfl_up_sync(FULL_MASK, kh, 1), kd = __shfl_down_sync(FULL_MASK, kh, 1);
-                if (pair != NONE && ((lane_c > 0 && pu == pair && ku < kh) || (lane_c < 31 && pd == pair && kd < kh)))
-                    pair = NONE;
-            }
-            if (pair == NONE) continue;
+            uint64_t entry = 0;
+            if (!candidate(u, ou, bu, ok[d], off[d], &entry)) continue;
             if (STATS) ++n_edges;
-            const uint64_t entry = (uint64_t(pair) << 12) | hi;
-            uint32_t h = pair_hash<TABLE>(pair);
-            for (uint32_t probe = 0;;) {
-                const uint64_t cur = sld64(table + h);
-                if (cur == EMPTY) {
-                    if (scas64(table + h, EMPTY, entry) == EMPTY) break;
-                    continue;                                        // lost the slot: re-read it
-                }
-                if (uint32_t(cur >> 12) != pair) {
-                    h = (h + 1) & (TABLE - 1);
-                    if (++probe < TABLE) continue;
-                    // table full (e.g. a checkerboard: every vertex pair of basins is adjacent):
-                    // record the edge in the overflow flag; phase d' merges all edges then
-                    s_overflow = 1;
-                    break;
-                }
-                if (kh >= key48(ord, uint32_t(cur) & 0xfffu)) break;  // the stored edge is lower
-                if (scas64(table + h, cur, entry) == cur) break;
-            }
+            insert_entry(entry);
         }
     }
+#endif
     __syncthreads();
     phase_time(ST_CYC_LIST);
 
