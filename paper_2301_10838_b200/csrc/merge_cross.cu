@@ -129,6 +129,9 @@ dedupe_cross_kernel(const float* __restrict__ f, const uint32_t* __restrict__ ba
     if (stats) atomicAdd(stats + ST_EDGES, n_edges);
 }
 
+#ifndef MQ_WALK
+#define MQ_WALK 1         // filter walks (with path splitting) before Alg. 3
+#endif
 #ifndef MQ_MIN_BLOCKS
 #define MQ_MIN_BLOCKS 6   // 6 x 256 threads per SM: <= 42 registers, 48 warps of loads in flight
 #endif
@@ -174,6 +177,12 @@ merge_queue_kernel(Cell* C, const QEntry* __restrict__ q, uint64_t cap, const un
                     lo = en.m_lo;
                     has_prev = false;
                     phase = CLIMB_HI;
+                    if (!MQ_WALK) {                   // Merge(T, R_hi, hi, R_lo) straight away
+                        u = en.m_hi;
+                        v = en.m_lo;
+                        ks = L;
+                        phase = MERGE_LD;
+                    }
                     if (STATS) n_edges++;
                 } else if (exhausted) {
                     phase = DONE;

@@ -49,6 +49,9 @@ namespace {
 #ifndef TILE_STOP
 #define TILE_STOP 0    // timing only (WRONG results): run phases < k: 1 load+descent, 2 +compress, 3 +list, 4 +merge
 #endif
+#ifndef TILE_WALK
+#define TILE_WALK 0    // merge phase: filter walks (with path splitting) before Alg. 3
+#endif
 #ifndef LIST_STAGE
 #define LIST_STAGE 1   // list phase: per-warp staging of the candidate edges, inserts 32 at a time
 #endif
@@ -500,6 +503,12 @@ tile_tmt_kernel(const float* __restrict__ f, Cell* __restrict__ C, uint32_t* __r
                     lo = bh == ba ? bb : ba;
                     has_prev = false;
                     ph = P_W0;
+                    if (!TILE_WALK) {                     // Merge(T, bh, hi, bl) straight away
+                        mu = bh;
+                        mv = lo;
+                        S = L;
+                        ph = P_A3;
+                    }
                 } else {
                     ph = P_DONE;
                 }
