@@ -37,6 +37,10 @@ namespace mt {
 
 namespace {
 
+#ifndef DC_MATCH
+#define DC_MATCH 1        // dedupe_cross: whole-warp groups by __match_any_sync (else neighbour lanes)
+#endif
+
 struct CrossGeom {
     uint32_t nx, ny, nz, tx, ty, tz;   // slab (nz = local planes) and tile shape
     uint64_t base;                     // global id of the slab's first vertex
@@ -101,14 +105,23 @@ dedupe_cross_kernel(const float* __restrict__ f, const uint32_t* __restrict__ ba
             pair = ba < bb ? (uint64_t(ba) << 32 | bb) : (uint64_t(bb) << 32 | ba);
             ++n_edges;
         }
-        // lanes with the same basin pair keep the lowest edge only
-        const uint32_t group = __match_any_sync(FULL_MASK, pair);
+        // lanes with the same pair keep the lowest edge only
         bool keep = valid;
+#if DC_MATCH
+        const uint32_t group = __match_any_sync(FULL_MASK, pair);
 #pragma unroll 4
         for (int j = 0; j < 32; ++j) {
             const uint64_t Lj = __shfl_sync(FULL_MASK, en.L, j);
             if (((group >> j) & 1u) && Lj < en.L) keep = false;
         }
+#else
+        {   // (cheaper) neighbouring lanes only: an edge with a lower one of the same pair in the
+            // previous or next lane is dropped; the lowest of every run of lanes survives
+            const uint64_t pu = __shfl_up_sync(FULL_MASK, pair, 1), pd = __shfl_down_sync(FULL_MASK, pair, 1);
+            const uint64_t lu = __shfl_up_sync(FULL_MASK, en.L, 1), ld = __shfl_down_sync(FULL_MASK, en.L, 1);
+            if ((lane > 0 && pu == pair && lu < en.L) || (lane < 31 && pd == pair && ld < en.L)) keep = false;
+        }
+#endif
         const uint32_t km = __ballot_sync(FULL_MASK, keep);
         if (lane == 0) s_warp[warp] = __popc(km);
         __syncthreads();
