@@ -94,7 +94,7 @@ struct BrickGeom {
     uint32_t by, bx_n, by_n;   // brick rows along y; bricks along x and y (brick mode)
 };
 
-template <class View, bool LINEAR>
+template <class View, int BY>
 __global__ void __launch_bounds__(RB_THREADS, MT_REPAIR_MINB)
 repair_brick_kernel(View view, const Cell* C, uint64_t* __restrict__ T, const float* __restrict__ f, Slab sl,
                     BrickGeom g, uint32_t flip, mt_pair* __restrict__ stage, uint64_t stage_cap,
@@ -102,6 +102,8 @@ repair_brick_kernel(View view, const Cell* C, uint64_t* __restrict__ T, const fl
                     unsigned long long* __restrict__ counters, unsigned long long* __restrict__ stats) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     RepairSmem& S = *reinterpret_cast<RepairSmem*>(smem_raw);
+    constexpr bool LINEAR = BY == 0;       // id-range bricks (graphs, thin grids)
+    constexpr uint32_t BYD = LINEAR ? 1u : uint32_t(BY);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t lt = (1u << lane) - 1u;
 
@@ -115,8 +117,8 @@ repair_brick_kernel(View view, const Cell* C, uint64_t* __restrict__ T, const fl
         const uint32_t b = blockIdx.x;
         bxi = b % g.bx_n;
         x0 = bxi * 32;
-        y0 = ((b / g.bx_n) % g.by_n) * g.by;
-        z0 = sl.z_begin + (b / g.bx_n / g.by_n) * (RB_ROWS / g.by);
+        y0 = ((b / g.bx_n) % g.by_n) * BYD;
+        z0 = sl.z_begin + (b / g.bx_n / g.by_n) * (RB_ROWS / BYD);
     }
     // the warp's rows (item k = row warp + 16 k): first id, valid lanes and segment number, computed
     // once by lanes 0..RB_PER-1 (integer divisions) and read back from shared memory
@@ -130,7 +132,7 @@ repair_brick_kernel(View view, const Cell* C, uint64_t* __restrict__ T, const fl
             lim = left > 32 ? 32u : uint32_t(left);
             seg = seg0 + r;
         } else {
-            const uint32_t y = y0 + r % g.by, z = z0 + r / g.by;
+            const uint32_t y = y0 + r % BYD, z = z0 + r / BYD;
             rb = (uint64_t(z) * sl.ny + y) * sl.nx + x0;
             lim = (y < sl.ny && z < sl.z_end) ? min(32u, sl.nx - x0) : 0u;
             seg = (uint64_t(z - sl.z_begin) * sl.ny + y) * g.bx_n + bxi;
@@ -151,9 +153,11 @@ repair_brick_kernel(View view, const Cell* C, uint64_t* __restrict__ T, const fl
     // diagram records of each row: finite pairs (s != u) and roots (v == u)
 #define FMASK(k) __ballot_sync(FULL_MASK, INB(k) && cs_of(cell[k]) != uint32_t(UID(k)))
 #define EMASK(k) __ballot_sync(FULL_MASK, INB(k) && cv_of(cell[k]) == uint32_t(UID(k)))
+    uint32_t recbits = 0;     // rows k where this lane holds a finite pair (bit k) / a root (bit 8 + k)
 #pragma unroll
     for (int k = 0; k < RB_PER; ++k) {
         const uint32_t fm = FMASK(k), em = EMASK(k);
+        recbits |= (((fm >> lane) & 1u) << k) | (((em >> lane) & 1u) << (8 + k));
         if (lane == 0) {
             S.rowcnt[warp + 16 * k] = __popc(fm) | (__popc(em) << 16);
             S.rowfm[warp + 16 * k] = fm;
@@ -198,31 +202,41 @@ repair_brick_kernel(View view, const Cell* C, uint64_t* __restrict__ T, const fl
     }
     __syncthreads();   // staging base and row offsets in
 
-    // staging records of every row, in id order within the row: finite pairs, then roots
+    // staging records of every row, in id order within the row: finite pairs, then roots.
+    // Lanes 0..7 publish the counts and staging offsets of the warp's 8 rows; then every lane
+    // stages only its own records (few: ~5 % of the vertices at c5), so the record code runs
+    // max-over-lanes times instead of once per row
     const uint32_t sbase = S.base;
-#pragma unroll
-    for (int k = 0; k < RB_PER; ++k) {
-        const int r = warp + 16 * k;
-        const uint32_t fm = S.rowfm[r], em = S.rowem[r];
-        const bool isf = (fm >> lane) & 1u, ise = (em >> lane) & 1u;
-        if (lane == 0 && INB(k)) {
-            // every row holding a vertex of the grid is a segment (lane 0 is its first vertex)
+    if (lane < RB_PER) {
+        const int r = warp + 16 * lane;
+        if (S.rowlim[r] > 0) {   // every row holding a vertex of the grid is a segment
             const uint64_t seg = S.rowseg[r];
             seg_cnt[seg] = uint16_t(S.rowcnt[r] & 0xffffu) | uint16_t((S.rowcnt[r] >> 16) << 8);
             seg_pos[seg] = sbase + S.rowoff[r];
         }
-        if (!(isf || ise)) continue;
-        const uint64_t u = UID(k);
+    }
+    uint32_t rm = (recbits | (recbits >> 8)) & 0xffu;
+#pragma unroll 1
+    while (rm) {
+        const int k = __ffs(rm) - 1;
+        rm &= rm - 1;
+        const int r = warp + 16 * k;
+        const uint32_t fm = S.rowfm[r], em = S.rowem[r];
+        const bool isf = (recbits >> k) & 1u;
+        const uint64_t u = S.rowbase[r] + lane;
+        // this row's cell again (an L1 hit: loaded above through the non-coherent path) rather
+        // than a dynamically indexed register array
+        const Cell cu = ld_cell_ro(C + u);
+        const uint32_t s = cs_of(cu), ou = uint32_t(cu.hi >> 32), os = uint32_t(cu.lo >> 32);
         const uint64_t pos = uint64_t(sbase) + S.rowoff[r] +
                              (isf ? __popc(fm & lt) : __popc(fm) + __popc(em & lt));
         mt_pair rec;
         if (isf) {
-            const uint32_t s = cs_of(cell[k]);
             // values f[u] and f[s]: the cell carries ord(f[u]) (hi) and ord(f[s]) (lo); invert
             // them (exact for every value but zero, whose sign the canonicalisation -0 -> +0
             // dropped: gather those, reading R14)
-            const uint32_t bb = inv_ord(uint32_t(cell[k].hi >> 32) ^ flip);
-            const uint32_t db = inv_ord(uint32_t(cell[k].lo >> 32) ^ flip);
+            const uint32_t bb = inv_ord(ou ^ flip);
+            const uint32_t db = inv_ord(os ^ flip);
             rec = mt_pair{uint32_t(u), s, bb == 0u ? __ldg(f + u) : __uint_as_float(bb),
                           db == 0u ? view.value(f, s) : __uint_as_float(db)};
         } else {
@@ -375,16 +389,16 @@ __global__ void finish_diagram_kernel(unsigned long long* __restrict__ counters,
     }
 }
 
-template <class View, bool LINEAR>
+template <class View, int BY>
 void launch_brick(const View& view, const Cell* C, uint64_t* T, const float* f, const Slab& sl, BrickGeom g,
                   uint64_t nb, uint32_t flip, const RepairOut& o, unsigned long long* stats, cudaStream_t stream) {
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(repair_brick_kernel<View, LINEAR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(repair_brick_kernel<View, BY>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              int(sizeof(RepairSmem)));
         attr = true;
     }
-    repair_brick_kernel<View, LINEAR><<<uint32_t(nb), RB_THREADS, sizeof(RepairSmem), stream>>>(
+    repair_brick_kernel<View, BY><<<uint32_t(nb), RB_THREADS, sizeof(RepairSmem), stream>>>(
         view, C, T, f, sl, g, flip, o.stage, o.stage_cap, o.seg_cnt, o.seg_pos, o.counters, stats);
 }
 
@@ -413,8 +427,9 @@ void launch_repair_view(const View& view, const Cell* C, uint64_t* T, const floa
                         const RepairOut& o, unsigned long long* stats, cudaStream_t stream) {
     BrickGeom g;
     uint64_t nb, nseg;
-    if (brick_mode(sl, &g, &nb, &nseg)) launch_brick<View, false>(view, C, T, f, sl, g, nb, flip, o, stats, stream);
-    else launch_brick<View, true>(view, C, T, f, sl, g, nb, flip, o, stats, stream);
+    if (!brick_mode(sl, &g, &nb, &nseg)) launch_brick<View, 0>(view, C, T, f, sl, g, nb, flip, o, stats, stream);
+    else if (g.by == 16) launch_brick<View, 16>(view, C, T, f, sl, g, nb, flip, o, stats, stream);
+    else launch_brick<View, 128>(view, C, T, f, sl, g, nb, flip, o, stats, stream);
 }
 
 }  // namespace
