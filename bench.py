@@ -334,15 +334,19 @@ def run_mt(args, rank, world):
     local_dims = (dims[0], dims[1], n_local // (dims[0] * dims[1]))
     alg = ALG_BYTES[dom](n_local, recs * n_local // n_global, _ecross(local_dims))
     achieved = alg / (avg[dom] * 1e-3) / 1e9
-    traffic = None
+    traffic, issue = None, None
     prof_path = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(prof_path):
         try:
-            traffic = json.load(open(prof_path)).get(args.config, {}).get(dom)
+            prof = json.load(open(prof_path))
+            traffic = prof.get(args.config, {}).get(dom)
+            issue = prof.get("issue", {}).get(args.config, {}).get(dom)
         except Exception:
-            traffic = None
+            traffic, issue = None, None
     roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
+                # what actually bounds the kernel (ncu, profiles/traffic.json): instruction issue
+                "issue": issue,
                 "alg_bytes_per_launch": alg, "kernel_ms": avg[dom],
                 "kernel_share_of_step": avg[dom] / ms_per_step,
                 "kernels_ms": avg,

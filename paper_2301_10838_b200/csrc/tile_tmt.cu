@@ -49,6 +49,9 @@ namespace {
 #ifndef TILE_STOP
 #define TILE_STOP 0    // timing only (WRONG results): run phases < k: 1 load+descent, 2 +compress, 3 +list, 4 +merge
 #endif
+#ifndef TILE_LEAN
+#define TILE_LEAN 1    // merge phase: Alg. 3 only, no phase variable (requires TILE_OWNRUN)
+#endif
 #ifndef TILE_WALK
 #define TILE_WALK 0    // merge phase: filter walks (with path splitting) before Alg. 3
 #endif
@@ -305,9 +308,11 @@ tile_tmt_kernel(const float* __restrict__ f, Cell* __restrict__ C, uint32_t* __r
         if (ow == ABSENT) return false;
         const uint32_t bw = c_v(cell[w]);
         if (bw == bu) return false;
-        const uint32_t hi = ((uint64_t(ow) << 16) | w) < ((uint64_t(ou) << 16) | u) ? u : w;
+        const bool u_hi = ((uint64_t(ow) << 16) | w) < ((uint64_t(ou) << 16) | u);
+        const uint32_t hi = u_hi ? u : w;
         const uint32_t pair = bu < bw ? (bu << 12) | bw : (bw << 12) | bu;
-        *entry = (uint64_t(pair) << 12) | hi;
+        // bit 63: the upper endpoint lies in the pair's first (smaller) basin
+        *entry = (uint64_t(pair) << 12) | hi | (uint64_t((u_hi ? bu : bw) == (bu < bw ? bu : bw)) << 63);
         return true;
     };
 #if LIST_STAGE
@@ -467,6 +472,62 @@ tile_tmt_kernel(const float* __restrict__ f, Cell* __restrict__ C, uint32_t* __r
         return table[w * REG + (j - s_wpre[w])];
     };
 #endif
+#if TILE_LEAN
+    // d1. Alg. 3 per lane, one iteration (the two cell loads, + the CAS) per loop iteration; a
+    // lane whose pair is done takes the next pair of the warp's run at the top of the next
+    // iteration (ballot + popc), so the lanes of a warp stay busy and converged instead of
+    // waiting for the longest merge of the warp.  Merge(T, bh, hi, bl) starts straight from
+    // the two basins (bh holds the edge's upper endpoint hi, level L = key(hi)).
+    bool busy = false;
+    uint64_t S = 0;
+    uint32_t mu = 0, mv = 0, run_pos = 0;
+#pragma unroll 1
+    while (true) {
+        const uint32_t need = __ballot_sync(FULL_MASK, !busy);
+        if (need) {
+            if (!busy) {
+                const uint32_t j = run_pos + __popc(need & ((1u << lane_c) - 1u));
+                if (j < run_len) {
+                    const uint64_t e = run[j];
+                    if (STATS) ++n_pairs;
+                    const uint32_t pair = uint32_t(e >> 12) & 0xffffffu, hi = uint32_t(e) & 0xfffu;
+                    const uint32_t ba = pair >> 12, bb = pair & 0xfffu;
+                    const bool first = e >> 63;
+                    mu = first ? ba : bb;
+                    mv = first ? bb : ba;
+                    S = key48(ord, hi);
+                    busy = true;
+                }
+            }
+            run_pos += __popc(need);
+        }
+        if (!__any_sync(FULL_MASK, busy)) break;
+        if (busy) {
+            if (STATS) ++n_iters;
+            const uint64_t cu = sld64(cell + mu), cv = sld64(cell + mv);
+            if (c_v(cu) != mu && c_key(cu) < S) {         // l.2-4 + R4
+                mu = c_v(cu);
+            } else if (c_v(cv) != mv && c_key(cv) < S) {  // l.5-8 + R4
+                mv = c_v(cv);
+            } else if (mu == mv) {                        // l.9-10
+                busy = false;
+            } else {
+                uint32_t uu = mu, vv = mv;
+                uint64_t cvv = cv;
+                if (key48(ord, mv) < key48(ord, mu)) { uu = mv; vv = mu; cvv = cu; }   // l.11-12
+                const uint64_t got = scas64(cell + vv, cvv, (S << 16) | uu);          // l.14
+                mu = uu;
+                if (got == cvv) {
+                    if (c_v(cvv) == vv) busy = false;      // R5: displaced a root
+                    S = c_key(cvv);                       // l.15: Merge(T, u, s_v, v')
+                    mv = c_v(cvv);
+                } else {
+                    mv = vv;                              // l.17: restart
+                }
+            }
+        }
+    }
+#else
     // d1. one state machine per lane, advanced by one shared-memory round trip per loop
     // iteration (a walk step, the pair of Alg. 3 loads (+ CAS)); a lane whose pair is done
     // takes the next listed pair at the top of the next iteration, so the lanes of a warp
@@ -569,6 +630,7 @@ tile_tmt_kernel(const float* __restrict__ f, Cell* __restrict__ C, uint32_t* __r
             }
         }
     }
+#endif
     if (s_overflow) {  // (uniform: written before the last barrier) the table dropped edges
 #pragma unroll 1
         for (int k = 0; k < PER; ++k) {
