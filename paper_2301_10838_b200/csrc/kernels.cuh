@@ -70,14 +70,17 @@ __device__ __forceinline__ bool forest_value(const ForestRef& F, uint32_t id, ui
 void tile_shape(uint32_t nz_global, uint32_t* ty, uint32_t* tz);
 
 // K1 + K2 + in-tile K3/K4: keys, steepest descent, tile-local merge tree (tile_tmt.cu)
-void launch_tile_tmt(const float* f, Cell* C, uint32_t* basin, const Slab& sl, uint32_t flip,
+// x-face records of the tiles (2 faces x rows per tile, 8 B each: order key << 32 | R)
+uint64_t xface_entries(const Slab& sl);
+void launch_tile_tmt(const float* f, Cell* C, uint32_t* basin, uint64_t* xface, const Slab& sl, uint32_t flip,
                      unsigned long long* counters, unsigned long long* stats, cudaStream_t stream);
 
 // K3: merge of the tile-crossing grid edges on the global store (merge_cross.cu)
 uint64_t cross_edges(const Slab& sl);
 size_t cross_queue_entry_bytes();
 // returns 0 when the slab has a single tile (no crossing edges, no kernel launched)
-int launch_dedupe_cross(const float* f, const uint32_t* basin, const Slab& sl, uint32_t flip, void* queue,
+int launch_dedupe_cross(const float* f, const uint32_t* basin, const uint64_t* xface, const Slab& sl, uint32_t flip,
+                        void* queue,
                         uint64_t cap, unsigned long long* qlen, unsigned long long* stats, int num_sms,
                         cudaStream_t stream);
 

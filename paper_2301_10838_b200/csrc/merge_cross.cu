@@ -37,12 +37,16 @@ namespace mt {
 
 namespace {
 
+#ifndef DC_XFACE
+#define DC_XFACE 1        // x-face edges read tile_tmt's compact face records
+#endif
 #ifndef DC_MATCH
 #define DC_MATCH 1        // dedupe_cross: whole-warp groups by __match_any_sync (else neighbour lanes)
 #endif
 
 struct CrossGeom {
     uint32_t nx, ny, nz, tx, ty, tz;   // slab (nz = local planes) and tile shape
+    uint32_t tiles_x, tiles_y;         // tiles along x and y
     uint64_t base;                     // global id of the slab's first vertex
     uint64_t ex, ey, ez;               // number of crossing edges on x-, y-, z-faces
 };
@@ -82,7 +86,8 @@ struct QEntry {
 };
 
 __global__ void __launch_bounds__(256)
-dedupe_cross_kernel(const float* __restrict__ f, const uint32_t* __restrict__ basin, CrossGeom g, uint32_t flip,
+dedupe_cross_kernel(const float* __restrict__ f, const uint32_t* __restrict__ basin,
+                    const uint64_t* __restrict__ xface, CrossGeom g, uint32_t flip,
                     QEntry* __restrict__ q, uint64_t cap, unsigned long long* __restrict__ qlen,
                     unsigned long long* __restrict__ stats) {
     __shared__ uint32_t s_warp[8];
@@ -99,8 +104,28 @@ dedupe_cross_kernel(const float* __restrict__ f, const uint32_t* __restrict__ ba
         if (valid) {
             uint32_t a, b;
             decode_edge(g, e, &a, &b);
-            const uint64_t ka = key_of(ord32(__ldg(f + a)) ^ flip, a), kb = key_of(ord32(__ldg(f + b)) ^ flip, b);
-            const uint32_t ba = __ldg(basin + a), bb = __ldg(basin + b);
+            uint64_t ka, kb;
+            uint32_t ba, bb;
+            if (DC_XFACE && e < g.ex) {
+                // x-face edge: both ends from tile_tmt's compact face records (order key, R)
+                // -- in the grid they sit 128 B apart, one line per lane
+                const uint32_t ee = uint32_t(e), per = g.ny * g.nz;
+                const uint32_t k = ee / per, rr = ee - k * per;
+                const uint32_t z = rr / g.ny, y = rr - z * g.ny;
+                const uint32_t rows = g.ty * g.tz, row = (z % g.tz) * g.ty + y % g.ty;
+                const uint64_t t = k + uint64_t(g.tiles_x) * (y / g.ty + uint64_t(g.tiles_y) * (z / g.tz));
+                const uint64_t ea = __ldg(xface + (t * 2 + 1) * rows + row);        // right face of tile k
+                const uint64_t eb = __ldg(xface + ((t + 1) * 2) * rows + row);      // left face of tile k + 1
+                ka = key_of(uint32_t(ea >> 32), a);
+                kb = key_of(uint32_t(eb >> 32), b);
+                ba = uint32_t(ea);
+                bb = uint32_t(eb);
+            } else {
+                ka = key_of(ord32(__ldg(f + a)) ^ flip, a);
+                kb = key_of(ord32(__ldg(f + b)) ^ flip, b);
+                ba = __ldg(basin + a);
+                bb = __ldg(basin + b);
+            }
             en = ka > kb ? QEntry{ka, ba, bb} : QEntry{kb, bb, ba};
             pair = ba < bb ? (uint64_t(ba) << 32 | bb) : (uint64_t(bb) << 32 | ba);
             ++n_edges;
@@ -282,7 +307,8 @@ merge_queue_kernel(Cell* C, const QEntry* __restrict__ q, uint64_t cap, const un
 
 }  // namespace
 
-int launch_dedupe_cross(const float* f, const uint32_t* basin, const Slab& sl, uint32_t flip, void* queue,
+int launch_dedupe_cross(const float* f, const uint32_t* basin, const uint64_t* xface, const Slab& sl, uint32_t flip,
+                        void* queue,
                         uint64_t cap, unsigned long long* qlen, unsigned long long* stats, int num_sms,
                         cudaStream_t stream) {
     CrossGeom g{};
@@ -292,6 +318,8 @@ int launch_dedupe_cross(const float* f, const uint32_t* basin, const Slab& sl, u
     g.base = sl.base;
     g.tx = 32;
     tile_shape(sl.nz, &g.ty, &g.tz);
+    g.tiles_x = (g.nx + g.tx - 1) / g.tx;
+    g.tiles_y = (g.ny + g.ty - 1) / g.ty;
     const uint64_t kx = (g.nx + g.tx - 1) / g.tx - 1, ky = (g.ny + g.ty - 1) / g.ty - 1,
                    kz = g.nz ? (g.nz + g.tz - 1) / g.tz - 1 : 0;
     g.ex = g.nz ? kx * g.ny * g.nz : 0;
@@ -302,7 +330,7 @@ int launch_dedupe_cross(const float* f, const uint32_t* basin, const Slab& sl, u
     QEntry* q = static_cast<QEntry*>(queue);
     uint64_t blocks = (total + 255) / 256;
     if (blocks > uint64_t(num_sms) * 32) blocks = uint64_t(num_sms) * 32;
-    dedupe_cross_kernel<<<uint32_t(blocks), 256, 0, stream>>>(f, basin, g, flip, q, cap, qlen, stats);
+    dedupe_cross_kernel<<<uint32_t(blocks), 256, 0, stream>>>(f, basin, xface, g, flip, q, cap, qlen, stats);
     return 1;
 }
 

@@ -24,7 +24,7 @@ constexpr int MAX_EVENTS = 12;
 size_t align_up(size_t x) { return (x + ALIGN - 1) / ALIGN * ALIGN; }
 
 struct Layout {
-    size_t counters, status, status_bytes, stats, ess, cells, basin, queue, pairs, stage, seg_cnt, seg_pos, flags, recs,
+    size_t counters, status, status_bytes, stats, ess, cells, basin, xface, queue, pairs, stage, seg_cnt, seg_pos, flags, recs,
         total;
     uint64_t pairs_cap, recs_cap, queue_cap, ess_cap, seg_cap;
 };
@@ -38,7 +38,7 @@ bool valid_dims(const uint32_t dims[3], int conn) {
 
 // n vertices; ncross queue entries; ess_cap essential records (components);
 // slab: add the boundary-forest buffers
-Layout layout_for(uint64_t n, uint64_t ncross, bool slab = false, uint64_t ess_cap = ESS_CAP) {
+Layout layout_for(uint64_t n, uint64_t ncross, bool slab = false, uint64_t ess_cap = ESS_CAP, uint64_t nxface = 0) {
     Layout L{};
     // records = #minima.  On a grid the strict minima form an independent set,
     // so at most ceil(n/2) (+1 slack); a general graph (ess_cap = n) may have n.
@@ -61,6 +61,8 @@ Layout layout_for(uint64_t n, uint64_t ncross, bool slab = false, uint64_t ess_c
     off += align_up(n * sizeof(mt::Cell));
     L.basin = off;  // descent basin of every vertex (tile_tmt -> dedupe_cross)
     off += align_up(n * sizeof(uint32_t));
+    L.xface = off;  // x-face records of the tiles (tile_tmt -> dedupe_cross)
+    off += align_up(nxface * sizeof(uint64_t));
     L.queue = off;  // deduplicated tile-crossing edges
     L.queue_cap = ncross;
     off += align_up(ncross * mt::cross_queue_entry_bytes());
@@ -81,6 +83,13 @@ Layout layout_for(uint64_t n, uint64_t ncross, bool slab = false, uint64_t ess_c
     }
     L.total = off;
     return L;
+}
+
+// workspace of a grid context owning planes [z_begin, z_end)
+Layout grid_layout(const uint32_t dims[3], uint32_t z_begin, uint32_t z_end, bool slab) {
+    const uint64_t n = uint64_t(dims[0]) * dims[1] * (z_end - z_begin);
+    const mt::Slab sl{dims[0], dims[1], dims[2], z_begin, z_end, uint64_t(dims[0]) * dims[1] * z_begin, n};
+    return layout_for(n, mt::cross_edges(sl), slab, ESS_CAP, mt::xface_entries(sl));
 }
 
 }  // namespace
@@ -184,10 +193,7 @@ mt_status create_ctx(mt_ctx** out, const uint32_t dims[3], int conn, uint32_t z_
     if (uint64_t(dims[0]) * dims[1] * dims[2] > 0xffffffffull) return MT_ERR_TOO_LARGE;
     const uint64_t n = uint64_t(dims[0]) * dims[1] * (z_end - z_begin);
     const Layout L = graph_layout ? *graph_layout
-                                  : layout_for(n,
-                                               mt::cross_edges(mt::Slab{dims[0], dims[1], dims[2], z_begin, z_end,
-                                                                        uint64_t(dims[0]) * dims[1] * z_begin, n}),
-                                               multi);
+                                  : grid_layout(dims, z_begin, z_end, multi);
     if (!workspace || workspace_bytes < L.total || (reinterpret_cast<uintptr_t>(workspace) % ALIGN))
         return MT_ERR_WORKSPACE;
     int ndev = 0;
@@ -243,9 +249,10 @@ mt_status start_compute(mt_ctx* c, const float* f, uint32_t flags, cudaStream_t 
         return c->sticky = MT_ERR_CUDA;
     uint32_t* basin = reinterpret_cast<uint32_t*>(c->ws + c->L.basin) - c->slab.base;
     mark(c, "tile_tmt", s);
-    mt::launch_tile_tmt(fs, cells, basin, c->slab, c->flip, ctr, stats, s);
+    uint64_t* xface = reinterpret_cast<uint64_t*>(c->ws + c->L.xface);
+    mt::launch_tile_tmt(fs, cells, basin, xface, c->slab, c->flip, ctr, stats, s);
     mark(c, "dedupe_cross", s);
-    int nl = mt::launch_dedupe_cross(fs, basin, c->slab, c->flip, c->ws + c->L.queue, c->L.queue_cap,
+    int nl = mt::launch_dedupe_cross(fs, basin, xface, c->slab, c->flip, c->ws + c->L.queue, c->L.queue_cap,
                                      ctr + mt::CTR_QLEN, stats, c->num_sms, s);
     if (nl) {
         mark(c, "merge_queue", s);
@@ -304,7 +311,7 @@ size_t mt_workspace_bytes(const uint32_t dims[3], int conn) {
     if (!valid_dims(dims, conn)) return 0;
     const uint64_t n = uint64_t(dims[0]) * dims[1] * dims[2];
     if (n > 0xffffffffull) return 0;
-    return layout_for(n, mt::cross_edges(mt::Slab{dims[0], dims[1], dims[2], 0, dims[2], 0, n})).total;
+    return grid_layout(dims, 0, dims[2], false).total;
 }
 
 mt_status mt_create(mt_ctx** out, const uint32_t dims[3], int conn, int cuda_device, void* workspace,
@@ -316,8 +323,7 @@ mt_status mt_create(mt_ctx** out, const uint32_t dims[3], int conn, int cuda_dev
 size_t mt_slab_workspace_bytes(const uint32_t dims[3], int conn, uint32_t z_begin, uint32_t z_end) {
     if (!valid_dims(dims, conn) || dims[2] < 2 || z_begin >= z_end || z_end > dims[2]) return 0;
     if (uint64_t(dims[0]) * dims[1] * dims[2] > 0xffffffffull) return 0;
-    const uint64_t n = uint64_t(dims[0]) * dims[1] * (z_end - z_begin);
-    return layout_for(n, mt::cross_edges(mt::Slab{dims[0], dims[1], dims[2], z_begin, z_end, 0, n}), true).total;
+    return grid_layout(dims, z_begin, z_end, true).total;
 }
 
 mt_status mt_create_slab(mt_ctx** out, const uint32_t dims[3], int conn, uint32_t z_begin, uint32_t z_end,

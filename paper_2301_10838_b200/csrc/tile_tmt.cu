@@ -73,6 +73,9 @@ namespace {
 #ifndef TILE_OWNRUN
 #define TILE_OWNRUN 1  // each warp merges the pairs of its own compacted run (no CTA counter)
 #endif
+#if TILE_LEAN && (TILE_WALK || !TILE_OWNRUN)
+#error "TILE_LEAN needs TILE_OWNRUN and no TILE_WALK"
+#endif
 
 constexpr int TX = 32;
 constexpr uint32_t ABSENT = 0xffffffffu;       // order key of a tile slot outside the grid
@@ -117,7 +120,8 @@ __device__ __forceinline__ uint64_t scas64(uint64_t* p, uint64_t cmp, uint64_t v
 
 template <int TY, int TZ, bool STATS, int NV = TX * TY * TZ, int THREADS = NV / 8, int TABLE = table_slots(NV)>
 __global__ void __launch_bounds__(THREADS, TILE_MINB)
-tile_tmt_kernel(const float* __restrict__ f, Cell* __restrict__ C, uint32_t* __restrict__ basin_out, uint32_t nx,
+tile_tmt_kernel(const float* __restrict__ f, Cell* __restrict__ C, uint32_t* __restrict__ basin_out,
+                uint64_t* __restrict__ xface, uint32_t nx,
                 uint32_t ny, uint32_t z_begin,
                 uint32_t z_end, uint32_t tiles_x, uint32_t tiles_y, uint32_t flip, unsigned long long* __restrict__ counters,
                 unsigned long long* __restrict__ stats) {
@@ -733,7 +737,12 @@ tile_tmt_kernel(const float* __restrict__ f, Cell* __restrict__ C, uint32_t* __r
         // the vertex the crossing-edge walks may start from: Rep_tile(u, key(u)), joined to u
         // below key(u) -- the v of a regular cell of the minimal tile store, u itself for a
         // minimum (DESIGN.md derivation C''')
-        basin_out[g] = gid(s == u ? v : u);
+        const uint32_t rep_u = gid(s == u ? v : u);
+        basin_out[g] = rep_u;
+        // the tile's x faces (lanes 0 and 31) again, compactly: (order key, R) per row, so that
+        // the crossing edges of the x faces read them coalesced (in the grid they are 128 B apart)
+        if (lx == 0 || lx == TX - 1)
+            xface[(uint64_t(b) * 2 + (lx == TX - 1)) * ROWS + r] = (uint64_t(ou) << 32) | rep_u;
 #else
         basin_out[g] = gid(bas[k]);
 #endif
@@ -750,6 +759,14 @@ tile_tmt_kernel(const float* __restrict__ f, Cell* __restrict__ C, uint32_t* __r
 }
 
 }  // namespace
+
+uint64_t xface_entries(const Slab& sl) {
+    uint32_t ty, tz;
+    tile_shape(sl.nz, &ty, &tz);
+    const uint64_t nzl = sl.z_end - sl.z_begin;
+    const uint64_t tiles = uint64_t((sl.nx + TX - 1) / TX) * ((sl.ny + ty - 1) / ty) * ((nzl + tz - 1) / tz);
+    return tiles * 2 * ty * tz;
+}
 
 int tile_vertices() {
     static int nv = 0;
@@ -772,7 +789,7 @@ void tile_shape(uint32_t nz_global, uint32_t* ty, uint32_t* tz) {
 }
 
 template <int TY, int TZ>
-void launch_tile(const float* f, Cell* C, uint32_t* basin, const Slab& sl, uint32_t tx, uint32_t tyn, uint32_t grid,
+void launch_tile(const float* f, Cell* C, uint32_t* basin, uint64_t* xface, const Slab& sl, uint32_t tx, uint32_t tyn, uint32_t grid,
                  uint32_t flip, unsigned long long* counters, unsigned long long* stats, cudaStream_t stream) {
     constexpr int NV = TX * TY * TZ;
     static bool attr = false;
@@ -784,15 +801,15 @@ void launch_tile(const float* f, Cell* C, uint32_t* basin, const Slab& sl, uint3
         attr = true;
     }
     if (stats)
-        tile_tmt_kernel<TY, TZ, true><<<grid, NV / 8, smem_bytes<NV>(), stream>>>(f, C, basin, sl.nx, sl.ny,
+        tile_tmt_kernel<TY, TZ, true><<<grid, NV / 8, smem_bytes<NV>(), stream>>>(f, C, basin, xface, sl.nx, sl.ny,
                                                                                  sl.z_begin, sl.z_end, tx, tyn,
                                                                                  flip, counters, stats);
     else
-        tile_tmt_kernel<TY, TZ, false><<<grid, NV / 8, smem_bytes<NV>(), stream>>>(f, C, basin, sl.nx, sl.ny, sl.z_begin, sl.z_end, tx,
+        tile_tmt_kernel<TY, TZ, false><<<grid, NV / 8, smem_bytes<NV>(), stream>>>(f, C, basin, xface, sl.nx, sl.ny, sl.z_begin, sl.z_end, tx,
                                                                        tyn, flip, counters, stats);
 }
 
-void launch_tile_tmt(const float* f, Cell* C, uint32_t* basin, const Slab& sl, uint32_t flip,
+void launch_tile_tmt(const float* f, Cell* C, uint32_t* basin, uint64_t* xface, const Slab& sl, uint32_t flip,
                      unsigned long long* counters, unsigned long long* stats, cudaStream_t stream) {
     uint32_t ty, tz;
     tile_shape(sl.nz, &ty, &tz);
@@ -802,13 +819,13 @@ void launch_tile_tmt(const float* f, Cell* C, uint32_t* basin, const Slab& sl, u
     if (grid == 0) return;
     const bool big = tile_vertices() == 4096;
     if (sl.nz == 1 && big)
-        launch_tile<128, 1>(f, C, basin, sl, tx, tyn, grid, flip, counters, stats, stream);
+        launch_tile<128, 1>(f, C, basin, xface, sl, tx, tyn, grid, flip, counters, stats, stream);
     else if (sl.nz == 1)
-        launch_tile<64, 1>(f, C, basin, sl, tx, tyn, grid, flip, counters, stats, stream);
+        launch_tile<64, 1>(f, C, basin, xface, sl, tx, tyn, grid, flip, counters, stats, stream);
     else if (big)
-        launch_tile<16, 8>(f, C, basin, sl, tx, tyn, grid, flip, counters, stats, stream);
+        launch_tile<16, 8>(f, C, basin, xface, sl, tx, tyn, grid, flip, counters, stats, stream);
     else
-        launch_tile<8, 8>(f, C, basin, sl, tx, tyn, grid, flip, counters, stats, stream);
+        launch_tile<8, 8>(f, C, basin, xface, sl, tx, tyn, grid, flip, counters, stats, stream);
 }
 
 }  // namespace mt
