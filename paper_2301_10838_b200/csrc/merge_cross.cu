@@ -40,6 +40,9 @@ namespace {
 #ifndef DC_XFACE
 #define DC_XFACE 1        // x-face edges read tile_tmt's compact face records
 #endif
+#ifndef DC_REDUCE
+#define DC_REDUCE 0       // group minimum by two __reduce_min_sync (else a 32-lane shuffle scan)
+#endif
 #ifndef DC_MATCH
 #define DC_MATCH 1        // dedupe_cross: whole-warp groups by __match_any_sync (else neighbour lanes)
 #endif
@@ -134,11 +137,21 @@ dedupe_cross_kernel(const float* __restrict__ f, const uint32_t* __restrict__ ba
         bool keep = valid;
 #if DC_MATCH
         const uint32_t group = __match_any_sync(FULL_MASK, pair);
+#if DC_REDUCE
+        {   // lowest L = (ord << 32 | id) of the group: min of the order keys, then of the ids
+            const uint32_t o = uint32_t(en.L >> 32), id = uint32_t(en.L);
+            const uint32_t m1 = __reduce_min_sync(group, o);
+            const uint32_t tie = group & __ballot_sync(FULL_MASK, o == m1);
+            if (o != m1) keep = false;
+            else if (id != __reduce_min_sync(tie, id)) keep = false;
+        }
+#else
 #pragma unroll 4
         for (int j = 0; j < 32; ++j) {
             const uint64_t Lj = __shfl_sync(FULL_MASK, en.L, j);
             if (((group >> j) & 1u) && Lj < en.L) keep = false;
         }
+#endif
 #else
         {   // (cheaper) neighbouring lanes only: an edge with a lower one of the same pair in the
             // previous or next lane is dropped; the lowest of every run of lanes survives
