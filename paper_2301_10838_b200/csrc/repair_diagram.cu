@@ -36,6 +36,9 @@ namespace {
 #ifndef MT_REPAIR_NC
 #define MT_REPAIR_NC 1      // the repair reads cells no thread writes: L1-cached non-coherent loads
 #endif
+#ifndef MT_REPAIR_ILP
+#define MT_REPAIR_ILP 1     // the 8 walks of a thread in lock-step rounds (else one after the other)
+#endif
 #ifndef MT_REPAIR_MINB
 #define MT_REPAIR_MINB 3    // __launch_bounds__ min blocks per SM (register budget knob)
 #endif
@@ -248,6 +251,33 @@ repair_brick_kernel(View view, const Cell* C, uint64_t* __restrict__ T, const fl
 
     // Rep(u, key(s)): walk from v through cells with key(s') <= key(s) that are not roots
     unsigned long long hops = 0;
+#if MT_REPAIR_ILP
+    // the thread's 8 walks advance in lock-step rounds: 8 independent load chains in flight
+    uint32_t xs[RB_PER];
+    uint32_t act = 0;
+#pragma unroll
+    for (int k = 0; k < RB_PER; ++k) {
+        xs[k] = cv_of(cell[k]);
+        if (INB(k) && xs[k] != uint32_t(UID(k))) act |= 1u << k;
+    }
+#pragma unroll 1
+    while (act) {
+#pragma unroll
+        for (int k = 0; k < RB_PER; ++k) {
+            if (!((act >> k) & 1u)) continue;
+            const Cell c = view.cell(C, xs[k]);
+            if (cv_of(c) == xs[k] || c.lo > key[k]) {     // Alg. 4, reading R20
+                act &= ~(1u << k);
+            } else {
+                xs[k] = cv_of(c);
+                ++hops;
+            }
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < RB_PER; ++k)
+        if (INB(k)) T[UID(k)] = pack(sv[k], xs[k]);
+#else
 #pragma unroll
     for (int k = 0; k < RB_PER; ++k) {
         if (!INB(k)) continue;
@@ -264,6 +294,7 @@ repair_brick_kernel(View view, const Cell* C, uint64_t* __restrict__ T, const fl
         }
         T[u] = pack(sv[k], x);
     }
+#endif
     if (stats && hops) atomicAdd(stats + ST_REPAIR_HOPS, hops);
 #undef UID
 #undef INB
