@@ -180,6 +180,9 @@ dedupe_cross_kernel(const float* __restrict__ f, const uint32_t* __restrict__ ba
     if (stats) atomicAdd(stats + ST_EDGES, n_edges);
 }
 
+#ifndef MQ_SPLIT
+#define MQ_SPLIT 1        // path splitting (128-bit CAS) in the merge_queue walks
+#endif
 #ifndef MQ_WALK
 #define MQ_WALK 1         // filter walks (with path splitting) before Alg. 3
 #endif
@@ -257,7 +260,7 @@ merge_queue_kernel(Cell* C, const QEntry* __restrict__ q, uint64_t cap, const un
         if (phase == CLIMB_HI || phase == CLIMB_LO) {
             if (cv_of(c) != x && c.lo <= L) {          // followable at level L
                 if (STATS) n_hops++;
-                if (has_prev && c.lo <= cp.lo)         // path splitting: prev skips x
+                if (MQ_SPLIT && has_prev && c.lo <= cp.lo)   // path splitting: prev skips x
                     cas_cell(C + xp, cp, Cell{cp.lo, (cp.hi & 0xffffffff00000000ull) | cv_of(c)});
                 xp = x;
                 cp = c;
