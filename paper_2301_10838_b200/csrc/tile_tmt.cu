@@ -18,14 +18,14 @@
 //      (derivation B);
 //   b. compress by synchronous pointer jumping: every regular cell points at
 //      its basin minimum (derivations F, F');
-//   c. compact the in-tile edges between two basins into a list;
-//   d. merge them: Alg. 4-style walks at the edge level with path splitting,
-//      then Alg. 3 with 64-bit shared-memory CAS and the root guards R4/R5
-//      (DESIGN.md), as a warp-converged state machine (one shared-memory
-//      round-trip per lane per step; idle lanes take the next pair of the
-//      warp's compacted run);
+//   c. list the in-tile edges between two basins, keeping the lowest per
+//      basin pair (staged per warp, inserted 32 at a time into a hash table);
+//   d. merge them: Alg. 3 from the two basins at the edge's level with 64-bit
+//      shared-memory CAS and the root guards R4/R5, one lane per
+//      pair, one shared-memory round trip per loop iteration; a lane whose
+//      pair is done takes the next pair of the warp's compacted run;
 //   e. repair (Alg. 5 with Alg. 4's walk, reading R20): the tile store is
-//      minimal for G_t;
+//      minimal for G_t (each thread's walks in lock-step rounds);
 //   f. write the 16-byte global cells (common.cuh) with global ids, and each
 //      vertex's tile representative at its own level for the crossing edges
 //      (derivation C''').

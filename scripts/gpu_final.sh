@@ -11,3 +11,6 @@ for tool in memcheck racecheck synccheck; do
   timeout 900 compute-sanitizer --tool $tool --error-exitcode 9 python scripts/sanitize.py > gpurun_out/${T}_san_${tool}.log 2>&1; echo "rc=$?" >> gpurun_out/${T}_san_${tool}.log
 done
 timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/${T}_ref.json 2>&1; echo "rc=$?" >> gpurun_out/${T}_ref.json
+timeout 600 python bench.py --config c3 --no-cpu-baseline > gpurun_out/${T}_bench_c3.json 2>&1
+timeout 600 python bench.py --config c2 --no-cpu-baseline > gpurun_out/${T}_bench_c2.json 2>&1
+MT_DIST_BACKEND=gloo MT_FORCE_DEVICE=0 timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29511 bench.py --gpus 2 --steps 3 --warmup 3 --config c4 --no-e2e > gpurun_out/${T}_multi2_gloo.log 2>&1; echo "rc=$?" >> gpurun_out/${T}_multi2_gloo.log
