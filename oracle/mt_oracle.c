@@ -283,3 +283,143 @@ static int sweep(const float *f, uint64_t n, const graph_t *G, int split, uint64
 
 /* Version tag so the Python loader can detect a stale build. */
 int oracle_abi_version(void) { return 1; }
+
+/* ------------------------------------------------------------------------------------------
+ * O4: the triplet of ONE vertex from the definition, by bounded floods (for sampled checks of
+ * full-size outputs that O1 cannot process in a test).  PAPER.md:185-200 (Sec. 2.1, "Triplet
+ * merge trees"): T[u] = (s, v) with f(v) < f(u) <= f(s), u and v in one component of the
+ * sublevel set G_{f(s)}, v the deepest vertex of that component (reading R12: of u's
+ * component), s = u unless u is a local minimum; a minimum's s is the lowest level at which
+ * its component reaches a deeper vertex; the component minimum is
+ * (u, u, u).  All comparisons are key_less (readings R1, R2, R16).
+ *   - s: a Prim-style flood from u that always enters the lowest vertex adjacent to the
+ *     region; the first deeper vertex it enters is reached at the smallest possible level,
+ *     and that level is the largest key entered so far (its vertex is s).  If u has a lower
+ *     neighbour the flood's first step enters it and s = u.
+ *   - v: breadth-first search of u's component of {x : key(x) <= key(s)}, keeping the least.
+ * Returns 1 and (s, v) on success, 0 when a flood would visit more than `cap` vertices
+ * (the caller skips that sample), negative on bad arguments or memory.
+ * ------------------------------------------------------------------------------------------ */
+typedef struct { uint32_t *keys; uint64_t mask, count; } idset;
+
+static int set_init(idset *S, uint64_t cap) {
+    uint64_t m = 1;
+    while (m < 2 * cap + 2) m <<= 1;
+    S->keys = (uint32_t *)malloc(m * sizeof(uint32_t));
+    if (!S->keys) return 0;
+    memset(S->keys, 0xff, m * sizeof(uint32_t));
+    S->mask = m - 1;
+    S->count = 0;
+    return 1;
+}
+/* 1 if inserted, 0 if already present (ids are < 2^32 - 1: 0xffffffff marks a free slot) */
+static int set_add(idset *S, uint32_t x) {
+    uint64_t h = ((uint64_t)x * 0x9E3779B97F4A7C15ull) >> 20;
+    for (;; ++h) {
+        uint32_t *k = &S->keys[h & S->mask];
+        if (*k == 0xffffffffu) { *k = x; ++S->count; return 1; }
+        if (*k == x) return 0;
+    }
+}
+
+typedef struct { vkey *a; uint64_t n, cap; } vheap;
+static int heap_less(const vkey *x, const vkey *y) { return key_less(x->g, x->id, y->g, y->id); }
+static int heap_push(vheap *H, vkey k) {
+    if (H->n == H->cap) {
+        uint64_t nc = H->cap ? 2 * H->cap : 1024;
+        vkey *na = (vkey *)realloc(H->a, nc * sizeof(vkey));
+        if (!na) return 0;
+        H->a = na;
+        H->cap = nc;
+    }
+    uint64_t i = H->n++;
+    H->a[i] = k;
+    while (i && heap_less(&H->a[i], &H->a[(i - 1) / 2])) {
+        vkey t = H->a[i]; H->a[i] = H->a[(i - 1) / 2]; H->a[(i - 1) / 2] = t;
+        i = (i - 1) / 2;
+    }
+    return 1;
+}
+static vkey heap_pop(vheap *H) {
+    vkey top = H->a[0];
+    H->a[0] = H->a[--H->n];
+    uint64_t i = 0;
+    for (;;) {
+        uint64_t l = 2 * i + 1, r = l + 1, m = i;
+        if (l < H->n && heap_less(&H->a[l], &H->a[m])) m = l;
+        if (r < H->n && heap_less(&H->a[r], &H->a[m])) m = r;
+        if (m == i) break;
+        vkey t = H->a[i]; H->a[i] = H->a[m]; H->a[m] = t;
+        i = m;
+    }
+    return top;
+}
+
+int oracle_triplet_at(const float *f, uint32_t nx, uint32_t ny, uint32_t nz, int conn, int split, uint32_t u,
+                      uint64_t cap, uint32_t *s_out, uint32_t *v_out) {
+    const uint64_t n = (uint64_t)nx * ny * nz;
+    if (!f || u >= n || (conn != 4 && conn != 6) || (conn == 4 && nz != 1) || n >= 0xffffffffull) return -1;
+    const float sg = split ? -1.0f : 1.0f;
+#define G_OF(x) (sg * f[(x)] + 0.0f)
+    uint32_t nb[6];
+    int rc = -2;
+    idset S = {0}, B = {0};
+    vheap H = {0};
+    uint32_t *queue = NULL;
+    if (!set_init(&S, cap) || !set_init(&B, cap)) goto out;
+    /* s: Prim flood from u */
+    const float gu = G_OF(u);
+    uint32_t s = u, found = 0;
+    float gs = gu;
+    set_add(&S, u);
+    if (!heap_push(&H, (vkey){gu, u})) goto out;
+    while (H.n) {
+        vkey x = heap_pop(&H);
+        if (key_less(x.g, x.id, gu, u)) { found = 1; break; }   /* entered a deeper vertex */
+        if (key_less(gs, s, x.g, x.id)) { gs = x.g; s = x.id; } /* the level rises to key(x) */
+        int d = grid_neighbours(x.id, nx, ny, nz, nb);
+        for (int i = 0; i < d; ++i)
+            if (set_add(&S, nb[i])) {
+                if (S.count > cap) { rc = 0; goto out; }
+                if (!heap_push(&H, (vkey){G_OF(nb[i]), nb[i]})) goto out;
+            }
+    }
+    if (!found) {                 /* the whole component lies above u: u is its minimum */
+        *s_out = u;
+        *v_out = u;
+        rc = 1;
+        goto out;
+    }
+    /* v: deepest vertex of u's component of {x : key(x) <= key(s)} */
+    queue = (uint32_t *)malloc((cap + 1) * sizeof(uint32_t));
+    if (!queue) goto out;
+    uint64_t qh = 0, qt = 0;
+    uint32_t v = u;
+    float gv = gu;
+    set_add(&B, u);
+    queue[qt++] = u;
+    while (qh < qt) {
+        const uint32_t x = queue[qh++];
+        const float gx = G_OF(x);
+        if (key_less(gx, x, gv, v)) { gv = gx; v = x; }
+        int d = grid_neighbours(x, nx, ny, nz, nb);
+        for (int i = 0; i < d; ++i) {
+            const float gy = G_OF(nb[i]);
+            if (!key_less(gy, nb[i], gs, s) && nb[i] != s) continue;   /* above level key(s) */
+            if (set_add(&B, nb[i])) {
+                if (B.count > cap) { rc = 0; goto out; }
+                queue[qt++] = nb[i];
+            }
+        }
+    }
+    *s_out = s;
+    *v_out = v;
+    rc = 1;
+out:
+#undef G_OF
+    free(S.keys);
+    free(B.keys);
+    free(H.a);
+    free(queue);
+    return rc;
+}

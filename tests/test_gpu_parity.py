@@ -231,3 +231,77 @@ def test_host_pipeline_outputs():
         assert np.array_equal(T.numpy().view(np.uint64), To)
         assert (a, b) == (npo, neo)
         assert rec[: a + b].numpy().view(_lib.PAIR_DTYPE).reshape(-1).tobytes() == po.tobytes()
+
+
+def test_full_size_c5_sampled():
+    """c5 at its full 1024^3 size in bench.py's launch configuration: O1 cannot run here, so
+    (1) properties that hold at any size, computed independently on the GPU with plain torch ops:
+    I1 key(v) < key(u) <= key(s) for non-roots, I2 s = u iff u has a lower neighbour, I3 one root,
+    I4 #finite pairs = #strict local minima - 1; (2) exact triplets and diagram records of sampled
+    vertices against O4 (the definition by bounded floods, oracle.triplet_at)."""
+    import resource
+    log = lambda msg: print(f"[c5] {msg}: maxrss {resource.getrusage(resource.RUSAGE_SELF).ru_maxrss >> 20} GB",
+                            flush=True)
+    f, dims, conn = fields.make("c5", device="cuda")
+    log("field")
+    nx, ny, nz = dims
+    n = nx * ny * nz
+    fd = torch.from_numpy(f).cuda()
+    mt = _lib.MergeTree(dims, conn, device=0)
+    T = mt.compute(fd)
+    rec, npairs, ness = mt.diagram()
+    torch.cuda.synchronize()
+    log("computed")
+    # (1) invariants, on the GPU with torch (ties broken by id: a lower-id neighbour is lower
+    # when equal, reading R1; -0.0 == +0.0 under float compares, reading R2)
+    g = fd.view(nz, ny, nx)
+    has_lower = torch.zeros((nz, ny, nx), dtype=torch.bool, device="cuda")
+    has_lower[:, :, 1:] |= g[:, :, :-1] <= g[:, :, 1:]
+    has_lower[:, :, :-1] |= g[:, :, 1:] < g[:, :, :-1]
+    has_lower[:, 1:, :] |= g[:, :-1, :] <= g[:, 1:, :]
+    has_lower[:, :-1, :] |= g[:, 1:, :] < g[:, :-1, :]
+    has_lower[1:, :, :] |= g[:-1, :, :] <= g[1:, :, :]
+    has_lower[:-1, :, :] |= g[1:, :, :] < g[:-1, :, :]
+    has_lower = has_lower.view(-1)
+    n_min = int((~has_lower).sum().item())
+    assert ness == 1 and npairs == n_min - 1, (npairs, ness, n_min)
+    s = (T >> 32) & 0xffffffff
+    v = T & 0xffffffff
+    ids = torch.arange(n, device="cuda", dtype=torch.int64)
+    is_reg = s == ids
+    root = is_reg & (v == ids)
+    bad_i2 = int(((is_reg != has_lower) & ~root).sum().item())    # I2 is about non-root cells
+    del has_lower
+    n_root = int(root.sum().item())
+    fv = fd[v]
+    bad_v = int((~(root | (fv < fd) | ((fv == fd) & (v < ids)))).sum().item())
+    del fv
+    fs = fd[s]
+    bad_s = int((~(root | (fs > fd) | ((fs == fd) & (s >= ids)))).sum().item())
+    del fs, root, ids, is_reg
+    log(f"I2 violations {bad_i2}, roots {n_root}, I1 violations {bad_v} / {bad_s}")
+    assert bad_i2 == 0, "I2: s = u exactly at the non-root vertices with a lower neighbour"
+    assert n_root == 1, "I3: one root"
+    assert bad_v == 0 and bad_s == 0, "I1: key(v) < key(u) <= key(s)"
+    log("invariants")
+    # (2) sampled exact triplets (O4) and the sampled minima's diagram records
+    rng = np.random.default_rng(2301)
+    branch = torch.nonzero(s != torch.arange(n, device="cuda", dtype=torch.int64), as_tuple=False).view(-1)
+    picks = np.concatenate([rng.integers(0, n, 48),
+                            branch[torch.from_numpy(rng.integers(0, branch.numel(), 48)).cuda()].cpu().numpy()])
+    Ts = T[torch.from_numpy(picks).cuda()].cpu().numpy().view(np.uint64)
+    recs = _lib.pairs_to_numpy(rec)
+    log("samples")
+    checked = 0
+    for u, t in zip(picks.tolist(), Ts.tolist()):
+        r = oracle.triplet_at(f, dims, conn, u, cap=1 << 21)   # floods past 2M vertices are skipped
+        if r is None:
+            continue
+        checked += 1
+        assert (r[0] << 32) | r[1] == t, (u, r, divmod(t, 1 << 32))
+        if r[0] != u:   # a branch born at u dies at s: its record, in ascending-birth order
+            k = int(np.searchsorted(recs["birth_v"][:npairs], u))
+            assert recs[k]["birth_v"] == u and recs[k]["death_v"] == r[0]
+            assert recs[k]["birth"].tobytes() == f[u].tobytes() and recs[k]["death"].tobytes() == f[r[0]].tobytes()
+    log(f"{checked} of {picks.size} sampled vertices checked against O4")
+    assert checked >= 32, checked

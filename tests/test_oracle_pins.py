@@ -216,3 +216,26 @@ def test_filter_by_persistence_definition():
     T, pairs, npairs, ness = oracle.merge_tree(np.array([1, 1, 0, 1], np.float32), (4, 1, 1), 4)
     assert all(p["death"] - p["birth"] == 0 for p in pairs[:npairs])
     assert oracle.filter_by_persistence(pairs, npairs, 0.0).size == ness
+
+
+@pytest.mark.parametrize("cfg,scale,split", [("c1", 16, False), ("c4", 20, True), ("c5", 24, False), ("c2", 48, False),
+                                             ("c3", 20, True)])
+def test_o4_single_vertex_triplets_equal_o1(cfg, scale, split):
+    """O4 (bounded floods from one vertex, the definition) against O1 on every
+    vertex of small grids of each recipe, both tree directions: O4 is what the full-size GPU test
+    samples with."""
+    f, dims, conn = fields.make(cfg, scale=scale)
+    T, _, _, _ = oracle.merge_tree(f, dims, conn=conn, split=split)
+    n = int(np.prod(dims))
+    for u in range(n):
+        r = oracle.triplet_at(f, dims, conn, u, split=split, cap=n)
+        assert r is not None
+        assert (np.uint64(r[0]) << np.uint64(32)) | np.uint64(r[1]) == T[u], (u, r, divmod(int(T[u]), 1 << 32))
+
+
+def test_o4_cap_skips():
+    f, dims, conn = fields.make("c1")
+    T, _, _, _ = oracle.merge_tree(f, dims, conn=conn)
+    root = int(np.flatnonzero((T >> np.uint64(32)) == (T & np.uint64(0xffffffff)))[0])
+    assert oracle.triplet_at(f, dims, conn, root, cap=100) is None   # the global minimum floods everything
+    assert oracle.triplet_at(f, dims, conn, root, cap=f.size) == (root, root)
