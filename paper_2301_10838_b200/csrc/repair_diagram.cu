@@ -307,6 +307,9 @@ repair_brick_kernel(View view, const Cell* C, uint64_t* __restrict__ T, const fl
 // place in the diagram (ordered compaction: CTA scan + decoupled look-back);
 // the records are copied from the staging runs the repair wrote.
 constexpr int THREADS = 256;
+#ifndef DG_SPT
+#define DG_SPT 1            // diagram: segments per thread (4: c5 1.31 -> 1.07 ms, c4 0.39 -> 0.56 ms)
+#endif
 constexpr uint64_t ST_AGG = 1ull << 62, ST_PRE = 2ull << 62, ST_VAL = (1ull << 62) - 1;
 
 __global__ void __launch_bounds__(THREADS)
@@ -321,9 +324,16 @@ diagram_kernel(const uint16_t* __restrict__ seg_cnt, const uint32_t* __restrict_
     if (threadIdx.x == 0) s_tile = atomicAdd(counters + CTR_TICKET, 1ull);
     __syncthreads();
     const uint64_t tile = s_tile;
-    const uint64_t seg = tile * THREADS + threadIdx.x;
-    const uint32_t cnt = seg < nseg ? seg_cnt[seg] : 0u;
-    const uint32_t cf = cnt & 0xffu, ce = cnt >> 8;
+    // DG_SPT consecutive segments per thread (fewer tiles in the look-back chain)
+    const uint64_t seg = (tile * THREADS + threadIdx.x) * DG_SPT;
+    uint32_t cnts[DG_SPT];
+    uint32_t cf = 0, ce = 0;
+#pragma unroll
+    for (int j = 0; j < DG_SPT; ++j) {
+        cnts[j] = seg + j < nseg ? seg_cnt[seg + j] : 0u;
+        cf += cnts[j] & 0xffu;
+        ce += cnts[j] >> 8;
+    }
     // block-wide exclusive scans (finite, essential)
     uint32_t incl = cf, eincl = ce;
 #pragma unroll
@@ -396,14 +406,22 @@ diagram_kernel(const uint16_t* __restrict__ seg_cnt, const uint32_t* __restrict_
     if (!(cf | ce)) return;
     const uint64_t pos = s_prefix + s_w[warp] + incl - cf;
     const uint64_t epos = s_eprefix + s_we[warp] + eincl - ce;
-    const mt_pair* src = stage + seg_pos[seg];
-    for (uint32_t i = 0; i < cf; ++i) {
-        if (pos + i < out_cap) out[pos + i] = src[i];
-        else atomicOr(counters + CTR_ERR, ERR_CAPACITY);
-    }
-    for (uint32_t i = 0; i < ce; ++i) {
-        if (epos + i < ess_cap) ess[epos + i] = src[cf + i];
-        else atomicOr(counters + CTR_ERR, ERR_ESS_CAPACITY);
+    uint64_t p = pos, ep = epos;
+#pragma unroll
+    for (int j = 0; j < DG_SPT; ++j) {
+        const uint32_t fj = cnts[j] & 0xffu, ej = cnts[j] >> 8;
+        if (!(fj | ej)) continue;
+        const mt_pair* src = stage + seg_pos[seg + j];
+        for (uint32_t i = 0; i < fj; ++i) {
+            if (p + i < out_cap) out[p + i] = src[i];
+            else atomicOr(counters + CTR_ERR, ERR_CAPACITY);
+        }
+        for (uint32_t i = 0; i < ej; ++i) {
+            if (ep + i < ess_cap) ess[ep + i] = src[fj + i];
+            else atomicOr(counters + CTR_ERR, ERR_ESS_CAPACITY);
+        }
+        p += fj;
+        ep += ej;
     }
 }
 
@@ -472,7 +490,7 @@ uint64_t repair_segments(const Slab& sl) {
     return nseg;
 }
 uint64_t repair_segments_bound(uint64_t n) { return n / 16 + 2; }
-uint64_t diagram_tiles(uint64_t nseg) { return (nseg + THREADS - 1) / THREADS; }
+uint64_t diagram_tiles(uint64_t nseg) { return (nseg + THREADS * DG_SPT - 1) / (THREADS * DG_SPT); }
 
 void launch_repair(const Cell* C, uint64_t* T, const float* f, const Slab& sl, uint32_t flip, const RepairOut& o,
                    unsigned long long* stats, const ForestRef* forest, cudaStream_t stream) {
