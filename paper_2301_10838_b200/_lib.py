@@ -185,7 +185,7 @@ def mt_set_profiling(ctx, enable: bool):
     _check(load().mt_set_profiling(ctx, int(bool(enable))), "mt_set_profiling")
 
 
-def mt_kernel_times(ctx, max_entries: int = 8):
+def mt_kernel_times(ctx, max_entries: int = 16):
     names = (ctypes.c_char_p * max_entries)()
     ms = (ctypes.c_float * max_entries)()
     k = load().mt_kernel_times(ctx, names, ms, max_entries)

@@ -19,7 +19,7 @@ namespace {
 
 constexpr size_t ALIGN = 256;
 constexpr uint32_t ESS_CAP = 64;  // essential classes = connected components (1 per grid)
-constexpr int MAX_EVENTS = 12;
+constexpr int MAX_EVENTS = 16;
 
 size_t align_up(size_t x) { return (x + ALIGN - 1) / ALIGN * ALIGN; }
 

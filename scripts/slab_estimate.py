@@ -38,11 +38,20 @@ for P in Ps:
         recs = [s.forest() for s in slabs]
         allr = torch.cat(recs)
         glob = [timed(lambda r=r: slabs[r].compute_global(allr, zb)) for r in range(P)]
+    # per-kernel split of one rank (library profiling marks)
+    from paper_2301_10838_b200 import _lib
+    _lib.mt_set_profiling(slabs[-1].ctx, True)
+    slabs[-1].compute_local(parts[-1])
+    slabs[-1].compute_global(allr, zb)
+    torch.cuda.synchronize()
+    split = _lib.mt_kernel_times(slabs[-1].ctx)
+    _lib.mt_set_profiling(slabs[-1].ctx, False)
     gather_ms = allr.numel() / 1e9 / NVLINK_GBPS * 1e3
     est = max(loc) + gather_ms + max(glob)
     print(json.dumps({"cfg": cfg, "P": P, "local_ms_max": max(loc), "local_ms": loc, "global_ms_max": max(glob),
                       "global_ms": glob, "forest_bytes_all": allr.numel(), "allgather_ms_est": gather_ms,
                       "step_ms_est": est, "Mv_s_est": nx * ny * nz / est / 1e3,
-                      "assumed_allgather_GBps": NVLINK_GBPS}), flush=True)
+                      "assumed_allgather_GBps": NVLINK_GBPS,
+                      "last_rank_kernels_ms": split}), flush=True)
     del slabs, parts, recs, allr
     torch.cuda.empty_cache()
