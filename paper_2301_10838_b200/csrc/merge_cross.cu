@@ -40,6 +40,9 @@ namespace {
 #ifndef DC_XFACE
 #define DC_XFACE 1        // x-face edges read tile_tmt's compact face records
 #endif
+#ifndef DC_PATCH
+#define DC_PATCH 1        // z faces in 32 x 8 patches with a CTA-wide dedupe
+#endif
 #ifndef DC_REDUCE
 #define DC_REDUCE 0       // group minimum by two __reduce_min_sync (else a 32-lane shuffle scan)
 #endif
@@ -50,6 +53,7 @@ namespace {
 struct CrossGeom {
     uint32_t nx, ny, nz, tx, ty, tz;   // slab (nz = local planes) and tile shape
     uint32_t tiles_x, tiles_y;         // tiles along x and y
+    uint32_t patch;                    // DC_PATCH: z faces first, in 32 x 8 patches (one per CTA step)
     uint64_t base;                     // global id of the slab's first vertex
     uint64_t ex, ey, ez;               // number of crossing edges on x-, y-, z-faces
 };
@@ -95,15 +99,31 @@ dedupe_cross_kernel(const float* __restrict__ f, const uint32_t* __restrict__ ba
                     unsigned long long* __restrict__ stats) {
     __shared__ uint32_t s_warp[8];
     __shared__ unsigned long long s_base;
+    __shared__ unsigned long long s_key[512], s_min[512];   // DC_PATCH: pair -> lowest level
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint64_t total = g.ex + g.ey + g.ez;
     const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
     unsigned long long n_edges = 0;
     for (uint64_t e0 = uint64_t(blockIdx.x) * blockDim.x; e0 < total; e0 += stride) {
-        const uint64_t e = e0 + threadIdx.x;
-        const bool valid = e < total;
+        const uint64_t e_raw = e0 + threadIdx.x;
+        const bool valid = e_raw < total;
         QEntry en{0, 0, 0};
         uint64_t pair = ~0ull;
+        // DC_PATCH order: the z faces first, each CTA step one 32 x 8 patch of a z face (so the
+        // CTA dedupe below sees 8 rows of one tile face), then the x and the y faces
+        const bool zpatch = g.patch && e0 < g.ez;   // uniform over the CTA (ez % 256 == 0)
+        uint64_t e = e_raw;
+        if (g.patch) {
+            if (e_raw < g.ez) {
+                const uint64_t sxy = uint64_t(g.nx) * g.ny;
+                const uint64_t k = e_raw / sxy, rp = e_raw - k * sxy;
+                const uint32_t pidx = uint32_t(rp >> 8), w = uint32_t(rp & 255), pxn = g.nx / 32;
+                const uint32_t x = (pidx % pxn) * 32 + (w & 31), y = (pidx / pxn) * 8 + (w >> 5);
+                e = g.ex + g.ey + k * sxy + uint64_t(y) * g.nx + x;
+            } else {
+                e = e_raw - g.ez;
+            }
+        }
         if (valid) {
             uint32_t a, b;
             decode_edge(g, e, &a, &b);
@@ -160,6 +180,26 @@ dedupe_cross_kernel(const float* __restrict__ f, const uint32_t* __restrict__ ba
             if ((lane > 0 && pu == pair && lu < en.L) || (lane < 31 && pd == pair && ld < en.L)) keep = false;
         }
 #endif
+        if (DC_PATCH && zpatch) {
+            // CTA-wide: the warps' survivors keep the lowest edge of each pair over the patch
+            s_key[threadIdx.x] = ~0ull;
+            s_key[threadIdx.x + 256] = ~0ull;
+            s_min[threadIdx.x] = ~0ull;
+            s_min[threadIdx.x + 256] = ~0ull;
+            __syncthreads();
+            uint32_t h = 0;
+            if (keep) {
+                h = uint32_t((pair * 0x9E3779B97F4A7C15ull) >> 55);   // 9 bits
+                while (true) {
+                    const unsigned long long k = atomicCAS(&s_key[h], ~0ull, pair);
+                    if (k == ~0ull || k == pair) break;
+                    h = (h + 1) & 511u;
+                }
+                atomicMin(&s_min[h], (unsigned long long)en.L);
+            }
+            __syncthreads();
+            if (keep && s_min[h] != en.L) keep = false;
+        }
         const uint32_t km = __ballot_sync(FULL_MASK, keep);
         if (lane == 0) s_warp[warp] = __popc(km);
         __syncthreads();
@@ -336,6 +376,7 @@ int launch_dedupe_cross(const float* f, const uint32_t* basin, const uint64_t* x
     tile_shape(sl.nz, &g.ty, &g.tz);
     g.tiles_x = (g.nx + g.tx - 1) / g.tx;
     g.tiles_y = (g.ny + g.ty - 1) / g.ty;
+    g.patch = DC_PATCH && g.nx % 32 == 0 && g.ny % 8 == 0 ? 1u : 0u;
     const uint64_t kx = (g.nx + g.tx - 1) / g.tx - 1, ky = (g.ny + g.ty - 1) / g.ty - 1,
                    kz = g.nz ? (g.nz + g.tz - 1) / g.tz - 1 : 0;
     g.ex = g.nz ? kx * g.ny * g.nz : 0;
