@@ -43,6 +43,9 @@ namespace {
 #ifndef DC_PATCH
 #define DC_PATCH 1        // z faces in 32 x 8 patches with a CTA-wide dedupe
 #endif
+#ifndef DC_YPATCH
+#define DC_YPATCH 1       // the y faces in 32 x 8 patches too
+#endif
 #ifndef DC_REDUCE
 #define DC_REDUCE 0       // group minimum by two __reduce_min_sync (else a 32-lane shuffle scan)
 #endif
@@ -54,6 +57,7 @@ struct CrossGeom {
     uint32_t nx, ny, nz, tx, ty, tz;   // slab (nz = local planes) and tile shape
     uint32_t tiles_x, tiles_y;         // tiles along x and y
     uint32_t patch;                    // DC_PATCH: z faces first, in 32 x 8 patches (one per CTA step)
+    uint32_t ypatch;                   // ... then the y faces in 32 (x) x 8 (z) patches
     uint64_t base;                     // global id of the slab's first vertex
     uint64_t ex, ey, ez;               // number of crossing edges on x-, y-, z-faces
 };
@@ -111,17 +115,27 @@ dedupe_cross_kernel(const float* __restrict__ f, const uint32_t* __restrict__ ba
         uint64_t pair = ~0ull;
         // DC_PATCH order: the z faces first, each CTA step one 32 x 8 patch of a z face (so the
         // CTA dedupe below sees 8 rows of one tile face), then the x and the y faces
-        const bool zpatch = g.patch && e0 < g.ez;   // uniform over the CTA (ez % 256 == 0)
+        const uint64_t yend = g.ez + (g.ypatch ? g.ey : 0);
+        const bool zpatch = g.patch && e0 < yend;   // uniform over the CTA (ez, ey % 256 == 0)
         uint64_t e = e_raw;
         if (g.patch) {
+            const uint32_t pxn = g.nx / 32;
             if (e_raw < g.ez) {
                 const uint64_t sxy = uint64_t(g.nx) * g.ny;
                 const uint64_t k = e_raw / sxy, rp = e_raw - k * sxy;
-                const uint32_t pidx = uint32_t(rp >> 8), w = uint32_t(rp & 255), pxn = g.nx / 32;
+                const uint32_t pidx = uint32_t(rp >> 8), w = uint32_t(rp & 255);
                 const uint32_t x = (pidx % pxn) * 32 + (w & 31), y = (pidx / pxn) * 8 + (w >> 5);
                 e = g.ex + g.ey + k * sxy + uint64_t(y) * g.nx + x;
+            } else if (e_raw < yend) {
+                const uint64_t sxz = uint64_t(g.nx) * g.nz, ey0 = e_raw - g.ez;
+                const uint64_t k = ey0 / sxz, rp = ey0 - k * sxz;
+                const uint32_t pidx = uint32_t(rp >> 8), w = uint32_t(rp & 255);
+                const uint32_t x = (pidx % pxn) * 32 + (w & 31), z = (pidx / pxn) * 8 + (w >> 5);
+                e = g.ex + k * sxz + uint64_t(z) * g.nx + x;
+            } else if (g.ypatch) {
+                e = e_raw - yend;                    // the x faces, in their own order
             } else {
-                e = e_raw - g.ez;
+                e = e_raw - g.ez;                    // x faces, then y faces
             }
         }
         if (valid) {
@@ -377,6 +391,7 @@ int launch_dedupe_cross(const float* f, const uint32_t* basin, const uint64_t* x
     g.tiles_x = (g.nx + g.tx - 1) / g.tx;
     g.tiles_y = (g.ny + g.ty - 1) / g.ty;
     g.patch = DC_PATCH && g.nx % 32 == 0 && g.ny % 8 == 0 ? 1u : 0u;
+    g.ypatch = g.patch && DC_YPATCH && g.nz % 8 == 0 ? 1u : 0u;
     const uint64_t kx = (g.nx + g.tx - 1) / g.tx - 1, ky = (g.ny + g.ty - 1) / g.ty - 1,
                    kz = g.nz ? (g.nz + g.tz - 1) / g.tz - 1 : 0;
     g.ex = g.nz ? kx * g.ny * g.nz : 0;
