@@ -46,6 +46,9 @@ namespace {
 #ifndef DC_YPATCH
 #define DC_YPATCH 1       // the y faces in 32 x 8 patches too
 #endif
+#ifndef DC_PATCH_ONLY
+#define DC_PATCH_ONLY 1   // patch steps: skip the warp dedupe (the CTA-wide one does it all)
+#endif
 #ifndef DC_REDUCE
 #define DC_REDUCE 0       // group minimum by two __reduce_min_sync (else a 32-lane shuffle scan)
 #endif
@@ -170,6 +173,7 @@ dedupe_cross_kernel(const float* __restrict__ f, const uint32_t* __restrict__ ba
         // lanes with the same pair keep the lowest edge only
         bool keep = valid;
 #if DC_MATCH
+        if (!(DC_PATCH_ONLY && zpatch)) {   // (patch steps: the CTA-wide dedupe alone)
         const uint32_t group = __match_any_sync(FULL_MASK, pair);
 #if DC_REDUCE
         {   // lowest L = (ord << 32 | id) of the group: min of the order keys, then of the ids
@@ -186,6 +190,7 @@ dedupe_cross_kernel(const float* __restrict__ f, const uint32_t* __restrict__ ba
             if (((group >> j) & 1u) && Lj < en.L) keep = false;
         }
 #endif
+        }
 #else
         {   // (cheaper) neighbouring lanes only: an edge with a lower one of the same pair in the
             // previous or next lane is dropped; the lowest of every run of lanes survives
