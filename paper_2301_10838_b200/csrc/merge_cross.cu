@@ -49,6 +49,9 @@ namespace {
 #ifndef DC_PATCH_ONLY
 #define DC_PATCH_ONLY 1   // patch steps: skip the warp dedupe (the CTA-wide one does it all)
 #endif
+#ifndef DC_XPATCH
+#define DC_XPATCH 1       // the x faces in 32 (y) x 8 (z) patches too
+#endif
 #ifndef DC_REDUCE
 #define DC_REDUCE 0       // group minimum by two __reduce_min_sync (else a 32-lane shuffle scan)
 #endif
@@ -61,6 +64,7 @@ struct CrossGeom {
     uint32_t tiles_x, tiles_y;         // tiles along x and y
     uint32_t patch;                    // DC_PATCH: z faces first, in 32 x 8 patches (one per CTA step)
     uint32_t ypatch;                   // ... then the y faces in 32 (x) x 8 (z) patches
+    uint32_t xpatch;                   // ... then the x faces in 32 (y) x 8 (z) patches
     uint64_t base;                     // global id of the slab's first vertex
     uint64_t ex, ey, ez;               // number of crossing edges on x-, y-, z-faces
 };
@@ -119,7 +123,8 @@ dedupe_cross_kernel(const float* __restrict__ f, const uint32_t* __restrict__ ba
         // DC_PATCH order: the z faces first, each CTA step one 32 x 8 patch of a z face (so the
         // CTA dedupe below sees 8 rows of one tile face), then the x and the y faces
         const uint64_t yend = g.ez + (g.ypatch ? g.ey : 0);
-        const bool zpatch = g.patch && e0 < yend;   // uniform over the CTA (ez, ey % 256 == 0)
+        const uint64_t xend = yend + (g.xpatch ? g.ex : 0);
+        const bool zpatch = g.patch && e0 < xend;   // uniform over the CTA (ez, ey, ex % 256 == 0)
         uint64_t e = e_raw;
         if (g.patch) {
             const uint32_t pxn = g.nx / 32;
@@ -135,6 +140,12 @@ dedupe_cross_kernel(const float* __restrict__ f, const uint32_t* __restrict__ ba
                 const uint32_t pidx = uint32_t(rp >> 8), w = uint32_t(rp & 255);
                 const uint32_t x = (pidx % pxn) * 32 + (w & 31), z = (pidx / pxn) * 8 + (w >> 5);
                 e = g.ex + k * sxz + uint64_t(z) * g.nx + x;
+            } else if (e_raw < xend) {
+                const uint64_t syz = uint64_t(g.ny) * g.nz, ex0 = e_raw - yend;
+                const uint64_t k = ex0 / syz, rp = ex0 - k * syz;
+                const uint32_t pidx = uint32_t(rp >> 8), w = uint32_t(rp & 255), pyn = g.ny / 32;
+                const uint32_t y = (pidx % pyn) * 32 + (w & 31), z = (pidx / pyn) * 8 + (w >> 5);
+                e = k * syz + uint64_t(z) * g.ny + y;
             } else if (g.ypatch) {
                 e = e_raw - yend;                    // the x faces, in their own order
             } else {
@@ -397,6 +408,7 @@ int launch_dedupe_cross(const float* f, const uint32_t* basin, const uint64_t* x
     g.tiles_y = (g.ny + g.ty - 1) / g.ty;
     g.patch = DC_PATCH && g.nx % 32 == 0 && g.ny % 8 == 0 ? 1u : 0u;
     g.ypatch = g.patch && DC_YPATCH && g.nz % 8 == 0 ? 1u : 0u;
+    g.xpatch = g.ypatch && DC_XPATCH && g.ny % 32 == 0 ? 1u : 0u;
     const uint64_t kx = (g.nx + g.tx - 1) / g.tx - 1, ky = (g.ny + g.ty - 1) / g.ty - 1,
                    kz = g.nz ? (g.nz + g.tz - 1) / g.tz - 1 : 0;
     g.ex = g.nz ? kx * g.ny * g.nz : 0;
