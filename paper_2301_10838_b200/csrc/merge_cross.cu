@@ -8,7 +8,11 @@
 // tile representatives of its ends at their own levels (tile_tmt's R array,
 // DESIGN.md derivation C''') and its level L = max(key(a), key(b)); lanes
 // holding the same pair (__match_any_sync) keep only the lowest edge
-// (derivation C''), and the survivors are queued as (L, R_hi, R_lo).
+// (derivation C''), and the survivors are queued as (L, R_hi, R_lo).  On
+// grids whose faces tile into 32 x 8 patches (nx % 32 = ny % 8 = nz % 8 = 0)
+// the faces are enumerated patch by patch instead (z, then y, then x faces),
+// one patch per CTA step, and the dedupe is CTA-wide: a shared-memory table
+// pair -> lowest level (CAS + 64-bit atomicMin) over the 8 rows of the patch.
 //
 // merge_queue: persistent warps take batches of 256 queue entries per global
 // atomic; each lane runs its entry as a state machine advanced by ONE memory
