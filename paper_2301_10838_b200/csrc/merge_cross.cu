@@ -9,10 +9,11 @@
 // DESIGN.md derivation C''') and its level L = max(key(a), key(b)); lanes
 // holding the same pair (__match_any_sync) keep only the lowest edge
 // (derivation C''), and the survivors are queued as (L, R_hi, R_lo).  On
-// grids whose faces tile into 32 x 8 patches (nx % 32 = ny % 8 = nz % 8 = 0)
-// the faces are enumerated patch by patch instead (z, then y, then x faces),
-// one patch per CTA step, and the dedupe is CTA-wide: a shared-memory table
-// pair -> lowest level (CAS + 64-bit atomicMin) over the 8 rows of the patch.
+// grids whose faces tile into 32 x 16 patches (nx % 32 = ny % 16 = nz % 16 =
+// 0) the faces are enumerated patch by patch instead (z, then y, then x
+// faces), one patch per CTA step of 512 threads, and the dedupe is CTA-wide:
+// a shared-memory table pair -> lowest level (CAS + 64-bit atomicMin) over the
+// 16 rows of the patch (a whole tile z face).
 //
 // merge_queue: persistent warps take batches of 256 queue entries per global
 // atomic; each lane runs its entry as a state machine advanced by ONE memory
@@ -44,6 +45,11 @@ namespace {
 #ifndef DC_XFACE
 #define DC_XFACE 1        // x-face edges read tile_tmt's compact face records
 #endif
+#ifndef DC_ROWS
+#define DC_ROWS 16        // patch rows (a CTA step = 32 x DC_ROWS face edges = DC_THREADS threads)
+#endif
+#define DC_THREADS (32 * DC_ROWS)
+#define DC_LOG2T (DC_ROWS == 16 ? 10 : 9)   // log2 of the 2 x DC_THREADS table slots
 #ifndef DC_PATCH
 #define DC_PATCH 1        // z faces in 32 x 8 patches with a CTA-wide dedupe
 #endif
@@ -107,14 +113,14 @@ struct QEntry {
     uint32_t m_lo;   // descent basin of the lower endpoint
 };
 
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(DC_THREADS)
 dedupe_cross_kernel(const float* __restrict__ f, const uint32_t* __restrict__ basin,
                     const uint64_t* __restrict__ xface, CrossGeom g, uint32_t flip,
                     QEntry* __restrict__ q, uint64_t cap, unsigned long long* __restrict__ qlen,
                     unsigned long long* __restrict__ stats) {
-    __shared__ uint32_t s_warp[8];
+    __shared__ uint32_t s_warp[DC_THREADS / 32];
     __shared__ unsigned long long s_base;
-    __shared__ unsigned long long s_key[512], s_min[512];   // DC_PATCH: pair -> lowest level
+    __shared__ unsigned long long s_key[2 * DC_THREADS], s_min[2 * DC_THREADS];   // DC_PATCH: pair -> lowest level
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint64_t total = g.ex + g.ey + g.ez;
     const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
@@ -128,27 +134,27 @@ dedupe_cross_kernel(const float* __restrict__ f, const uint32_t* __restrict__ ba
         // CTA dedupe below sees 8 rows of one tile face), then the x and the y faces
         const uint64_t yend = g.ez + (g.ypatch ? g.ey : 0);
         const uint64_t xend = yend + (g.xpatch ? g.ex : 0);
-        const bool zpatch = g.patch && e0 < xend;   // uniform over the CTA (ez, ey, ex % 256 == 0)
+        const bool zpatch = g.patch && e0 < xend;   // uniform over the CTA (ez, ey, ex % DC_THREADS == 0)
         uint64_t e = e_raw;
         if (g.patch) {
             const uint32_t pxn = g.nx / 32;
             if (e_raw < g.ez) {
                 const uint64_t sxy = uint64_t(g.nx) * g.ny;
                 const uint64_t k = e_raw / sxy, rp = e_raw - k * sxy;
-                const uint32_t pidx = uint32_t(rp >> 8), w = uint32_t(rp & 255);
-                const uint32_t x = (pidx % pxn) * 32 + (w & 31), y = (pidx / pxn) * 8 + (w >> 5);
+                const uint32_t pidx = uint32_t(rp / DC_THREADS), w = uint32_t(rp % DC_THREADS);
+                const uint32_t x = (pidx % pxn) * 32 + (w & 31), y = (pidx / pxn) * DC_ROWS + (w >> 5);
                 e = g.ex + g.ey + k * sxy + uint64_t(y) * g.nx + x;
             } else if (e_raw < yend) {
                 const uint64_t sxz = uint64_t(g.nx) * g.nz, ey0 = e_raw - g.ez;
                 const uint64_t k = ey0 / sxz, rp = ey0 - k * sxz;
-                const uint32_t pidx = uint32_t(rp >> 8), w = uint32_t(rp & 255);
-                const uint32_t x = (pidx % pxn) * 32 + (w & 31), z = (pidx / pxn) * 8 + (w >> 5);
+                const uint32_t pidx = uint32_t(rp / DC_THREADS), w = uint32_t(rp % DC_THREADS);
+                const uint32_t x = (pidx % pxn) * 32 + (w & 31), z = (pidx / pxn) * DC_ROWS + (w >> 5);
                 e = g.ex + k * sxz + uint64_t(z) * g.nx + x;
             } else if (e_raw < xend) {
                 const uint64_t syz = uint64_t(g.ny) * g.nz, ex0 = e_raw - yend;
                 const uint64_t k = ex0 / syz, rp = ex0 - k * syz;
-                const uint32_t pidx = uint32_t(rp >> 8), w = uint32_t(rp & 255), pyn = g.ny / 32;
-                const uint32_t y = (pidx % pyn) * 32 + (w & 31), z = (pidx / pyn) * 8 + (w >> 5);
+                const uint32_t pidx = uint32_t(rp / DC_THREADS), w = uint32_t(rp % DC_THREADS), pyn = g.ny / 32;
+                const uint32_t y = (pidx % pyn) * 32 + (w & 31), z = (pidx / pyn) * DC_ROWS + (w >> 5);
                 e = k * syz + uint64_t(z) * g.ny + y;
             } else if (g.ypatch) {
                 e = e_raw - yend;                    // the x faces, in their own order
@@ -217,17 +223,17 @@ dedupe_cross_kernel(const float* __restrict__ f, const uint32_t* __restrict__ ba
         if (DC_PATCH && zpatch) {
             // CTA-wide: the warps' survivors keep the lowest edge of each pair over the patch
             s_key[threadIdx.x] = ~0ull;
-            s_key[threadIdx.x + 256] = ~0ull;
+            s_key[threadIdx.x + DC_THREADS] = ~0ull;
             s_min[threadIdx.x] = ~0ull;
-            s_min[threadIdx.x + 256] = ~0ull;
+            s_min[threadIdx.x + DC_THREADS] = ~0ull;
             __syncthreads();
             uint32_t h = 0;
             if (keep) {
-                h = uint32_t((pair * 0x9E3779B97F4A7C15ull) >> 55);   // 9 bits
+                h = uint32_t((pair * 0x9E3779B97F4A7C15ull) >> (64 - DC_LOG2T));
                 while (true) {
                     const unsigned long long k = atomicCAS(&s_key[h], ~0ull, pair);
                     if (k == ~0ull || k == pair) break;
-                    h = (h + 1) & 511u;
+                    h = (h + 1) & (2u * DC_THREADS - 1u);
                 }
                 atomicMin(&s_min[h], (unsigned long long)en.L);
             }
@@ -239,7 +245,7 @@ dedupe_cross_kernel(const float* __restrict__ f, const uint32_t* __restrict__ ba
         __syncthreads();
         if (threadIdx.x == 0) {
             uint32_t tot = 0;
-            for (int w = 0; w < 8; ++w) {
+            for (int w = 0; w < DC_THREADS / 32; ++w) {
                 const uint32_t t = s_warp[w];
                 s_warp[w] = tot;
                 tot += t;
@@ -410,8 +416,8 @@ int launch_dedupe_cross(const float* f, const uint32_t* basin, const uint64_t* x
     tile_shape(sl.nz, &g.ty, &g.tz);
     g.tiles_x = (g.nx + g.tx - 1) / g.tx;
     g.tiles_y = (g.ny + g.ty - 1) / g.ty;
-    g.patch = DC_PATCH && g.nx % 32 == 0 && g.ny % 8 == 0 ? 1u : 0u;
-    g.ypatch = g.patch && DC_YPATCH && g.nz % 8 == 0 ? 1u : 0u;
+    g.patch = DC_PATCH && g.nx % 32 == 0 && g.ny % DC_ROWS == 0 ? 1u : 0u;
+    g.ypatch = g.patch && DC_YPATCH && g.nz % DC_ROWS == 0 ? 1u : 0u;
     g.xpatch = g.ypatch && DC_XPATCH && g.ny % 32 == 0 ? 1u : 0u;
     const uint64_t kx = (g.nx + g.tx - 1) / g.tx - 1, ky = (g.ny + g.ty - 1) / g.ty - 1,
                    kz = g.nz ? (g.nz + g.tz - 1) / g.tz - 1 : 0;
@@ -421,9 +427,9 @@ int launch_dedupe_cross(const float* f, const uint32_t* basin, const uint64_t* x
     const uint64_t total = cross_edges(sl);
     if (total == 0) return 0;
     QEntry* q = static_cast<QEntry*>(queue);
-    uint64_t blocks = (total + 255) / 256;
+    uint64_t blocks = (total + DC_THREADS - 1) / DC_THREADS;
     if (blocks > uint64_t(num_sms) * 32) blocks = uint64_t(num_sms) * 32;
-    dedupe_cross_kernel<<<uint32_t(blocks), 256, 0, stream>>>(f, basin, xface, g, flip, q, cap, qlen, stats);
+    dedupe_cross_kernel<<<uint32_t(blocks), DC_THREADS, 0, stream>>>(f, basin, xface, g, flip, q, cap, qlen, stats);
     return 1;
 }
 
