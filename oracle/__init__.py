@@ -39,7 +39,7 @@ _lib = None
 
 PAIR_DTYPE = np.dtype([("birth_v", "<u4"), ("death_v", "<u4"), ("birth", "<f4"), ("death", "<f4")])
 
-OK, INVALID, TOO_LARGE, NONFINITE, NOMEM = 0, 1, 2, 3, 8
+OK, INVALID, TOO_LARGE, NONFINITE, NOMEM, CAPACITY = 0, 1, 2, 3, 8, 9
 
 
 class OracleError(RuntimeError):
@@ -66,7 +66,7 @@ def _load():
             lib.oracle_merge_tree.restype = ctypes.c_int
             lib.oracle_merge_tree.argtypes = [
                 ctypes.c_void_p, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32,
-                ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p,
+                ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64,
                 ctypes.POINTER(ctypes.c_uint64), ctypes.POINTER(ctypes.c_uint64)]
             lib.oracle_triplet_at.restype = ctypes.c_int
             lib.oracle_triplet_at.argtypes = [
@@ -75,7 +75,8 @@ def _load():
             lib.oracle_merge_tree_graph.restype = ctypes.c_int
             lib.oracle_merge_tree_graph.argtypes = [
                 ctypes.c_void_p, ctypes.c_uint32, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int,
-                ctypes.c_void_p, ctypes.c_void_p, ctypes.POINTER(ctypes.c_uint64), ctypes.POINTER(ctypes.c_uint64)]
+                ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64, ctypes.POINTER(ctypes.c_uint64),
+                ctypes.POINTER(ctypes.c_uint64)]
             _lib = lib
     return _lib
 
@@ -94,11 +95,13 @@ def merge_tree(f: np.ndarray, dims, conn: int = 6, split: bool = False, want_pai
     if f.size != n:
         raise ValueError("f size does not match dims")
     T = np.empty(n, dtype=np.uint64)
-    pairs = np.empty(n if want_pairs else 0, dtype=PAIR_DTYPE)
+    # a grid's strict minima form an independent set: at most ceil(n/2) diagram records
+    cap = (n + 1) // 2 + 1 if want_pairs else 0
+    pairs = np.empty(cap, dtype=PAIR_DTYPE)
     npairs, ness = ctypes.c_uint64(0), ctypes.c_uint64(0)
     st = lib.oracle_merge_tree(f.ctypes.data if n else None, nx, ny, nz, int(conn), int(bool(split)),
                                T.ctypes.data if n else None,
-                               pairs.ctypes.data if (want_pairs and n) else None,
+                               pairs.ctypes.data if (want_pairs and n) else None, cap,
                                ctypes.byref(npairs), ctypes.byref(ness))
     if st != OK:
         raise OracleError(st)
@@ -135,7 +138,7 @@ def merge_tree_graph(f: np.ndarray, row: np.ndarray, col: np.ndarray, split: boo
     npairs, ness = ctypes.c_uint64(0), ctypes.c_uint64(0)
     st = lib.oracle_merge_tree_graph(f.ctypes.data if n else None, n, row.ctypes.data,
                                      col.ctypes.data if col.size else None, int(bool(split)),
-                                     T.ctypes.data if n else None, pairs.ctypes.data, ctypes.byref(npairs),
+                                     T.ctypes.data if n else None, pairs.ctypes.data, pairs.size, ctypes.byref(npairs),
                                      ctypes.byref(ness))
     if st != OK:
         raise OracleError(st)

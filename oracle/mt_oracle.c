@@ -43,6 +43,7 @@
 #define OR_TOO_LARGE 2
 #define OR_NONFINITE 3
 #define OR_NOMEM 8
+#define OR_CAPACITY 9
 
 typedef struct {
     uint32_t birth_v, death_v;
@@ -106,36 +107,39 @@ static int grid_neighbours(uint64_t u, uint32_t nx, uint32_t ny, uint32_t nz, ui
  *   conn     : 4 (2D, nz must be 1) or 6
  *   split    : 0 = merge (join) tree of f; 1 = split tree (merge tree of -f)
  *   T        : out, n words (s << 32 | v), may be NULL
- *   pairs    : out, capacity >= n records, may be NULL; finite pairs by
+ *   pairs    : out, room for pairs_cap records, may be NULL; finite pairs by
  *              ascending birth vertex, then essential classes by ascending
  *              vertex (death_v = birth_v, death = +inf)
+ *   pairs_cap: records `pairs` holds (OR_CAPACITY when the diagram needs more; a grid
+ *              has at most ceil(n/2) records: strict minima are an independent set)
  *   n_pairs, n_ess : out counts
  */
 static int sweep(const float *f, uint64_t n, const graph_t *G, int split, uint64_t *T, oracle_pair *pairs,
-                 uint64_t *n_pairs, uint64_t *n_ess);
+                 uint64_t pairs_cap, uint64_t *n_pairs, uint64_t *n_ess);
 
 int oracle_merge_tree(const float *f, uint32_t nx, uint32_t ny, uint32_t nz, int conn, int split,
-                      uint64_t *T, oracle_pair *pairs, uint64_t *n_pairs, uint64_t *n_ess) {
+                      uint64_t *T, oracle_pair *pairs, uint64_t pairs_cap, uint64_t *n_pairs, uint64_t *n_ess) {
     if (!f && (uint64_t)nx * ny * nz != 0) return OR_INVALID;
     if (conn != 4 && conn != 6) return OR_INVALID;
     if (conn == 4 && nz != 1) return OR_INVALID;
     graph_t G = {nx, ny, nz, NULL, NULL};
-    return sweep(f, (uint64_t)nx * ny * nz, &G, split, T, pairs, n_pairs, n_ess);
+    return sweep(f, (uint64_t)nx * ny * nz, &G, split, T, pairs, pairs_cap, n_pairs, n_ess);
 }
 
 /* Explicit graph: the neighbours of u are col[row[u] .. row[u+1]). */
 int oracle_merge_tree_graph(const float *f, uint32_t n, const uint64_t *row, const uint32_t *col, int split,
-                            uint64_t *T, oracle_pair *pairs, uint64_t *n_pairs, uint64_t *n_ess) {
+                            uint64_t *T, oracle_pair *pairs, uint64_t pairs_cap, uint64_t *n_pairs,
+                            uint64_t *n_ess) {
     if (n && (!f || !row)) return OR_INVALID;
     for (uint32_t u = 0; u < n; u++)
         for (uint64_t j = row[u]; j < row[u + 1]; j++)
             if (col[j] >= n) return OR_INVALID;
     graph_t G = {n, 1, 1, row, col};
-    return sweep(f, n, &G, split, T, pairs, n_pairs, n_ess);
+    return sweep(f, n, &G, split, T, pairs, pairs_cap, n_pairs, n_ess);
 }
 
 static int sweep(const float *f, uint64_t n, const graph_t *G, int split, uint64_t *T, oracle_pair *pairs,
-                 uint64_t *n_pairs, uint64_t *n_ess) {
+                 uint64_t pairs_cap, uint64_t *n_pairs, uint64_t *n_ess) {
     if (n > 4294967295ull) return OR_TOO_LARGE; /* 32-bit ids */
     if (n_pairs) *n_pairs = 0;
     if (n_ess) *n_ess = 0;
@@ -246,30 +250,32 @@ static int sweep(const float *f, uint64_t n, const graph_t *G, int split, uint64
         uint32_t r = ds_find(parent, (uint32_t)u);
         if (cmin[r] == u) Tl[u] = ((uint64_t)u << 32) | u;
     }
-    if (pairs) {
+    for (uint64_t u = 0; u < n; u++) {
+        if (death[u] != UINT32_MAX) np++;
+        else if (cmin[ds_find(parent, (uint32_t)u)] == u) ne++;
+    }
+    int status = OR_OK;
+    if (pairs && np + ne > pairs_cap) status = OR_CAPACITY;
+    if (pairs && status == OR_OK) {
+        uint64_t k = 0;
         for (uint64_t u = 0; u < n; u++) {
             if (death[u] != UINT32_MAX) {
-                pairs[np].birth_v = (uint32_t)u;
-                pairs[np].death_v = death[u];
-                pairs[np].birth = f[u];          /* values copied from the input f (reading R14) */
-                pairs[np].death = f[death[u]];
-                np++;
+                pairs[k].birth_v = (uint32_t)u;
+                pairs[k].death_v = death[u];
+                pairs[k].birth = f[u];          /* values copied from the input f (reading R14) */
+                pairs[k].death = f[death[u]];
+                k++;
             }
         }
         for (uint64_t u = 0; u < n; u++) {
             uint32_t r = ds_find(parent, (uint32_t)u);
             if (cmin[r] == u) {
-                pairs[np + ne].birth_v = (uint32_t)u;
-                pairs[np + ne].death_v = (uint32_t)u;
-                pairs[np + ne].birth = f[u];
-                pairs[np + ne].death = INFINITY;
-                ne++;
+                pairs[k].birth_v = (uint32_t)u;
+                pairs[k].death_v = (uint32_t)u;
+                pairs[k].birth = f[u];
+                pairs[k].death = INFINITY;
+                k++;
             }
-        }
-    } else {
-        for (uint64_t u = 0; u < n; u++) {
-            if (death[u] != UINT32_MAX) np++;
-            else if (cmin[ds_find(parent, (uint32_t)u)] == u) ne++;
         }
     }
     if (n_pairs) *n_pairs = np;
@@ -278,7 +284,7 @@ static int sweep(const float *f, uint64_t n, const graph_t *G, int split, uint64
     free(R);
     free(order); free(parent); free(size); free(cmin); free(death); free(done); free(g);
     if (!T) free(Tl);
-    return OR_OK;
+    return status;
 }
 
 /* Version tag so the Python loader can detect a stale build. */

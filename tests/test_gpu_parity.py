@@ -234,11 +234,12 @@ def test_host_pipeline_outputs():
 
 
 def test_full_size_c5_sampled():
-    """c5 at its full 1024^3 size in bench.py's launch configuration: O1 cannot run here, so
-    (1) properties that hold at any size, computed independently on the GPU with plain torch ops:
-    I1 key(v) < key(u) <= key(s) for non-roots, I2 s = u iff u has a lower neighbour, I3 one root,
-    I4 #finite pairs = #strict local minima - 1; (2) exact triplets and diagram records of sampled
-    vertices against O4 (the definition by bounded floods, oracle.triplet_at)."""
+    """c5 at its full 1024^3 size in bench.py's launch configuration (the full O1 memcmp is
+    tests/test_gpu_full_c5.py, opt-in): (1) properties that hold at any size, computed
+    independently on the GPU with plain torch ops: I1 key(v) < key(u) <= key(s) for non-roots,
+    I2 s = u iff u has a lower neighbour, I3 one root, I4 #finite pairs = #strict local minima - 1;
+    (2) exact triplets and diagram records of level-stratified samples against O4 (the definition
+    by bounded floods, oracle.triplet_at), every sample checked."""
     import resource
     log = lambda msg: print(f"[c5] {msg}: maxrss {resource.getrusage(resource.RUSAGE_SELF).ru_maxrss >> 20} GB",
                             flush=True)
@@ -284,24 +285,43 @@ def test_full_size_c5_sampled():
     assert n_root == 1, "I3: one root"
     assert bad_v == 0 and bad_s == 0, "I1: key(v) < key(u) <= key(s)"
     log("invariants")
-    # (2) sampled exact triplets (O4) and the sampled minima's diagram records
+    # (2) exact triplets (O4) of samples stratified by level, none skipped.  O4 floods the
+    # sublevel component of u, so it can only reach levels below 3-D percolation: regular
+    # vertices are stratified by their own level over the lowest 20 % (4 strata of 5 %), branches
+    # (minima) by their death level over the same range (4 strata), 12 samples per stratum.
+    # Every sample must be checked: a flood past the cap FAILS the test (a wrong, too-low saddle
+    # from the GPU would otherwise be skipped).  Vertices above percolation are covered by the
+    # invariants above and by the full O1 memcmp (tests/test_gpu_full_c5.py, MT_FULL_C5=1).
     rng = np.random.default_rng(2301)
-    branch = torch.nonzero(s != torch.arange(n, device="cuda", dtype=torch.int64), as_tuple=False).view(-1)
-    picks = np.concatenate([rng.integers(0, n, 48),
-                            branch[torch.from_numpy(rng.integers(0, branch.numel(), 48)).cuda()].cpu().numpy()])
+    ids = torch.arange(n, device="cuda", dtype=torch.int64)
+    is_branch = s != ids
+    lev_u = fd
+    lev_d = fd[s]
+    qs = torch.quantile(fd[torch.from_numpy(rng.integers(0, n, 1 << 23)).cuda()],
+                        torch.tensor([0.0, 0.05, 0.10, 0.15, 0.20], device="cuda")).tolist()
+    qs[0] = -float("inf")
+    picks, labels = [], []
+    for kind, mask, lev in (("regular", ~is_branch & (v != ids), lev_u), ("branch", is_branch, lev_d)):
+        for j in range(4):
+            cand = torch.nonzero(mask & (lev > qs[j]) & (lev <= qs[j + 1]), as_tuple=False).view(-1)
+            assert cand.numel() >= 12, (kind, j, cand.numel())
+            sel = cand[torch.from_numpy(rng.integers(0, cand.numel(), 12)).cuda()].cpu().numpy()
+            picks.extend(sel.tolist())
+            labels.extend([f"{kind} level q{5 * j}-{5 * j + 5}%"] * sel.size)
+            del cand
+    del ids, is_branch, lev_d
+    picks = np.asarray(picks, dtype=np.int64)
     Ts = T[torch.from_numpy(picks).cuda()].cpu().numpy().view(np.uint64)
     recs = _lib.pairs_to_numpy(rec)
     log("samples")
-    checked = 0
-    for u, t in zip(picks.tolist(), Ts.tolist()):
-        r = oracle.triplet_at(f, dims, conn, u, cap=1 << 21)   # floods past 2M vertices are skipped
-        if r is None:
-            continue
-        checked += 1
-        assert (r[0] << 32) | r[1] == t, (u, r, divmod(t, 1 << 32))
+    checked = {}
+    for u, t, lab in zip(picks.tolist(), Ts.tolist(), labels):
+        r = oracle.triplet_at(f, dims, conn, u, cap=1 << 23)
+        assert r is not None, f"O4 flood of sample u={u} ({lab}) passed 2^23 vertices"
+        assert (r[0] << 32) | r[1] == t, (u, lab, r, divmod(t, 1 << 32))
         if r[0] != u:   # a branch born at u dies at s: its record, in ascending-birth order
             k = int(np.searchsorted(recs["birth_v"][:npairs], u))
             assert recs[k]["birth_v"] == u and recs[k]["death_v"] == r[0]
             assert recs[k]["birth"].tobytes() == f[u].tobytes() and recs[k]["death"].tobytes() == f[r[0]].tobytes()
-    log(f"{checked} of {picks.size} sampled vertices checked against O4")
-    assert checked >= 32, checked
+        checked[lab] = checked.get(lab, 0) + 1
+    log(f"all {picks.size} stratified samples checked against O4: {checked}")
