@@ -172,7 +172,8 @@ mt_status mt_compute_local(mt_ctx *ctx, const float *f_slab, uint32_t flags, mt_
  * mt_compute_local) and their number. */
 mt_status mt_forest_view(mt_ctx *ctx, const mt_forest_record **records, uint64_t *n_records,
                          mt_stream_t stream);
-/* Device scratch bytes mt_compute_global needs for n_all gathered records. */
+/* Device scratch bytes mt_compute_global needs for n_all gathered records; 0 when the id
+ * tables would pass 2^31 slots (n_all > 2^29: mt_compute_global returns MT_ERR_TOO_LARGE). */
 size_t mt_forest_scratch_bytes(uint64_t n_all);
 /* all (device): the records of every slab, n_all of them; z_bounds (host):
  * the P+1 plane boundaries of all slabs (z_bounds[0] = 0, z_bounds[P] = nz);
@@ -195,7 +196,10 @@ size_t mt_graph_workspace_bytes(uint32_t n, uint64_t n_adj);
 mt_status mt_create_graph(mt_ctx **out, uint32_t n, uint64_t n_adj, int cuda_device, void *workspace,
                           size_t workspace_bytes);
 /* Asynchronous like mt_compute; f, row, col borrowed until the stream passes
- * this call's work; triplets (device, n uint64) out.  mt_diagram as usual. */
+ * this call's work; triplets (device, n uint64) out.  mt_diagram as usual; an
+ * adjacency longer than the context's n_adj (row[n] > n_adj) is never dropped
+ * silently: the sticky status becomes MT_ERR_CAPACITY (mt_diagram /
+ * mt_last_error). */
 mt_status mt_compute_graph(mt_ctx *ctx, const float *f, const uint64_t *row, const uint32_t *col,
                            uint64_t *triplets, uint32_t flags, mt_stream_t stream);
 

@@ -291,6 +291,10 @@ class GraphMergeTree:
         import torch
         if f.numel() != self.n or row.numel() != self.n + 1 or col.numel() > self.n_adj:
             raise ValueError("graph sizes do not match the context")
+        for t, dts, name in ((f, (torch.float32,), "f"), (row, (torch.int64, torch.uint64), "row"),
+                             (col, (torch.int32, torch.uint32), "col")):
+            if t.dtype not in dts or not t.is_cuda or not t.is_contiguous() or t.device != self.device:
+                raise ValueError(f"{name} must be a contiguous {dts[0]} tensor on {self.device}")
         if triplets is None:
             triplets = torch.empty(self.n, dtype=torch.int64, device=f.device)
         mt_compute_graph(self.ctx, f.data_ptr(), row.data_ptr(), col.data_ptr() if col.numel() else 0,

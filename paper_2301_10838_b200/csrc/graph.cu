@@ -66,7 +66,8 @@ __global__ void __launch_bounds__(256) graph_compress_kernel(Cell* C, uint32_t n
 
 __global__ void __launch_bounds__(256)
 graph_edges_kernel(const uint64_t* __restrict__ row, const uint32_t* __restrict__ col, uint32_t n, const Cell* C,
-                   QEntryG* __restrict__ q, uint64_t cap, unsigned long long* __restrict__ qlen) {
+                   QEntryG* __restrict__ q, uint64_t cap, unsigned long long* __restrict__ qlen,
+                   unsigned long long* __restrict__ counters) {
     for (uint64_t u = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; u < n; u += uint64_t(gridDim.x) * blockDim.x) {
         const Cell cu = ld_cell(C + u);
         const uint32_t bu = cv_of(cu);               // after compress: the basin (a root is its own)
@@ -80,6 +81,7 @@ graph_edges_kernel(const uint64_t* __restrict__ row, const uint32_t* __restrict_
             const uint64_t kw = self_key(cw, w);
             const unsigned long long pos = atomicAdd(qlen, 1ull);
             if (pos < cap) q[pos] = ku > kw ? QEntryG{ku, bu, bw} : QEntryG{kw, bw, bu};
+            else atomicOr(counters + CTR_ERR, ERR_CAPACITY);   // row[n] > n_adj: reported, never dropped
         }
     }
 }
@@ -100,10 +102,11 @@ void launch_graph_init(const float* f, const uint64_t* row, const uint32_t* col,
 }
 
 void launch_graph_edges(const uint64_t* row, const uint32_t* col, uint32_t n, Cell* C, uint32_t* /*basin*/,
-                        void* queue, uint64_t cap, unsigned long long* qlen, int num_sms, cudaStream_t stream) {
+                        void* queue, uint64_t cap, unsigned long long* qlen, unsigned long long* counters,
+                        int num_sms, cudaStream_t stream) {
     if (!n) return;
     graph_edges_kernel<<<grid_of(n, num_sms), 256, 0, stream>>>(row, col, n, C, static_cast<QEntryG*>(queue), cap,
-                                                                qlen);
+                                                                qlen, counters);
 }
 
 }  // namespace mt

@@ -8,6 +8,14 @@
 
 namespace mt {
 
+// Per-device launch attributes (mt_api.cu).  A CUfunction's attributes belong to the device's
+// context, so each device a context runs on needs its own opt-in; both helpers are thread safe
+// and cache per (kernel, current device).
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize, bytes) once per kernel and device
+cudaError_t ensure_smem_attr(const void* func, int bytes);
+// resident CTAs per SM of a kernel on the current device (cached)
+int occupancy_per_sm(const void* func, int threads, size_t smem);
+
 // The part of the global grid one context computes: planes [z_begin, z_end) of an
 // nx x ny x nz grid (the whole grid on one GPU; a z-slab per rank on several).
 // Vertex ids are global; device pointers handed to the launchers are shifted by
@@ -92,7 +100,8 @@ void launch_merge_queue(Cell* C, const void* queue, uint64_t cap, const unsigned
 void launch_graph_init(const float* f, const uint64_t* row, const uint32_t* col, uint32_t n, uint32_t flip, Cell* C,
                        uint32_t* basin, unsigned long long* counters, int num_sms, cudaStream_t stream);
 void launch_graph_edges(const uint64_t* row, const uint32_t* col, uint32_t n, Cell* C, uint32_t* basin, void* queue,
-                        uint64_t cap, unsigned long long* qlen, int num_sms, cudaStream_t stream);
+                        uint64_t cap, unsigned long long* qlen, unsigned long long* counters, int num_sms,
+                        cudaStream_t stream);
 
 // K4: repair (memoised walks per brick, diagram records staged per segment)
 // and K5: the ordered diagram (repair_diagram.cu)
@@ -127,7 +136,9 @@ struct SlabBounds {
 void launch_forest_mark(const Cell* C, const Slab& sl, uint8_t* flag, cudaStream_t stream);
 void launch_forest_compact(const Cell* C, const float* f, const Slab& sl, const uint8_t* flag, mt_forest_record* recs,
                            uint64_t cap, unsigned long long* count, int num_sms, cudaStream_t stream);
-uint32_t forest_table_size(uint64_t n_all);
+// open-addressing table slots for n_all gathered records (>= 4 n_all, a power of two), or 0
+// when that exceeds 2^31 (32-bit table indices)
+uint64_t forest_table_size(uint64_t n_all);
 void launch_forest_build(const mt_forest_record* all, uint64_t n_all, uint64_t* table, uint64_t* vtable,
                          uint32_t mask, Cell* cells, int num_sms, cudaStream_t stream);
 void launch_forest_merge(const ForestRef& F, const Slab& sl, const SlabBounds& b, unsigned long long* fetch,

@@ -436,16 +436,10 @@ int launch_dedupe_cross(const float* f, const uint32_t* basin, const uint64_t* x
 void launch_merge_queue(Cell* C, const void* queue, uint64_t cap, const unsigned long long* qlen,
                         unsigned long long* fetch, unsigned long long* stats, int num_sms, cudaStream_t stream) {
     const QEntry* q = static_cast<const QEntry*>(queue);
-    static int per_sm[2] = {0, 0};  // persistent grid: as many CTAs as fit on every SM
-    const int t = stats ? 1 : 0;
-    if (!per_sm[t]) {
-        if (stats)
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[t], merge_queue_kernel<true>, 256, 0);
-        else
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[t], merge_queue_kernel<false>, 256, 0);
-        if (per_sm[t] < 1) per_sm[t] = 1;
-    }
-    const uint32_t pblocks = uint32_t(num_sms) * per_sm[t];
+    // persistent grid: as many CTAs as fit on every SM of this device
+    const int per_sm = stats ? occupancy_per_sm(reinterpret_cast<const void*>(merge_queue_kernel<true>), 256, 0)
+                             : occupancy_per_sm(reinterpret_cast<const void*>(merge_queue_kernel<false>), 256, 0);
+    const uint32_t pblocks = uint32_t(num_sms) * per_sm;
     if (stats)
         merge_queue_kernel<true><<<pblocks, 256, 0, stream>>>(C, q, cap, qlen, fetch, stats);
     else

@@ -9,11 +9,48 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <new>
+#include <set>
+#include <utility>
 
 #include "common.cuh"
 #include "kernels.cuh"
 #include "mt.h"
+
+namespace mt {
+
+namespace {
+std::mutex g_attr_mutex;
+std::set<std::pair<const void*, int>> g_smem_done;
+std::map<std::pair<const void*, int>, int> g_occupancy;
+}  // namespace
+
+cudaError_t ensure_smem_attr(const void* func, int bytes) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    std::lock_guard<std::mutex> lock(g_attr_mutex);
+    if (g_smem_done.count({func, dev})) return cudaSuccess;
+    e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (e == cudaSuccess) g_smem_done.insert({func, dev});
+    return e;
+}
+
+int occupancy_per_sm(const void* func, int threads, size_t smem) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return 1;
+    std::lock_guard<std::mutex> lock(g_attr_mutex);
+    auto it = g_occupancy.find({func, dev});
+    if (it != g_occupancy.end()) return it->second;
+    int per = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, func, threads, smem) != cudaSuccess || per < 1) per = 1;
+    g_occupancy[{func, dev}] = per;
+    return per;
+}
+
+}  // namespace mt
 
 namespace {
 
@@ -386,7 +423,7 @@ mt_status mt_compute_graph(mt_ctx* c, const float* f, const uint64_t* row, const
                           ctr, c->num_sms, s);
     mark(c, "graph_edges", s);
     mt::launch_graph_edges(row, col, uint32_t(c->n), cells, nullptr, c->ws + c->L.queue, c->L.queue_cap,
-                           ctr + mt::CTR_QLEN, c->num_sms, s);
+                           ctr + mt::CTR_QLEN, ctr, c->num_sms, s);
     mark(c, "merge_queue", s);
     mt::launch_merge_queue(cells, c->ws + c->L.queue, c->L.queue_cap, ctr + mt::CTR_QLEN, ctr + mt::CTR_QFETCH, stats,
                            c->num_sms, s);
@@ -451,7 +488,9 @@ mt_status mt_forest_view(mt_ctx* c, const mt_forest_record** records, uint64_t* 
 }
 
 size_t mt_forest_scratch_bytes(uint64_t n_all) {
-    return 2 * align_up(size_t(mt::forest_table_size(n_all)) * sizeof(uint64_t)) + align_up(n_all * sizeof(mt::Cell));
+    const uint64_t t = mt::forest_table_size(n_all);
+    if (t == 0) return 0;
+    return 2 * align_up(size_t(t) * sizeof(uint64_t)) + align_up(n_all * sizeof(mt::Cell));
 }
 
 mt_status mt_compute_global(mt_ctx* c, const mt_forest_record* all, uint64_t n_all, const uint32_t* z_bounds,
@@ -466,13 +505,13 @@ mt_status mt_compute_global(mt_ctx* c, const mt_forest_record* all, uint64_t n_a
         found |= z_bounds[k] == c->slab.z_begin && z_bounds[k + 1] == c->slab.z_end;
     }
     if (!found) return MT_ERR_INVALID_ARG;
-    if (n_all > 0xffffffffull) return MT_ERR_TOO_LARGE;
+    if (n_all > 0xffffffffull || mt::forest_table_size(n_all) == 0) return MT_ERR_TOO_LARGE;
     if (!scratch || scratch_bytes < mt_forest_scratch_bytes(n_all) || reinterpret_cast<uintptr_t>(scratch) % ALIGN)
         return MT_ERR_WORKSPACE;
     DeviceGuard g(c->device);
     if (!g.ok) return MT_ERR_CUDA;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    const uint32_t tsize = mt::forest_table_size(n_all);
+    const uint32_t tsize = uint32_t(mt::forest_table_size(n_all));
     uint64_t* table = static_cast<uint64_t*>(scratch);
     uint64_t* vtable = reinterpret_cast<uint64_t*>(static_cast<char*>(scratch) + align_up(size_t(tsize) * 8));
     mt::Cell* fcells = reinterpret_cast<mt::Cell*>(static_cast<char*>(scratch) + 2 * align_up(size_t(tsize) * 8));

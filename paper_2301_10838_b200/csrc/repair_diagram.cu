@@ -441,12 +441,7 @@ __global__ void finish_diagram_kernel(unsigned long long* __restrict__ counters,
 template <class View, int BY>
 void launch_brick(const View& view, const Cell* C, uint64_t* T, const float* f, const Slab& sl, BrickGeom g,
                   uint64_t nb, uint32_t flip, const RepairOut& o, unsigned long long* stats, cudaStream_t stream) {
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(repair_brick_kernel<View, BY>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             int(sizeof(RepairSmem)));
-        attr = true;
-    }
+    ensure_smem_attr(reinterpret_cast<const void*>(repair_brick_kernel<View, BY>), int(sizeof(RepairSmem)));
     repair_brick_kernel<View, BY><<<uint32_t(nb), RB_THREADS, sizeof(RepairSmem), stream>>>(
         view, C, T, f, sl, g, flip, o.stage, o.stage_cap, o.seg_cnt, o.seg_pos, o.counters, stats);
 }

@@ -283,10 +283,10 @@ void launch_forest_compact(const Cell* C, const float* f, const Slab& sl, const 
     forest_compact_kernel<<<grid_for(sl.n, num_sms), 256, 0, stream>>>(C, f, sl.base, sl.n, flag, recs, cap, count);
 }
 
-uint32_t forest_table_size(uint64_t n_all) {
+uint64_t forest_table_size(uint64_t n_all) {
     uint64_t s = 1024;
     while (s < 4 * n_all) s <<= 1;   // the value table holds up to 2 entries per record
-    return uint32_t(s);
+    return s > (1ull << 31) ? 0 : s; // table indices and the mask are 32-bit
 }
 
 void launch_forest_build(const mt_forest_record* all, uint64_t n_all, uint64_t* table, uint64_t* vtable,

@@ -34,8 +34,6 @@
 // Layout: f float32[n] x fastest (reading R10) read once (coalesced 128-B
 // rows); 16-B cells written once (coalesced 512-B rows).  One CTA of 512
 // threads per tile; 112 KB of dynamic shared memory (2 CTAs per SM).
-#include <cstdlib>
-
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -768,14 +766,10 @@ uint64_t xface_entries(const Slab& sl) {
     return tiles * 2 * ty * tz;
 }
 
-int tile_vertices() {
-    static int nv = 0;
-    if (!nv) {
-        const char* e = getenv("MT_TILE_NV");  // 4096 (default) or 2048; tile_shape follows it
-        nv = (e && atoi(e) == 2048) ? 2048 : 4096;
-    }
-    return nv;
-}
+#ifndef MT_TILE_NV
+#define MT_TILE_NV 4096   // vertices per tile (build knob: 4096 or 2048); tile_shape follows it
+#endif
+constexpr int tile_vertices() { return MT_TILE_NV; }
 
 void tile_shape(uint32_t nz_global, uint32_t* ty, uint32_t* tz) {
     const int nv = tile_vertices();
@@ -792,14 +786,8 @@ template <int TY, int TZ>
 void launch_tile(const float* f, Cell* C, uint32_t* basin, uint64_t* xface, const Slab& sl, uint32_t tx, uint32_t tyn, uint32_t grid,
                  uint32_t flip, unsigned long long* counters, unsigned long long* stats, cudaStream_t stream) {
     constexpr int NV = TX * TY * TZ;
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(tile_tmt_kernel<TY, TZ, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             int(smem_bytes<NV>()));
-        cudaFuncSetAttribute(tile_tmt_kernel<TY, TZ, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             int(smem_bytes<NV>()));
-        attr = true;
-    }
+    ensure_smem_attr(reinterpret_cast<const void*>(tile_tmt_kernel<TY, TZ, false>), int(smem_bytes<NV>()));
+    ensure_smem_attr(reinterpret_cast<const void*>(tile_tmt_kernel<TY, TZ, true>), int(smem_bytes<NV>()));
     if (stats)
         tile_tmt_kernel<TY, TZ, true><<<grid, NV / 8, smem_bytes<NV>(), stream>>>(f, C, basin, xface, sl.nx, sl.ny,
                                                                                  sl.z_begin, sl.z_end, tx, tyn,

@@ -80,7 +80,8 @@ class SlabMergeTree:
             self.ctx = None
 
     def compute_local(self, f_slab: torch.Tensor, split: bool = False, stream=None):
-        if f_slab.dtype != torch.float32 or not f_slab.is_cuda or f_slab.numel() != self.n:
+        if f_slab.dtype != torch.float32 or not f_slab.is_cuda or not f_slab.is_contiguous() or \
+                f_slab.numel() != self.n:
             raise ValueError("f_slab must be a float32 CUDA tensor with the slab's nx*ny*(z_end-z_begin) values")
         self._f = f_slab  # borrowed by the library until compute_global's work completes
         _lib.mt_compute_local(self.ctx, f_slab.data_ptr(), _lib.MT_FLAG_SPLIT_TREE if split else 0, stream)

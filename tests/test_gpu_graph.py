@@ -54,3 +54,37 @@ def test_edgeless_and_tiny():
     for n in (1, 2, 7):
         row, col = oracle.csr_from_edges(n, [])
         check(np.arange(n, dtype=np.float32)[::-1].copy(), row, col)
+
+
+def test_adjacency_longer_than_context_is_reported():
+    """row[n] > n_adj through the raw C ABI: MT_ERR_CAPACITY at mt_diagram, never a silently
+    wrong tree (the queue would drop edges)."""
+    n = 2000
+    rng = np.random.default_rng(7)
+    row, col = oracle.csr_from_edges(n, er_graph(rng, n, 6.0))
+    small = 100
+    nbytes = _lib.mt_graph_workspace_bytes(n, small)
+    ws = torch.empty(nbytes + 256, dtype=torch.uint8, device="cuda")
+    ctx = _lib.mt_create_graph(n, small, 0, (ws.data_ptr() + 255) // 256 * 256, nbytes)
+    try:
+        f = torch.from_numpy(rng.random(n).astype(np.float32)).cuda()
+        r = torch.from_numpy(row.astype(np.int64)).cuda()
+        c = torch.from_numpy(col.astype(np.int32)).cuda()
+        T = torch.empty(n, dtype=torch.int64, device="cuda")
+        _lib.mt_compute_graph(ctx, f.data_ptr(), r.data_ptr(), c.data_ptr(), T.data_ptr())
+        st, _, _ = _lib.mt_diagram(ctx)
+        assert st == _lib.MT_ERR_CAPACITY
+    finally:
+        _lib.mt_destroy(ctx)
+
+
+def test_graph_compute_rejects_wrong_dtypes():
+    n = 10
+    row, col = oracle.csr_from_edges(n, [(i, i + 1) for i in range(n - 1)])
+    g = _lib.GraphMergeTree(n, col.size, device=0)
+    f = torch.zeros(n, dtype=torch.float32, device="cuda")
+    r = torch.from_numpy(row.astype(np.int64)).cuda()
+    with pytest.raises(ValueError):
+        g.compute(f, r, torch.from_numpy(col.astype(np.int64)).cuda())
+    with pytest.raises(ValueError):
+        g.compute(f.double(), r, torch.from_numpy(col.astype(np.int32)).cuda())
