@@ -50,6 +50,10 @@ int occupancy_per_sm(const void* func, int threads, size_t smem) {
     return per;
 }
 
+struct DistState;
+void dist_destroy(DistState* d);
+mt_status dist_compute(mt_ctx* c, DistState* d, const float* f, uint64_t* T, uint32_t flags, cudaStream_t s);
+
 }  // namespace mt
 
 namespace {
@@ -158,7 +162,17 @@ struct mt_ctx {
     cudaEvent_t ev[MAX_EVENTS + 1] = {};
     const char* ev_name[MAX_EVENTS] = {};
     int nev = 0;
+    mt::DistState* dist = nullptr;  // mt_create_dist: communicator + exchange buffers (dist.cu)
 };
+
+namespace mt {
+void slab_forest(mt_ctx* c, mt_forest_record** recs, unsigned long long** count_dev, uint64_t* cap) {
+    *recs = reinterpret_cast<mt_forest_record*>(c->ws + c->L.recs);
+    *count_dev = reinterpret_cast<unsigned long long*>(c->ws + c->L.counters) + CTR_FCOUNT;
+    *cap = c->L.recs_cap;
+}
+void attach_dist(mt_ctx* c, DistState* d) { c->dist = d; }
+}  // namespace mt
 
 namespace {
 
@@ -434,6 +448,14 @@ mt_status mt_compute_graph(mt_ctx* c, const float* f, const uint64_t* row, const
 mt_status mt_compute(mt_ctx* c, const float* f, uint64_t* T, uint32_t flags, mt_stream_t stream) {
     if (!c) return MT_ERR_INVALID_ARG;
     if (flags & ~uint32_t(MT_FLAG_SPLIT_TREE)) return MT_ERR_INVALID_ARG;
+    if (c->dist) {   // mt_create_dist: local phase, NCCL exchange, global phase (dist.cu)
+        if (!f || !T) return MT_ERR_INVALID_ARG;
+        DeviceGuard g(c->device);
+        if (!g.ok) return MT_ERR_CUDA;
+        const mt_status st = mt::dist_compute(c, c->dist, f, T, flags, static_cast<cudaStream_t>(stream));
+        if (st != MT_OK && c->sticky == MT_OK) c->sticky = st;
+        return st;
+    }
     if (c->multi || c->graph) return MT_ERR_STATE;  // slab contexts use mt_compute_local / mt_compute_global
     if (c->n == 0) {
         c->computed = true;
@@ -651,6 +673,7 @@ int mt_stats(mt_ctx* c, uint64_t* out, int max, mt_stream_t stream) {
 void mt_destroy(mt_ctx* c) {
     if (!c) return;
     DeviceGuard g(c->device);
+    mt::dist_destroy(c->dist);
     for (int i = 0; i <= MAX_EVENTS; ++i)
         if (c->ev[i]) cudaEventDestroy(c->ev[i]);
     if (c->host_ctr) cudaFreeHost(c->host_ctr);

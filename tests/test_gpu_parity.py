@@ -286,9 +286,11 @@ def test_full_size_c5_sampled():
     assert bad_v == 0 and bad_s == 0, "I1: key(v) < key(u) <= key(s)"
     log("invariants")
     # (2) exact triplets (O4) of samples stratified by level, none skipped.  O4 floods the
-    # sublevel component of u, so it can only reach levels below 3-D percolation: regular
-    # vertices are stratified by their own level over the lowest 20 % (4 strata of 5 %), branches
-    # (minima) by their death level over the same range (4 strata), 12 samples per stratum.
+    # sublevel component of u, so it can only reach levels below 3-D percolation (the first run,
+    # gpurun_out r2a, saw a flood past 2^23 vertices in the 15-20 % stratum: this field's sublevel
+    # sets percolate there): regular vertices are stratified by their own level over the lowest
+    # 12 % (4 strata of 3 %), branches (minima) by their death level over the same range,
+    # 12 samples per stratum.
     # Every sample must be checked: a flood past the cap FAILS the test (a wrong, too-low saddle
     # from the GPU would otherwise be skipped).  Vertices above percolation are covered by the
     # invariants above and by the full O1 memcmp (tests/test_gpu_full_c5.py, MT_FULL_C5=1).
@@ -298,7 +300,7 @@ def test_full_size_c5_sampled():
     lev_u = fd
     lev_d = fd[s]
     qs = torch.quantile(fd[torch.from_numpy(rng.integers(0, n, 1 << 23)).cuda()],
-                        torch.tensor([0.0, 0.05, 0.10, 0.15, 0.20], device="cuda")).tolist()
+                        torch.tensor([0.0, 0.03, 0.06, 0.09, 0.12], device="cuda")).tolist()
     qs[0] = -float("inf")
     picks, labels = [], []
     for kind, mask, lev in (("regular", ~is_branch & (v != ids), lev_u), ("branch", is_branch, lev_d)):
@@ -307,7 +309,7 @@ def test_full_size_c5_sampled():
             assert cand.numel() >= 12, (kind, j, cand.numel())
             sel = cand[torch.from_numpy(rng.integers(0, cand.numel(), 12)).cuda()].cpu().numpy()
             picks.extend(sel.tolist())
-            labels.extend([f"{kind} level q{5 * j}-{5 * j + 5}%"] * sel.size)
+            labels.extend([f"{kind} level q{3 * j}-{3 * j + 3}%"] * sel.size)
             del cand
     del ids, is_branch, lev_d
     picks = np.asarray(picks, dtype=np.int64)
