@@ -243,7 +243,9 @@ class SlabRunner:
         from paper_2301_10838_b200 import _lib
         from paper_2301_10838_b200.dist import DistMergeTree
         self.lib = _lib
-        self.d = DistMergeTree(dims, device=dev)
+        import torch.distributed as dist
+        # the library's own NCCL exchange (mt_create_dist) on NCCL groups; torch's collectives otherwise
+        self.d = DistMergeTree(dims, device=dev, transport="nccl" if dist.get_backend() == "nccl" else "torch")
         self.ctx = self.d.slab.ctx
         self.n = self.d.slab.n
         self.f = f_slab

@@ -51,7 +51,7 @@ typedef enum {
     MT_ERR_TOO_LARGE = 2,   /* nx*ny*nz > 2^32 - 1: 32-bit vertex ids */
     MT_ERR_NONFINITE = 3,   /* NaN or +-Inf in f (reading R3); sticky */
     MT_ERR_CUDA = 4,        /* a CUDA runtime call failed */
-    MT_ERR_NCCL = 5,        /* reserved for the multi-GPU exchange */
+    MT_ERR_NCCL = 5,        /* NCCL missing or an NCCL call failed (mt_create_dist contexts) */
     MT_ERR_STATE = 6,       /* call out of order, e.g. mt_diagram before mt_compute */
     MT_ERR_CAPACITY = 7,    /* output buffer too small; required count returned */
     MT_ERR_WORKSPACE = 8    /* workspace NULL, too small or misaligned (needs 256 B) */
@@ -182,6 +182,31 @@ size_t mt_forest_scratch_bytes(uint64_t n_all);
 mt_status mt_compute_global(mt_ctx *ctx, const mt_forest_record *all, uint64_t n_all,
                             const uint32_t *z_bounds, uint32_t nslabs, void *scratch,
                             size_t scratch_bytes, uint64_t *triplets_slab, mt_stream_t stream);
+
+/* ---- Multi-GPU with the exchange inside the library ----------
+ * One process per GPU.  Rank 0 calls mt_get_unique_id and the caller
+ * broadcasts the 128 bytes to every rank (e.g. over torch.distributed); each
+ * rank then creates its context with mt_create_dist and calls mt_compute /
+ * mt_diagram exactly as on one GPU, with its slab of f and of the triplets
+ * (planes [z_begin, z_end) of mt_dist_slab_bounds; global vertex ids).
+ * mt_compute on such a context runs the local phase, then on `stream` an
+ * ncclAllGather of the boundary-forest sizes (8 B per rank), ONE host sync to
+ * read them, a grouped ncclBroadcast of every rank's records (exact length,
+ * rank order) and the global phase (mt_compute_local / mt_compute_global
+ * above), so it is not fully asynchronous.  NCCL (libnccl.so.2) is loaded at
+ * run time: MT_ERR_NCCL if it is missing or a collective fails.  The
+ * gathered records and the forest tables are device buffers the context owns
+ * and grows on demand (cudaMalloc only when a step needs more than any
+ * earlier one); mt_destroy frees them and the communicator.  3-D grids, conn
+ * 6, 1 <= nranks <= min(64, nz). */
+mt_status mt_get_unique_id(uint8_t id[128]);
+/* bounds (host, nranks + 1): the planes of each rank's slab -- as equal as
+ * possible, on multiples of 8 (the tile depth) when nz >= 8 nranks. */
+mt_status mt_dist_slab_bounds(uint32_t nz, int nranks, uint32_t *bounds);
+size_t mt_dist_workspace_bytes(const uint32_t global_dims[3], int conn, int rank, int nranks);
+mt_status mt_create_dist(mt_ctx **out, const uint32_t global_dims[3], int conn, int rank, int nranks,
+                         const uint8_t nccl_id[128], int cuda_device, void *workspace,
+                         size_t workspace_bytes);
 
 /* ---- Explicit graphs ----------------------------------
  * The same computation on an undirected graph G = (V, E) (PAPER.md:128-131:

@@ -31,7 +31,8 @@ EXPORTS = ["mt_workspace_bytes", "mt_create", "mt_compute", "mt_set_diagram_outp
            "mt_diagram_view", "mt_last_error", "mt_last_launch_count", "mt_set_profiling", "mt_kernel_times",
            "mt_status_string", "mt_destroy", "mt_abi_version", "mt_set_stats", "mt_stats", "mt_slab_workspace_bytes",
            "mt_create_slab", "mt_compute_local", "mt_forest_view", "mt_forest_scratch_bytes", "mt_compute_global",
-           "mt_filter_diagram", "mt_graph_workspace_bytes", "mt_create_graph", "mt_compute_graph"]
+           "mt_filter_diagram", "mt_graph_workspace_bytes", "mt_create_graph", "mt_compute_graph",
+           "mt_get_unique_id", "mt_dist_slab_bounds", "mt_dist_workspace_bytes", "mt_create_dist"]
 
 
 class MTError(RuntimeError):
@@ -89,6 +90,11 @@ def load(build_if_missing: bool = False):
         "mt_compute_global": (ctypes.c_int, [vp, vp, ctypes.c_uint64, u32p, ctypes.c_uint32, vp, ctypes.c_size_t,
                                              vp, vp]),
         "mt_abi_version": (ctypes.c_int, []),
+        "mt_get_unique_id": (ctypes.c_int, [ctypes.c_void_p]),
+        "mt_dist_slab_bounds": (ctypes.c_int, [ctypes.c_uint32, ctypes.c_int, u32p]),
+        "mt_dist_workspace_bytes": (ctypes.c_size_t, [u32p, ctypes.c_int, ctypes.c_int, ctypes.c_int]),
+        "mt_create_dist": (ctypes.c_int, [ctypes.POINTER(vp), u32p, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                          ctypes.c_void_p, ctypes.c_int, vp, ctypes.c_size_t]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -245,6 +251,36 @@ def mt_compute_global(ctx, all_ptr: int, n_all: int, z_bounds, scratch_ptr: int,
     _check(load().mt_compute_global(ctx, ctypes.c_void_p(all_ptr or None), ctypes.c_uint64(n_all), zb,
                                     len(z_bounds) - 1, ctypes.c_void_p(scratch_ptr), ctypes.c_size_t(scratch_bytes),
                                     ctypes.c_void_p(triplets_ptr), _stream_handle(stream)), "mt_compute_global")
+
+
+# ---- multi-GPU with the NCCL exchange inside the library -------------------------
+
+def mt_get_unique_id() -> bytes:
+    buf = (ctypes.c_uint8 * 128)()
+    _check(load().mt_get_unique_id(buf), "mt_get_unique_id")
+    return bytes(buf)
+
+
+def mt_dist_slab_bounds(nz: int, nranks: int) -> list[int]:
+    b = (ctypes.c_uint32 * (int(nranks) + 1))()
+    _check(load().mt_dist_slab_bounds(int(nz), int(nranks), b), "mt_dist_slab_bounds")
+    return [int(x) for x in b]
+
+
+def mt_dist_workspace_bytes(dims, conn: int, rank: int, nranks: int) -> int:
+    return int(load().mt_dist_workspace_bytes(_dims(dims), int(conn), int(rank), int(nranks)))
+
+
+def mt_create_dist(dims, conn: int, rank: int, nranks: int, nccl_id: bytes, device: int, workspace_ptr: int,
+                   workspace_bytes: int):
+    if len(nccl_id) != 128:
+        raise ValueError("an NCCL unique id is 128 bytes")
+    h = ctypes.c_void_p()
+    idbuf = (ctypes.c_uint8 * 128)(*nccl_id)
+    _check(load().mt_create_dist(ctypes.byref(h), _dims(dims), int(conn), int(rank), int(nranks), idbuf,
+                                 int(device), ctypes.c_void_p(workspace_ptr), ctypes.c_size_t(workspace_bytes)),
+           "mt_create_dist")
+    return h
 
 
 # ---- explicit graphs ------------------------------------------------------------

@@ -1,12 +1,15 @@
-"""Multi-GPU z-slab decomposition: one process per GPU, NCCL for the exchange.
+"""Multi-GPU z-slab decomposition: one process per GPU.
 
 Rank r owns planes [z_bounds[r], z_bounds[r+1]) of the global grid (3D, 6-connectivity).
-Per step (include/mt.h, "Multi-GPU"):
-  1. ``mt_compute_local``   -- the slab's merge tree + its boundary forest (device kernels);
-  2. all-gather of the forest records over the process group (``torch.distributed``: NCCL
-     over NVLink on GPUs; gloo in the CPU tests of the exchange logic);
-  3. ``mt_compute_global``  -- every rank merges all inter-slab edges on the gathered forest,
-     writes back its cells, repairs its slab and extracts its part of the diagram.
+Two transports for the one exchange step:
+  * ``transport="nccl"`` (the product path): ``mt_create_dist`` -- the library owns an NCCL
+    communicator and ``mt_compute`` runs local phase -> NCCL exchange -> global phase itself;
+    Python only broadcasts rank 0's 128-byte NCCL unique id.
+  * ``transport="torch"`` (pluggable, for gloo and tests): the three-call ABI
+      1. ``mt_compute_local``   -- the slab's merge tree + its boundary forest (device kernels);
+      2. all-gather of the forest records over the process group (``torch.distributed``);
+      3. ``mt_compute_global``  -- every rank merges all inter-slab edges on the gathered
+         forest, writes back its cells, repairs its slab and extracts its part of the diagram.
 The triplets hold global ids; the finite pairs of rank r are the branches born in its slab
 (ascending), so concatenating the ranks in order gives the single-GPU diagram.
 This module is plumbing (argument marshalling + the collective); all computation runs in
@@ -21,19 +24,13 @@ from . import _lib
 RECORD_BYTES = _lib.FOREST_RECORD_BYTES
 
 
-def slab_bounds(nz: int, nranks: int, align: int = 8) -> list[int]:
-    """z boundaries of ``nranks`` slabs covering ``nz`` planes: as equal as possible, on
-    multiples of the tile depth ``align`` when the grid allows it."""
-    if nranks < 1 or nranks > nz:
-        raise ValueError("need 1 <= nranks <= nz")
-    b = [0]
-    for k in range(1, nranks):
-        z = round(k * nz / nranks / align) * align if nz >= nranks * align else round(k * nz / nranks)
-        z = max(z, b[-1] + 1)
-        z = min(z, nz - (nranks - k))
-        b.append(z)
-    b.append(nz)
-    return b
+def slab_bounds(nz: int, nranks: int) -> list[int]:
+    """z boundaries of ``nranks`` slabs covering ``nz`` planes (the library's rule,
+    ``mt_dist_slab_bounds``: as equal as possible, on multiples of the tile depth 8 when
+    nz >= 8 nranks)."""
+    if nranks < 1 or nranks > nz or nranks > 64:
+        raise ValueError("need 1 <= nranks <= min(nz, 64)")
+    return _lib.mt_dist_slab_bounds(nz, nranks)
 
 
 def allgather_varsize(t: torch.Tensor, group=None) -> torch.Tensor:
@@ -120,10 +117,61 @@ class SlabMergeTree:
         return out, npairs, ness
 
 
-class DistMergeTree:
-    """The global grid split into z-slabs over a torch.distributed group, one slab per rank."""
+class NcclSlab:
+    """A ``mt_create_dist`` context: the rank's slab with the NCCL exchange inside the library."""
 
-    def __init__(self, dims, group=None, device=None):
+    def __init__(self, dims, rank: int, nranks: int, nccl_id: bytes, device=None):
+        self.dims = tuple(int(d) for d in dims)
+        self.z_bounds = slab_bounds(self.dims[2], nranks)
+        self.z_begin, self.z_end = self.z_bounds[rank], self.z_bounds[rank + 1]
+        nx, ny, _ = self.dims
+        self.n = nx * ny * (self.z_end - self.z_begin)
+        dev = torch.device("cuda", torch.cuda.current_device() if device is None else int(device)) \
+            if not isinstance(device, torch.device) else device
+        self.device = dev
+        nbytes = _lib.mt_dist_workspace_bytes(self.dims, 6, rank, nranks)
+        if nbytes == 0:
+            raise _lib.MTError(_lib.MT_ERR_INVALID_ARG, "mt_dist_workspace_bytes")
+        self.workspace = torch.empty(nbytes + 256, dtype=torch.uint8, device=dev)
+        ptr = (self.workspace.data_ptr() + 255) // 256 * 256
+        self.ctx = _lib.mt_create_dist(self.dims, 6, rank, nranks, nccl_id, dev.index, ptr, nbytes)
+        self._f = None
+
+    def __del__(self):
+        ctx = getattr(self, "ctx", None)
+        if ctx is not None and _lib._lib is not None:
+            _lib._lib.mt_destroy(ctx)
+            self.ctx = None
+
+    def compute(self, f_slab: torch.Tensor, split: bool = False, triplets=None, stream=None) -> torch.Tensor:
+        if f_slab.dtype != torch.float32 or not f_slab.is_cuda or not f_slab.is_contiguous() or \
+                f_slab.numel() != self.n:
+            raise ValueError("f_slab must be a contiguous float32 CUDA tensor with the slab's values")
+        if triplets is None:
+            triplets = torch.empty(self.n, dtype=torch.int64, device=self.device)
+        self._f = f_slab
+        _lib.mt_compute(self.ctx, f_slab.data_ptr(), triplets.data_ptr(),
+                        _lib.MT_FLAG_SPLIT_TREE if split else 0, stream)
+        return triplets
+
+    diagram = SlabMergeTree.diagram
+
+
+def broadcast_unique_id(group=None) -> bytes:
+    """Rank 0's NCCL unique id (mt_get_unique_id), broadcast over the torch.distributed group."""
+    import torch.distributed as dist
+
+    obj = [_lib.mt_get_unique_id() if dist.get_rank(group) == 0 else None]
+    dist.broadcast_object_list(obj, src=0, group=group)
+    return obj[0]
+
+
+class DistMergeTree:
+    """The global grid split into z-slabs over a torch.distributed group, one slab per rank.
+    transport "nccl": the library's own NCCL exchange (mt_create_dist); "torch": the three-call
+    ABI with the records all-gathered by torch.distributed (any backend, e.g. gloo)."""
+
+    def __init__(self, dims, group=None, device=None, transport: str = "nccl"):
         import torch.distributed as dist
 
         self.group = group
@@ -132,10 +180,18 @@ class DistMergeTree:
         self.dims = tuple(int(d) for d in dims)
         self.z_bounds = slab_bounds(self.dims[2], self.world)
         zb, ze = self.z_bounds[self.rank], self.z_bounds[self.rank + 1]
-        self.slab = SlabMergeTree(self.dims, zb, ze, device)
+        self.transport = transport
+        if transport == "nccl":
+            self.slab = NcclSlab(self.dims, self.rank, self.world, broadcast_unique_id(group), device)
+        elif transport == "torch":
+            self.slab = SlabMergeTree(self.dims, zb, ze, device)
+        else:
+            raise ValueError(transport)
         self.forest_records = 0
 
     def compute(self, f_slab: torch.Tensor, split: bool = False, triplets=None) -> torch.Tensor:
+        if self.transport == "nccl":
+            return self.slab.compute(f_slab, split, triplets)
         self.slab.compute_local(f_slab, split)
         mine = self.slab.forest()
         everything = allgather_varsize(mine, self.group)

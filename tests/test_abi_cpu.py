@@ -64,3 +64,19 @@ def test_sass_is_sm100a():
     so = build.build()
     out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", so], capture_output=True, text=True).stdout
     assert "sm_100a" in out
+
+
+def test_dist_host_entry_points_without_gpu(lib):
+    """NCCL is loaded at run time (no link-time dependency); the unique id and the slab rule are
+    host-only; creating a distributed context validates its arguments before touching NCCL."""
+    uid = _lib.mt_get_unique_id()
+    assert len(uid) == 128 and any(uid)
+    assert _lib.mt_dist_slab_bounds(1024, 8) == [0, 128, 256, 384, 512, 640, 768, 896, 1024]
+    assert _lib.mt_dist_workspace_bytes((64, 64, 64), 6, 0, 2) > 0
+    assert _lib.mt_dist_workspace_bytes((64, 64, 64), 6, 2, 2) == 0      # rank out of range
+    h = ctypes.c_void_p()
+    dims = (ctypes.c_uint32 * 3)(64, 64, 64)
+    idbuf = (ctypes.c_uint8 * 128)(*uid)
+    assert lib.mt_create_dist(ctypes.byref(h), dims, 6, 3, 2, idbuf, 0, None, 0) == _lib.MT_ERR_INVALID_ARG
+    assert lib.mt_create_dist(ctypes.byref(h), dims, 6, 0, 65, idbuf, 0, None, 0) == _lib.MT_ERR_INVALID_ARG
+    assert lib.mt_create_dist(ctypes.byref(h), dims, 6, 0, 2, None, 0, None, 0) == _lib.MT_ERR_INVALID_ARG

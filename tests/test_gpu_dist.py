@@ -54,3 +54,22 @@ def test_virtual_ranks_closed_forms():
     z, y, x = np.meshgrid(np.arange(16), np.arange(20), np.arange(24), indexing="ij")
     check(((x + y + z) % 2).astype(np.float32).reshape(-1), dims, 4)     # 50% minima
     check(np.full(24 * 20 * 16, 1.5, np.float32), dims, 4)               # id order only
+
+
+@pytest.mark.parametrize("cfg,scale,split", [("c4", 48, False), ("c5", 64, True)])
+def test_nccl_dist_one_rank_through_c_abi(cfg, scale, split):
+    """mt_get_unique_id + mt_create_dist with a 1-rank NCCL communicator (one GPU per box here),
+    then mt_compute / mt_diagram exactly as on one GPU: the library's own exchange path (NCCL
+    all-gather of the forest size, grouped broadcasts of the records, global phase) must give
+    the oracle's store and diagram bit for bit."""
+    from paper_2301_10838_b200.dist import NcclSlab
+    f, dims, _ = fields.make(cfg, scale=scale)
+    s = NcclSlab(dims, 0, 1, _lib.mt_get_unique_id(), device=0)
+    for _ in range(2):   # the second step reuses the grown exchange buffers
+        T = s.compute(torch.from_numpy(f).cuda(), split=split)
+        rec, npairs, ness = s.diagram()
+        To, po, npo, neo = oracle.merge_tree(f, dims, conn=6, split=split)
+        assert np.array_equal(T.cpu().numpy().view(np.uint64), To)
+        assert (npairs, ness) == (npo, neo)
+        assert _lib.pairs_to_numpy(rec).tobytes() == po.tobytes()
+    assert _lib.mt_last_launch_count(s.ctx) >= 6
