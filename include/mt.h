@@ -80,7 +80,8 @@ mt_status mt_create(mt_ctx **out, const uint32_t dims[3], int conn, int cuda_dev
 
 /* Compute the merge tree of f (device, n float32, x fastest; borrowed until
  * the stream reaches the end of this call's work) into `triplets` (device,
- * n uint64, written: the normalized minimal store T[u] = s << 32 | v), and the
+ * n uint64, written: the normalized minimal store T[u] = s << 32 | v; it also
+ * holds the tile store between the tile and repair kernels), and the
  * persistence diagram into the context (see mt_diagram).  Asynchronous on
  * `stream`: kernels only, no host synchronisation, no allocation.
  * flags: 0 or MT_FLAG_SPLIT_TREE.
@@ -166,8 +167,11 @@ size_t mt_slab_workspace_bytes(const uint32_t global_dims[3], int conn, uint32_t
 mt_status mt_create_slab(mt_ctx **out, const uint32_t global_dims[3], int conn, uint32_t z_begin,
                          uint32_t z_end, int cuda_device, void *workspace, size_t workspace_bytes);
 /* f_slab (device): the slab's nx*ny*(z_end-z_begin) values, borrowed until
- * mt_compute_global's work completes.  Asynchronous. */
-mt_status mt_compute_local(mt_ctx *ctx, const float *f_slab, uint32_t flags, mt_stream_t stream);
+ * mt_compute_global's work completes; triplets_slab (device, n_local uint64):
+ * receives the slab's tile store now and the final triplets from
+ * mt_compute_global, which must be given the same buffer.  Asynchronous. */
+mt_status mt_compute_local(mt_ctx *ctx, const float *f_slab, uint64_t *triplets_slab, uint32_t flags,
+                           mt_stream_t stream);
 /* Syncs; device pointer to the slab's forest records (valid until the next
  * mt_compute_local) and their number. */
 mt_status mt_forest_view(mt_ctx *ctx, const mt_forest_record **records, uint64_t *n_records,
@@ -178,7 +182,8 @@ size_t mt_forest_scratch_bytes(uint64_t n_all);
 /* all (device): the records of every slab, n_all of them; z_bounds (host):
  * the P+1 plane boundaries of all slabs (z_bounds[0] = 0, z_bounds[P] = nz);
  * scratch (device, >= mt_forest_scratch_bytes(n_all), 256-B aligned);
- * triplets_slab (device, out): the slab's n_local cells.  Asynchronous. */
+ * triplets_slab (device): the buffer given to mt_compute_local (MT_ERR_INVALID_ARG
+ * otherwise), overwritten with the slab's n_local cells.  Asynchronous. */
 mt_status mt_compute_global(mt_ctx *ctx, const mt_forest_record *all, uint64_t n_all,
                             const uint32_t *z_bounds, uint32_t nslabs, void *scratch,
                             size_t scratch_bytes, uint64_t *triplets_slab, mt_stream_t stream);
@@ -245,7 +250,8 @@ int mt_stats(mt_ctx *ctx, uint64_t *out, int max, mt_stream_t stream);
 const char *mt_status_string(mt_status s);
 void mt_destroy(mt_ctx *ctx);
 
-/* Version of this ABI (bumped on any signature change). */
+/* Version of this ABI (bumped on any signature change; 2: mt_compute_local takes the
+ * triplet buffer). */
 int mt_abi_version(void);
 
 #ifdef __cplusplus

@@ -84,7 +84,7 @@ def load(build_if_missing: bool = False):
         "mt_slab_workspace_bytes": (ctypes.c_size_t, [u32p, ctypes.c_int, ctypes.c_uint32, ctypes.c_uint32]),
         "mt_create_slab": (ctypes.c_int, [ctypes.POINTER(vp), u32p, ctypes.c_int, ctypes.c_uint32, ctypes.c_uint32,
                                           ctypes.c_int, vp, ctypes.c_size_t]),
-        "mt_compute_local": (ctypes.c_int, [vp, vp, ctypes.c_uint32, vp]),
+        "mt_compute_local": (ctypes.c_int, [vp, vp, vp, ctypes.c_uint32, vp]),
         "mt_forest_view": (ctypes.c_int, [vp, ctypes.POINTER(vp), u64p, vp]),
         "mt_forest_scratch_bytes": (ctypes.c_size_t, [ctypes.c_uint64]),
         "mt_compute_global": (ctypes.c_int, [vp, vp, ctypes.c_uint64, u32p, ctypes.c_uint32, vp, ctypes.c_size_t,
@@ -230,9 +230,9 @@ def mt_create_slab(dims, conn: int, z_begin: int, z_end: int, device: int, works
     return h
 
 
-def mt_compute_local(ctx, f_ptr: int, flags: int = 0, stream=None):
-    _check(load().mt_compute_local(ctx, ctypes.c_void_p(f_ptr), int(flags), _stream_handle(stream)),
-           "mt_compute_local")
+def mt_compute_local(ctx, f_ptr: int, triplets_ptr: int, flags: int = 0, stream=None):
+    _check(load().mt_compute_local(ctx, ctypes.c_void_p(f_ptr), ctypes.c_void_p(triplets_ptr), int(flags),
+                                   _stream_handle(stream)), "mt_compute_local")
 
 
 def mt_forest_view(ctx, stream=None):

@@ -124,7 +124,7 @@ void attach_dist(mt_ctx* c, DistState* d);
 mt_status dist_compute(mt_ctx* c, DistState* d, const float* f, uint64_t* T, uint32_t flags, cudaStream_t s) {
     const NcclApi& N = nccl();
     if (!N.ok) return MT_ERR_NCCL;
-    mt_status st = mt_compute_local(c, f, flags, s);
+    mt_status st = mt_compute_local(c, f, T, flags, s);
     if (st != MT_OK) return st;
     mt_forest_record* recs = nullptr;
     unsigned long long* count_dev = nullptr;

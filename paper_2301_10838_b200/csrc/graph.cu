@@ -26,7 +26,7 @@ struct QEntryG {
 
 __global__ void __launch_bounds__(256)
 graph_descent_kernel(const float* __restrict__ f, const uint64_t* __restrict__ row, const uint32_t* __restrict__ col,
-                     uint32_t n, uint32_t flip, Cell* __restrict__ C, uint32_t* __restrict__ basin,
+                     uint32_t n, uint32_t flip, Cell* __restrict__ C,
                      unsigned long long* __restrict__ counters) {
     bool bad = false;
     for (uint64_t u = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; u < n; u += uint64_t(gridDim.x) * blockDim.x) {
@@ -45,7 +45,6 @@ graph_descent_kernel(const float* __restrict__ f, const uint64_t* __restrict__ r
             }
         }
         C[u] = make_cell(ku, ou, best);   // (u, u, lowest lower neighbour) or the root (u, u, u)
-        basin[u] = best;                  // == u exactly for the minima (diagram_kernel's candidates)
     }
     if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(counters + CTR_ERR, ERR_NONFINITE);
 }
@@ -95,9 +94,9 @@ uint32_t grid_of(uint64_t n, int num_sms) {
 }  // namespace
 
 void launch_graph_init(const float* f, const uint64_t* row, const uint32_t* col, uint32_t n, uint32_t flip, Cell* C,
-                       uint32_t* basin, unsigned long long* counters, int num_sms, cudaStream_t stream) {
+                       unsigned long long* counters, int num_sms, cudaStream_t stream) {
     if (!n) return;
-    graph_descent_kernel<<<grid_of(n, num_sms), 256, 0, stream>>>(f, row, col, n, flip, C, basin, counters);
+    graph_descent_kernel<<<grid_of(n, num_sms), 256, 0, stream>>>(f, row, col, n, flip, C, counters);
     graph_compress_kernel<<<grid_of(n, num_sms), 256, 0, stream>>>(C, n);
 }
 

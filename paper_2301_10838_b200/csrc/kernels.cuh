@@ -80,14 +80,16 @@ void tile_shape(uint32_t nz_global, uint32_t* ty, uint32_t* tz);
 // K1 + K2 + in-tile K3/K4: keys, steepest descent, tile-local merge tree (tile_tmt.cu)
 // x-face records of the tiles (2 faces x rows per tile, 8 B each: order key << 32 | R)
 uint64_t xface_entries(const Slab& sl);
-void launch_tile_tmt(const float* f, Cell* C, uint32_t* basin, uint64_t* xface, const Slab& sl, uint32_t flip,
+// writes the tile store T0 (8 B per vertex, s << 32 | v, global ids) into the triplet buffer,
+// 16-B cells for the tile minima only, and the x-face records
+void launch_tile_tmt(const float* f, Cell* C, uint64_t* T0, uint64_t* xface, const Slab& sl, uint32_t flip,
                      unsigned long long* counters, unsigned long long* stats, cudaStream_t stream);
 
 // K3: merge of the tile-crossing grid edges on the global store (merge_cross.cu)
 uint64_t cross_edges(const Slab& sl);
 size_t cross_queue_entry_bytes();
 // returns 0 when the slab has a single tile (no crossing edges, no kernel launched)
-int launch_dedupe_cross(const float* f, const uint32_t* basin, const uint64_t* xface, const Slab& sl, uint32_t flip,
+int launch_dedupe_cross(const float* f, const uint64_t* T0, const uint64_t* xface, const Slab& sl, uint32_t flip,
                         void* queue,
                         uint64_t cap, unsigned long long* qlen, unsigned long long* stats, int num_sms,
                         cudaStream_t stream);
@@ -98,7 +100,7 @@ void launch_merge_queue(Cell* C, const void* queue, uint64_t cap, const unsigned
 
 // explicit graphs in CSR form (graph.cu)
 void launch_graph_init(const float* f, const uint64_t* row, const uint32_t* col, uint32_t n, uint32_t flip, Cell* C,
-                       uint32_t* basin, unsigned long long* counters, int num_sms, cudaStream_t stream);
+                       unsigned long long* counters, int num_sms, cudaStream_t stream);
 void launch_graph_edges(const uint64_t* row, const uint32_t* col, uint32_t n, Cell* C, uint32_t* basin, void* queue,
                         uint64_t cap, unsigned long long* qlen, unsigned long long* counters, int num_sms,
                         cudaStream_t stream);
@@ -115,8 +117,10 @@ struct RepairOut {
 uint64_t repair_segments(const Slab& sl);     // segments of the slab
 uint64_t repair_segments_bound(uint64_t n);   // >= repair_segments of any slab of n vertices
 uint64_t diagram_tiles(uint64_t nseg);        // diagram tiles; one 16-B status record each
+// tiled: T holds tile_tmt's T0 and only tile minima have cells (grids); else every vertex has a
+// cell and T is output only (explicit graphs)
 void launch_repair(const Cell* C, uint64_t* T, const float* f, const Slab& sl, uint32_t flip, const RepairOut& o,
-                   unsigned long long* stats, const ForestRef* forest, cudaStream_t stream);
+                   bool tiled, unsigned long long* stats, const ForestRef* forest, cudaStream_t stream);
 void launch_diagram(const Slab& sl, const RepairOut& o, void* status, mt_pair* out, uint64_t out_cap, mt_pair* ess,
                     uint64_t ess_cap, cudaStream_t stream);
 void launch_finish_diagram(unsigned long long* counters, mt_pair* out, uint64_t out_cap, mt_pair* ess,
@@ -133,9 +137,11 @@ struct SlabBounds {
     uint32_t z[MAX_SLABS + 1];
     uint32_t count;             // number of slabs
 };
-void launch_forest_mark(const Cell* C, const Slab& sl, uint8_t* flag, cudaStream_t stream);
-void launch_forest_compact(const Cell* C, const float* f, const Slab& sl, const uint8_t* flag, mt_forest_record* recs,
-                           uint64_t cap, unsigned long long* count, int num_sms, cudaStream_t stream);
+// T0: the slab's tile store (regular vertices have no working cell, see launch_tile_tmt)
+void launch_forest_mark(const Cell* C, const uint64_t* T0, const Slab& sl, uint8_t* flag, cudaStream_t stream);
+void launch_forest_compact(const Cell* C, const uint64_t* T0, const float* f, const Slab& sl, uint32_t flip,
+                           const uint8_t* flag, mt_forest_record* recs, uint64_t cap, unsigned long long* count,
+                           int num_sms, cudaStream_t stream);
 // open-addressing table slots for n_all gathered records (>= 4 n_all, a power of two), or 0
 // when that exceeds 2^31 (32-bit table indices)
 uint64_t forest_table_size(uint64_t n_all);
@@ -143,7 +149,7 @@ void launch_forest_build(const mt_forest_record* all, uint64_t n_all, uint64_t* 
                          uint32_t mask, Cell* cells, int num_sms, cudaStream_t stream);
 void launch_forest_merge(const ForestRef& F, const Slab& sl, const SlabBounds& b, unsigned long long* fetch,
                          int num_sms, cudaStream_t stream);
-void launch_forest_writeback(const ForestRef& F, uint64_t n_all, Cell* C, const Slab& sl, int num_sms,
-                             cudaStream_t stream);
+void launch_forest_writeback(const ForestRef& F, uint64_t n_all, Cell* C, const uint64_t* T0, const Slab& sl,
+                             int num_sms, cudaStream_t stream);
 
 }  // namespace mt

@@ -114,7 +114,7 @@ struct QEntry {
 };
 
 __global__ void __launch_bounds__(DC_THREADS)
-dedupe_cross_kernel(const float* __restrict__ f, const uint32_t* __restrict__ basin,
+dedupe_cross_kernel(const float* __restrict__ f, const uint64_t* __restrict__ T0,
                     const uint64_t* __restrict__ xface, CrossGeom g, uint32_t flip,
                     QEntry* __restrict__ q, uint64_t cap, unsigned long long* __restrict__ qlen,
                     unsigned long long* __restrict__ stats) {
@@ -184,8 +184,12 @@ dedupe_cross_kernel(const float* __restrict__ f, const uint32_t* __restrict__ ba
             } else {
                 ka = key_of(ord32(__ldg(f + a)) ^ flip, a);
                 kb = key_of(ord32(__ldg(f + b)) ^ flip, b);
-                ba = __ldg(basin + a);
-                bb = __ldg(basin + b);
+                // tile representative at the vertex's own level (DESIGN.md derivation C'''): the
+                // tile store's v for a regular vertex (s = u), the vertex itself for a minimum
+                const uint64_t ta = __ldg(reinterpret_cast<const unsigned long long*>(T0 + a));
+                const uint64_t tb = __ldg(reinterpret_cast<const unsigned long long*>(T0 + b));
+                ba = cell_s(ta) == a ? cell_v(ta) : a;
+                bb = cell_s(tb) == b ? cell_v(tb) : b;
             }
             en = ka > kb ? QEntry{ka, ba, bb} : QEntry{kb, bb, ba};
             pair = ba < bb ? (uint64_t(ba) << 32 | bb) : (uint64_t(bb) << 32 | ba);
@@ -403,7 +407,7 @@ merge_queue_kernel(Cell* C, const QEntry* __restrict__ q, uint64_t cap, const un
 
 }  // namespace
 
-int launch_dedupe_cross(const float* f, const uint32_t* basin, const uint64_t* xface, const Slab& sl, uint32_t flip,
+int launch_dedupe_cross(const float* f, const uint64_t* T0, const uint64_t* xface, const Slab& sl, uint32_t flip,
                         void* queue,
                         uint64_t cap, unsigned long long* qlen, unsigned long long* stats, int num_sms,
                         cudaStream_t stream) {
@@ -429,7 +433,7 @@ int launch_dedupe_cross(const float* f, const uint32_t* basin, const uint64_t* x
     QEntry* q = static_cast<QEntry*>(queue);
     uint64_t blocks = (total + DC_THREADS - 1) / DC_THREADS;
     if (blocks > uint64_t(num_sms) * 32) blocks = uint64_t(num_sms) * 32;
-    dedupe_cross_kernel<<<uint32_t(blocks), DC_THREADS, 0, stream>>>(f, basin, xface, g, flip, q, cap, qlen, stats);
+    dedupe_cross_kernel<<<uint32_t(blocks), DC_THREADS, 0, stream>>>(f, T0, xface, g, flip, q, cap, qlen, stats);
     return 1;
 }
 

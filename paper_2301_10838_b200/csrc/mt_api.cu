@@ -65,7 +65,7 @@ constexpr int MAX_EVENTS = 16;
 size_t align_up(size_t x) { return (x + ALIGN - 1) / ALIGN * ALIGN; }
 
 struct Layout {
-    size_t counters, status, status_bytes, stats, ess, cells, basin, xface, queue, pairs, stage, seg_cnt, seg_pos, flags, recs,
+    size_t counters, status, status_bytes, stats, ess, cells, xface, queue, pairs, stage, seg_cnt, seg_pos, flags, recs,
         total;
     uint64_t pairs_cap, recs_cap, queue_cap, ess_cap, seg_cap;
 };
@@ -98,10 +98,8 @@ Layout layout_for(uint64_t n, uint64_t ncross, bool slab = false, uint64_t ess_c
     L.ess = off;
     L.ess_cap = ess_cap;
     off += align_up(ess_cap * sizeof(mt_pair));
-    L.cells = off;  // 16-byte working cells of the merge phase
+    L.cells = off;  // 16-byte working cells of the merge phase (grids: written for tile minima only)
     off += align_up(n * sizeof(mt::Cell));
-    L.basin = off;  // descent basin of every vertex (tile_tmt -> dedupe_cross)
-    off += align_up(n * sizeof(uint32_t));
     L.xface = off;  // x-face records of the tiles (tile_tmt -> dedupe_cross)
     off += align_up(nxface * sizeof(uint64_t));
     L.queue = off;  // deduplicated tile-crossing edges
@@ -142,6 +140,7 @@ struct mt_ctx {
     bool multi = false;      // created by mt_create_slab
     bool graph = false;      // created by mt_create_graph (CSR adjacency instead of a grid)
     bool local_done = false; // mt_compute_local ran, mt_compute_global pending
+    uint64_t* local_T = nullptr;  // the triplet buffer mt_compute_local wrote the tile store into
     const float* f = nullptr;
     uint32_t flip = 0;
     uint64_t n_adj = 0;      // graph contexts: adjacency entries (the queue capacity)
@@ -280,8 +279,9 @@ mt_status create_ctx(mt_ctx** out, const uint32_t dims[3], int conn, uint32_t z_
     return MT_OK;
 }
 
-// shared by mt_compute and mt_compute_local: reset, then the slab's own merge tree
-mt_status start_compute(mt_ctx* c, const float* f, uint32_t flags, cudaStream_t s) {
+// shared by mt_compute and mt_compute_local: reset, then the slab's own merge tree; T (the
+// caller's triplet buffer, indexed from the slab's first vertex) receives the tile store T0
+mt_status start_compute(mt_ctx* c, const float* f, uint64_t* T, uint32_t flags, cudaStream_t s) {
     c->launches = 0;
     c->nev = 0;
     c->sticky = MT_OK;
@@ -298,12 +298,12 @@ mt_status start_compute(mt_ctx* c, const float* f, uint32_t flags, cudaStream_t 
     if (cudaMemsetAsync(c->ws + c->L.counters, 0, c->L.status - c->L.counters + c->L.status_bytes,
                         s) != cudaSuccess)
         return c->sticky = MT_ERR_CUDA;
-    uint32_t* basin = reinterpret_cast<uint32_t*>(c->ws + c->L.basin) - c->slab.base;
+    uint64_t* T0 = T - c->slab.base;
     mark(c, "tile_tmt", s);
     uint64_t* xface = reinterpret_cast<uint64_t*>(c->ws + c->L.xface);
-    mt::launch_tile_tmt(fs, cells, basin, xface, c->slab, c->flip, ctr, stats, s);
+    mt::launch_tile_tmt(fs, cells, T0, xface, c->slab, c->flip, ctr, stats, s);
     mark(c, "dedupe_cross", s);
-    int nl = mt::launch_dedupe_cross(fs, basin, xface, c->slab, c->flip, c->ws + c->L.queue, c->L.queue_cap,
+    int nl = mt::launch_dedupe_cross(fs, T0, xface, c->slab, c->flip, c->ws + c->L.queue, c->L.queue_cap,
                                      ctr + mt::CTR_QLEN, stats, c->num_sms, s);
     if (nl) {
         mark(c, "merge_queue", s);
@@ -326,7 +326,7 @@ mt_status finish_compute(mt_ctx* c, uint64_t* T, const mt::ForestRef* forest, cu
                            reinterpret_cast<uint16_t*>(c->ws + c->L.seg_cnt),
                            reinterpret_cast<uint32_t*>(c->ws + c->L.seg_pos), ctr};
     mark(c, "repair", s);
-    mt::launch_repair(cells_of(c), T - base, c->f - base, c->slab, c->flip, ro, stats_of(c), forest, s);
+    mt::launch_repair(cells_of(c), T - base, c->f - base, c->slab, c->flip, ro, !c->graph, stats_of(c), forest, s);
     mark(c, "diagram", s);
     mt::launch_diagram(c->slab, ro, c->ws + c->L.status, out, cap, ess, c->L.ess_cap, s);
     mark(c, "finish_diagram", s);
@@ -341,7 +341,7 @@ mt_status finish_compute(mt_ctx* c, uint64_t* T, const mt::ForestRef* forest, cu
 
 extern "C" {
 
-int mt_abi_version(void) { return 1; }
+int mt_abi_version(void) { return 2; }
 
 const char* mt_status_string(mt_status s) {
     switch (s) {
@@ -433,8 +433,7 @@ mt_status mt_compute_graph(mt_ctx* c, const float* f, const uint64_t* row, const
                         s) != cudaSuccess)
         return c->sticky = MT_ERR_CUDA;
     mark(c, "graph_init", s);
-    mt::launch_graph_init(f, row, col, uint32_t(c->n), c->flip, cells, reinterpret_cast<uint32_t*>(c->ws + c->L.basin),
-                          ctr, c->num_sms, s);
+    mt::launch_graph_init(f, row, col, uint32_t(c->n), c->flip, cells, ctr, c->num_sms, s);
     mark(c, "graph_edges", s);
     mt::launch_graph_edges(row, col, uint32_t(c->n), cells, nullptr, c->ws + c->L.queue, c->L.queue_cap,
                            ctr + mt::CTR_QLEN, ctr, c->num_sms, s);
@@ -467,13 +466,13 @@ mt_status mt_compute(mt_ctx* c, const float* f, uint64_t* T, uint32_t flags, mt_
     DeviceGuard g(c->device);
     if (!g.ok) return MT_ERR_CUDA;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    const mt_status st = start_compute(c, f, flags, s);
+    const mt_status st = start_compute(c, f, T, flags, s);
     if (st != MT_OK) return st;
     return finish_compute(c, T, nullptr, s);
 }
 
-mt_status mt_compute_local(mt_ctx* c, const float* f, uint32_t flags, mt_stream_t stream) {
-    if (!c || !f) return MT_ERR_INVALID_ARG;
+mt_status mt_compute_local(mt_ctx* c, const float* f, uint64_t* T, uint32_t flags, mt_stream_t stream) {
+    if (!c || !f || !T) return MT_ERR_INVALID_ARG;
     if (flags & ~uint32_t(MT_FLAG_SPLIT_TREE)) return MT_ERR_INVALID_ARG;
     if (!c->multi) return MT_ERR_STATE;
     DeviceGuard g(c->device);
@@ -481,12 +480,13 @@ mt_status mt_compute_local(mt_ctx* c, const float* f, uint32_t flags, mt_stream_
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     uint8_t* flag = reinterpret_cast<uint8_t*>(c->ws + c->L.flags);
     if (cudaMemsetAsync(flag, 0, c->n, s) != cudaSuccess) return c->sticky = MT_ERR_CUDA;
-    mt_status st = start_compute(c, f, flags, s);
+    mt_status st = start_compute(c, f, T, flags, s);
     if (st != MT_OK) return st;
+    c->local_T = T;
     mark(c, "forest_mark", s);
-    mt::launch_forest_mark(cells_of(c), c->slab, flag, s);
+    mt::launch_forest_mark(cells_of(c), T - c->slab.base, c->slab, flag, s);
     mark(c, "forest_compact", s);
-    mt::launch_forest_compact(cells_of(c), f - c->slab.base, c->slab, flag,
+    mt::launch_forest_compact(cells_of(c), T - c->slab.base, f - c->slab.base, c->slab, c->flip, flag,
                               reinterpret_cast<mt_forest_record*>(c->ws + c->L.recs), c->L.recs_cap,
                               counters_of(c) + mt::CTR_FCOUNT, c->num_sms, s);
     mark(c, "exchange", s);  // closes at mt_compute_global's first mark: host sync + all-gather
@@ -519,6 +519,7 @@ mt_status mt_compute_global(mt_ctx* c, const mt_forest_record* all, uint64_t n_a
                             uint32_t nslabs, void* scratch, size_t scratch_bytes, uint64_t* T, mt_stream_t stream) {
     if (!c || !z_bounds || !T || (n_all && !all)) return MT_ERR_INVALID_ARG;
     if (!c->multi || !c->local_done) return MT_ERR_STATE;
+    if (T != c->local_T) return MT_ERR_INVALID_ARG;   // the buffer holding mt_compute_local's tile store
     if (nslabs < 1 || nslabs > uint32_t(mt::MAX_SLABS) || z_bounds[0] != 0 || z_bounds[nslabs] != c->nz)
         return MT_ERR_INVALID_ARG;
     bool found = false;
@@ -548,7 +549,7 @@ mt_status mt_compute_global(mt_ctx* c, const mt_forest_record* all, uint64_t n_a
     mark(c, "forest_merge", s);
     mt::launch_forest_merge(F, c->slab, b, counters_of(c) + mt::CTR_FFETCH, c->num_sms, s);
     mark(c, "forest_writeback", s);
-    mt::launch_forest_writeback(F, n_all, cells_of(c), c->slab, c->num_sms, s);
+    mt::launch_forest_writeback(F, n_all, cells_of(c), T - c->slab.base, c->slab, c->num_sms, s);
     c->launches += 3;
     c->local_done = false;
     return finish_compute(c, T, &F, s);

@@ -36,9 +36,6 @@ namespace {
 #ifndef MT_REPAIR_NC
 #define MT_REPAIR_NC 1      // the repair reads cells no thread writes: L1-cached non-coherent loads
 #endif
-#ifndef MT_REPAIR_ILP
-#define MT_REPAIR_ILP 1     // the 8 walks of a thread in lock-step rounds (else one after the other)
-#endif
 #ifndef MT_REPAIR_MINB
 #define MT_REPAIR_MINB 3    // __launch_bounds__ min blocks per SM (register budget knob)
 #endif
@@ -97,12 +94,16 @@ struct BrickGeom {
     uint32_t by, bx_n, by_n;   // brick rows along y; bricks along x and y (brick mode)
 };
 
-template <class View, int BY>
+template <class View, int BY, bool TILED>
 __global__ void __launch_bounds__(RB_THREADS, MT_REPAIR_MINB)
 repair_brick_kernel(View view, const Cell* C, uint64_t* __restrict__ T, const float* __restrict__ f, Slab sl,
                     BrickGeom g, uint32_t flip, mt_pair* __restrict__ stage, uint64_t stage_cap,
                     uint16_t* __restrict__ seg_cnt, uint32_t* __restrict__ seg_pos,
                     unsigned long long* __restrict__ counters, unsigned long long* __restrict__ stats) {
+    // TILED (grids): T holds the tile store T0 written by tile_tmt and only tile minima have
+    // working cells; a regular vertex's walk starts at its tile representative T0.v with
+    // threshold key(u) (its s = u is final).  Otherwise (explicit graphs) every vertex has a
+    // working cell and T is output only.
     extern __shared__ __align__(16) unsigned char smem_raw[];
     RepairSmem& S = *reinterpret_cast<RepairSmem*>(smem_raw);
     constexpr bool LINEAR = BY == 0;       // id-range bricks (graphs, thin grids)
@@ -150,12 +151,33 @@ repair_brick_kernel(View view, const Cell* C, uint64_t* __restrict__ T, const fl
     for (int k = 0; k < RB_PER; ++k) inb |= uint32_t(uint32_t(lane) < S.rowlim[warp + 16 * k]) << k;
 #define UID(k) (S.rowbase[warp + 16 * (k)] + lane)
 #define INB(k) ((inb >> (k)) & 1u)
-    Cell cell[RB_PER];
+    uint64_t key[RB_PER];     // threshold key(s)
+    uint32_t sv[RB_PER];      // s of the vertex
+    uint32_t xs[RB_PER];      // walk start (then position)
 #pragma unroll
-    for (int k = 0; k < RB_PER; ++k) cell[k] = INB(k) ? ld_cell_ro(C + UID(k)) : Cell{0, 0};
+    for (int k = 0; k < RB_PER; ++k) {
+        key[k] = 0;
+        sv[k] = 0;
+        xs[k] = 0;
+        if (!INB(k)) continue;
+        const uint32_t u = uint32_t(UID(k));
+        if (TILED) {
+            const uint64_t t0 = T[UID(k)];
+            if (cell_s(t0) == u && cell_v(t0) != u) {        // regular in its tile: s = u is final
+                key[k] = key_of(ord32(__ldg(f + UID(k))) ^ flip, u);
+                sv[k] = u;
+                xs[k] = cell_v(t0);
+                continue;
+            }
+        }
+        const Cell c = ld_cell_ro(C + UID(k));               // a minimum's working cell
+        key[k] = c.lo;
+        sv[k] = cs_of(c);
+        xs[k] = cv_of(c);
+    }
     // diagram records of each row: finite pairs (s != u) and roots (v == u)
-#define FMASK(k) __ballot_sync(FULL_MASK, INB(k) && cs_of(cell[k]) != uint32_t(UID(k)))
-#define EMASK(k) __ballot_sync(FULL_MASK, INB(k) && cv_of(cell[k]) == uint32_t(UID(k)))
+#define FMASK(k) __ballot_sync(FULL_MASK, INB(k) && sv[k] != uint32_t(UID(k)))
+#define EMASK(k) __ballot_sync(FULL_MASK, INB(k) && xs[k] == uint32_t(UID(k)))
     uint32_t recbits = 0;     // rows k where this lane holds a finite pair (bit k) / a root (bit 8 + k)
 #pragma unroll
     for (int k = 0; k < RB_PER; ++k) {
@@ -196,13 +218,6 @@ repair_brick_kernel(View view, const Cell* C, uint64_t* __restrict__ T, const fl
         if (lane == 0) S.base = base;
     }
 
-    uint64_t key[RB_PER];     // threshold key(s)
-    uint32_t sv[RB_PER];      // s of the vertex
-#pragma unroll
-    for (int k = 0; k < RB_PER; ++k) {
-        key[k] = cell[k].lo;
-        sv[k] = cs_of(cell[k]);
-    }
     __syncthreads();   // staging base and row offsets in
 
     // staging records of every row, in id order within the row: finite pairs, then roots.
@@ -251,15 +266,11 @@ repair_brick_kernel(View view, const Cell* C, uint64_t* __restrict__ T, const fl
 
     // Rep(u, key(s)): walk from v through cells with key(s') <= key(s) that are not roots
     unsigned long long hops = 0;
-#if MT_REPAIR_ILP
     // the thread's 8 walks advance in lock-step rounds: 8 independent load chains in flight
-    uint32_t xs[RB_PER];
     uint32_t act = 0;
 #pragma unroll
-    for (int k = 0; k < RB_PER; ++k) {
-        xs[k] = cv_of(cell[k]);
+    for (int k = 0; k < RB_PER; ++k)
         if (INB(k) && xs[k] != uint32_t(UID(k))) act |= 1u << k;
-    }
 #pragma unroll 1
     while (act) {
 #pragma unroll
@@ -277,24 +288,6 @@ repair_brick_kernel(View view, const Cell* C, uint64_t* __restrict__ T, const fl
 #pragma unroll
     for (int k = 0; k < RB_PER; ++k)
         if (INB(k)) T[UID(k)] = pack(sv[k], xs[k]);
-#else
-#pragma unroll
-    for (int k = 0; k < RB_PER; ++k) {
-        if (!INB(k)) continue;
-        const uint64_t u = UID(k);
-        uint32_t x = cv_of(cell[k]);
-        if (x != uint32_t(u)) {
-            const uint64_t a = key[k];
-            while (true) {                        // Alg. 4, reading R20
-                const Cell c = view.cell(C, x);
-                if (cv_of(c) == x || c.lo > a) break;
-                x = cv_of(c);
-                ++hops;
-            }
-        }
-        T[u] = pack(sv[k], x);
-    }
-#endif
     if (stats && hops) atomicAdd(stats + ST_REPAIR_HOPS, hops);
 #undef UID
 #undef INB
@@ -440,10 +433,18 @@ __global__ void finish_diagram_kernel(unsigned long long* __restrict__ counters,
 
 template <class View, int BY>
 void launch_brick(const View& view, const Cell* C, uint64_t* T, const float* f, const Slab& sl, BrickGeom g,
-                  uint64_t nb, uint32_t flip, const RepairOut& o, unsigned long long* stats, cudaStream_t stream) {
-    ensure_smem_attr(reinterpret_cast<const void*>(repair_brick_kernel<View, BY>), int(sizeof(RepairSmem)));
-    repair_brick_kernel<View, BY><<<uint32_t(nb), RB_THREADS, sizeof(RepairSmem), stream>>>(
-        view, C, T, f, sl, g, flip, o.stage, o.stage_cap, o.seg_cnt, o.seg_pos, o.counters, stats);
+                  uint64_t nb, uint32_t flip, const RepairOut& o, bool tiled, unsigned long long* stats,
+                  cudaStream_t stream) {
+    if (tiled) {
+        ensure_smem_attr(reinterpret_cast<const void*>(repair_brick_kernel<View, BY, true>), int(sizeof(RepairSmem)));
+        repair_brick_kernel<View, BY, true><<<uint32_t(nb), RB_THREADS, sizeof(RepairSmem), stream>>>(
+            view, C, T, f, sl, g, flip, o.stage, o.stage_cap, o.seg_cnt, o.seg_pos, o.counters, stats);
+    } else {
+        ensure_smem_attr(reinterpret_cast<const void*>(repair_brick_kernel<View, BY, false>),
+                         int(sizeof(RepairSmem)));
+        repair_brick_kernel<View, BY, false><<<uint32_t(nb), RB_THREADS, sizeof(RepairSmem), stream>>>(
+            view, C, T, f, sl, g, flip, o.stage, o.stage_cap, o.seg_cnt, o.seg_pos, o.counters, stats);
+    }
 }
 
 // brick geometry: 3-D bricks 32 x 16 x 8 on volumes, 32 x 128 on images, id ranges otherwise
@@ -468,12 +469,12 @@ bool brick_mode(const Slab& sl, BrickGeom* g, uint64_t* nb, uint64_t* nseg) {
 
 template <class View>
 void launch_repair_view(const View& view, const Cell* C, uint64_t* T, const float* f, const Slab& sl, uint32_t flip,
-                        const RepairOut& o, unsigned long long* stats, cudaStream_t stream) {
+                        const RepairOut& o, bool tiled, unsigned long long* stats, cudaStream_t stream) {
     BrickGeom g;
     uint64_t nb, nseg;
-    if (!brick_mode(sl, &g, &nb, &nseg)) launch_brick<View, 0>(view, C, T, f, sl, g, nb, flip, o, stats, stream);
-    else if (g.by == 16) launch_brick<View, 16>(view, C, T, f, sl, g, nb, flip, o, stats, stream);
-    else launch_brick<View, 128>(view, C, T, f, sl, g, nb, flip, o, stats, stream);
+    if (!brick_mode(sl, &g, &nb, &nseg)) launch_brick<View, 0>(view, C, T, f, sl, g, nb, flip, o, tiled, stats, stream);
+    else if (g.by == 16) launch_brick<View, 16>(view, C, T, f, sl, g, nb, flip, o, tiled, stats, stream);
+    else launch_brick<View, 128>(view, C, T, f, sl, g, nb, flip, o, tiled, stats, stream);
 }
 
 }  // namespace
@@ -488,10 +489,10 @@ uint64_t repair_segments_bound(uint64_t n) { return n / 16 + 2; }
 uint64_t diagram_tiles(uint64_t nseg) { return (nseg + THREADS * DG_SPT - 1) / (THREADS * DG_SPT); }
 
 void launch_repair(const Cell* C, uint64_t* T, const float* f, const Slab& sl, uint32_t flip, const RepairOut& o,
-                   unsigned long long* stats, const ForestRef* forest, cudaStream_t stream) {
+                   bool tiled, unsigned long long* stats, const ForestRef* forest, cudaStream_t stream) {
     if (sl.n == 0) return;
-    if (forest) launch_repair_view(ForestView{*forest, sl.base, sl.n}, C, T, f, sl, flip, o, stats, stream);
-    else launch_repair_view(LocalView{}, C, T, f, sl, flip, o, stats, stream);
+    if (forest) launch_repair_view(ForestView{*forest, sl.base, sl.n}, C, T, f, sl, flip, o, tiled, stats, stream);
+    else launch_repair_view(LocalView{}, C, T, f, sl, flip, o, tiled, stats, stream);
 }
 
 void launch_diagram(const Slab& sl, const RepairOut& o, void* status, mt_pair* out, uint64_t out_cap, mt_pair* ess,

@@ -26,9 +26,16 @@ namespace mt {
 
 namespace {
 
+// a vertex that is regular in its tile has no working cell: its tile triplet (u, u, R) is in T0
+__device__ __forceinline__ bool tile_regular(const uint64_t* T0, uint32_t x, uint32_t* rep) {
+    const uint64_t t = T0[x];
+    *rep = cell_v(t);
+    return cell_s(t) == x && cell_v(t) != x;
+}
+
 __global__ void __launch_bounds__(256)
-forest_mark_kernel(const Cell* C, uint32_t nx, uint32_t ny, uint64_t bottom, uint64_t top, bool has_bottom,
-                   bool has_top, uint64_t base, uint8_t* flag) {
+forest_mark_kernel(const Cell* C, const uint64_t* T0, uint32_t nx, uint32_t ny, uint64_t bottom, uint64_t top,
+                   bool has_bottom, bool has_top, uint64_t base, uint8_t* flag) {
     const uint64_t sxy = uint64_t(nx) * ny;
     const uint64_t nface = uint64_t(has_bottom) + uint64_t(has_top);
     for (uint64_t t = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; t < nface * sxy;
@@ -36,9 +43,21 @@ forest_mark_kernel(const Cell* C, uint32_t nx, uint32_t ny, uint64_t bottom, uin
         const bool first = t < sxy;
         const uint64_t plane = (first && has_bottom) ? bottom : top;
         uint32_t x = uint32_t(plane + (t % sxy));
-        // walk the chain, flagging each cell; stop at a flagged cell (its chain is taken)
+        // the face vertex itself, then (from its tile representative on) the chain of minima cells,
+        // flagging each; stop at a flagged cell (its chain is taken)
+        uint8_t* fl = flag + (uint64_t(x) - base);
+        if (*reinterpret_cast<volatile uint8_t*>(fl)) continue;
+        *reinterpret_cast<volatile uint8_t*>(fl) = 1;
+        uint32_t rep;
+        if (tile_regular(T0, x, &rep)) {
+            x = rep;
+        } else {
+            const Cell c = ld_cell(C + x);
+            if (cv_of(c) == x) continue;
+            x = cv_of(c);
+        }
         while (true) {
-            uint8_t* fl = flag + (uint64_t(x) - base);
+            fl = flag + (uint64_t(x) - base);
             if (*reinterpret_cast<volatile uint8_t*>(fl)) break;
             *reinterpret_cast<volatile uint8_t*>(fl) = 1;
             const Cell c = ld_cell(C + x);
@@ -49,8 +68,9 @@ forest_mark_kernel(const Cell* C, uint32_t nx, uint32_t ny, uint64_t bottom, uin
 }
 
 __global__ void __launch_bounds__(256)
-forest_compact_kernel(const Cell* C, const float* f, uint64_t base, uint64_t n, const uint8_t* __restrict__ flag,
-                      mt_forest_record* __restrict__ recs, uint64_t cap, unsigned long long* count) {
+forest_compact_kernel(const Cell* C, const uint64_t* T0, const float* f, uint32_t flip, uint64_t base, uint64_t n,
+                      const uint8_t* __restrict__ flag, mt_forest_record* __restrict__ recs, uint64_t cap,
+                      unsigned long long* count) {
     const int lane = threadIdx.x & 31;
     const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
     for (uint64_t l0 = uint64_t(blockIdx.x) * blockDim.x; l0 < n; l0 += stride) {
@@ -62,11 +82,19 @@ forest_compact_kernel(const Cell* C, const float* f, uint64_t base, uint64_t n, 
         b = __shfl_sync(FULL_MASK, b, 0);
         if (take) {
             const uint64_t pos = b + __popc(m & ((1u << lane) - 1u));
-            const uint64_t u = base + l;
-            const Cell c = ld_cell(C + u);
-            if (pos < cap)
-                recs[pos] = mt_forest_record{uint32_t(u), __float_as_uint(f[u]), c.lo, c.hi,
-                                             __float_as_uint(f[cs_of(c)]), 0u};
+            const uint32_t u = uint32_t(base + l);
+            uint32_t rep;
+            const uint32_t fb = __float_as_uint(f[u]);
+            mt_forest_record rec;
+            if (tile_regular(T0, u, &rep)) {
+                // the cell the vertex would have: (u, u, R) at its own key
+                const uint32_t o = ord32(f[u]) ^ flip;
+                rec = mt_forest_record{u, fb, key_of(o, u), (uint64_t(o) << 32) | rep, fb, 0u};
+            } else {
+                const Cell c = ld_cell(C + u);
+                rec = mt_forest_record{u, fb, c.lo, c.hi, __float_as_uint(f[cs_of(c)]), 0u};
+            }
+            if (pos < cap) recs[pos] = rec;
         }
     }
 }
@@ -247,11 +275,13 @@ forest_merge_kernel(ForestRef F, BoundaryGeom g, unsigned long long* __restrict_
 }
 
 __global__ void __launch_bounds__(256)
-forest_writeback_kernel(ForestRef F, uint64_t n_all, Cell* C, uint64_t base, uint64_t n) {
+forest_writeback_kernel(ForestRef F, uint64_t n_all, Cell* C, const uint64_t* T0, uint64_t base, uint64_t n) {
     for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n_all;
          i += uint64_t(gridDim.x) * blockDim.x) {
         const uint32_t id = F.recs[i].id;
-        if (uint64_t(id) - base < n) {
+        uint32_t rep;
+        // (a tile-regular face vertex keeps its T0: the repair walks from its R through the forest)
+        if (uint64_t(id) - base < n && !tile_regular(T0, id, &rep)) {
             const Cell c = F.cells[i];
             st_cell(C + id, c);
         }
@@ -267,20 +297,22 @@ uint32_t grid_for(uint64_t work, int num_sms) {
 
 }  // namespace
 
-void launch_forest_mark(const Cell* C, const Slab& sl, uint8_t* flag, cudaStream_t stream) {
+void launch_forest_mark(const Cell* C, const uint64_t* T0, const Slab& sl, uint8_t* flag, cudaStream_t stream) {
     const bool has_bottom = sl.z_begin > 0, has_top = sl.z_end < sl.nz;
     if (!has_bottom && !has_top) return;
     const uint64_t sxy = uint64_t(sl.nx) * sl.ny;
     const uint64_t work = sxy * (uint64_t(has_bottom) + uint64_t(has_top));
-    forest_mark_kernel<<<grid_for(work, 148), 256, 0, stream>>>(C, sl.nx, sl.ny, uint64_t(sl.z_begin) * sxy,
+    forest_mark_kernel<<<grid_for(work, 148), 256, 0, stream>>>(C, T0, sl.nx, sl.ny, uint64_t(sl.z_begin) * sxy,
                                                                 uint64_t(sl.z_end - 1) * sxy, has_bottom, has_top,
                                                                 sl.base, flag);
 }
 
-void launch_forest_compact(const Cell* C, const float* f, const Slab& sl, const uint8_t* flag, mt_forest_record* recs,
-                           uint64_t cap, unsigned long long* count, int num_sms, cudaStream_t stream) {
+void launch_forest_compact(const Cell* C, const uint64_t* T0, const float* f, const Slab& sl, uint32_t flip,
+                           const uint8_t* flag, mt_forest_record* recs, uint64_t cap, unsigned long long* count,
+                           int num_sms, cudaStream_t stream) {
     if (sl.n == 0) return;
-    forest_compact_kernel<<<grid_for(sl.n, num_sms), 256, 0, stream>>>(C, f, sl.base, sl.n, flag, recs, cap, count);
+    forest_compact_kernel<<<grid_for(sl.n, num_sms), 256, 0, stream>>>(C, T0, f, flip, sl.base, sl.n, flag, recs, cap,
+                                                                       count);
 }
 
 uint64_t forest_table_size(uint64_t n_all) {
@@ -308,10 +340,10 @@ void launch_forest_merge(const ForestRef& F, const Slab& sl, const SlabBounds& b
     forest_merge_kernel<<<uint32_t(num_sms) * 4, 256, 0, stream>>>(F, g, fetch);
 }
 
-void launch_forest_writeback(const ForestRef& F, uint64_t n_all, Cell* C, const Slab& sl, int num_sms,
-                             cudaStream_t stream) {
+void launch_forest_writeback(const ForestRef& F, uint64_t n_all, Cell* C, const uint64_t* T0, const Slab& sl,
+                             int num_sms, cudaStream_t stream) {
     if (n_all == 0) return;
-    forest_writeback_kernel<<<grid_for(n_all, num_sms), 256, 0, stream>>>(F, n_all, C, sl.base, sl.n);
+    forest_writeback_kernel<<<grid_for(n_all, num_sms), 256, 0, stream>>>(F, n_all, C, T0, sl.base, sl.n);
 }
 
 }  // namespace mt

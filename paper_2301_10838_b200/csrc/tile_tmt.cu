@@ -65,9 +65,6 @@ namespace {
 #ifndef TILE_PJ
 #define TILE_PJ 1      // compress by synchronous pointer jumping (else walks + path compression)
 #endif
-#ifndef TILE_REP
-#define TILE_REP 1     // crossing edges grouped by tile representative at own level (else descent basin)
-#endif
 #ifndef TILE_OWNRUN
 #define TILE_OWNRUN 1  // each warp merges the pairs of its own compacted run (no CTA counter)
 #endif
@@ -118,7 +115,7 @@ __device__ __forceinline__ uint64_t scas64(uint64_t* p, uint64_t cmp, uint64_t v
 
 template <int TY, int TZ, bool STATS, int NV = TX * TY * TZ, int THREADS = NV / 8, int TABLE = table_slots(NV)>
 __global__ void __launch_bounds__(THREADS, TILE_MINB)
-tile_tmt_kernel(const float* __restrict__ f, Cell* __restrict__ C, uint32_t* __restrict__ basin_out,
+tile_tmt_kernel(const float* __restrict__ f, Cell* __restrict__ C, uint64_t* __restrict__ T0,
                 uint64_t* __restrict__ xface, uint32_t nx,
                 uint32_t ny, uint32_t z_begin,
                 uint32_t z_end, uint32_t tiles_x, uint32_t tiles_y, uint32_t flip, unsigned long long* __restrict__ counters,
@@ -266,11 +263,6 @@ tile_tmt_kernel(const float* __restrict__ f, Cell* __restrict__ C, uint32_t* __r
     }
 #endif
     __syncthreads();
-#if !TILE_REP
-    uint16_t bas[PER];  // descent basin of each owned vertex, for the crossing-edge dedupe
-#pragma unroll
-    for (int k = 0; k < PER; ++k) bas[k] = uint16_t(c_v(cell[(r0 + k * RSTEP) * TX + lx]));
-#endif
     phase_time(ST_CYC_COMPRESS);
 
     // ---- c. one edge per pair of adjacent basins: the lowest --------------------------------
@@ -710,7 +702,14 @@ tile_tmt_kernel(const float* __restrict__ f, Cell* __restrict__ C, uint32_t* __r
 #endif
     phase_time(ST_CYC_REPAIR);
 
-    // ---- f. write the global 16-byte cells ---------------------------------------------
+    // ---- f. write the tile store T0 (8 B per vertex) and the tile minima's 16-byte cells ------
+    // T0[u] = s << 32 | v with global ids, into the caller's triplet buffer: for a regular vertex
+    // (u, Rep_tile(u, key(u))) -- its s is final and the repair only re-points v; for a tile
+    // minimum its tile triplet.  Only tile minima (s != u, or the tile root) get a 16-byte
+    // working cell: the global merge only ever reads or writes cells of tile minima (the
+    // crossing edges start at tile representatives, which are minima, and every cell on a v
+    // chain from a minimum is a minimum's; DESIGN.md derivation C'''), so regular vertices need
+    // none (the x-face records carry (order key, R) for the tile's x faces, coalesced).
     const uint64_t gbase = uint64_t(z0) * sxy + uint64_t(y0) * nx + x0;
     auto gid = [&](uint32_t l) -> uint32_t {
         const uint32_t l_x = l % TX, l_r = l / TX;
@@ -730,20 +729,16 @@ tile_tmt_kernel(const float* __restrict__ f, Cell* __restrict__ C, uint32_t* __r
         const uint32_t s = c_s(cu), v = c_v(cu);
 #endif
         const uint64_t g = gbase + uint64_t(lz) * sxy + uint64_t(ly) * nx + lx;
-        C[g] = make_cell(key_of(uint32_t(cu >> 32), gid(s)), ou, gid(v));
-#if TILE_REP
-        // the vertex the crossing-edge walks may start from: Rep_tile(u, key(u)), joined to u
-        // below key(u) -- the v of a regular cell of the minimal tile store, u itself for a
-        // minimum (DESIGN.md derivation C''')
-        const uint32_t rep_u = gid(s == u ? v : u);
-        basin_out[g] = rep_u;
-        // the tile's x faces (lanes 0 and 31) again, compactly: (order key, R) per row, so that
-        // the crossing edges of the x faces read them coalesced (in the grid they are 128 B apart)
+        const uint32_t gu = uint32_t(g), gv = gid(v);
+        const bool minimum = s != u || v == u;
+        const uint32_t gs = s == u ? gu : gid(s);
+        T0[g] = pack(gs, gv);
+        if (minimum) C[g] = make_cell(key_of(uint32_t(cu >> 32), gs), ou, gv);
+        // the tile's x faces (lanes 0 and 31) again, compactly: (order key, R) per row, R =
+        // Rep_tile(u, key(u)) for a regular vertex, u for a minimum, so that the crossing edges of
+        // the x faces read them coalesced (in the grid they are 128 B apart)
         if (lx == 0 || lx == TX - 1)
-            xface[(uint64_t(b) * 2 + (lx == TX - 1)) * ROWS + r] = (uint64_t(ou) << 32) | rep_u;
-#else
-        basin_out[g] = gid(bas[k]);
-#endif
+            xface[(uint64_t(b) * 2 + (lx == TX - 1)) * ROWS + r] = (uint64_t(ou) << 32) | (s == u ? gv : gu);
     }
     phase_time(ST_CYC_WRITE);
     if (STATS) {
@@ -783,21 +778,21 @@ void tile_shape(uint32_t nz_global, uint32_t* ty, uint32_t* tz) {
 }
 
 template <int TY, int TZ>
-void launch_tile(const float* f, Cell* C, uint32_t* basin, uint64_t* xface, const Slab& sl, uint32_t tx, uint32_t tyn, uint32_t grid,
+void launch_tile(const float* f, Cell* C, uint64_t* T0, uint64_t* xface, const Slab& sl, uint32_t tx, uint32_t tyn, uint32_t grid,
                  uint32_t flip, unsigned long long* counters, unsigned long long* stats, cudaStream_t stream) {
     constexpr int NV = TX * TY * TZ;
     ensure_smem_attr(reinterpret_cast<const void*>(tile_tmt_kernel<TY, TZ, false>), int(smem_bytes<NV>()));
     ensure_smem_attr(reinterpret_cast<const void*>(tile_tmt_kernel<TY, TZ, true>), int(smem_bytes<NV>()));
     if (stats)
-        tile_tmt_kernel<TY, TZ, true><<<grid, NV / 8, smem_bytes<NV>(), stream>>>(f, C, basin, xface, sl.nx, sl.ny,
+        tile_tmt_kernel<TY, TZ, true><<<grid, NV / 8, smem_bytes<NV>(), stream>>>(f, C, T0, xface, sl.nx, sl.ny,
                                                                                  sl.z_begin, sl.z_end, tx, tyn,
                                                                                  flip, counters, stats);
     else
-        tile_tmt_kernel<TY, TZ, false><<<grid, NV / 8, smem_bytes<NV>(), stream>>>(f, C, basin, xface, sl.nx, sl.ny, sl.z_begin, sl.z_end, tx,
+        tile_tmt_kernel<TY, TZ, false><<<grid, NV / 8, smem_bytes<NV>(), stream>>>(f, C, T0, xface, sl.nx, sl.ny, sl.z_begin, sl.z_end, tx,
                                                                        tyn, flip, counters, stats);
 }
 
-void launch_tile_tmt(const float* f, Cell* C, uint32_t* basin, uint64_t* xface, const Slab& sl, uint32_t flip,
+void launch_tile_tmt(const float* f, Cell* C, uint64_t* T0, uint64_t* xface, const Slab& sl, uint32_t flip,
                      unsigned long long* counters, unsigned long long* stats, cudaStream_t stream) {
     uint32_t ty, tz;
     tile_shape(sl.nz, &ty, &tz);
@@ -807,13 +802,13 @@ void launch_tile_tmt(const float* f, Cell* C, uint32_t* basin, uint64_t* xface, 
     if (grid == 0) return;
     const bool big = tile_vertices() == 4096;
     if (sl.nz == 1 && big)
-        launch_tile<128, 1>(f, C, basin, xface, sl, tx, tyn, grid, flip, counters, stats, stream);
+        launch_tile<128, 1>(f, C, T0, xface, sl, tx, tyn, grid, flip, counters, stats, stream);
     else if (sl.nz == 1)
-        launch_tile<64, 1>(f, C, basin, xface, sl, tx, tyn, grid, flip, counters, stats, stream);
+        launch_tile<64, 1>(f, C, T0, xface, sl, tx, tyn, grid, flip, counters, stats, stream);
     else if (big)
-        launch_tile<16, 8>(f, C, basin, xface, sl, tx, tyn, grid, flip, counters, stats, stream);
+        launch_tile<16, 8>(f, C, T0, xface, sl, tx, tyn, grid, flip, counters, stats, stream);
     else
-        launch_tile<8, 8>(f, C, basin, xface, sl, tx, tyn, grid, flip, counters, stats, stream);
+        launch_tile<8, 8>(f, C, T0, xface, sl, tx, tyn, grid, flip, counters, stats, stream);
 }
 
 }  // namespace mt

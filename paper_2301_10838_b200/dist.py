@@ -69,6 +69,7 @@ class SlabMergeTree:
         self.ctx = _lib.mt_create_slab(self.dims, 6, self.z_begin, self.z_end, dev.index, ptr, nbytes)
         self._scratch = None
         self._f = None
+        self._T = None
 
     def __del__(self):
         ctx = getattr(self, "ctx", None)
@@ -76,12 +77,18 @@ class SlabMergeTree:
             _lib._lib.mt_destroy(ctx)
             self.ctx = None
 
-    def compute_local(self, f_slab: torch.Tensor, split: bool = False, stream=None):
+    def compute_local(self, f_slab: torch.Tensor, split: bool = False, triplets=None, stream=None):
+        """Local phase; ``triplets`` (int64, the slab's n values) receives the tile store now and
+        the final store from compute_global."""
         if f_slab.dtype != torch.float32 or not f_slab.is_cuda or not f_slab.is_contiguous() or \
                 f_slab.numel() != self.n:
             raise ValueError("f_slab must be a float32 CUDA tensor with the slab's nx*ny*(z_end-z_begin) values")
+        if triplets is None:
+            triplets = torch.empty(self.n, dtype=torch.int64, device=self.device)
         self._f = f_slab  # borrowed by the library until compute_global's work completes
-        _lib.mt_compute_local(self.ctx, f_slab.data_ptr(), _lib.MT_FLAG_SPLIT_TREE if split else 0, stream)
+        self._T = triplets
+        _lib.mt_compute_local(self.ctx, f_slab.data_ptr(), triplets.data_ptr(),
+                              _lib.MT_FLAG_SPLIT_TREE if split else 0, stream)
 
     def forest(self, stream=None) -> torch.Tensor:
         """The slab's boundary-forest records as a uint8 CUDA tensor (a view into the workspace)."""
@@ -91,14 +98,14 @@ class SlabMergeTree:
         off = ptr - self.workspace.data_ptr()
         return self.workspace[off: off + n * RECORD_BYTES]
 
-    def compute_global(self, all_records: torch.Tensor, z_bounds, triplets=None, stream=None) -> torch.Tensor:
+    def compute_global(self, all_records: torch.Tensor, z_bounds, stream=None) -> torch.Tensor:
+        """Global phase into the triplet buffer of compute_local (returned)."""
         n_all = all_records.numel() // RECORD_BYTES
         need = _lib.mt_forest_scratch_bytes(n_all)
         if self._scratch is None or self._scratch.numel() < need + 256:
             self._scratch = torch.empty(need + 256, dtype=torch.uint8, device=self.device)
         sp = (self._scratch.data_ptr() + 255) // 256 * 256
-        if triplets is None:
-            triplets = torch.empty(self.n, dtype=torch.int64, device=self.device)
+        triplets = self._T
         _lib.mt_compute_global(self.ctx, all_records.data_ptr() if n_all else 0, n_all, z_bounds, sp, need,
                                triplets.data_ptr(), stream)
         return triplets
@@ -192,11 +199,11 @@ class DistMergeTree:
     def compute(self, f_slab: torch.Tensor, split: bool = False, triplets=None) -> torch.Tensor:
         if self.transport == "nccl":
             return self.slab.compute(f_slab, split, triplets)
-        self.slab.compute_local(f_slab, split)
+        self.slab.compute_local(f_slab, split, triplets)
         mine = self.slab.forest()
         everything = allgather_varsize(mine, self.group)
         self.forest_records = everything.numel() // RECORD_BYTES
-        return self.slab.compute_global(everything, self.z_bounds, triplets)
+        return self.slab.compute_global(everything, self.z_bounds)
 
     def diagram(self):
         return self.slab.diagram()

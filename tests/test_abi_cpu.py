@@ -32,7 +32,7 @@ def test_exports_every_declared_symbol(lib):
 
 
 def test_abi_version_and_status_strings(lib):
-    assert lib.mt_abi_version() == 1
+    assert lib.mt_abi_version() == 2
     for st in range(9):
         assert lib.mt_status_string(st)
     assert b"non-finite" in lib.mt_status_string(3)
