@@ -91,6 +91,18 @@ mt_status mt_create(mt_ctx **out, const uint32_t dims[3], int conn, int cuda_dev
 mt_status mt_compute(mt_ctx *ctx, const float *f, uint64_t *triplets, uint32_t flags,
                      mt_stream_t stream);
 
+/* Both trees of one field from ONE read of f (the join and
+ * split trees are the two inputs of a contour tree; the paper
+ * computes the split tree of its densities): ctx_join and
+ * ctx_split are two contexts of the same grid and device (mt_create).  The tile
+ * kernel loads f once and builds both tile stores; each tree then runs its own
+ * crossing-edge merge, repair and diagram on its context, so mt_diagram(ctx_join)
+ * reports the merge tree's diagram and mt_diagram(ctx_split) the split tree's
+ * (exactly mt_compute with flags 0 and MT_FLAG_SPLIT_TREE).  T_join / T_split:
+ * device, n uint64 each, distinct.  Asynchronous like mt_compute. */
+mt_status mt_compute_join_split(mt_ctx *ctx_join, mt_ctx *ctx_split, const float *f, uint64_t *T_join,
+                                uint64_t *T_split, mt_stream_t stream);
+
 /* Register a caller-owned device buffer that later mt_compute calls write
  * the diagram into directly (zero-copy); capacity in records.  NULL detaches.
  * Without a registered buffer the diagram is kept in the workspace. */

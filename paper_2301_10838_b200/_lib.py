@@ -32,7 +32,8 @@ EXPORTS = ["mt_workspace_bytes", "mt_create", "mt_compute", "mt_set_diagram_outp
            "mt_status_string", "mt_destroy", "mt_abi_version", "mt_set_stats", "mt_stats", "mt_slab_workspace_bytes",
            "mt_create_slab", "mt_compute_local", "mt_forest_view", "mt_forest_scratch_bytes", "mt_compute_global",
            "mt_filter_diagram", "mt_graph_workspace_bytes", "mt_create_graph", "mt_compute_graph",
-           "mt_get_unique_id", "mt_dist_slab_bounds", "mt_dist_workspace_bytes", "mt_create_dist"]
+           "mt_get_unique_id", "mt_dist_slab_bounds", "mt_dist_workspace_bytes", "mt_create_dist",
+           "mt_compute_join_split"]
 
 
 class MTError(RuntimeError):
@@ -64,6 +65,7 @@ def load(build_if_missing: bool = False):
         "mt_workspace_bytes": (ctypes.c_size_t, [u32p, ctypes.c_int]),
         "mt_create": (ctypes.c_int, [ctypes.POINTER(vp), u32p, ctypes.c_int, ctypes.c_int, vp, ctypes.c_size_t]),
         "mt_compute": (ctypes.c_int, [vp, vp, vp, ctypes.c_uint32, vp]),
+        "mt_compute_join_split": (ctypes.c_int, [vp, vp, vp, vp, vp, vp]),
         "mt_set_diagram_output": (ctypes.c_int, [vp, vp, ctypes.c_uint64]),
         "mt_diagram": (ctypes.c_int, [vp, vp, ctypes.c_uint64, u64p, u64p, vp]),
         "mt_diagram_view": (ctypes.c_int, [vp, ctypes.POINTER(vp), u64p, u64p, vp]),
@@ -143,6 +145,11 @@ def mt_create(dims, conn: int, device: int, workspace_ptr: int, workspace_bytes:
 def mt_compute(ctx, f_ptr: int, triplets_ptr: int, flags: int = 0, stream=None):
     _check(load().mt_compute(ctx, ctypes.c_void_p(f_ptr), ctypes.c_void_p(triplets_ptr), int(flags),
                              _stream_handle(stream)), "mt_compute")
+
+
+def mt_compute_join_split(ctx_join, ctx_split, f_ptr: int, tj_ptr: int, ts_ptr: int, stream=None):
+    _check(load().mt_compute_join_split(ctx_join, ctx_split, ctypes.c_void_p(f_ptr), ctypes.c_void_p(tj_ptr),
+                                        ctypes.c_void_p(ts_ptr), _stream_handle(stream)), "mt_compute_join_split")
 
 
 def mt_set_diagram_output(ctx, buf_ptr: int, capacity: int):
@@ -409,6 +416,18 @@ class MergeTree:
 
     def last_launch_count(self):
         return mt_last_launch_count(self.ctx)
+
+
+def join_split(mt_join: "MergeTree", mt_split: "MergeTree", f, stream=None):
+    """Merge and split tree of f from one read of f (mt_compute_join_split): returns the two
+    int64 triplet tensors; each context's diagram() then reports its tree's diagram."""
+    import torch
+    if f.dtype != torch.float32 or not f.is_cuda or not f.is_contiguous() or f.numel() != mt_join.n:
+        raise ValueError("f must be a contiguous float32 CUDA tensor with nx*ny*nz elements")
+    tj = torch.empty(mt_join.n, dtype=torch.int64, device=f.device)
+    ts = torch.empty(mt_split.n, dtype=torch.int64, device=f.device)
+    mt_compute_join_split(mt_join.ctx, mt_split.ctx, f.data_ptr(), tj.data_ptr(), ts.data_ptr(), stream)
+    return tj, ts
 
 
 GraphMergeTree.diagram = MergeTree.diagram

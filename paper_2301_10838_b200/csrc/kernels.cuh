@@ -85,6 +85,13 @@ uint64_t xface_entries(const Slab& sl);
 void launch_tile_tmt(const float* f, Cell* C, uint64_t* T0, uint64_t* xface, const Slab& sl, uint32_t flip,
                      unsigned long long* counters, unsigned long long* stats, cudaStream_t stream);
 
+// both trees from one read of f: the merge tree into the first set of
+// buffers, the split tree into the second
+void launch_tile_tmt_dual(const float* f, Cell* C_join, uint64_t* T0_join, uint64_t* xface_join,
+                          unsigned long long* counters_join, Cell* C_split, uint64_t* T0_split,
+                          uint64_t* xface_split, unsigned long long* counters_split, const Slab& sl,
+                          unsigned long long* stats, cudaStream_t stream);
+
 // K3: merge of the tile-crossing grid edges on the global store (merge_cross.cu)
 uint64_t cross_edges(const Slab& sl);
 size_t cross_queue_entry_bytes();

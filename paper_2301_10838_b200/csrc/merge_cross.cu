@@ -265,7 +265,7 @@ dedupe_cross_kernel(const float* __restrict__ f, const uint64_t* __restrict__ T0
 }
 
 #ifndef MQ_SPLIT
-#define MQ_SPLIT 1        // path splitting (128-bit CAS) in the merge_queue walks
+#define MQ_SPLIT 1        // merge_queue walks: 1 path splitting, 2 path halving (128-bit CAS), 0 none
 #endif
 #ifndef MQ_WALK
 #define MQ_WALK 1         // filter walks (with path splitting) before Alg. 3
@@ -344,11 +344,16 @@ merge_queue_kernel(Cell* C, const QEntry* __restrict__ q, uint64_t cap, const un
         if (phase == CLIMB_HI || phase == CLIMB_LO) {
             if (cv_of(c) != x && c.lo <= L) {          // followable at level L
                 if (STATS) n_hops++;
-                if (MQ_SPLIT && has_prev && c.lo <= cp.lo)   // path splitting: prev skips x
+                const bool split = MQ_SPLIT && has_prev && c.lo <= cp.lo;
+                if (split)                                 // path splitting: prev skips x
                     cas_cell(C + xp, cp, Cell{cp.lo, (cp.hi & 0xffffffff00000000ull) | cv_of(c)});
-                xp = x;
-                cp = c;
-                has_prev = true;
+                if (MQ_SPLIT == 2 && split) {
+                    has_prev = false;                      // path halving: every other cell
+                } else {
+                    xp = x;
+                    cp = c;
+                    has_prev = true;
+                }
                 x = cv_of(c);
             } else if (phase == CLIMB_HI) {
                 rh = x;

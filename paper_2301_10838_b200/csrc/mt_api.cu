@@ -281,37 +281,53 @@ mt_status create_ctx(mt_ctx** out, const uint32_t dims[3], int conn, uint32_t z_
 
 // shared by mt_compute and mt_compute_local: reset, then the slab's own merge tree; T (the
 // caller's triplet buffer, indexed from the slab's first vertex) receives the tile store T0
-mt_status start_compute(mt_ctx* c, const float* f, uint64_t* T, uint32_t flags, cudaStream_t s) {
+// reset the context for a new compute: state, statistics, counters and chunk status records
+mt_status prepare_compute(mt_ctx* c, const float* f, uint32_t flags, cudaStream_t s) {
     c->launches = 0;
     c->nev = 0;
     c->sticky = MT_OK;
     c->computed = true;
     c->f = f;
     c->flip = (flags & MT_FLAG_SPLIT_TREE) ? 0xffffffffu : 0u;
-    unsigned long long* ctr = counters_of(c);
-    mt::Cell* cells = cells_of(c);
     unsigned long long* stats = stats_of(c);
-    const float* fs = f - c->slab.base;  // every kernel indexes f, T and the cells by global id
     if (stats && cudaMemsetAsync(stats, 0, mt::ST_COUNT * sizeof(uint64_t), s) != cudaSuccess)
         return c->sticky = MT_ERR_CUDA;
     mark(c, "zero", s);
     if (cudaMemsetAsync(c->ws + c->L.counters, 0, c->L.status - c->L.counters + c->L.status_bytes,
                         s) != cudaSuccess)
         return c->sticky = MT_ERR_CUDA;
-    uint64_t* T0 = T - c->slab.base;
-    mark(c, "tile_tmt", s);
-    uint64_t* xface = reinterpret_cast<uint64_t*>(c->ws + c->L.xface);
-    mt::launch_tile_tmt(fs, cells, T0, xface, c->slab, c->flip, ctr, stats, s);
+    return MT_OK;
+}
+
+uint64_t* xface_of(mt_ctx* c) { return reinterpret_cast<uint64_t*>(c->ws + c->L.xface); }
+
+// the tile-crossing edges: dedupe + the queue merge (none on a single-tile grid)
+void launch_cross(mt_ctx* c, uint64_t* T0, cudaStream_t s) {
+    unsigned long long* ctr = counters_of(c);
+    unsigned long long* stats = stats_of(c);
     mark(c, "dedupe_cross", s);
-    int nl = mt::launch_dedupe_cross(fs, T0, xface, c->slab, c->flip, c->ws + c->L.queue, c->L.queue_cap,
-                                     ctr + mt::CTR_QLEN, stats, c->num_sms, s);
+    int nl = mt::launch_dedupe_cross(c->f - c->slab.base, T0, xface_of(c), c->slab, c->flip, c->ws + c->L.queue,
+                                     c->L.queue_cap, ctr + mt::CTR_QLEN, stats, c->num_sms, s);
     if (nl) {
         mark(c, "merge_queue", s);
-        mt::launch_merge_queue(cells, c->ws + c->L.queue, c->L.queue_cap, ctr + mt::CTR_QLEN, ctr + mt::CTR_QFETCH,
-                               stats, c->num_sms, s);
+        mt::launch_merge_queue(cells_of(c), c->ws + c->L.queue, c->L.queue_cap, ctr + mt::CTR_QLEN,
+                               ctr + mt::CTR_QFETCH, stats, c->num_sms, s);
         ++nl;
     }
-    c->launches = 1 + nl;
+    c->launches += nl;
+}
+
+// shared by mt_compute and mt_compute_local: reset, then the slab's own merge tree; T (the
+// caller's triplet buffer, indexed from the slab's first vertex) receives the tile store T0
+mt_status start_compute(mt_ctx* c, const float* f, uint64_t* T, uint32_t flags, cudaStream_t s) {
+    const mt_status st = prepare_compute(c, f, flags, s);
+    if (st != MT_OK) return st;
+    uint64_t* T0 = T - c->slab.base;
+    mark(c, "tile_tmt", s);
+    mt::launch_tile_tmt(f - c->slab.base, cells_of(c), T0, xface_of(c), c->slab, c->flip, counters_of(c),
+                        stats_of(c), s);
+    c->launches = 1;
+    launch_cross(c, T0, s);
     return MT_OK;
 }
 
@@ -469,6 +485,38 @@ mt_status mt_compute(mt_ctx* c, const float* f, uint64_t* T, uint32_t flags, mt_
     const mt_status st = start_compute(c, f, T, flags, s);
     if (st != MT_OK) return st;
     return finish_compute(c, T, nullptr, s);
+}
+
+mt_status mt_compute_join_split(mt_ctx* cj, mt_ctx* cs, const float* f, uint64_t* T_join, uint64_t* T_split,
+                                mt_stream_t stream) {
+    if (!cj || !cs || cj == cs) return MT_ERR_INVALID_ARG;
+    if (cj->multi || cj->graph || cj->dist || cs->multi || cs->graph || cs->dist) return MT_ERR_STATE;
+    if (cj->nx != cs->nx || cj->ny != cs->ny || cj->nz != cs->nz || cj->conn != cs->conn || cj->device != cs->device)
+        return MT_ERR_INVALID_ARG;
+    if (cj->n == 0) {
+        for (mt_ctx* c : {cj, cs}) {
+            c->computed = true;
+            c->sticky = MT_OK;
+            c->launches = 0;
+        }
+        return MT_OK;
+    }
+    if (!f || !T_join || !T_split || T_join == T_split) return MT_ERR_INVALID_ARG;
+    DeviceGuard g(cj->device);
+    if (!g.ok) return MT_ERR_CUDA;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    mt_status st = prepare_compute(cj, f, 0, s);
+    if (st == MT_OK) st = prepare_compute(cs, f, MT_FLAG_SPLIT_TREE, s);
+    if (st != MT_OK) return st;
+    mark(cj, "tile_tmt", s);
+    mt::launch_tile_tmt_dual(f, cells_of(cj), T_join, xface_of(cj), counters_of(cj), cells_of(cs), T_split,
+                             xface_of(cs), counters_of(cs), cj->slab, stats_of(cj), s);
+    cj->launches = 1;
+    launch_cross(cj, T_join, s);
+    launch_cross(cs, T_split, s);
+    st = finish_compute(cj, T_join, nullptr, s);
+    if (st != MT_OK) return st;
+    return finish_compute(cs, T_split, nullptr, s);
 }
 
 mt_status mt_compute_local(mt_ctx* c, const float* f, uint64_t* T, uint32_t flags, mt_stream_t stream) {

@@ -76,7 +76,10 @@ __device__ __forceinline__ uint32_t inv_ord(uint32_t o) { return (o & 0x80000000
 // 4096 consecutive ids instead (graphs, thin grids).  A row of a brick is a
 // "segment" of at most 32 consecutive ids; segments are numbered in id order.
 constexpr int RB_THREADS = 512;
-constexpr int RB_ROWS = 128;
+#ifndef MT_REPAIR_ROWS
+#define MT_REPAIR_ROWS 64   // rows of 32 per brick (a 32 x 16 x 4 brick; 2-D: 32 x 64): 4 vertices per thread
+#endif
+constexpr int RB_ROWS = MT_REPAIR_ROWS;
 constexpr int RB_PER = RB_ROWS / (RB_THREADS / 32);   // rows (vertices) per thread
 constexpr int RB_NV = RB_ROWS * 32;
 
@@ -154,22 +157,36 @@ repair_brick_kernel(View view, const Cell* C, uint64_t* __restrict__ T, const fl
     uint64_t key[RB_PER];     // threshold key(s)
     uint32_t sv[RB_PER];      // s of the vertex
     uint32_t xs[RB_PER];      // walk start (then position)
+    uint32_t mins = 0;        // rows k whose vertex has a working cell (bit k)
+    if (TILED) {
+        // every load of the thread in flight at once: the tile store and f of all its vertices,
+        // then the working cells of the (few) tile minima among them
+        uint64_t t0[RB_PER];
+        uint32_t fo[RB_PER];
 #pragma unroll
-    for (int k = 0; k < RB_PER; ++k) {
-        key[k] = 0;
-        sv[k] = 0;
-        xs[k] = 0;
-        if (!INB(k)) continue;
-        const uint32_t u = uint32_t(UID(k));
-        if (TILED) {
-            const uint64_t t0 = T[UID(k)];
-            if (cell_s(t0) == u && cell_v(t0) != u) {        // regular in its tile: s = u is final
-                key[k] = key_of(ord32(__ldg(f + UID(k))) ^ flip, u);
+        for (int k = 0; k < RB_PER; ++k) t0[k] = INB(k) ? T[UID(k)] : 0;
+#pragma unroll
+        for (int k = 0; k < RB_PER; ++k) fo[k] = INB(k) ? ord32(__ldg(f + UID(k))) ^ flip : 0u;
+#pragma unroll
+        for (int k = 0; k < RB_PER; ++k) {
+            const uint32_t u = uint32_t(UID(k));
+            if (cell_s(t0[k]) == u && cell_v(t0[k]) != u) {   // regular in its tile: s = u is final
+                key[k] = key_of(fo[k], u);
                 sv[k] = u;
-                xs[k] = cell_v(t0);
-                continue;
+                xs[k] = cell_v(t0[k]);
+            } else {
+                mins |= uint32_t(INB(k)) << k;
+                key[k] = 0;
+                sv[k] = u;
+                xs[k] = u;
             }
         }
+    } else {
+        mins = inb;
+    }
+#pragma unroll
+    for (int k = 0; k < RB_PER; ++k) {
+        if (!((mins >> k) & 1u)) continue;
         const Cell c = ld_cell_ro(C + UID(k));               // a minimum's working cell
         key[k] = c.lo;
         sv[k] = cs_of(c);
@@ -447,12 +464,12 @@ void launch_brick(const View& view, const Cell* C, uint64_t* T, const float* f, 
     }
 }
 
-// brick geometry: 3-D bricks 32 x 16 x 8 on volumes, 32 x 128 on images, id ranges otherwise
+// brick geometry: 3-D bricks 32 x 16 x (RB_ROWS / 16) on volumes, 32 x RB_ROWS on images, id ranges otherwise
 bool brick_mode(const Slab& sl, BrickGeom* g, uint64_t* nb, uint64_t* nseg) {
     const uint32_t nzl = sl.z_end - sl.z_begin;
     uint32_t by = 0;
-    if (nzl >= 8 && sl.ny >= 16) by = 16;
-    else if (sl.nz == 1 && sl.ny >= 128) by = 128;
+    if (nzl >= uint32_t(RB_ROWS / 16) && sl.ny >= 16) by = 16;
+    else if (sl.nz == 1 && sl.ny >= uint32_t(RB_ROWS)) by = RB_ROWS;
     if (by && sl.nx >= 32) {
         const uint32_t bz = RB_ROWS / by;
         const uint32_t bx_n = (sl.nx + 31) / 32, by_n = (sl.ny + by - 1) / by, bz_n = (nzl + bz - 1) / bz;
@@ -474,7 +491,7 @@ void launch_repair_view(const View& view, const Cell* C, uint64_t* T, const floa
     uint64_t nb, nseg;
     if (!brick_mode(sl, &g, &nb, &nseg)) launch_brick<View, 0>(view, C, T, f, sl, g, nb, flip, o, tiled, stats, stream);
     else if (g.by == 16) launch_brick<View, 16>(view, C, T, f, sl, g, nb, flip, o, tiled, stats, stream);
-    else launch_brick<View, 128>(view, C, T, f, sl, g, nb, flip, o, tiled, stats, stream);
+    else launch_brick<View, RB_ROWS>(view, C, T, f, sl, g, nb, flip, o, tiled, stats, stream);
 }
 
 }  // namespace

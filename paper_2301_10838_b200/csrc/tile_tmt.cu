@@ -18,22 +18,29 @@
 //      (derivation B);
 //   b. compress by synchronous pointer jumping: every regular cell points at
 //      its basin minimum (derivations F, F');
-//   c. list the in-tile edges between two basins, keeping the lowest per
-//      basin pair (staged per warp, inserted 32 at a time into a hash table);
-//   d. merge them: Alg. 3 from the two basins at the edge's level with 64-bit
-//      shared-memory CAS and the root guards R4/R5, one lane per
-//      pair, one shared-memory round trip per loop iteration; a lane whose
-//      pair is done takes the next pair of the warp's compacted run;
+//   c. choose the inter-basin edges the merge needs (TILE_KRUSKAL, default):
+//      the vertices are counting-sorted into NB level buckets; bucket by
+//      bucket, an edge (u, w) from u down to a lower neighbour w of another
+//      basin is kept only if a union-find over the basins, holding every kept
+//      edge of the LOWER buckets, does not already join the two basins (an
+//      edge whose basins are joined below its level changes no sublevel
+//      component: derivation K); then the bucket's kept edges are united.
+//      This is Kruskal's filter at bucket granularity: the kept edges are the
+//      basin graph's minimum spanning forest plus the few edges that close a
+//      cycle inside one bucket.  (TILE_KRUSKAL=0: the earlier lowest-edge-per-
+//      basin-pair hash table, derivation C''.)
+//   d. merge the kept edges: Alg. 3 from the two basins at the edge's level
+//      with 64-bit shared-memory CAS and the root guards R4/R5,
+//      one lane per edge, one shared-memory round trip per loop iteration; a
+//      lane whose edge is done takes the next one of the warp's slice;
 //   e. repair (Alg. 5 with Alg. 4's walk, reading R20): the tile store is
 //      minimal for G_t (each thread's walks in lock-step rounds);
-//   f. write the 16-byte global cells (common.cuh) with global ids, and each
-//      vertex's tile representative at its own level for the crossing edges
-//      (derivation C''').
+//   f. write the tile store T0 (8 B per vertex) and the tile minima's 16-byte
+//      working cells (common.cuh) with global ids, and the x-face records.
 // No halo is needed: only in-tile edges are used here.
 //
 // Layout: f float32[n] x fastest (reading R10) read once (coalesced 128-B
-// rows); 16-B cells written once (coalesced 512-B rows).  One CTA of 512
-// threads per tile; 112 KB of dynamic shared memory (2 CTAs per SM).
+// rows).  One CTA of 512 threads per tile.
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -41,46 +48,37 @@ namespace mt {
 
 namespace {
 
-#ifndef TILE_SPLIT
-#define TILE_SPLIT 1   // path splitting in the merge-phase walks (A/B knob)
+#ifndef TILE_KRUSKAL
+#define TILE_KRUSKAL 0 // phase c: bucketed Kruskal filter (1) or the basin-pair hash table (0)
 #endif
-#ifndef TILE_STOP
-#define TILE_STOP 0    // timing only (WRONG results): run phases < k: 1 load+descent, 2 +compress, 3 +list, 4 +merge
+#ifndef TILE_NB
+#define TILE_NB 16     // level buckets of the Kruskal filter (4, 8, 16 or 32)
 #endif
-#ifndef TILE_LEAN
-#define TILE_LEAN 1    // merge phase: Alg. 3 only, no phase variable (requires TILE_OWNRUN)
-#endif
-#ifndef TILE_WALK
-#define TILE_WALK 0    // merge phase: filter walks (with path splitting) before Alg. 3
-#endif
-#ifndef LIST_STAGE
-#define LIST_STAGE 1   // list phase: per-warp staging of the candidate edges, inserts 32 at a time
+#ifndef TILE_KCAP
+#define TILE_KCAP 2048 // kept edges a tile can hold (more: the overflow path merges every edge)
 #endif
 #ifndef TILE_MINB
 #define TILE_MINB 2    // __launch_bounds__ min blocks per SM (register budget knob)
 #endif
-#ifndef TILE_REP_ILP
-#define TILE_REP_ILP 1 // in-tile repair: own vertices in lock-step rounds, results in registers
+#ifndef TILE_NDEDUP
+#define TILE_NDEDUP 0  // hash list: drop +y/+z edges whose neighbour lane has the same basin pair lower
 #endif
-#ifndef TILE_PJ
-#define TILE_PJ 1      // compress by synchronous pointer jumping (else walks + path compression)
-#endif
-#ifndef TILE_OWNRUN
-#define TILE_OWNRUN 1  // each warp merges the pairs of its own compacted run (no CTA counter)
-#endif
-#if TILE_LEAN && (TILE_WALK || !TILE_OWNRUN)
-#error "TILE_LEAN needs TILE_OWNRUN and no TILE_WALK"
+#ifndef TILE_STOP
+#define TILE_STOP 0    // timing only (WRONG results): run phases < k: 1 load+descent, 2 +compress, 3 +list, 4 +merge
 #endif
 
 constexpr int TX = 32;
 constexpr uint32_t ABSENT = 0xffffffffu;       // order key of a tile slot outside the grid
 constexpr uint64_t EMPTY = ~0ull;
-// tile of NV vertices, NV / 8 threads (8 vertices each), basin-pair table of 1.5 NV slots
-// (2 NV without the staging buffers), staging buffer of 128 entries per warp
-constexpr int table_slots(int nv) { return LIST_STAGE ? 3 * nv / 2 : 2 * nv; }
+constexpr int LOG2NB = TILE_NB == 32 ? 5 : TILE_NB == 16 ? 4 : TILE_NB == 8 ? 3 : 2;
+static_assert((1 << LOG2NB) == TILE_NB, "TILE_NB: 4, 8, 16 or 32");
+// hash variant: basin-pair table of 1.5 NV slots + a staging buffer of 128 entries per warp
+constexpr int table_slots(int nv) { return 3 * nv / 2; }
 template <int NV>
 constexpr size_t smem_bytes() {
-    return size_t(NV) * 8 + size_t(NV) * 4 + size_t(table_slots(NV)) * 8 + (LIST_STAGE ? size_t(NV) * 4 : 0);
+    return TILE_KRUSKAL ? size_t(NV) * 8 + size_t(NV) * 4 + size_t(NV) * 2 /* uf */ + size_t(NV) * 2 /* vlist */ +
+                              size_t(TILE_KCAP) * 4
+                        : size_t(NV) * 8 + size_t(NV) * 4 + size_t(table_slots(NV)) * 8 + size_t(NV) * 4;
 }
 
 template <int TABLE>
@@ -106,35 +104,79 @@ __device__ __forceinline__ bool lkey_lt(const uint32_t* ord, uint32_t a, uint32_
 __device__ __forceinline__ uint64_t sld64(const uint64_t* p) {
     return *reinterpret_cast<const volatile uint64_t*>(p);
 }
-[[maybe_unused]] __device__ __forceinline__ void sst64(uint64_t* p, uint64_t v) {
-    *reinterpret_cast<volatile uint64_t*>(p) = v;
-}
 __device__ __forceinline__ uint64_t scas64(uint64_t* p, uint64_t cmp, uint64_t val) {
     return atomicCAS(reinterpret_cast<unsigned long long*>(p), cmp, val);
 }
+__device__ __forceinline__ uint32_t sld16(const uint16_t* p) { return *reinterpret_cast<const volatile uint16_t*>(p); }
 
-template <int TY, int TZ, bool STATS, int NV = TX * TY * TZ, int THREADS = NV / 8, int TABLE = table_slots(NV)>
+// union-find over basin minima (local ids, 16-bit parents): find with path halving -- the
+// halving stores only ever shortcut to an ancestor in the same tree, so they are safe next to
+// concurrent finds and unions
+__device__ __forceinline__ uint32_t uf_find(uint16_t* uf, uint32_t x) {
+    while (true) {
+        const uint32_t p = sld16(uf + x);
+        if (p == x) return x;
+        const uint32_t g = sld16(uf + p);
+        if (g == p) return p;
+        *reinterpret_cast<volatile uint16_t*>(uf + x) = uint16_t(g);
+        x = g;
+    }
+}
+// link the younger root under the older (a fixed order: no cycles); retried on a lost race
+__device__ __forceinline__ void uf_union(uint16_t* uf, const uint32_t* ord, uint32_t a, uint32_t b) {
+    while (true) {
+        a = uf_find(uf, a);
+        b = uf_find(uf, b);
+        if (a == b) return;
+        if (lkey_lt(ord, a, b)) {
+            const uint32_t t = a;
+            a = b;
+            b = t;
+        }
+        if (atomicCAS(reinterpret_cast<unsigned short*>(uf + a), (unsigned short)a, (unsigned short)b) ==
+            (unsigned short)a)
+            return;
+    }
+}
+
+// Output pointers of one tree.  DUAL launches compute two trees from one read of f: the merge
+// (join) tree into the first set and the split tree (complemented order keys, reading R16) into
+// the second.
+struct TileOut {
+    Cell* C;
+    uint64_t* T0;
+    uint64_t* xface;
+    unsigned long long* counters;
+};
+
+template <int TY, int TZ, bool STATS, bool DUAL, int NV = TX * TY * TZ, int THREADS = NV / 8,
+          int TABLE = table_slots(NV)>
 __global__ void __launch_bounds__(THREADS, TILE_MINB)
-tile_tmt_kernel(const float* __restrict__ f, Cell* __restrict__ C, uint64_t* __restrict__ T0,
-                uint64_t* __restrict__ xface, uint32_t nx,
+tile_tmt_kernel(const float* __restrict__ f, TileOut out0, TileOut out1, uint32_t nx,
                 uint32_t ny, uint32_t z_begin,
-                uint32_t z_end, uint32_t tiles_x, uint32_t tiles_y, uint32_t flip, unsigned long long* __restrict__ counters,
+                uint32_t z_end, uint32_t tiles_x, uint32_t tiles_y, uint32_t flip,
                 unsigned long long* __restrict__ stats) {
     constexpr int ROWS = TY * TZ;               // 128 rows of 32
     static_assert(TX * ROWS == NV, "tile size");
     constexpr int RSTEP = THREADS / TX;         // 16 rows per pass
     constexpr int PER = ROWS / RSTEP;           // 8 vertices per thread
+    constexpr int NW = THREADS / 32;
     extern __shared__ __align__(16) unsigned char smem[];
     uint64_t* cell = reinterpret_cast<uint64_t*>(smem);
     uint32_t* ord = reinterpret_cast<uint32_t*>(smem + NV * 8);
-    uint64_t* table = reinterpret_cast<uint64_t*>(smem + NV * 12);
     __shared__ int s_overflow;
-    __shared__ uint32_t s_fetch, s_row, s_row_b, s_row_e;
-#if !TILE_OWNRUN
-    __shared__ uint32_t s_wcnt[THREADS / 32], s_wpre[THREADS / 32 + 1];
+    __shared__ uint32_t s_omin, s_omax, s_nkept;
+#if TILE_KRUSKAL
+    uint16_t* uf = reinterpret_cast<uint16_t*>(smem + NV * 12);
+    uint16_t* vlist = reinterpret_cast<uint16_t*>(smem + NV * 14);
+    uint32_t* kept = reinterpret_cast<uint32_t*>(smem + NV * 16);
+    __shared__ uint32_t s_hist[TILE_NB][NW];    // per bucket and warp: count, then offset
+    __shared__ uint32_t s_boff[TILE_NB + 1];
+#else
+    uint64_t* table = reinterpret_cast<uint64_t*>(smem + NV * 12);
 #endif
 
-    unsigned long long n_edges = 0, n_pairs = 0, n_hops = 0, n_iters = 0, n_rep = 0, n_cmp = 0;
+    unsigned long long n_edges = 0, n_pairs = 0, n_iters = 0, n_rep = 0, n_cmp = 0;
     long long t_mark = clock64();
     // per-phase SM cycles (stats mode): thread 0 accumulates the time between barriers
     auto phase_time = [&](int slot) {
@@ -153,6 +195,8 @@ tile_tmt_kernel(const float* __restrict__ f, Cell* __restrict__ C, uint64_t* __r
     const uint64_t sxy = uint64_t(nx) * ny;
     const int lx = threadIdx.x & (TX - 1);
     const int r0 = threadIdx.x / TX;
+    const int lane_c = threadIdx.x & 31;
+    const int warp_d = threadIdx.x >> 5;
 
     // ---- K1: load f once, order keys into shared memory ------------------------------
     bool bad = false;
@@ -169,109 +213,249 @@ tile_tmt_kernel(const float* __restrict__ f, Cell* __restrict__ C, uint64_t* __r
         }
         ord[r * TX + lx] = o;
     }
+#if TILE_KRUSKAL
+    for (int i = threadIdx.x; i < NV; i += THREADS) uf[i] = uint16_t(i);
+    if (threadIdx.x < TILE_NB * NW) (&s_hist[0][0])[threadIdx.x] = 0;
+#else
     for (int i = threadIdx.x; i < TABLE; i += THREADS) table[i] = EMPTY;
+#endif
     if (threadIdx.x == 0) {
         s_overflow = 0;
-        s_fetch = 0;
-        s_row = 0;
-        s_row_b = 0;
-        s_row_e = 0;
+        s_omin = ~0u;
+        s_omax = 0;
+        s_nkept = 0;
     }
-    if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(counters + CTR_ERR, ERR_NONFINITE);
+    if (__syncthreads_or(bad) && threadIdx.x == 0) {
+        atomicOr(out0.counters + CTR_ERR, ERR_NONFINITE);
+        if (DUAL) atomicOr(out1.counters + CTR_ERR, ERR_NONFINITE);
+    }
     phase_time(ST_CYC_LOAD);
 
+#pragma unroll 1
+    for (int pass = 0; pass < (DUAL ? 2 : 1); ++pass) {
+    Cell* const C = pass ? out1.C : out0.C;
+    uint64_t* const T0 = pass ? out1.T0 : out0.T0;
+    uint64_t* const xface = pass ? out1.xface : out0.xface;
+    if (DUAL && pass) {
+        // the split tree of the same values: complemented order keys (reading R16), state reset
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+            const uint32_t i = (r0 + k * RSTEP) * TX + lx;
+            if (ord[i] != ABSENT) ord[i] = ~ord[i];
+        }
+#if TILE_KRUSKAL
+        for (int i = threadIdx.x; i < NV; i += THREADS) uf[i] = uint16_t(i);
+        if (threadIdx.x < TILE_NB * NW) (&s_hist[0][0])[threadIdx.x] = 0;
+#else
+        for (int i = threadIdx.x; i < TABLE; i += THREADS) table[i] = EMPTY;
+#endif
+        if (threadIdx.x == 0) {
+            s_overflow = 0;
+            s_omin = ~0u;
+            s_omax = 0;
+            s_nkept = 0;
+        }
+        __syncthreads();
+    }
+
     // ---- a. steepest descent over in-tile neighbours -----------------------------------
-    uint32_t par[PER];  // descent pointer of each owned vertex (then its basin, phase b)
+    // the key-least of u and its neighbours: visiting them in ascending id order (-z, -y, -x,
+    // u, +x, +y, +z: local ids are lexicographic in (z, y, x) like global ids) and taking a
+    // strictly smaller order key breaks ties by id (reading R1) with 32-bit compares only
 #pragma unroll
     for (int k = 0; k < PER; ++k) {
         const int r = r0 + k * RSTEP;
         const int ly = r % TY, lz = r / TY;
         const uint32_t u = r * TX + lx;
-        uint32_t best = u;
         const uint32_t ou = ord[u];
+        uint32_t best = u;
         if (ou != ABSENT) {
-            uint64_t kb = (uint64_t(ou) << 16) | u;
-            const uint32_t nb[6] = {lx > 0 ? u - 1 : u, lx + 1 < TX ? u + 1 : u,
-                                    ly > 0 ? u - TX : u, ly + 1 < TY ? u + TX : u,
-                                    lz > 0 ? u - TX * TY : u, lz + 1 < TZ ? u + TX * TY : u};
-#pragma unroll
-            for (int d = 0; d < 6; ++d) {
-                const uint32_t w = nb[d];
+            uint32_t bo = ABSENT;
+            auto visit = [&](bool ok, uint32_t w) {
+                if (!ok) return;
                 const uint32_t ow = ord[w];
-                const uint64_t kw = (uint64_t(ow) << 16) | w;
-                if (w != u && ow != ABSENT && kw < kb) {
-                    kb = kw;
+                if (ow < bo) {
+                    bo = ow;
                     best = w;
                 }
-            }
+            };
+            visit(lz > 0, u - TX * TY);
+            visit(ly > 0, u - TX);
+            visit(lx > 0, u - 1);
+            visit(true, u);
+            visit(lx + 1 < TX, u + 1);
+            visit(ly + 1 < TY, u + TX);
+            visit(lz + 1 < TZ, u + TX * TY);
         }
         cell[u] = c_make(ou, u, best);
-        par[k] = best;
     }
     __syncthreads();
     phase_time(ST_CYC_DESCENT);
 
     // ---- b. compress: every regular cell points at its basin minimum ----------------------
-#if TILE_PJ
     // synchronous pointer jumping, par <- par(par), on the thread's own 8 vertices (8
     // independent load chains per round), until every pointer is a root: ceil(log2 depth) + 1
     // rounds.  Rounds run in place: a pointer read while its owner rewrites it is the old or
     // the new ancestor, both in the same descent tree (derivation F), so the v fields (16-bit
     // stores) only ever move up the tree.
-#pragma unroll 1
-    while (TILE_STOP == 0 || TILE_STOP > 1) {
-        bool changed = false;
+    {
+        uint32_t par[PER];
 #pragma unroll
-        for (int k = 0; k < PER; ++k) {
-            const uint32_t q = *reinterpret_cast<const volatile uint16_t*>(cell + par[k]);
-            if (q != par[k]) {
-                par[k] = q;
-                changed = true;
-                *reinterpret_cast<volatile uint16_t*>(cell + (r0 + k * RSTEP) * TX + lx) = uint16_t(q);
-                if (STATS) ++n_cmp;
-            }
-        }
-        if (!__syncthreads_or(changed)) break;
-    }
-#else
-    // rows handed out dynamically, one warp per row (no warp waits on a long walk of another)
+        for (int k = 0; k < PER; ++k) par[k] = c_v(cell[(r0 + k * RSTEP) * TX + lx]);
 #pragma unroll 1
-    while (TILE_STOP == 0 || TILE_STOP > 1) {
-        int rr = 0;
-        if ((threadIdx.x & 31) == 0) rr = int(atomicAdd(&s_row_b, 1u));
-        rr = __shfl_sync(FULL_MASK, rr, 0);
-        if (rr >= ROWS) break;
-        const uint32_t u = rr * TX + lx;
-        const uint32_t v = c_v(cell[u]);
-        if (v == u) continue;
-        uint32_t x = v;
-        while (true) {
-            const uint32_t y = c_v(sld64(cell + x));
-            if (y == x) break;
-            x = y;
-            if (STATS) ++n_cmp;
+        while (TILE_STOP == 0 || TILE_STOP > 1) {
+            bool changed = false;
+#pragma unroll
+            for (int k = 0; k < PER; ++k) {
+                const uint32_t q = *reinterpret_cast<const volatile uint16_t*>(cell + par[k]);
+                if (q != par[k]) {
+                    par[k] = q;
+                    changed = true;
+                    *reinterpret_cast<volatile uint16_t*>(cell + (r0 + k * RSTEP) * TX + lx) = uint16_t(q);
+                    if (STATS) ++n_cmp;
+                }
+            }
+            if (!__syncthreads_or(changed)) break;
         }
-        // every regular cell on the path gets the root too (same tree, same basin)
-        uint32_t y = v;
-        while (y != x) {
-            const uint64_t cy = sld64(cell + y);
-            const uint32_t nxt = c_v(cy);
-            if (nxt != x) sst64(cell + y, (cy & ~0xffffull) | x);
-            y = nxt;
-        }
-        sst64(cell + u, (cell[u] & ~0xffffull) | x);
     }
-#endif
     __syncthreads();
     phase_time(ST_CYC_COMPRESS);
 
+    // basin of x after the compress: a regular cell (s = x) is static and points at the minimum
+    auto basin = [&](uint32_t x) {
+        const uint64_t c = sld64(cell + x);
+        return c_s(c) == x ? c_v(c) : x;
+    };
+
+#if TILE_KRUSKAL
+    // ---- c. bucketed Kruskal filter over the basin graph --------------------------------
+    // Level buckets: the order keys' range of the tile split at a power-of-two shift, so that a
+    // bucket is (ord - omin) >> sh (at least NB/2 of the NB buckets in use).
+    {
+        uint32_t omin = ~0u, omax = 0;
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+            const uint32_t o = ord[(r0 + k * RSTEP) * TX + lx];
+            if (o != ABSENT) {
+                omin = min(omin, o);
+                omax = max(omax, o);
+            }
+        }
+        omin = __reduce_min_sync(FULL_MASK, omin);
+        omax = __reduce_max_sync(FULL_MASK, omax);
+        if (lane_c == 0) {
+            atomicMin(&s_omin, omin);
+            atomicMax(&s_omax, omax);
+        }
+    }
+    __syncthreads();
+    const uint32_t omin = s_omin;
+    const uint32_t range = s_omax >= omin ? s_omax - omin : 0u;
+    const int rbits = range ? 32 - __clz(range) : 0;
+    const int sh = rbits > LOG2NB ? rbits - LOG2NB : 0;
+    // counting sort of the vertices by bucket: per-warp counts, bucket-major prefix, scatter
+    {
+        uint32_t rank[PER];
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+            const uint32_t o = ord[(r0 + k * RSTEP) * TX + lx];
+            rank[k] = o != ABSENT ? atomicAdd(&s_hist[(o - omin) >> sh][warp_d], 1u) : 0u;
+        }
+        __syncthreads();
+        if (warp_d == 0) {                     // exclusive prefix over (bucket, warp), bucket-major
+            constexpr int E = TILE_NB * NW / 32;   // entries per lane
+            static_assert(E * 32 == TILE_NB * NW, "prefix layout");
+            uint32_t* h = &s_hist[0][0];
+            uint32_t c[E], tot = 0;
+#pragma unroll
+            for (int j = 0; j < E; ++j) {
+                c[j] = h[lane_c * E + j];
+                tot += c[j];
+            }
+            uint32_t incl = tot;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t t = __shfl_up_sync(FULL_MASK, incl, o);
+                if (lane_c >= o) incl += t;
+            }
+            uint32_t off = incl - tot;
+#pragma unroll
+            for (int j = 0; j < E; ++j) {
+                h[lane_c * E + j] = off;
+                if ((lane_c * E + j) % NW == 0) s_boff[(lane_c * E + j) / NW] = off;
+                off += c[j];
+            }
+            if (lane_c == 31) s_boff[TILE_NB] = off;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+            const uint32_t u = (r0 + k * RSTEP) * TX + lx;
+            const uint32_t o = ord[u];
+            if (o != ABSENT) vlist[s_hist[(o - omin) >> sh][warp_d] + rank[k]] = uint16_t(u);
+        }
+    }
+    __syncthreads();
+    // bucket by bucket: A. keep the down-edges of the bucket's vertices whose basins the
+    // union-find (kept edges of the lower buckets) does not join yet; B. unite them
+#pragma unroll 1
+    for (int bk = 0; bk < TILE_NB && (TILE_STOP == 0 || TILE_STOP > 2); ++bk) {
+        const uint32_t vb = s_boff[bk], ve = s_boff[bk + 1];
+        if (vb == ve) continue;                               // (uniform)
+        const uint32_t kb = s_nkept;
+        for (uint32_t i = vb + threadIdx.x; i < ve; i += THREADS) {
+            const uint32_t u = vlist[i];
+            const uint32_t ou = ord[u];
+            const uint32_t bu = basin(u);
+            const uint32_t ux = u % TX, uy = (u / TX) % TY, uz = u / (TX * TY);
+            uint32_t ru = 0xffffu;
+            auto down = [&](bool ok, uint32_t w, bool lower_id) {
+                if (!ok) return;
+                const uint32_t ow = ord[w];
+                if (ow == ABSENT || !(ow < ou || (ow == ou && lower_id))) return;   // not below u
+                const uint32_t bw = basin(w);
+                if (bw == bu) return;
+                if (STATS) ++n_edges;
+                if (ru == 0xffffu) ru = uf_find(uf, bu);
+                if (uf_find(uf, bw) == ru) return;            // joined below this bucket: redundant
+                const uint32_t j = atomicAdd(&s_nkept, 1u);
+                if (j < TILE_KCAP) kept[j] = (u << 16) | w;
+                else s_overflow = 1;
+            };
+            down(uz > 0, u - TX * TY, true);
+            down(uy > 0, u - TX, true);
+            down(ux > 0, u - 1, true);
+            down(ux + 1 < TX, u + 1, false);
+            down(uy + 1 < TY, u + TX, false);
+            down(uz + 1 < TZ, u + TX * TY, false);
+        }
+        __syncthreads();
+        const uint32_t ke = min(s_nkept, uint32_t(TILE_KCAP));
+        for (uint32_t j = kb + threadIdx.x; j < ke; j += THREADS) {
+            const uint32_t e = kept[j];
+            uf_union(uf, ord, basin(e >> 16), basin(e & 0xffffu));
+        }
+        __syncthreads();
+    }
+    phase_time(ST_CYC_LIST);
+    const uint32_t n_kept = min(s_nkept, uint32_t(TILE_KCAP));
+    // this warp's slice of the kept edges
+    const uint32_t run_b = uint32_t(uint64_t(n_kept) * warp_d / NW);
+    const uint32_t run_len = uint32_t(uint64_t(n_kept) * (warp_d + 1) / NW) - run_b;
+    auto run_edge = [&](uint32_t j, uint32_t* mu, uint32_t* mv, uint64_t* S) {
+        const uint32_t e = kept[run_b + j];
+        const uint32_t hi = e >> 16;
+        *mu = basin(hi);
+        *mv = basin(e & 0xffffu);
+        *S = key48(ord, hi);
+    };
+#else
     // ---- c. one edge per pair of adjacent basins: the lowest --------------------------------
     // Between two basins A and B only the lowest edge matters: any other A-B edge at level
     // L' joins vertices that are already connected at L' through their descent paths and
     // that lowest edge (DESIGN.md derivation C'').  A shared-memory hash table keyed by the
     // basin pair keeps, per pair, the edge's upper endpoint of lowest key.
-    const int lane_c = threadIdx.x & 31;
-    // keep, per basin pair, the edge of lowest level (entry = pair << 12 | upper endpoint)
     auto insert_entry = [&](uint64_t entry) {
         const uint32_t pair = uint32_t(entry >> 12);
         const uint64_t kh = key48(ord, uint32_t(entry) & 0xfffu);
@@ -285,16 +469,13 @@ tile_tmt_kernel(const float* __restrict__ f, Cell* __restrict__ C, uint64_t* __r
             if (uint32_t(cur >> 12) != pair) {
                 h = h + 1 == uint32_t(TABLE) ? 0u : h + 1;
                 if (++probe < uint32_t(TABLE)) continue;
-                // table full (e.g. a checkerboard: every vertex pair of basins is adjacent):
-                // record the edge in the overflow flag; phase d' merges all edges then
-                s_overflow = 1;
+                s_overflow = 1;                                  // table full: merge every edge
                 break;
             }
             if (kh >= key48(ord, uint32_t(cur) & 0xfffu)) break;  // the stored edge is lower
             if (scas64(table + h, cur, entry) == cur) break;
         }
     };
-    // the in-tile edge (u, w) in direction d (+x, +y, +z) if its ends lie in two basins
     auto candidate = [&](uint32_t u, uint32_t ou, uint32_t bu, bool ok, uint32_t off, uint64_t* entry) {
         if (ou == ABSENT || !ok) return false;
         const uint32_t w = u + off;
@@ -309,12 +490,8 @@ tile_tmt_kernel(const float* __restrict__ f, Cell* __restrict__ C, uint64_t* __r
         *entry = (uint64_t(pair) << 12) | hi | (uint64_t((u_hi ? bu : bw) == (bu < bw ? bu : bw)) << 63);
         return true;
     };
-#if LIST_STAGE
-    // each warp lists the edges of its own rows into a 128-entry staging buffer (ballot +
-    // popc) and inserts them 32 at a time, so the insert code runs with every lane busy
-    // (about 40 % of the in-tile edges join two basins)
     if (TILE_STOP == 0 || TILE_STOP > 2) {
-        uint64_t* stage = reinterpret_cast<uint64_t*>(smem + NV * 12 + TABLE * 8) + (threadIdx.x >> 5) * 128;
+        uint64_t* stage = reinterpret_cast<uint64_t*>(smem + NV * 12 + TABLE * 8) + warp_d * 128;
         const uint32_t lt = (1u << lane_c) - 1u;
         uint32_t nst = 0;
 #pragma unroll 1
@@ -329,7 +506,23 @@ tile_tmt_kernel(const float* __restrict__ f, Cell* __restrict__ C, uint64_t* __r
 #pragma unroll
             for (int d = 0; d < 3; ++d) {
                 uint64_t entry = 0;
-                const bool valid = candidate(u, ou, bu, ok[d], off[d], &entry);
+                bool valid = candidate(u, ou, bu, ok[d], off[d], &entry);
+#if TILE_NDEDUP
+                if (d > 0) {
+                    // +y / +z edges of consecutive lanes run along a basin boundary: an edge whose
+                    // left or right lane holds an edge of the same basin pair at a lower level is
+                    // redundant (derivation C''), so it is not inserted at all
+                    const uint32_t pr = valid ? uint32_t(entry >> 12) & 0xffffffu : 0xffffffffu;
+                    const uint32_t hi = uint32_t(entry) & 0xfffu;
+                    const uint32_t oh = valid ? ord[hi] : 0u;
+                    const uint32_t prl = __shfl_up_sync(FULL_MASK, pr, 1), prr = __shfl_down_sync(FULL_MASK, pr, 1);
+                    const uint32_t ohl = __shfl_up_sync(FULL_MASK, oh, 1), ohr = __shfl_down_sync(FULL_MASK, oh, 1);
+                    const uint32_t hil = __shfl_up_sync(FULL_MASK, hi, 1), hir = __shfl_down_sync(FULL_MASK, hi, 1);
+                    const bool lower_l = lane_c > 0 && prl == pr && (ohl < oh || (ohl == oh && hil < hi));
+                    const bool lower_r = lane_c < 31 && prr == pr && (ohr < oh || (ohr == oh && hir < hi));
+                    if (lower_l || lower_r) valid = false;
+                }
+#endif
                 const uint32_t m = __ballot_sync(FULL_MASK, valid);
                 if (valid) stage[nst + __popc(m & lt)] = entry;
                 nst += __popc(m);
@@ -345,92 +538,13 @@ tile_tmt_kernel(const float* __restrict__ f, Cell* __restrict__ C, uint64_t* __r
         }
         if (uint32_t(lane_c) < nst) insert_entry(stage[lane_c]);
     }
-#else
-    // rows of 32 vertices are handed out dynamically (a warp per row) so that warps with
-    // contended inserts do not hold the barrier for the others
-#pragma unroll 1
-    while (TILE_STOP == 0 || TILE_STOP > 2) {
-        int r = 0;
-        if (lane_c == 0) r = int(atomicAdd(&s_row, 1u));
-        r = __shfl_sync(FULL_MASK, r, 0);
-        if (r >= ROWS) break;
-        const int ly = r % TY, lz = r / TY;
-        const uint32_t u = r * TX + lx;
-        const uint32_t ou = ord[u];
-        const uint32_t bu = c_v(cell[u]);      // basin (a minimum points at itself)
-        const bool ok[3] = {lx + 1 < TX, ly + 1 < TY, lz + 1 < TZ};
-        const uint32_t off[3] = {1u, uint32_t(TX), uint32_t(TX * TY)};
-#pragma unroll
-        for (int d = 0; d < 3; ++d) {
-            uint64_t entry = 0;
-            if (!candidate(u, ou, bu, ok[d], off[d], &entry)) continue;
-            if (STATS) ++n_edges;
-            insert_entry(entry);
-        }
-    }
-#endif
     __syncthreads();
     phase_time(ST_CYC_LIST);
-
-    // ---- d. merge one edge per basin pair ------------------------------------------------
-    // join basins bh (the one holding the edge's upper endpoint) and bl at level L
-    auto merge_at = [&](uint32_t bh, uint32_t bl, uint64_t L) {
-        uint32_t rr[2];
-#pragma unroll
-        for (int side = 0; side < 2; ++side) {           // walks at level L with path splitting
-            uint32_t x = side == 0 ? bh : bl;
-            uint64_t c = sld64(cell + x);
-            uint32_t xp = x;
-            uint64_t cp = 0;
-            bool has_prev = false;
-            while (c_v(c) != x && c_key(c) <= L) {
-                if (TILE_SPLIT && has_prev && c_key(c) <= c_key(cp))
-                    scas64(cell + xp, cp, (cp & ~0xffffull) | c_v(c));
-                xp = x;
-                cp = c;
-                has_prev = true;
-                x = c_v(c);
-                c = sld64(cell + x);
-                if (STATS) ++n_hops;
-            }
-            rr[side] = x;
-        }
-        if (rr[0] == rr[1]) return;
-        uint32_t mu = rr[0], mv = rr[1];
-        uint64_t S = L;
-        while (true) {                                    // Alg. 3
-            if (STATS) ++n_iters;
-            const uint64_t cu = sld64(cell + mu), cv = sld64(cell + mv);
-            if (c_v(cu) != mu && c_key(cu) < S) { mu = c_v(cu); continue; }   // l.2-4 + R4
-            if (c_v(cv) != mv && c_key(cv) < S) { mv = c_v(cv); continue; }   // l.5-8 + R4
-            if (mu == mv) break;                                                // l.9-10
-            uint32_t uu = mu, vv = mv;
-            uint64_t cvv = cv;
-            if (key48(ord, mv) < key48(ord, mu)) { uu = mv; vv = mu; cvv = cu; }  // l.11-12
-            if (scas64(cell + vv, cvv, (S << 16) | uu) == cvv) {               // l.14
-                if (c_v(cvv) == vv) break;                                      // R5
-                mu = uu;                                                        // l.15
-                S = c_key(cvv);
-                mv = c_v(cvv);
-            } else {
-                mu = uu;                                                        // l.17
-                mv = vv;
-            }
-        }
-    };
-    // basin of x: a regular cell (s = x) is static and points at the minimum
-    auto basin = [&](uint32_t x) {
-        const uint64_t c = sld64(cell + x);
-        return c_s(c) == x ? c_v(c) : x;
-    };
-    // d0. most table slots are empty (c5: ~1200 pairs in 8192 slots): every warp compacts
-    // its 1/NW of the table in place (a chunk of 32 slots is read before any of its lanes
-    // writes, and a write never lands past the chunk being read), then the pairs are handed
-    // out one per fetch from a CTA counter over the concatenated runs, so that every
-    // fetch yields a pair and every lane of a warp works on one
-    constexpr int NW = THREADS / 32, REG = TABLE / NW;
-    const int warp_d = threadIdx.x >> 5;
-    uint64_t* const run = table + warp_d * REG;          // this warp's run of pairs
+    // most table slots are empty: every warp compacts its 1/NW of the table in place (a chunk of
+    // 32 slots is read before any of its lanes writes, and a write never lands past the chunk
+    // being read); the warp then merges the pairs of its own run
+    constexpr int REG = TABLE / NW;
+    uint64_t* const run = table + warp_d * REG;
     uint32_t run_len = 0;
 #pragma unroll 4
     for (int c = 0; c < REG; c += 32) {
@@ -440,192 +554,95 @@ tile_tmt_kernel(const float* __restrict__ f, Cell* __restrict__ C, uint64_t* __r
         if (e != EMPTY) run[run_len + __popc(m & ((1u << lane_c) - 1u))] = e;
         run_len += __popc(m);
     }
-    if (TILE_STOP != 0 && TILE_STOP <= 3) run_len = 0;
-#if !TILE_OWNRUN
-    if (lane_c == 0) s_wcnt[warp_d] = run_len;
-    __syncthreads();
-    if (threadIdx.x < 32) {     // exclusive prefix of the NW run lengths
-        const uint32_t c = threadIdx.x < NW ? s_wcnt[threadIdx.x] : 0u;
-        uint32_t incl = c;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t t = __shfl_up_sync(FULL_MASK, incl, o);
-            if (lane_c >= o) incl += t;
-        }
-        if (threadIdx.x <= NW) s_wpre[threadIdx.x] = incl - c;
-    }
-    __syncthreads();
-#endif
-#if !TILE_OWNRUN
-    const uint32_t n_listed = s_wpre[NW];
-    auto listed = [&](uint32_t j) {                       // pair j of the concatenated runs
-        int w = 0;                                        // (binary search over the run starts)
-#pragma unroll
-        for (int step = NW / 2; step > 0; step >>= 1)
-            if (s_wpre[w + step] <= j) w += step;
-        return table[w * REG + (j - s_wpre[w])];
+    auto run_edge = [&](uint32_t j, uint32_t* mu, uint32_t* mv, uint64_t* S) {
+        const uint64_t e = run[j];
+        const uint32_t pair = uint32_t(e >> 12) & 0xffffffu, hi = uint32_t(e) & 0xfffu;
+        const uint32_t ba = pair >> 12, bb = pair & 0xfffu;
+        const bool first = e >> 63;
+        *mu = first ? ba : bb;
+        *mv = first ? bb : ba;
+        *S = key48(ord, hi);
     };
 #endif
-#if TILE_LEAN
-    // d1. Alg. 3 per lane, one iteration (the two cell loads, + the CAS) per loop iteration; a
-    // lane whose pair is done takes the next pair of the warp's run at the top of the next
-    // iteration (ballot + popc), so the lanes of a warp stay busy and converged instead of
-    // waiting for the longest merge of the warp.  Merge(T, bh, hi, bl) starts straight from
-    // the two basins (bh holds the edge's upper endpoint hi, level L = key(hi)).
-    bool busy = false;
-    uint64_t S = 0;
-    uint32_t mu = 0, mv = 0, run_pos = 0;
+
+    // ---- d. merge: Alg. 3 per lane --------------------------------------------------------
+    // One iteration (the two cell loads, + the CAS) per loop iteration; a lane whose edge is done
+    // takes the next edge of the warp's slice at the top of the next iteration (ballot + popc),
+    // so the lanes of a warp stay busy and converged instead of waiting for the longest merge of
+    // the warp.  Merge(T, bh, hi, bl) starts straight from the two basins (bh holds the edge's
+    // upper endpoint hi, level L = key(hi)).
+    {
+        bool busy = false;
+        uint64_t S = 0;
+        uint32_t mu = 0, mv = 0, run_pos = 0;
+        const uint32_t run_n = (TILE_STOP == 0 || TILE_STOP > 3) ? run_len : 0u;
 #pragma unroll 1
-    while (true) {
-        const uint32_t need = __ballot_sync(FULL_MASK, !busy);
-        if (need) {
-            if (!busy) {
-                const uint32_t j = run_pos + __popc(need & ((1u << lane_c) - 1u));
-                if (j < run_len) {
-                    const uint64_t e = run[j];
-                    if (STATS) ++n_pairs;
-                    const uint32_t pair = uint32_t(e >> 12) & 0xffffffu, hi = uint32_t(e) & 0xfffu;
-                    const uint32_t ba = pair >> 12, bb = pair & 0xfffu;
-                    const bool first = e >> 63;
-                    mu = first ? ba : bb;
-                    mv = first ? bb : ba;
-                    S = key48(ord, hi);
-                    busy = true;
+        while (true) {
+            const uint32_t need = __ballot_sync(FULL_MASK, !busy);
+            if (need) {
+                if (!busy) {
+                    const uint32_t j = run_pos + __popc(need & ((1u << lane_c) - 1u));
+                    if (j < run_n) {
+                        if (STATS) ++n_pairs;
+                        run_edge(j, &mu, &mv, &S);
+                        busy = true;
+                    }
                 }
+                run_pos += __popc(need);
             }
-            run_pos += __popc(need);
-        }
-        if (!__any_sync(FULL_MASK, busy)) break;
-        if (busy) {
-            if (STATS) ++n_iters;
-            const uint64_t cu = sld64(cell + mu), cv = sld64(cell + mv);
-            if (c_v(cu) != mu && c_key(cu) < S) {         // l.2-4 + R4
-                mu = c_v(cu);
-            } else if (c_v(cv) != mv && c_key(cv) < S) {  // l.5-8 + R4
-                mv = c_v(cv);
-            } else if (mu == mv) {                        // l.9-10
-                busy = false;
-            } else {
-                uint32_t uu = mu, vv = mv;
-                uint64_t cvv = cv;
-                if (key48(ord, mv) < key48(ord, mu)) { uu = mv; vv = mu; cvv = cu; }   // l.11-12
-                const uint64_t got = scas64(cell + vv, cvv, (S << 16) | uu);          // l.14
-                mu = uu;
-                if (got == cvv) {
-                    if (c_v(cvv) == vv) busy = false;      // R5: displaced a root
-                    S = c_key(cvv);                       // l.15: Merge(T, u, s_v, v')
-                    mv = c_v(cvv);
+            if (!__any_sync(FULL_MASK, busy)) break;
+            if (busy) {
+                if (STATS) ++n_iters;
+                const uint64_t cu = sld64(cell + mu), cv = sld64(cell + mv);
+                if (c_v(cu) != mu && c_key(cu) < S) {         // l.2-4 + R4
+                    mu = c_v(cu);
+                } else if (c_v(cv) != mv && c_key(cv) < S) {  // l.5-8 + R4
+                    mv = c_v(cv);
+                } else if (mu == mv) {                        // l.9-10
+                    busy = false;
                 } else {
-                    mv = vv;                              // l.17: restart
+                    uint32_t uu = mu, vv = mv;
+                    uint64_t cvv = cv;
+                    if (key48(ord, mv) < key48(ord, mu)) { uu = mv; vv = mu; cvv = cu; }   // l.11-12
+                    const uint64_t got = scas64(cell + vv, cvv, (S << 16) | uu);          // l.14
+                    mu = uu;
+                    if (got == cvv) {
+                        if (c_v(cvv) == vv) busy = false;      // R5: displaced a root
+                        S = c_key(cvv);                       // l.15: Merge(T, u, s_v, v')
+                        mv = c_v(cvv);
+                    } else {
+                        mv = vv;                              // l.17: restart
+                    }
                 }
             }
         }
     }
-#else
-    // d1. one state machine per lane, advanced by one shared-memory round trip per loop
-    // iteration (a walk step, the pair of Alg. 3 loads (+ CAS)); a lane whose pair is done
-    // takes the next listed pair at the top of the next iteration, so the lanes of a warp
-    // stay busy and converged instead of waiting for the longest merge of the warp
-    enum { P_IDLE = 0, P_W0 = 1, P_W1 = 2, P_A3 = 3, P_DONE = 4 };
-    int ph = P_IDLE;
-    uint64_t L = 0, S = 0, cp = 0;
-    uint32_t x = 0, xp = 0, lo = 0, r0v = 0, mu = 0, mv = 0;
-    bool has_prev = false;
-    uint32_t run_pos = 0;
-#pragma unroll 1
-    while (true) {
-#if TILE_OWNRUN
-        // the warp's own run is its pool: idle lanes take the next pairs in lane order
-        const uint32_t need = __ballot_sync(FULL_MASK, ph == P_IDLE);
-        if (need) {
-            if (ph == P_IDLE) {
-                const uint32_t j = run_pos + __popc(need & ((1u << lane_c) - 1u));
-                if (j < run_len) {
-                    const uint64_t e = run[j];
-#else
-        if (ph == P_IDLE) {
-            {
-                const uint32_t j = atomicAdd(&s_fetch, 1u);
-                if (j < n_listed) {
-                    const uint64_t e = listed(j);
-#endif
-                    if (STATS) ++n_pairs;
-                    const uint32_t pair = uint32_t(e >> 12), hi = uint32_t(e) & 0xfffu;
-                    const uint32_t ba = pair >> 12, bb = pair & 0xfffu;
-                    const uint32_t bh = basin(hi);
-                    L = key48(ord, hi);                   // join bh and the other basin at level L
-                    x = bh;
-                    lo = bh == ba ? bb : ba;
-                    has_prev = false;
-                    ph = P_W0;
-                    if (!TILE_WALK) {                     // Merge(T, bh, hi, bl) straight away
-                        mu = bh;
-                        mv = lo;
-                        S = L;
-                        ph = P_A3;
-                    }
-                } else {
-                    ph = P_DONE;
-                }
-            }
-#if TILE_OWNRUN
-            run_pos += __popc(need);
-#endif
-        }
-        if (__all_sync(FULL_MASK, ph == P_DONE)) break;
-        if (ph == P_W0 || ph == P_W1) {                   // walks at level L with path splitting
-            const uint64_t c = sld64(cell + x);
-            if (c_v(c) != x && c_key(c) <= L) {
-                if (TILE_SPLIT && has_prev && c_key(c) <= c_key(cp))
-                    scas64(cell + xp, cp, (cp & ~0xffffull) | c_v(c));
-                xp = x;
-                cp = c;
-                has_prev = true;
-                x = c_v(c);
-                if (STATS) ++n_hops;
-            } else if (ph == P_W0) {
-                r0v = x;
-                x = lo;
-                has_prev = false;
-                ph = P_W1;
-            } else if (x == r0v) {
-                ph = P_IDLE;                              // joined below L already
-            } else {
-                mu = r0v;
-                mv = x;
-                S = L;
-                ph = P_A3;
-            }
-        } else if (ph == P_A3) {                          // Alg. 3, one iteration
-            if (STATS) ++n_iters;
-            const uint64_t cu = sld64(cell + mu), cv = sld64(cell + mv);
-            if (c_v(cu) != mu && c_key(cu) < S) {         // l.2-4 + R4
-                mu = c_v(cu);
-            } else if (c_v(cv) != mv && c_key(cv) < S) {  // l.5-8 + R4
-                mv = c_v(cv);
-            } else if (mu == mv) {                        // l.9-10
-                ph = P_IDLE;
-            } else {
+    __syncthreads();
+    if (s_overflow) {  // (uniform) kept edges / table entries were dropped: merge every edge
+        // Merge(T, bh, hi, bl) at level L for every in-tile edge between two basins, one edge at a
+        // time per thread (Alg. 3 accepts the edges in any order, redundant ones included)
+        auto merge_at = [&](uint32_t bh, uint32_t bl, uint64_t L) {
+            uint32_t mu = bh, mv = bl;
+            uint64_t S = L;
+            while (true) {                                    // Alg. 3
+                const uint64_t cu = sld64(cell + mu), cv = sld64(cell + mv);
+                if (c_v(cu) != mu && c_key(cu) < S) { mu = c_v(cu); continue; }   // l.2-4 + R4
+                if (c_v(cv) != mv && c_key(cv) < S) { mv = c_v(cv); continue; }   // l.5-8 + R4
+                if (mu == mv) break;                                                // l.9-10
                 uint32_t uu = mu, vv = mv;
                 uint64_t cvv = cv;
-                if (key48(ord, mv) < key48(ord, mu)) { uu = mv; vv = mu; cvv = cu; }   // l.11-12
-                if (scas64(cell + vv, cvv, (S << 16) | uu) == cvv) {                  // l.14
-                    if (c_v(cvv) == vv) {
-                        ph = P_IDLE;                      // R5
-                    } else {
-                        mu = uu;                          // l.15
-                        S = c_key(cvv);
-                        mv = c_v(cvv);
-                    }
+                if (key48(ord, mv) < key48(ord, mu)) { uu = mv; vv = mu; cvv = cu; }  // l.11-12
+                if (scas64(cell + vv, cvv, (S << 16) | uu) == cvv) {               // l.14
+                    if (c_v(cvv) == vv) break;                                      // R5
+                    mu = uu;                                                        // l.15
+                    S = c_key(cvv);
+                    mv = c_v(cvv);
                 } else {
-                    mu = uu;                              // l.17
+                    mu = uu;                                                        // l.17
                     mv = vv;
                 }
             }
-        }
-    }
-#endif
-    if (s_overflow) {  // (uniform: written before the last barrier) the table dropped edges
+        };
 #pragma unroll 1
         for (int k = 0; k < PER; ++k) {
             const int r = r0 + k * RSTEP;
@@ -645,12 +662,11 @@ tile_tmt_kernel(const float* __restrict__ f, Cell* __restrict__ C, uint64_t* __r
                 merge_at(u_hi ? bu : bw, u_hi ? bw : bu, key48(ord, u_hi ? u : w));
             }
         }
+        __syncthreads();
     }
-    __syncthreads();
     phase_time(ST_CYC_MERGE);
 
     // ---- e. repair: every cell points at its representative (minimal tile store) -------
-#if TILE_REP_ILP
     // each thread walks its own 8 vertices in lock-step rounds (8 independent shared-memory
     // load chains in flight); the cells are final after the merge barrier and this phase only
     // reads them, so the representatives stay in registers and go straight to phase f
@@ -677,29 +693,6 @@ tile_tmt_kernel(const float* __restrict__ f, Cell* __restrict__ C, uint64_t* __r
             }
         }
     }
-#else
-#pragma unroll 1
-    while (TILE_STOP == 0 || TILE_STOP > 4) {
-        int rr = 0;
-        if ((threadIdx.x & 31) == 0) rr = int(atomicAdd(&s_row_e, 1u));
-        rr = __shfl_sync(FULL_MASK, rr, 0);
-        if (rr >= ROWS) break;
-        const uint32_t u = rr * TX + lx;
-        const uint64_t cu = cell[u];
-        const uint32_t v = c_v(cu);
-        if (v == u) continue;
-        const uint64_t a = c_key(cu);
-        uint32_t x = v;
-        while (true) {
-            const uint64_t cx = sld64(cell + x);
-            if (c_v(cx) == x || c_key(cx) > a) break;
-            x = c_v(cx);
-            if (STATS) ++n_rep;
-        }
-        if (x != v) sst64(cell + u, (cu & ~0xffffull) | x);
-    }
-    __syncthreads();
-#endif
     phase_time(ST_CYC_REPAIR);
 
     // ---- f. write the tile store T0 (8 B per vertex) and the tile minima's 16-byte cells ------
@@ -723,11 +716,7 @@ tile_tmt_kernel(const float* __restrict__ f, Cell* __restrict__ C, uint64_t* __r
         const uint32_t ou = ord[u];
         if (ou == ABSENT) continue;
         const uint64_t cu = cell[u];
-#if TILE_REP_ILP
         const uint32_t s = c_s(cu), v = rep[k];
-#else
-        const uint32_t s = c_s(cu), v = c_v(cu);
-#endif
         const uint64_t g = gbase + uint64_t(lz) * sxy + uint64_t(ly) * nx + lx;
         const uint32_t gu = uint32_t(g), gv = gid(v);
         const bool minimum = s != u || v == u;
@@ -741,9 +730,9 @@ tile_tmt_kernel(const float* __restrict__ f, Cell* __restrict__ C, uint64_t* __r
             xface[(uint64_t(b) * 2 + (lx == TX - 1)) * ROWS + r] = (uint64_t(ou) << 32) | (s == u ? gv : gu);
     }
     phase_time(ST_CYC_WRITE);
+    }   // pass
     if (STATS) {
         atomicAdd(stats + ST_TILE_EDGES, n_edges);
-        atomicAdd(stats + ST_TILE_HOPS, n_hops);
         atomicAdd(stats + ST_TILE_ITERS, n_iters);
         atomicAdd(stats + ST_TILE_REPAIR, n_rep);
         atomicAdd(stats + ST_TILE_COMPRESS, n_cmp);
@@ -777,23 +766,30 @@ void tile_shape(uint32_t nz_global, uint32_t* ty, uint32_t* tz) {
     }
 }
 
-template <int TY, int TZ>
-void launch_tile(const float* f, Cell* C, uint64_t* T0, uint64_t* xface, const Slab& sl, uint32_t tx, uint32_t tyn, uint32_t grid,
-                 uint32_t flip, unsigned long long* counters, unsigned long long* stats, cudaStream_t stream) {
+template <int TY, int TZ, bool STATS, bool DUAL>
+void launch_tile_v(const float* f, const TileOut& o0, const TileOut& o1, const Slab& sl, uint32_t tx, uint32_t tyn,
+                   uint32_t grid, uint32_t flip, unsigned long long* stats, cudaStream_t stream) {
     constexpr int NV = TX * TY * TZ;
-    ensure_smem_attr(reinterpret_cast<const void*>(tile_tmt_kernel<TY, TZ, false>), int(smem_bytes<NV>()));
-    ensure_smem_attr(reinterpret_cast<const void*>(tile_tmt_kernel<TY, TZ, true>), int(smem_bytes<NV>()));
-    if (stats)
-        tile_tmt_kernel<TY, TZ, true><<<grid, NV / 8, smem_bytes<NV>(), stream>>>(f, C, T0, xface, sl.nx, sl.ny,
-                                                                                 sl.z_begin, sl.z_end, tx, tyn,
-                                                                                 flip, counters, stats);
-    else
-        tile_tmt_kernel<TY, TZ, false><<<grid, NV / 8, smem_bytes<NV>(), stream>>>(f, C, T0, xface, sl.nx, sl.ny, sl.z_begin, sl.z_end, tx,
-                                                                       tyn, flip, counters, stats);
+    auto kern = tile_tmt_kernel<TY, TZ, STATS, DUAL>;
+    ensure_smem_attr(reinterpret_cast<const void*>(kern), int(smem_bytes<NV>()));
+    kern<<<grid, NV / 8, smem_bytes<NV>(), stream>>>(f, o0, o1, sl.nx, sl.ny, sl.z_begin, sl.z_end, tx, tyn, flip,
+                                                     stats);
 }
 
-void launch_tile_tmt(const float* f, Cell* C, uint64_t* T0, uint64_t* xface, const Slab& sl, uint32_t flip,
-                     unsigned long long* counters, unsigned long long* stats, cudaStream_t stream) {
+template <int TY, int TZ>
+void launch_tile(const float* f, const TileOut& o0, const TileOut* o1, const Slab& sl, uint32_t tx, uint32_t tyn,
+                 uint32_t grid, uint32_t flip, unsigned long long* stats, cudaStream_t stream) {
+    if (o1) {
+        if (stats) launch_tile_v<TY, TZ, true, true>(f, o0, *o1, sl, tx, tyn, grid, 0u, stats, stream);
+        else launch_tile_v<TY, TZ, false, true>(f, o0, *o1, sl, tx, tyn, grid, 0u, stats, stream);
+    } else {
+        if (stats) launch_tile_v<TY, TZ, true, false>(f, o0, o0, sl, tx, tyn, grid, flip, stats, stream);
+        else launch_tile_v<TY, TZ, false, false>(f, o0, o0, sl, tx, tyn, grid, flip, stats, stream);
+    }
+}
+
+void launch_tile_any(const float* f, const TileOut& o0, const TileOut* o1, const Slab& sl, uint32_t flip,
+                     unsigned long long* stats, cudaStream_t stream) {
     uint32_t ty, tz;
     tile_shape(sl.nz, &ty, &tz);
     const uint32_t nzl = sl.z_end - sl.z_begin;
@@ -802,13 +798,26 @@ void launch_tile_tmt(const float* f, Cell* C, uint64_t* T0, uint64_t* xface, con
     if (grid == 0) return;
     const bool big = tile_vertices() == 4096;
     if (sl.nz == 1 && big)
-        launch_tile<128, 1>(f, C, T0, xface, sl, tx, tyn, grid, flip, counters, stats, stream);
+        launch_tile<128, 1>(f, o0, o1, sl, tx, tyn, grid, flip, stats, stream);
     else if (sl.nz == 1)
-        launch_tile<64, 1>(f, C, T0, xface, sl, tx, tyn, grid, flip, counters, stats, stream);
+        launch_tile<64, 1>(f, o0, o1, sl, tx, tyn, grid, flip, stats, stream);
     else if (big)
-        launch_tile<16, 8>(f, C, T0, xface, sl, tx, tyn, grid, flip, counters, stats, stream);
+        launch_tile<16, 8>(f, o0, o1, sl, tx, tyn, grid, flip, stats, stream);
     else
-        launch_tile<8, 8>(f, C, T0, xface, sl, tx, tyn, grid, flip, counters, stats, stream);
+        launch_tile<8, 8>(f, o0, o1, sl, tx, tyn, grid, flip, stats, stream);
+}
+
+void launch_tile_tmt(const float* f, Cell* C, uint64_t* T0, uint64_t* xface, const Slab& sl, uint32_t flip,
+                     unsigned long long* counters, unsigned long long* stats, cudaStream_t stream) {
+    launch_tile_any(f, TileOut{C, T0, xface, counters}, nullptr, sl, flip, stats, stream);
+}
+
+void launch_tile_tmt_dual(const float* f, Cell* C_join, uint64_t* T0_join, uint64_t* xface_join,
+                          unsigned long long* counters_join, Cell* C_split, uint64_t* T0_split,
+                          uint64_t* xface_split, unsigned long long* counters_split, const Slab& sl,
+                          unsigned long long* stats, cudaStream_t stream) {
+    const TileOut o1{C_split, T0_split, xface_split, counters_split};
+    launch_tile_any(f, TileOut{C_join, T0_join, xface_join, counters_join}, &o1, sl, 0u, stats, stream);
 }
 
 }  // namespace mt

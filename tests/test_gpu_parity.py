@@ -327,3 +327,20 @@ def test_full_size_c5_sampled():
             assert recs[k]["birth"].tobytes() == f[u].tobytes() and recs[k]["death"].tobytes() == f[r[0]].tobytes()
         checked[lab] = checked.get(lab, 0) + 1
     log(f"all {picks.size} stratified samples checked against O4: {checked}")
+
+
+@pytest.mark.parametrize("cfg,scale", [("c1", None), ("c4", 64), ("c5", 96), ("c3", 48), ("c2", 512)])
+def test_join_and_split_from_one_read(cfg, scale):
+    """f1: mt_compute_join_split reads f once (one tile pass, two tile stores) and gives the merge
+    tree of f and the split tree (merge tree of -f, ids still ascending: reading R16) -- each
+    bit-exact against O1 with and without the split flag, diagrams included."""
+    f, dims, conn = fields.make(cfg, scale=scale)
+    a = _lib.MergeTree(dims, conn, device=0)
+    b = _lib.MergeTree(dims, conn, device=0)
+    tj, ts = _lib.join_split(a, b, torch.from_numpy(f).cuda())
+    for mt, T, split in ((a, tj, False), (b, ts, True)):
+        rec, npairs, ness = mt.diagram()
+        To, po, npo, neo = oracle.merge_tree(f, dims, conn=conn, split=split)
+        assert np.array_equal(T.cpu().numpy().view(np.uint64), To), split
+        assert (npairs, ness) == (npo, neo)
+        assert _lib.pairs_to_numpy(rec).tobytes() == po.tobytes()
