@@ -218,7 +218,7 @@ mt_status mt_compute_global(mt_ctx *ctx, const mt_forest_record *all, uint64_t n
  * 6, 1 <= nranks <= min(64, nz). */
 mt_status mt_get_unique_id(uint8_t id[128]);
 /* bounds (host, nranks + 1): the planes of each rank's slab -- as equal as
- * possible, on multiples of 8 (the tile depth) when nz >= 8 nranks. */
+ * possible, on multiples of the tile depth (8) when nz >= 8 nranks. */
 mt_status mt_dist_slab_bounds(uint32_t nz, int nranks, uint32_t *bounds);
 size_t mt_dist_workspace_bytes(const uint32_t global_dims[3], int conn, int rank, int nranks);
 mt_status mt_create_dist(mt_ctx **out, const uint32_t global_dims[3], int conn, int rank, int nranks,

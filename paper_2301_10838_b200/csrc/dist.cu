@@ -81,11 +81,13 @@ struct DistState {
     size_t scratch_cap = 0;
 };
 
-// z boundaries of the slabs: as equal as possible, on multiples of the tile depth (8) when the
+// z boundaries of the slabs: as equal as possible, on multiples of the tile depth when the
 // grid allows it (the cut faces are then tile faces), every slab at least one plane
 bool slab_bounds(uint32_t nz, int nranks, uint32_t* b) {
     if (nranks < 1 || nranks > MAX_SLABS || uint32_t(nranks) > nz) return false;
-    const uint64_t align = nz >= uint64_t(nranks) * 8 ? 8 : 1, P = uint64_t(nranks);
+    uint32_t ty = 0, tz = 0;
+    tile_shape(nz, &ty, &tz);
+    const uint64_t P = uint64_t(nranks), align = nz >= P * tz ? tz : 1;
     b[0] = 0;
     for (uint64_t k = 1; k < P; ++k) {
         uint64_t z = (2 * k * nz + P * align) / (2 * P * align) * align;   // round half up

@@ -267,6 +267,9 @@ dedupe_cross_kernel(const float* __restrict__ f, const uint64_t* __restrict__ T0
 #ifndef MQ_SPLIT
 #define MQ_SPLIT 1        // merge_queue walks: 1 path splitting, 2 path halving (128-bit CAS), 0 none
 #endif
+#ifndef MQ_BOTHCLIMB
+#define MQ_BOTHCLIMB 1    // Alg. 3 step: climb u and v in the same round trip when both can climb
+#endif
 #ifndef MQ_WALK
 #define MQ_WALK 1         // filter walks (with path splitting) before Alg. 3
 #endif
@@ -371,9 +374,14 @@ merge_queue_kernel(Cell* C, const QEntry* __restrict__ q, uint64_t cap, const un
             }
         } else if (phase == MERGE_LD) {
             if (STATS) n_iters++;
-            if (cv_of(cu) != u && cu.lo < ks) {        // l.2-4 (+ R4): climb u, restart
+            const bool up_u = cv_of(cu) != u && cu.lo < ks;   // l.2-4 (+ R4)
+            const bool up_v = cv_of(cv) != v && cv.lo < ks;   // l.5-8 (+ R4)
+            if (MQ_BOTHCLIMB && (up_u || up_v)) {             // independent climbs: both advance
+                if (up_u) u = cv_of(cu);
+                if (up_v) v = cv_of(cv);
+            } else if (up_u) {                         // climb u, restart
                 u = cv_of(cu);
-            } else if (cv_of(cv) != v && cv.lo < ks) { // l.5-8 (+ R4): climb v, restart
+            } else if (up_v) {                         // climb v, restart
                 v = cv_of(cv);
             } else if (u == v) {                       // l.9-10
                 phase = IDLE;

@@ -36,6 +36,12 @@ namespace {
 #ifndef MT_REPAIR_NC
 #define MT_REPAIR_NC 1      // the repair reads cells no thread writes: L1-cached non-coherent loads
 #endif
+#ifndef MT_REPAIR_SEQ
+#define MT_REPAIR_SEQ 0     // walks one after the other (else lock-step rounds over the thread's vertices)
+#endif
+#ifndef MT_REPAIR_SKIPW
+#define MT_REPAIR_SKIPW 0   // tiled: no store for a tile-regular vertex whose T0 is already final
+#endif
 #ifndef MT_REPAIR_MINB
 #define MT_REPAIR_MINB 3    // __launch_bounds__ min blocks per SM (register budget knob)
 #endif
@@ -283,7 +289,26 @@ repair_brick_kernel(View view, const Cell* C, uint64_t* __restrict__ T, const fl
 
     // Rep(u, key(s)): walk from v through cells with key(s') <= key(s) that are not roots
     unsigned long long hops = 0;
-    // the thread's 8 walks advance in lock-step rounds: 8 independent load chains in flight
+    uint32_t moved = 0;       // rows whose walk left its start (bit k)
+#if MT_REPAIR_SEQ
+    // one walk after the other (the loop runs the sum of the chain lengths, not RB_PER times
+    // the longest)
+#pragma unroll
+    for (int k = 0; k < RB_PER; ++k) {
+        if (!INB(k) || xs[k] == uint32_t(UID(k))) continue;
+        uint32_t x = xs[k];
+#pragma unroll 1
+        while (true) {
+            const Cell c = view.cell(C, x);
+            if (cv_of(c) == x || c.lo > key[k]) break;   // Alg. 4, reading R20
+            x = cv_of(c);
+            ++hops;
+        }
+        moved |= uint32_t(x != xs[k]) << k;
+        xs[k] = x;
+    }
+#else
+    // the thread's walks advance in lock-step rounds: independent load chains in flight
     uint32_t act = 0;
 #pragma unroll
     for (int k = 0; k < RB_PER; ++k)
@@ -298,13 +323,17 @@ repair_brick_kernel(View view, const Cell* C, uint64_t* __restrict__ T, const fl
                 act &= ~(1u << k);
             } else {
                 xs[k] = cv_of(c);
+                moved |= 1u << k;
                 ++hops;
             }
         }
     }
+#endif
+    // a tile-regular vertex whose walk stayed at its tile representative keeps T0 = (u, R)
+    const uint32_t keep = (TILED && MT_REPAIR_SKIPW) ? ~(moved | mins) : 0u;
 #pragma unroll
     for (int k = 0; k < RB_PER; ++k)
-        if (INB(k)) T[UID(k)] = pack(sv[k], xs[k]);
+        if (INB(k) && !((keep >> k) & 1u)) T[UID(k)] = pack(sv[k], xs[k]);
     if (stats && hops) atomicAdd(stats + ST_REPAIR_HOPS, hops);
 #undef UID
 #undef INB

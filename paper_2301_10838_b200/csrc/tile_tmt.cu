@@ -60,8 +60,14 @@ namespace {
 #ifndef TILE_MINB
 #define TILE_MINB 2    // __launch_bounds__ min blocks per SM (register budget knob)
 #endif
-#ifndef TILE_NDEDUP
-#define TILE_NDEDUP 0  // hash list: drop +y/+z edges whose neighbour lane has the same basin pair lower
+#ifndef TILE_BOTHCLIMB
+#define TILE_BOTHCLIMB 1  // Alg. 3 loop: climb u and v in the same iteration when both can climb
+#endif
+#ifndef TILE_ZRUN
+#define TILE_ZRUN 0    // hash list: a thread's z column keeps one edge per run of equal basin pairs
+#endif
+#ifndef TILE_VPT
+#define TILE_VPT 8     // vertices per thread (8: 512 threads per tile, 4: 1024)
 #endif
 #ifndef TILE_STOP
 #define TILE_STOP 0    // timing only (WRONG results): run phases < k: 1 load+descent, 2 +compress, 3 +list, 4 +merge
@@ -149,7 +155,7 @@ struct TileOut {
     unsigned long long* counters;
 };
 
-template <int TY, int TZ, bool STATS, bool DUAL, int NV = TX * TY * TZ, int THREADS = NV / 8,
+template <int TY, int TZ, bool STATS, bool DUAL, int NV = TX * TY * TZ, int THREADS = NV / TILE_VPT,
           int TABLE = table_slots(NV)>
 __global__ void __launch_bounds__(THREADS, TILE_MINB)
 tile_tmt_kernel(const float* __restrict__ f, TileOut out0, TileOut out1, uint32_t nx,
@@ -161,6 +167,9 @@ tile_tmt_kernel(const float* __restrict__ f, TileOut out0, TileOut out1, uint32_
     constexpr int RSTEP = THREADS / TX;         // 16 rows per pass
     constexpr int PER = ROWS / RSTEP;           // 8 vertices per thread
     constexpr int NW = THREADS / 32;
+    constexpr int LB = NV > 4096 ? 13 : 12;          // bits of a local vertex id
+    constexpr uint32_t LMASK = (1u << LB) - 1u, PMASK = (1u << (2 * LB)) - 1u;
+    static_assert(NV <= 8192, "local ids: 13 bits (and 16-bit cell fields)");
     extern __shared__ __align__(16) unsigned char smem[];
     uint64_t* cell = reinterpret_cast<uint64_t*>(smem);
     uint32_t* ord = reinterpret_cast<uint32_t*>(smem + NV * 8);
@@ -456,9 +465,13 @@ tile_tmt_kernel(const float* __restrict__ f, TileOut out0, TileOut out1, uint32_
     // L' joins vertices that are already connected at L' through their descent paths and
     // that lowest edge (DESIGN.md derivation C'').  A shared-memory hash table keyed by the
     // basin pair keeps, per pair, the edge's upper endpoint of lowest key.
+    // entry = orientation << 63 | top OB bits of ord(hi) << 3 LB | pair << LB | hi: the level is
+    // compared from the entries themselves, with a lookup of ord only on a tie of those bits
+    constexpr int OB = 63 - 3 * LB;
+    constexpr uint64_t OBMASK = (1ull << OB) - 1;
     auto insert_entry = [&](uint64_t entry) {
-        const uint32_t pair = uint32_t(entry >> 12);
-        const uint64_t kh = key48(ord, uint32_t(entry) & 0xfffu);
+        const uint32_t pair = uint32_t(entry >> LB) & PMASK;
+        const uint64_t mo = (entry >> (3 * LB)) & OBMASK;
         uint32_t h = pair_hash<TABLE>(pair);
         for (uint32_t probe = 0;;) {
             const uint64_t cur = sld64(table + h);
@@ -466,13 +479,15 @@ tile_tmt_kernel(const float* __restrict__ f, TileOut out0, TileOut out1, uint32_
                 if (scas64(table + h, EMPTY, entry) == EMPTY) break;
                 continue;                                        // lost the slot: re-read it
             }
-            if (uint32_t(cur >> 12) != pair) {
+            if ((uint32_t(cur >> LB) & PMASK) != pair) {
                 h = h + 1 == uint32_t(TABLE) ? 0u : h + 1;
                 if (++probe < uint32_t(TABLE)) continue;
                 s_overflow = 1;                                  // table full: merge every edge
                 break;
             }
-            if (kh >= key48(ord, uint32_t(cur) & 0xfffu)) break;  // the stored edge is lower
+            const uint64_t co = (cur >> (3 * LB)) & OBMASK;
+            if (mo > co) break;                                  // the stored edge is lower
+            if (mo == co && key48(ord, uint32_t(entry) & LMASK) >= key48(ord, uint32_t(cur) & LMASK)) break;
             if (scas64(table + h, cur, entry) == cur) break;
         }
     };
@@ -483,17 +498,43 @@ tile_tmt_kernel(const float* __restrict__ f, TileOut out0, TileOut out1, uint32_
         if (ow == ABSENT) return false;
         const uint32_t bw = c_v(cell[w]);
         if (bw == bu) return false;
-        const bool u_hi = ((uint64_t(ow) << 16) | w) < ((uint64_t(ou) << 16) | u);
-        const uint32_t hi = u_hi ? u : w;
-        const uint32_t pair = bu < bw ? (bu << 12) | bw : (bw << 12) | bu;
+        const bool u_hi = ow < ou;   // w = u + off has the larger id: on a tie w is the upper end
+        const uint32_t hi = u_hi ? u : w, oh = u_hi ? ou : ow;
+        const bool lo_first = bu < bw;
+        const uint32_t pair = lo_first ? (bu << LB) | bw : (bw << LB) | bu;
         // bit 63: the upper endpoint lies in the pair's first (smaller) basin
-        *entry = (uint64_t(pair) << 12) | hi | (uint64_t((u_hi ? bu : bw) == (bu < bw ? bu : bw)) << 63);
+        *entry = (uint64_t(u_hi == lo_first) << 63) | (uint64_t(oh >> (32 - OB)) << (3 * LB)) |
+                 (uint64_t(pair) << LB) | hi;
         return true;
     };
     if (TILE_STOP == 0 || TILE_STOP > 2) {
-        uint64_t* stage = reinterpret_cast<uint64_t*>(smem + NV * 12 + TABLE * 8) + warp_d * 128;
+        constexpr int STAGE = NV / (2 * NW);   // per-warp staging entries (>= 64: flushed per direction)
+        static_assert(STAGE >= 64, "staging buffer");
+        uint64_t* stage = reinterpret_cast<uint64_t*>(smem + NV * 12 + TABLE * 8) + warp_d * STAGE;
         const uint32_t lt = (1u << lane_c) - 1u;
         uint32_t nst = 0;
+        // append the lanes' valid entries to the warp's staging buffer; insert 32 at a time
+        auto stage_entry = [&](bool valid, uint64_t entry, bool flush_now) {
+            const uint32_t m = __ballot_sync(FULL_MASK, valid);
+            if (valid) stage[nst + __popc(m & lt)] = entry;
+            nst += __popc(m);
+            if (flush_now) {
+                __syncwarp();
+                while (nst >= 32) {
+                    const uint64_t e = stage[nst - 32 + lane_c];
+                    __syncwarp();
+                    nst -= 32;
+                    insert_entry(e);
+                }
+            }
+        };
+#if TILE_ZRUN
+        // a thread's 8 vertices are one z column: its consecutive +x (+y, +z) edges often cross
+        // the same basin boundary, so a run of edges of one basin pair keeps only its lowest edge
+        // in registers (derivation C'') and stages that one when the pair changes
+        uint64_t run_e[3] = {0, 0, 0};
+        uint32_t run_p[3] = {~0u, ~0u, ~0u}, run_o[3] = {0, 0, 0};
+#endif
 #pragma unroll 1
         for (int k = 0; k < PER; ++k) {
             const int r = r0 + k * RSTEP;
@@ -507,35 +548,38 @@ tile_tmt_kernel(const float* __restrict__ f, TileOut out0, TileOut out1, uint32_
             for (int d = 0; d < 3; ++d) {
                 uint64_t entry = 0;
                 bool valid = candidate(u, ou, bu, ok[d], off[d], &entry);
-#if TILE_NDEDUP
-                if (d > 0) {
-                    // +y / +z edges of consecutive lanes run along a basin boundary: an edge whose
-                    // left or right lane holds an edge of the same basin pair at a lower level is
-                    // redundant (derivation C''), so it is not inserted at all
-                    const uint32_t pr = valid ? uint32_t(entry >> 12) & 0xffffffu : 0xffffffffu;
-                    const uint32_t hi = uint32_t(entry) & 0xfffu;
-                    const uint32_t oh = valid ? ord[hi] : 0u;
-                    const uint32_t prl = __shfl_up_sync(FULL_MASK, pr, 1), prr = __shfl_down_sync(FULL_MASK, pr, 1);
-                    const uint32_t ohl = __shfl_up_sync(FULL_MASK, oh, 1), ohr = __shfl_down_sync(FULL_MASK, oh, 1);
-                    const uint32_t hil = __shfl_up_sync(FULL_MASK, hi, 1), hir = __shfl_down_sync(FULL_MASK, hi, 1);
-                    const bool lower_l = lane_c > 0 && prl == pr && (ohl < oh || (ohl == oh && hil < hi));
-                    const bool lower_r = lane_c < 31 && prr == pr && (ohr < oh || (ohr == oh && hir < hi));
-                    if (lower_l || lower_r) valid = false;
-                }
-#endif
-                const uint32_t m = __ballot_sync(FULL_MASK, valid);
-                if (valid) stage[nst + __popc(m & lt)] = entry;
-                nst += __popc(m);
                 if (STATS && valid) ++n_edges;
+#if TILE_ZRUN
+                bool out = false;
+                uint64_t oe = 0;
+                if (valid) {
+                    const uint32_t pr = uint32_t(entry >> LB) & PMASK, hi = uint32_t(entry) & LMASK;
+                    const uint32_t oh = hi == u ? ou : ord[hi];
+                    if (pr == run_p[d]) {
+                        const uint32_t rhi = uint32_t(run_e[d]) & LMASK;
+                        if (oh < run_o[d] || (oh == run_o[d] && hi < rhi)) {
+                            run_e[d] = entry;
+                            run_o[d] = oh;
+                        }
+                    } else {
+                        out = run_p[d] != ~0u;
+                        oe = run_e[d];
+                        run_p[d] = pr;
+                        run_e[d] = entry;
+                        run_o[d] = oh;
+                    }
+                }
+                stage_entry(out, oe, STAGE < 128);
+#else
+                stage_entry(valid, entry, STAGE < 128);
+#endif
             }
-            __syncwarp();
-            while (nst >= 32) {
-                const uint64_t e = stage[nst - 32 + lane_c];
-                __syncwarp();
-                nst -= 32;
-                insert_entry(e);
-            }
+            if (STAGE >= 128) stage_entry(false, 0, true);   // flush after the vertex's directions
         }
+#if TILE_ZRUN
+#pragma unroll
+        for (int d = 0; d < 3; ++d) stage_entry(run_p[d] != ~0u, run_e[d], true);
+#endif
         if (uint32_t(lane_c) < nst) insert_entry(stage[lane_c]);
     }
     __syncthreads();
@@ -556,8 +600,8 @@ tile_tmt_kernel(const float* __restrict__ f, TileOut out0, TileOut out1, uint32_
     }
     auto run_edge = [&](uint32_t j, uint32_t* mu, uint32_t* mv, uint64_t* S) {
         const uint64_t e = run[j];
-        const uint32_t pair = uint32_t(e >> 12) & 0xffffffu, hi = uint32_t(e) & 0xfffu;
-        const uint32_t ba = pair >> 12, bb = pair & 0xfffu;
+        const uint32_t pair = uint32_t(e >> LB) & PMASK, hi = uint32_t(e) & LMASK;
+        const uint32_t ba = pair >> LB, bb = pair & LMASK;
         const bool first = e >> 63;
         *mu = first ? ba : bb;
         *mv = first ? bb : ba;
@@ -594,9 +638,15 @@ tile_tmt_kernel(const float* __restrict__ f, TileOut out0, TileOut out1, uint32_
             if (busy) {
                 if (STATS) ++n_iters;
                 const uint64_t cu = sld64(cell + mu), cv = sld64(cell + mv);
-                if (c_v(cu) != mu && c_key(cu) < S) {         // l.2-4 + R4
+                const bool up_u = c_v(cu) != mu && c_key(cu) < S;   // l.2-4 + R4
+                const bool up_v = c_v(cv) != mv && c_key(cv) < S;   // l.5-8 + R4
+                if (TILE_BOTHCLIMB && (up_u || up_v)) {
+                    // the two climbs are independent under one S: both advance in this iteration
+                    if (up_u) mu = c_v(cu);
+                    if (up_v) mv = c_v(cv);
+                } else if (up_u) {
                     mu = c_v(cu);
-                } else if (c_v(cv) != mv && c_key(cv) < S) {  // l.5-8 + R4
+                } else if (up_v) {
                     mv = c_v(cv);
                 } else if (mu == mv) {                        // l.9-10
                     busy = false;
@@ -751,7 +801,7 @@ uint64_t xface_entries(const Slab& sl) {
 }
 
 #ifndef MT_TILE_NV
-#define MT_TILE_NV 4096   // vertices per tile (build knob: 4096 or 2048); tile_shape follows it
+#define MT_TILE_NV 4096   // vertices per tile (build knob: 8192, 4096 or 2048); tile_shape follows it
 #endif
 constexpr int tile_vertices() { return MT_TILE_NV; }
 
@@ -761,8 +811,8 @@ void tile_shape(uint32_t nz_global, uint32_t* ty, uint32_t* tz) {
         *ty = uint32_t(nv / TX);
         *tz = 1;
     } else {
-        *ty = nv == 4096 ? 16 : 8;
-        *tz = 8;
+        *ty = nv == 2048 ? 8 : 16;
+        *tz = nv == 8192 ? 16 : 8;
     }
 }
 
@@ -772,7 +822,7 @@ void launch_tile_v(const float* f, const TileOut& o0, const TileOut& o1, const S
     constexpr int NV = TX * TY * TZ;
     auto kern = tile_tmt_kernel<TY, TZ, STATS, DUAL>;
     ensure_smem_attr(reinterpret_cast<const void*>(kern), int(smem_bytes<NV>()));
-    kern<<<grid, NV / 8, smem_bytes<NV>(), stream>>>(f, o0, o1, sl.nx, sl.ny, sl.z_begin, sl.z_end, tx, tyn, flip,
+    kern<<<grid, NV / TILE_VPT, smem_bytes<NV>(), stream>>>(f, o0, o1, sl.nx, sl.ny, sl.z_begin, sl.z_end, tx, tyn, flip,
                                                      stats);
 }
 
@@ -796,15 +846,16 @@ void launch_tile_any(const float* f, const TileOut& o0, const TileOut* o1, const
     const uint32_t tx = (sl.nx + TX - 1) / TX, tyn = (sl.ny + ty - 1) / ty, tzn = (nzl + tz - 1) / tz;
     const uint32_t grid = tx * tyn * tzn;
     if (grid == 0) return;
-    const bool big = tile_vertices() == 4096;
-    if (sl.nz == 1 && big)
-        launch_tile<128, 1>(f, o0, o1, sl, tx, tyn, grid, flip, stats, stream);
-    else if (sl.nz == 1)
-        launch_tile<64, 1>(f, o0, o1, sl, tx, tyn, grid, flip, stats, stream);
-    else if (big)
-        launch_tile<16, 8>(f, o0, o1, sl, tx, tyn, grid, flip, stats, stream);
-    else
-        launch_tile<8, 8>(f, o0, o1, sl, tx, tyn, grid, flip, stats, stream);
+#if MT_TILE_NV == 8192
+    if (sl.nz == 1) launch_tile<256, 1>(f, o0, o1, sl, tx, tyn, grid, flip, stats, stream);
+    else launch_tile<16, 16>(f, o0, o1, sl, tx, tyn, grid, flip, stats, stream);
+#elif MT_TILE_NV == 4096
+    if (sl.nz == 1) launch_tile<128, 1>(f, o0, o1, sl, tx, tyn, grid, flip, stats, stream);
+    else launch_tile<16, 8>(f, o0, o1, sl, tx, tyn, grid, flip, stats, stream);
+#else
+    if (sl.nz == 1) launch_tile<64, 1>(f, o0, o1, sl, tx, tyn, grid, flip, stats, stream);
+    else launch_tile<8, 8>(f, o0, o1, sl, tx, tyn, grid, flip, stats, stream);
+#endif
 }
 
 void launch_tile_tmt(const float* f, Cell* C, uint64_t* T0, uint64_t* xface, const Slab& sl, uint32_t flip,
