@@ -37,7 +37,7 @@ namespace {
 #define MT_REPAIR_NC 1      // the repair reads cells no thread writes: L1-cached non-coherent loads
 #endif
 #ifndef MT_REPAIR_SEQ
-#define MT_REPAIR_SEQ 0     // walks one after the other (else lock-step rounds over the thread's vertices)
+#define MT_REPAIR_SEQ 1     // walks one after the other (else lock-step rounds over the thread's vertices)
 #endif
 #ifndef MT_REPAIR_SKIPW
 #define MT_REPAIR_SKIPW 0   // tiled: no store for a tile-regular vertex whose T0 is already final

@@ -60,6 +60,12 @@ namespace {
 #ifndef TILE_MINB
 #define TILE_MINB 2    // __launch_bounds__ min blocks per SM (register budget knob)
 #endif
+#ifndef TILE_ORDBITS
+#define TILE_ORDBITS 0 // hash insert: compare levels by the order-key bits the entries carry first
+#endif
+#ifndef TILE_MPASS
+#define TILE_MPASS 1   // hash variant: merge the pairs in this many level passes (1: one pass)
+#endif
 #ifndef TILE_BOTHCLIMB
 #define TILE_BOTHCLIMB 1  // Alg. 3 loop: climb u and v in the same iteration when both can climb
 #endif
@@ -471,7 +477,7 @@ tile_tmt_kernel(const float* __restrict__ f, TileOut out0, TileOut out1, uint32_
     constexpr uint64_t OBMASK = (1ull << OB) - 1;
     auto insert_entry = [&](uint64_t entry) {
         const uint32_t pair = uint32_t(entry >> LB) & PMASK;
-        const uint64_t mo = (entry >> (3 * LB)) & OBMASK;
+        const uint64_t mo = TILE_ORDBITS ? (entry >> (3 * LB)) & OBMASK : 0;
         uint32_t h = pair_hash<TABLE>(pair);
         for (uint32_t probe = 0;;) {
             const uint64_t cur = sld64(table + h);
@@ -485,7 +491,7 @@ tile_tmt_kernel(const float* __restrict__ f, TileOut out0, TileOut out1, uint32_
                 s_overflow = 1;                                  // table full: merge every edge
                 break;
             }
-            const uint64_t co = (cur >> (3 * LB)) & OBMASK;
+            const uint64_t co = TILE_ORDBITS ? (cur >> (3 * LB)) & OBMASK : 0;
             if (mo > co) break;                                  // the stored edge is lower
             if (mo == co && key48(ord, uint32_t(entry) & LMASK) >= key48(ord, uint32_t(cur) & LMASK)) break;
             if (scas64(table + h, cur, entry) == cur) break;
@@ -503,7 +509,7 @@ tile_tmt_kernel(const float* __restrict__ f, TileOut out0, TileOut out1, uint32_
         const bool lo_first = bu < bw;
         const uint32_t pair = lo_first ? (bu << LB) | bw : (bw << LB) | bu;
         // bit 63: the upper endpoint lies in the pair's first (smaller) basin
-        *entry = (uint64_t(u_hi == lo_first) << 63) | (uint64_t(oh >> (32 - OB)) << (3 * LB)) |
+        *entry = (uint64_t(u_hi == lo_first) << 63) | (TILE_ORDBITS ? uint64_t(oh >> (32 - OB)) << (3 * LB) : 0ull) |
                  (uint64_t(pair) << LB) | hi;
         return true;
     };
@@ -615,7 +621,38 @@ tile_tmt_kernel(const float* __restrict__ f, TileOut out0, TileOut out1, uint32_
     // so the lanes of a warp stay busy and converged instead of waiting for the longest merge of
     // the warp.  Merge(T, bh, hi, bl) starts straight from the two basins (bh holds the edge's
     // upper endpoint hi, level L = key(hi)).
+#if !TILE_KRUSKAL && TILE_MPASS > 1
+    // TILE_MPASS level passes: pass p merges the pairs whose upper endpoint's order key (its top
+    // OB bits, carried by the entry) falls in the p-th slice of the tile's range, so most merges
+    // arrive after the lower ones they would otherwise displace (Alg. 3 accepts any order)
+    uint32_t lev_lo = 0, lev_step = 0;
     {
+        uint32_t omin = ~0u, omax = 0;
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+            const uint32_t o = ord[(r0 + k * RSTEP) * TX + lx];
+            if (o != ABSENT) {
+                omin = min(omin, o);
+                omax = max(omax, o);
+            }
+        }
+        omin = __reduce_min_sync(FULL_MASK, omin);
+        omax = __reduce_max_sync(FULL_MASK, omax);
+        if (lane_c == 0) {
+            atomicMin(&s_omin, omin);
+            atomicMax(&s_omax, omax);
+        }
+        __syncthreads();
+        lev_lo = s_omin >> (32 - OB);
+        const uint32_t hi_b = s_omax >> (32 - OB);
+        lev_step = hi_b >= lev_lo ? (hi_b - lev_lo) / TILE_MPASS + 1 : 1;
+    }
+    constexpr int NPASS = TILE_MPASS;
+#else
+    constexpr int NPASS = 1;
+#endif
+#pragma unroll 1
+    for (int mp = 0; mp < NPASS; ++mp) {
         bool busy = false;
         uint64_t S = 0;
         uint32_t mu = 0, mv = 0, run_pos = 0;
@@ -627,14 +664,22 @@ tile_tmt_kernel(const float* __restrict__ f, TileOut out0, TileOut out1, uint32_
                 if (!busy) {
                     const uint32_t j = run_pos + __popc(need & ((1u << lane_c) - 1u));
                     if (j < run_n) {
-                        if (STATS) ++n_pairs;
-                        run_edge(j, &mu, &mv, &S);
-                        busy = true;
+#if !TILE_KRUSKAL && TILE_MPASS > 1
+                        const uint32_t lv = uint32_t((run[j] >> (3 * LB)) & OBMASK);
+                        const int p = min(int((lv - lev_lo) / lev_step), NPASS - 1);
+                        if (p == mp) {
+#else
+                        {
+#endif
+                            if (STATS) ++n_pairs;
+                            run_edge(j, &mu, &mv, &S);
+                            busy = true;
+                        }
                     }
                 }
                 run_pos += __popc(need);
             }
-            if (!__any_sync(FULL_MASK, busy)) break;
+            if (!__any_sync(FULL_MASK, busy) && run_pos >= run_n) break;
             if (busy) {
                 if (STATS) ++n_iters;
                 const uint64_t cu = sld64(cell + mu), cv = sld64(cell + mv);
@@ -666,6 +711,7 @@ tile_tmt_kernel(const float* __restrict__ f, TileOut out0, TileOut out1, uint32_
                 }
             }
         }
+        if (NPASS > 1) __syncthreads();
     }
     __syncthreads();
     if (s_overflow) {  // (uniform) kept edges / table entries were dropped: merge every edge
