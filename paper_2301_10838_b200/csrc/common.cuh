@@ -132,6 +132,7 @@ enum CounterSlot : int {
     CTR_FILT_TICKET = 8,  // mt_filter_diagram: tile tickets
     CTR_FILT_KEPT = 9,    // mt_filter_diagram: records kept
     CTR_STAGE = 10,       // diagram records staged by the repair bricks
+    CTR_FQLEN = 11,       // deduplicated inter-slab edges queued (forest_dedupe)
     CTR_COUNT = 16
 };
 

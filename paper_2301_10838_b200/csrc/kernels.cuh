@@ -154,8 +154,10 @@ void launch_forest_compact(const Cell* C, const uint64_t* T0, const float* f, co
 uint64_t forest_table_size(uint64_t n_all);
 void launch_forest_build(const mt_forest_record* all, uint64_t n_all, uint64_t* table, uint64_t* vtable,
                          uint32_t mask, Cell* cells, int num_sms, cudaStream_t stream);
-void launch_forest_merge(const ForestRef& F, const Slab& sl, const SlabBounds& b, unsigned long long* fetch,
-                         int num_sms, cudaStream_t stream);
+// inter-slab edges: deduplicated by tile-representative pairs into `queue`, then merged
+size_t forest_queue_entry_bytes();
+void launch_forest_merge(const ForestRef& F, const Slab& sl, const SlabBounds& b, void* queue,
+                         unsigned long long* qlen, unsigned long long* fetch, int num_sms, cudaStream_t stream);
 void launch_forest_writeback(const ForestRef& F, uint64_t n_all, Cell* C, const uint64_t* T0, const Slab& sl,
                              int num_sms, cudaStream_t stream);
 

@@ -557,10 +557,13 @@ mt_status mt_forest_view(mt_ctx* c, const mt_forest_record** records, uint64_t* 
     return st;
 }
 
+// id tables (2) | merged cells | queue of deduplicated inter-slab edges (every face vertex of a
+// boundary has a record, so a boundary's nx ny edges are at most half of the records)
 size_t mt_forest_scratch_bytes(uint64_t n_all) {
     const uint64_t t = mt::forest_table_size(n_all);
     if (t == 0) return 0;
-    return 2 * align_up(size_t(t) * sizeof(uint64_t)) + align_up(n_all * sizeof(mt::Cell));
+    return 2 * align_up(size_t(t) * sizeof(uint64_t)) + align_up(n_all * sizeof(mt::Cell)) +
+           align_up((n_all / 2 + 1) * mt::forest_queue_entry_bytes());
 }
 
 mt_status mt_compute_global(mt_ctx* c, const mt_forest_record* all, uint64_t n_all, const uint32_t* z_bounds,
@@ -595,7 +598,9 @@ mt_status mt_compute_global(mt_ctx* c, const mt_forest_record* all, uint64_t n_a
         return c->sticky = MT_ERR_CUDA;
     mt::launch_forest_build(all, n_all, table, vtable, tsize - 1, fcells, c->num_sms, s);
     mark(c, "forest_merge", s);
-    mt::launch_forest_merge(F, c->slab, b, counters_of(c) + mt::CTR_FFETCH, c->num_sms, s);
+    void* fqueue = static_cast<char*>(scratch) + 2 * align_up(size_t(tsize) * 8) + align_up(n_all * sizeof(mt::Cell));
+    mt::launch_forest_merge(F, c->slab, b, fqueue, counters_of(c) + mt::CTR_FQLEN, counters_of(c) + mt::CTR_FFETCH,
+                            c->num_sms, s);
     mark(c, "forest_writeback", s);
     mt::launch_forest_writeback(F, n_all, cells_of(c), T - c->slab.base, c->slab, c->num_sms, s);
     c->launches += 3;

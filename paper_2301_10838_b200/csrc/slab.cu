@@ -129,23 +129,99 @@ struct BoundaryGeom {
     uint32_t zb[MAX_SLABS];        // plane index of the upper side of boundary k
 };
 
-enum Phase : int { IDLE = 0, LOAD_AB = 1, CLIMB_HI = 2, CLIMB_LO = 3, MERGE_LD = 4, MERGE_CAS = 5, DONE = 6 };
+// Inter-slab edges reduced to pairs of tile representatives (DESIGN.md derivation C-3, the
+// reduction dedupe_cross applies to the tile faces): edge (a, b) at level L = max(key a, key b)
+// joins R(a) and R(b) at L, R = the tile representative at the vertex's own level (its forest
+// record's v for a tile-regular vertex, the vertex itself for a minimum), so of the edges with
+// one pair only the lowest is queued.  One CTA step = 512 consecutive edges of one boundary; a
+// shared-memory table keeps, per pair, the lowest level.  Every rank runs it on the gathered
+// records (the result is the same on all).
+struct FQEntry {
+    uint64_t L;
+    uint32_t r_hi, r_lo;
+};
+constexpr int FD_THREADS = 512;
+
+__global__ void __launch_bounds__(FD_THREADS)
+forest_dedupe_kernel(ForestRef F, BoundaryGeom g, FQEntry* __restrict__ q, unsigned long long* __restrict__ qlen) {
+    __shared__ unsigned long long s_key[2 * FD_THREADS], s_min[2 * FD_THREADS];
+    __shared__ uint32_t s_warp[FD_THREADS / 32];
+    __shared__ unsigned long long s_base;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint64_t sxy = uint64_t(g.nx) * g.ny;
+    const uint64_t total = sxy * g.nb;
+    for (uint64_t e0 = uint64_t(blockIdx.x) * FD_THREADS; e0 < total; e0 += uint64_t(gridDim.x) * FD_THREADS) {
+        const uint64_t e = e0 + threadIdx.x;
+        bool keep = false;
+        FQEntry en{0, 0, 0};
+        uint64_t pair = ~0ull;
+        if (e < total) {
+            const uint64_t k = e / sxy, r = e % sxy;
+            const uint32_t a = uint32_t((uint64_t(g.zb[k]) - 1) * sxy + r), b = uint32_t(a + sxy);
+            const uint32_t ia = forest_lookup(F, a), ib = forest_lookup(F, b);
+            if (ia == FOREST_MISS || ib == FOREST_MISS) {
+                atomicOr(F.err, ERR_FOREST);
+            } else {
+                const Cell ca = F.cells[ia], cb = F.cells[ib];
+                const uint64_t ka = self_key(ca, a), kb = self_key(cb, b);
+                const uint32_t ra = cs_of(ca) == a ? cv_of(ca) : a, rb = cs_of(cb) == b ? cv_of(cb) : b;
+                en = ka > kb ? FQEntry{ka, ra, rb} : FQEntry{kb, rb, ra};
+                pair = ra < rb ? (uint64_t(ra) << 32 | rb) : (uint64_t(rb) << 32 | ra);
+                keep = true;
+            }
+        }
+        s_key[threadIdx.x] = ~0ull;
+        s_key[threadIdx.x + FD_THREADS] = ~0ull;
+        s_min[threadIdx.x] = ~0ull;
+        s_min[threadIdx.x + FD_THREADS] = ~0ull;
+        __syncthreads();
+        uint32_t h = 0;
+        if (keep) {
+            h = uint32_t((pair * 0x9E3779B97F4A7C15ull) >> 54);   // 10 bits: 2 x FD_THREADS slots
+            while (true) {
+                const unsigned long long old = atomicCAS(&s_key[h], ~0ull, pair);
+                if (old == ~0ull || old == pair) break;
+                h = (h + 1) & (2u * FD_THREADS - 1u);
+            }
+            atomicMin(&s_min[h], (unsigned long long)en.L);
+        }
+        __syncthreads();
+        if (keep && s_min[h] != en.L) keep = false;
+        const uint32_t km = __ballot_sync(FULL_MASK, keep);
+        if (lane == 0) s_warp[warp] = __popc(km);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            uint32_t tot = 0;
+            for (int w = 0; w < FD_THREADS / 32; ++w) {
+                const uint32_t t = s_warp[w];
+                s_warp[w] = tot;
+                tot += t;
+            }
+            s_base = tot ? atomicAdd(qlen, (unsigned long long)tot) : 0;
+        }
+        __syncthreads();
+        if (keep) q[s_base + s_warp[warp] + __popc(km & ((1u << lane) - 1u))] = en;
+        __syncthreads();
+    }
+}
+
+enum Phase : int { IDLE = 0, CLIMB_HI = 2, CLIMB_LO = 3, MERGE_LD = 4, MERGE_CAS = 5, DONE = 6 };
 
 // merge_cross.cu's state machine on the forest: every cell access goes through the table
 __global__ void __launch_bounds__(256)
-forest_merge_kernel(ForestRef F, BoundaryGeom g, unsigned long long* __restrict__ fetch) {
+forest_merge_kernel(ForestRef F, const FQEntry* __restrict__ q, const unsigned long long* __restrict__ qlen,
+                    unsigned long long* __restrict__ fetch) {
     constexpr uint64_t BATCH = 256;
     const int lane = threadIdx.x & 31;
-    const uint64_t sxy = uint64_t(g.nx) * g.ny;
-    const uint64_t total = sxy * g.nb;
+    const uint64_t total = *reinterpret_cast<const volatile unsigned long long*>(qlen);
     uint64_t pool_next = 0, pool_end = 0;
     bool exhausted = false;
     int phase = IDLE;
     uint64_t L = 0, ks = 0;
     uint32_t x = 0, lo = 0, rh = 0, u = 0, v = 0;
     uint32_t ix = 0, ixp = 0, iu = 0, iv = 0, ilo = 0, irh = 0;   // table indices
-    bool has_prev = false, have_c = false;
-    Cell c{0, 0}, cp{0, 0}, clo{0, 0}, cu{0, 0}, cv{0, 0}, desired{0, 0}, got{0, 0};
+    bool has_prev = false;
+    Cell c{0, 0}, cp{0, 0}, cu{0, 0}, cv{0, 0}, desired{0, 0}, got{0, 0};
     auto at = [&](uint32_t i) { return F.cells + i; };
     while (true) {
         const uint32_t need = __ballot_sync(FULL_MASK, phase == IDLE);
@@ -162,14 +238,16 @@ forest_merge_kernel(ForestRef F, BoundaryGeom g, unsigned long long* __restrict_
             const uint64_t avail = pool_end - pool_next;
             if (phase == IDLE) {
                 if (rank < avail) {
-                    const uint64_t e = pool_next + rank;
-                    const uint64_t k = e / sxy, r = e % sxy;
-                    u = uint32_t((uint64_t(g.zb[k]) - 1) * sxy + r);     // lower side of boundary k
-                    v = uint32_t(u + sxy);
-                    iu = forest_lookup(F, u);
-                    iv = forest_lookup(F, v);
-                    phase = LOAD_AB;
-                    if (iu == FOREST_MISS || iv == FOREST_MISS) {
+                    // a deduplicated edge: walk from R_hi, then R_lo, at level L (forest_dedupe_kernel)
+                    const FQEntry en = q[pool_next + rank];
+                    L = en.L;
+                    x = en.r_hi;
+                    lo = en.r_lo;
+                    ix = forest_lookup(F, x);
+                    ilo = forest_lookup(F, lo);
+                    has_prev = false;
+                    phase = CLIMB_HI;
+                    if (ix == FOREST_MISS || ilo == FOREST_MISS) {
                         atomicOr(F.err, ERR_FOREST);
                         phase = IDLE;
                     }
@@ -181,28 +259,15 @@ forest_merge_kernel(ForestRef F, BoundaryGeom g, unsigned long long* __restrict_
         }
         if (__ballot_sync(FULL_MASK, phase != DONE) == 0) break;
 
-        if (phase == LOAD_AB || phase == MERGE_LD) {
+        if (phase == MERGE_LD) {
             cu = ld_cell(at(iu));
             cv = ld_cell(at(iv));
-        } else if ((phase == CLIMB_HI || phase == CLIMB_LO) && !have_c) {
+        } else if (phase == CLIMB_HI || phase == CLIMB_LO) {
             c = ld_cell(at(ix));
         } else if (phase == MERGE_CAS) {
             got = cas_cell(at(iv), cv, desired);
         }
-        have_c = false;
 
-        if (phase == LOAD_AB) {
-            const uint64_t ka = self_key(cu, u), kb = self_key(cv, v);
-            L = ka > kb ? ka : kb;
-            x = ka > kb ? u : v;
-            ix = ka > kb ? iu : iv;
-            c = ka > kb ? cu : cv;
-            lo = ka > kb ? v : u;
-            ilo = ka > kb ? iv : iu;
-            clo = ka > kb ? cv : cu;
-            has_prev = false;
-            phase = CLIMB_HI;
-        }
         if (phase == CLIMB_HI || phase == CLIMB_LO) {
             if (cv_of(c) != x && c.lo <= L) {                       // followable at level L
                 if (has_prev && c.lo <= cp.lo)                      // path splitting
@@ -221,8 +286,6 @@ forest_merge_kernel(ForestRef F, BoundaryGeom g, unsigned long long* __restrict_
                 irh = ix;
                 x = lo;
                 ix = ilo;
-                c = clo;
-                have_c = true;
                 has_prev = false;
                 phase = CLIMB_LO;
             } else if (x == rh) {
@@ -329,15 +392,22 @@ void launch_forest_build(const mt_forest_record* all, uint64_t n_all, uint64_t* 
         cells);
 }
 
-void launch_forest_merge(const ForestRef& F, const Slab& sl, const SlabBounds& b, unsigned long long* fetch,
-                         int num_sms, cudaStream_t stream) {
+size_t forest_queue_entry_bytes() { return sizeof(FQEntry); }
+
+void launch_forest_merge(const ForestRef& F, const Slab& sl, const SlabBounds& b, void* queue,
+                         unsigned long long* qlen, unsigned long long* fetch, int num_sms, cudaStream_t stream) {
     if (b.count < 2) return;
     BoundaryGeom g{};
     g.nx = sl.nx;
     g.ny = sl.ny;
     g.nb = b.count - 1;
     for (uint32_t k = 0; k + 1 < b.count; ++k) g.zb[k] = b.z[k + 1];
-    forest_merge_kernel<<<uint32_t(num_sms) * 4, 256, 0, stream>>>(F, g, fetch);
+    FQEntry* q = static_cast<FQEntry*>(queue);
+    const uint64_t total = uint64_t(g.nx) * g.ny * g.nb;
+    uint64_t blocks = (total + FD_THREADS - 1) / FD_THREADS;
+    if (blocks > uint64_t(num_sms) * 8) blocks = uint64_t(num_sms) * 8;
+    forest_dedupe_kernel<<<uint32_t(blocks), FD_THREADS, 0, stream>>>(F, g, q, qlen);
+    forest_merge_kernel<<<uint32_t(num_sms) * 4, 256, 0, stream>>>(F, q, qlen, fetch);
 }
 
 void launch_forest_writeback(const ForestRef& F, uint64_t n_all, Cell* C, const uint64_t* T0, const Slab& sl,

@@ -60,6 +60,12 @@ namespace {
 #ifndef TILE_MINB
 #define TILE_MINB 2    // __launch_bounds__ min blocks per SM (register budget knob)
 #endif
+#ifndef TILE_B16
+#define TILE_B16 0     // hash list: the neighbour's basin by a 16-bit load of its cell's v field
+#endif
+#ifndef TILE_REP_SEQ
+#define TILE_REP_SEQ 0 // in-tile repair: walks one after the other (else lock-step rounds)
+#endif
 #ifndef TILE_ORDBITS
 #define TILE_ORDBITS 0 // hash insert: compare levels by the order-key bits the entries carry first
 #endif
@@ -502,7 +508,7 @@ tile_tmt_kernel(const float* __restrict__ f, TileOut out0, TileOut out1, uint32_
         const uint32_t w = u + off;
         const uint32_t ow = ord[w];
         if (ow == ABSENT) return false;
-        const uint32_t bw = c_v(cell[w]);
+        const uint32_t bw = TILE_B16 ? uint32_t(reinterpret_cast<const uint16_t*>(cell + w)[0]) : c_v(cell[w]);
         if (bw == bu) return false;
         const bool u_hi = ow < ou;   // w = u + off has the larger id: on a tie w is the upper end
         const uint32_t hi = u_hi ? u : w, oh = u_hi ? ou : ow;
@@ -767,6 +773,25 @@ tile_tmt_kernel(const float* __restrict__ f, TileOut out0, TileOut out1, uint32_
     // load chains in flight); the cells are final after the merge barrier and this phase only
     // reads them, so the representatives stay in registers and go straight to phase f
     uint32_t rep[PER];
+#if TILE_REP_SEQ
+    // one walk after the other (the loops run the sum of the chain lengths)
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+        const uint64_t cu = cell[(r0 + k * RSTEP) * TX + lx];
+        uint32_t x = c_v(cu);
+        if (TILE_STOP == 0 || TILE_STOP > 4) {
+            const uint64_t a = c_key(cu);
+#pragma unroll 1
+            while (true) {
+                const uint64_t cx = cell[x];
+                if (c_v(cx) == x || c_key(cx) > a) break;
+                x = c_v(cx);
+                if (STATS) ++n_rep;
+            }
+        }
+        rep[k] = x;
+    }
+#else
     uint32_t act = 0;
 #pragma unroll
     for (int k = 0; k < PER; ++k) {
@@ -789,6 +814,7 @@ tile_tmt_kernel(const float* __restrict__ f, TileOut out0, TileOut out1, uint32_
             }
         }
     }
+#endif
     phase_time(ST_CYC_REPAIR);
 
     // ---- f. write the tile store T0 (8 B per vertex) and the tile minima's 16-byte cells ------
