@@ -375,10 +375,10 @@ def run_mt(args, rank, world):
             pipe.run([f_host], T_hosts[:1], rec_hosts[:1], args.split)      # warm-up
             torch.cuda.synchronize()
             t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            t0.record(pipe.s_h2d)
+            t0.record(stream)     # mt_compute_host starts after, and `stream` waits for, its pipeline
             counts = pipe.run([f_host] * e2e_steps, [T_hosts[i % 2] for i in range(e2e_steps)],
-                              [rec_hosts[i % 2] for i in range(e2e_steps)], args.split)
-            t1.record(pipe.s_d2h)
+                              [rec_hosts[i % 2] for i in range(e2e_steps)], args.split, stream)
+            t1.record(stream)
             torch.cuda.synchronize()
             e_ms = t0.elapsed_time(t1)
             a, b = counts[-1]
@@ -410,7 +410,8 @@ def run_mt(args, rank, world):
             e_ms, h2d, d2h = float(tm[0].item()), int(t[1].item()), int(t[2].item())
         e2e = {"value": n_global * e2e_steps / (e_ms * 1e-3) / 1e6, "unit": "Mvertices/s",
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": e2e_steps,
-               "overlap": "H2D(i+1) | compute(i) | D2H(i-1) on 3 streams" if world == 1 else "none"}
+               "overlap": "mt_compute_host (C ABI): H2D(i+1) | compute(i) | D2H(i-1) on the library's 3 streams"
+               if world == 1 else "none"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

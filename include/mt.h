@@ -91,6 +91,23 @@ mt_status mt_create(mt_ctx **out, const uint32_t dims[3], int conn, int cuda_dev
 mt_status mt_compute(mt_ctx *ctx, const float *f, uint64_t *triplets, uint32_t flags,
                      mt_stream_t stream);
 
+/* End to end from host memory (the e2e path): k fields f_hosts[i] (host, n
+ * float32; pinned for overlap) in, their triplet stores T_hosts[i] (host, n
+ * uint64) and diagrams rec_hosts[i] (host, rec_cap records each) out, counts
+ * (host, 2k: n_pairs, n_essential per field).  Three streams the context
+ * creates at first use overlap, step by step, the host->device copy of field
+ * i+1, the computation of field i and the device->host copies of field i-1;
+ * `staging` (device, >= mt_host_staging_bytes, 256-B aligned, caller-owned)
+ * holds the double-buffered device copies.  The pipeline starts after the work
+ * already queued on `stream` and `stream` waits for the pipeline, so events the
+ * caller records on it around the call bracket the whole host->host run.
+ * Synchronous: returns when every output is in host memory.  MT_ERR_CAPACITY
+ * when a diagram exceeds rec_cap. */
+size_t mt_host_staging_bytes(const mt_ctx *ctx);
+mt_status mt_compute_host(mt_ctx *ctx, uint32_t k, const float *const *f_hosts, uint64_t *const *T_hosts,
+                          mt_pair *const *rec_hosts, uint64_t rec_cap, uint64_t *counts, uint32_t flags,
+                          void *staging, size_t staging_bytes, mt_stream_t stream);
+
 /* Both trees of one field from ONE read of f (the join and
  * split trees are the two inputs of a contour tree; the paper
  * computes the split tree of its densities): ctx_join and

@@ -33,7 +33,7 @@ EXPORTS = ["mt_workspace_bytes", "mt_create", "mt_compute", "mt_set_diagram_outp
            "mt_create_slab", "mt_compute_local", "mt_forest_view", "mt_forest_scratch_bytes", "mt_compute_global",
            "mt_filter_diagram", "mt_graph_workspace_bytes", "mt_create_graph", "mt_compute_graph",
            "mt_get_unique_id", "mt_dist_slab_bounds", "mt_dist_workspace_bytes", "mt_create_dist",
-           "mt_compute_join_split"]
+           "mt_compute_join_split", "mt_host_staging_bytes", "mt_compute_host"]
 
 
 class MTError(RuntimeError):
@@ -66,6 +66,9 @@ def load(build_if_missing: bool = False):
         "mt_create": (ctypes.c_int, [ctypes.POINTER(vp), u32p, ctypes.c_int, ctypes.c_int, vp, ctypes.c_size_t]),
         "mt_compute": (ctypes.c_int, [vp, vp, vp, ctypes.c_uint32, vp]),
         "mt_compute_join_split": (ctypes.c_int, [vp, vp, vp, vp, vp, vp]),
+        "mt_host_staging_bytes": (ctypes.c_size_t, [vp]),
+        "mt_compute_host": (ctypes.c_int, [vp, ctypes.c_uint32, vp, vp, vp, ctypes.c_uint64, vp, ctypes.c_uint32, vp,
+                                           ctypes.c_size_t, vp]),
         "mt_set_diagram_output": (ctypes.c_int, [vp, vp, ctypes.c_uint64]),
         "mt_diagram": (ctypes.c_int, [vp, vp, ctypes.c_uint64, u64p, u64p, vp]),
         "mt_diagram_view": (ctypes.c_int, [vp, ctypes.POINTER(vp), u64p, u64p, vp]),
@@ -150,6 +153,22 @@ def mt_compute(ctx, f_ptr: int, triplets_ptr: int, flags: int = 0, stream=None):
 def mt_compute_join_split(ctx_join, ctx_split, f_ptr: int, tj_ptr: int, ts_ptr: int, stream=None):
     _check(load().mt_compute_join_split(ctx_join, ctx_split, ctypes.c_void_p(f_ptr), ctypes.c_void_p(tj_ptr),
                                         ctypes.c_void_p(ts_ptr), _stream_handle(stream)), "mt_compute_join_split")
+
+
+def mt_host_staging_bytes(ctx) -> int:
+    return int(load().mt_host_staging_bytes(ctx))
+
+
+def mt_compute_host(ctx, f_ptrs, T_ptrs, rec_ptrs, rec_cap: int, flags: int, staging_ptr: int, staging_bytes: int,
+                    stream=None):
+    """Host->host steps (pointers to pinned host buffers); returns [(n_pairs, n_essential)] per field."""
+    k = len(f_ptrs)
+    arr = lambda xs: (ctypes.c_void_p * max(k, 1))(*[ctypes.c_void_p(x) for x in xs])
+    counts = (ctypes.c_uint64 * (2 * max(k, 1)))()
+    _check(load().mt_compute_host(ctx, k, arr(f_ptrs), arr(T_ptrs), arr(rec_ptrs), ctypes.c_uint64(rec_cap), counts,
+                                  int(flags), ctypes.c_void_p(staging_ptr), ctypes.c_size_t(staging_bytes),
+                                  _stream_handle(stream)), "mt_compute_host")
+    return [(int(counts[2 * i]), int(counts[2 * i + 1])) for i in range(k)]
 
 
 def mt_set_diagram_output(ctx, buf_ptr: int, capacity: int):

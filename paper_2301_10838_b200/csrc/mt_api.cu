@@ -162,6 +162,9 @@ struct mt_ctx {
     const char* ev_name[MAX_EVENTS] = {};
     int nev = 0;
     mt::DistState* dist = nullptr;  // mt_create_dist: communicator + exchange buffers (dist.cu)
+    // mt_compute_host: streams and events of the host pipeline (created at first use)
+    cudaStream_t hs[3] = {nullptr, nullptr, nullptr};
+    cudaEvent_t hev[6] = {};
 };
 
 namespace mt {
@@ -519,6 +522,103 @@ mt_status mt_compute_join_split(mt_ctx* cj, mt_ctx* cs, const float* f, uint64_t
     return finish_compute(cs, T_split, nullptr, s);
 }
 
+size_t mt_host_staging_bytes(const mt_ctx* c) {
+    if (!c || c->multi || c->graph) return 0;
+    return 2 * (align_up(c->n * sizeof(float)) + align_up(c->n * sizeof(uint64_t)) +
+                align_up(c->L.pairs_cap * sizeof(mt_pair)));
+}
+
+mt_status mt_compute_host(mt_ctx* c, uint32_t k, const float* const* f_hosts, uint64_t* const* T_hosts,
+                          mt_pair* const* rec_hosts, uint64_t rec_cap, uint64_t* counts, uint32_t flags,
+                          void* staging, size_t staging_bytes, mt_stream_t stream) {
+    if (!c || (k && (!f_hosts || !T_hosts || !rec_hosts || !counts))) return MT_ERR_INVALID_ARG;
+    if (c->multi || c->graph) return MT_ERR_STATE;
+    if (flags & ~uint32_t(MT_FLAG_SPLIT_TREE)) return MT_ERR_INVALID_ARG;
+    if (k == 0) return MT_OK;
+    if (!staging || staging_bytes < mt_host_staging_bytes(c) || reinterpret_cast<uintptr_t>(staging) % ALIGN)
+        return MT_ERR_WORKSPACE;
+    DeviceGuard g(c->device);
+    if (!g.ok) return MT_ERR_CUDA;
+    if (!c->hs[0]) {
+        for (cudaStream_t& st : c->hs)
+            if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess) return MT_ERR_CUDA;
+        for (cudaEvent_t& e : c->hev)
+            if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return MT_ERR_CUDA;
+    }
+    cudaStream_t s_h2d = c->hs[0], s_comp = c->hs[1], s_d2h = c->hs[2];
+    cudaStream_t caller = static_cast<cudaStream_t>(stream);
+    // the pipeline starts after the work already on the caller's stream and the caller's stream
+    // continues after the pipeline (events recorded on it bracket the whole host->host run)
+    if (cudaEventRecord(c->hev[0], caller) != cudaSuccess) return MT_ERR_CUDA;
+    for (cudaStream_t sx : c->hs)
+        if (cudaStreamWaitEvent(sx, c->hev[0], 0) != cudaSuccess) return MT_ERR_CUDA;
+    cudaEvent_t* h2d_done = c->hev;          // [2]
+    cudaEvent_t* comp_done = c->hev + 2;     // [2]
+    cudaEvent_t* d2h_done = c->hev + 4;      // [2]
+    // double-buffered device staging: f, T, diagram records (the registered diagram output)
+    char* p = static_cast<char*>(staging);
+    float* f_dev[2];
+    uint64_t* T_dev[2];
+    mt_pair* r_dev[2];
+    for (int b = 0; b < 2; ++b) {
+        f_dev[b] = reinterpret_cast<float*>(p);
+        p += align_up(c->n * sizeof(float));
+        T_dev[b] = reinterpret_cast<uint64_t*>(p);
+        p += align_up(c->n * sizeof(uint64_t));
+        r_dev[b] = reinterpret_cast<mt_pair*>(p);
+        p += align_up(c->L.pairs_cap * sizeof(mt_pair));
+    }
+    mt_pair* const saved_out = c->reg_out;
+    const uint64_t saved_cap = c->reg_cap;
+    for (int b = 0; b < 2; ++b)
+        if (cudaEventRecord(comp_done[b], s_comp) != cudaSuccess || cudaEventRecord(d2h_done[b], s_comp) != cudaSuccess)
+            return MT_ERR_CUDA;
+    auto h2d = [&](uint32_t i) {   // field i into f_dev[i % 2] once compute i-2 stopped reading it
+        const int b = int(i % 2);
+        return cudaStreamWaitEvent(s_h2d, comp_done[b], 0) == cudaSuccess &&
+               cudaMemcpyAsync(f_dev[b], f_hosts[i], c->n * sizeof(float), cudaMemcpyHostToDevice, s_h2d) ==
+                   cudaSuccess &&
+               cudaEventRecord(h2d_done[b], s_h2d) == cudaSuccess;
+    };
+    mt_status st = MT_OK;
+    if (!h2d(0)) st = MT_ERR_CUDA;
+    for (uint32_t i = 0; i < k && st == MT_OK; ++i) {
+        const int b = int(i % 2);
+        if (cudaStreamWaitEvent(s_comp, h2d_done[b], 0) != cudaSuccess ||
+            cudaStreamWaitEvent(s_comp, d2h_done[b], 0) != cudaSuccess) {
+            st = MT_ERR_CUDA;
+            break;
+        }
+        c->reg_out = r_dev[b];
+        c->reg_cap = c->L.pairs_cap;
+        st = mt_compute(c, f_dev[b], T_dev[b], flags, s_comp);
+        if (st != MT_OK) break;
+        if (cudaEventRecord(comp_done[b], s_comp) != cudaSuccess) { st = MT_ERR_CUDA; break; }
+        if (i + 1 < k && !h2d(i + 1)) { st = MT_ERR_CUDA; break; }   // overlaps compute i
+        uint64_t np = 0, ne = 0;
+        st = mt_diagram(c, nullptr, 0, &np, &ne, s_comp);              // waits for compute i
+        if (st != MT_OK) break;
+        counts[2 * i] = np;
+        counts[2 * i + 1] = ne;
+        if (np + ne > rec_cap) { st = MT_ERR_CAPACITY; break; }
+        if (cudaStreamWaitEvent(s_d2h, comp_done[b], 0) != cudaSuccess ||
+            cudaMemcpyAsync(T_hosts[i], T_dev[b], c->n * sizeof(uint64_t), cudaMemcpyDeviceToHost, s_d2h) !=
+                cudaSuccess ||
+            (np + ne && cudaMemcpyAsync(rec_hosts[i], r_dev[b], (np + ne) * sizeof(mt_pair), cudaMemcpyDeviceToHost,
+                                        s_d2h) != cudaSuccess) ||
+            cudaEventRecord(d2h_done[b], s_d2h) != cudaSuccess)   // overlaps compute i + 1
+            st = MT_ERR_CUDA;
+    }
+    for (int j = 0; j < 3; ++j)
+        if ((cudaEventRecord(c->hev[j], c->hs[j]) != cudaSuccess ||
+             cudaStreamWaitEvent(caller, c->hev[j], 0) != cudaSuccess) && st == MT_OK)
+            st = MT_ERR_CUDA;
+    if (cudaStreamSynchronize(caller) != cudaSuccess && st == MT_OK) st = MT_ERR_CUDA;
+    c->reg_out = saved_out;
+    c->reg_cap = saved_cap;
+    return st;
+}
+
 mt_status mt_compute_local(mt_ctx* c, const float* f, uint64_t* T, uint32_t flags, mt_stream_t stream) {
     if (!c || !f || !T) return MT_ERR_INVALID_ARG;
     if (flags & ~uint32_t(MT_FLAG_SPLIT_TREE)) return MT_ERR_INVALID_ARG;
@@ -728,6 +828,10 @@ void mt_destroy(mt_ctx* c) {
     if (!c) return;
     DeviceGuard g(c->device);
     mt::dist_destroy(c->dist);
+    for (cudaStream_t& st : c->hs)
+        if (st) cudaStreamDestroy(st);
+    for (cudaEvent_t& e : c->hev)
+        if (e) cudaEventDestroy(e);
     for (int i = 0; i <= MAX_EVENTS; ++i)
         if (c->ev[i]) cudaEventDestroy(c->ev[i]);
     if (c->host_ctr) cudaFreeHost(c->host_ctr);

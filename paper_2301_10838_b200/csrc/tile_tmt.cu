@@ -60,11 +60,8 @@ namespace {
 #ifndef TILE_MINB
 #define TILE_MINB 2    // __launch_bounds__ min blocks per SM (register budget knob)
 #endif
-#ifndef TILE_B16
-#define TILE_B16 0     // hash list: the neighbour's basin by a 16-bit load of its cell's v field
-#endif
 #ifndef TILE_REP_SEQ
-#define TILE_REP_SEQ 0 // in-tile repair: walks one after the other (else lock-step rounds)
+#define TILE_REP_SEQ 1 // in-tile repair: walks one after the other (else lock-step rounds)
 #endif
 #ifndef TILE_ORDBITS
 #define TILE_ORDBITS 0 // hash insert: compare levels by the order-key bits the entries carry first
@@ -508,7 +505,7 @@ tile_tmt_kernel(const float* __restrict__ f, TileOut out0, TileOut out1, uint32_
         const uint32_t w = u + off;
         const uint32_t ow = ord[w];
         if (ow == ABSENT) return false;
-        const uint32_t bw = TILE_B16 ? uint32_t(reinterpret_cast<const uint16_t*>(cell + w)[0]) : c_v(cell[w]);
+        const uint32_t bw = c_v(cell[w]);
         if (bw == bu) return false;
         const bool u_hi = ow < ou;   // w = u + off has the larger id: on a tie w is the upper end
         const uint32_t hi = u_hi ? u : w, oh = u_hi ? ou : ow;
