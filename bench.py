@@ -203,10 +203,10 @@ def _ecross(dims):
 
 
 ALG_BYTES = {
-    "tile_tmt": lambda n, rec, ec: 12 * n,                 # read f (4) + write the store (8)
-    "dedupe_cross": lambda n, rec, ec: 16 * ec,            # read f + basin of both ends of every crossing edge
+    "tile_tmt": lambda n, rec, ec: 12 * n,                 # read f (4) + write the tile store (8)
+    "dedupe_cross": lambda n, rec, ec: 24 * ec,            # f + tile store of both ends of every crossing edge
     "merge_queue": lambda n, rec, ec: 2 * 8 * ec,          # (lower bound) both end cells of every crossing edge
-    "repair": lambda n, rec, ec: 16 * n,                   # read the store (8) + write T (8)
+    "repair": lambda n, rec, ec: 20 * n,                   # read the tile store (8) + f (4), write T (8)
     "diagram": lambda n, rec, ec: 4 * n + 16 * rec,        # one 4-B word per vertex to find the minima + records
     "finish_diagram": lambda n, rec, ec: 0,
 }
@@ -345,6 +345,22 @@ def run_mt(args, rank, world):
             issue = prof.get("issue", {}).get(args.config, {}).get(dom)
         except Exception:
             traffic, issue = None, None
+    # secondary ceilings (SURVEY.md 8d, N11 microbenchmarks in profiles/): the global merge is
+    # bound by 128-bit L2 CAS throughput, the repair by random 16-B cell gathers; per-launch event
+    # counts from one ncu capture (profiles/traffic.json "secondary"), live kernel times here
+    secondary = None
+    if os.path.exists(prof_path):
+        try:
+            sec = json.load(open(prof_path)).get("secondary", {}).get(args.config, {})
+            secondary = {}
+            for k, d in sec.items():
+                if k in avg and not k.startswith("_"):
+                    rate = d["count_per_launch"] / (avg[k] * 1e-3)
+                    secondary[k] = {"bound": d["bound"], "achieved": rate, "peak": d["peak"], "unit": d["unit"],
+                                    "frac": rate / d["peak"], "count_per_launch": d["count_per_launch"],
+                                    "source": d["source"]}
+        except Exception:
+            secondary = None
     roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
                 # what actually bounds the kernel (ncu, profiles/traffic.json): instruction issue
@@ -430,7 +446,8 @@ def run_mt(args, rank, world):
             "config": _config(args, dims, conn, world),
             "pairs": npairs, "essential": ness,
             "step_ms": {"median": statistics.median(step_ms), "min": min(step_ms), "max": max(step_ms)},
-            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "roofline": roofline, "secondary_ceilings": secondary, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": launches,
             "clocks": clk.summary(),
         }
         if world > 1:
