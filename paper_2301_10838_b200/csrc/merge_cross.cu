@@ -136,26 +136,46 @@ dedupe_cross_kernel(const float* __restrict__ f, const uint64_t* __restrict__ T0
         const uint64_t xend = yend + (g.xpatch ? g.ex : 0);
         const bool zpatch = g.patch && e0 < xend;   // uniform over the CTA (ez, ey, ex % DC_THREADS == 0)
         uint64_t e = e_raw;
+        // patch steps know their edge's face, plane and position directly: the ends a, b (and,
+        // for an x face, its record's tile and row) without decode_edge's divisions.  A step's
+        // 512 edges lie in one patch (every face size is a multiple of 512), so k and the patch
+        // index derive from the CTA-uniform e0.
+        bool direct = false;
+        uint32_t a = 0, b = 0, xk = 0, xy = 0, xz = 0;
+        bool xrec = false;
         if (g.patch) {
-            const uint32_t pxn = g.nx / 32;
-            if (e_raw < g.ez) {
-                const uint64_t sxy = uint64_t(g.nx) * g.ny;
-                const uint64_t k = e_raw / sxy, rp = e_raw - k * sxy;
-                const uint32_t pidx = uint32_t(rp / DC_THREADS), w = uint32_t(rp % DC_THREADS);
+            const uint32_t pxn = g.nx / 32, w = threadIdx.x;
+            const uint64_t sxy = uint64_t(g.nx) * g.ny;
+            if (e0 < g.ez) {
+                const uint64_t k = e0 / sxy;
+                const uint32_t pidx = uint32_t((e0 - k * sxy) / DC_THREADS);
                 const uint32_t x = (pidx % pxn) * 32 + (w & 31), y = (pidx / pxn) * DC_ROWS + (w >> 5);
-                e = g.ex + g.ey + k * sxy + uint64_t(y) * g.nx + x;
-            } else if (e_raw < yend) {
-                const uint64_t sxz = uint64_t(g.nx) * g.nz, ey0 = e_raw - g.ez;
-                const uint64_t k = ey0 / sxz, rp = ey0 - k * sxz;
-                const uint32_t pidx = uint32_t(rp / DC_THREADS), w = uint32_t(rp % DC_THREADS);
+                const uint64_t u = (uint64_t(k + 1) * g.tz - 1) * sxy + uint64_t(y) * g.nx + x;
+                a = uint32_t(g.base + u);
+                b = uint32_t(g.base + u + sxy);
+                direct = true;
+            } else if (e0 < yend) {
+                const uint64_t sxz = uint64_t(g.nx) * g.nz, ey0 = e0 - g.ez;
+                const uint64_t k = ey0 / sxz;
+                const uint32_t pidx = uint32_t((ey0 - k * sxz) / DC_THREADS);
                 const uint32_t x = (pidx % pxn) * 32 + (w & 31), z = (pidx / pxn) * DC_ROWS + (w >> 5);
-                e = g.ex + k * sxz + uint64_t(z) * g.nx + x;
-            } else if (e_raw < xend) {
-                const uint64_t syz = uint64_t(g.ny) * g.nz, ex0 = e_raw - yend;
-                const uint64_t k = ex0 / syz, rp = ex0 - k * syz;
-                const uint32_t pidx = uint32_t(rp / DC_THREADS), w = uint32_t(rp % DC_THREADS), pyn = g.ny / 32;
+                const uint64_t u = uint64_t(z) * sxy + (uint64_t(k + 1) * g.ty - 1) * g.nx + x;
+                a = uint32_t(g.base + u);
+                b = uint32_t(g.base + u + g.nx);
+                direct = true;
+            } else if (e0 < xend) {
+                const uint64_t syz = uint64_t(g.ny) * g.nz, ex0 = e0 - yend;
+                const uint64_t k = ex0 / syz;
+                const uint32_t pidx = uint32_t((ex0 - k * syz) / DC_THREADS), pyn = g.ny / 32;
                 const uint32_t y = (pidx % pyn) * 32 + (w & 31), z = (pidx / pyn) * DC_ROWS + (w >> 5);
-                e = k * syz + uint64_t(z) * g.ny + y;
+                const uint64_t u = uint64_t(z) * sxy + uint64_t(y) * g.nx + (uint64_t(k + 1) * g.tx - 1);
+                a = uint32_t(g.base + u);
+                b = uint32_t(g.base + u + 1);
+                xk = uint32_t(k);
+                xy = y;
+                xz = z;
+                xrec = DC_XFACE;
+                direct = true;
             } else if (g.ypatch) {
                 e = e_raw - yend;                    // the x faces, in their own order
             } else {
@@ -163,18 +183,24 @@ dedupe_cross_kernel(const float* __restrict__ f, const uint64_t* __restrict__ T0
             }
         }
         if (valid) {
-            uint32_t a, b;
-            decode_edge(g, e, &a, &b);
+            if (!direct) {
+                decode_edge(g, e, &a, &b);
+                if (DC_XFACE && e < g.ex) {
+                    const uint32_t ee = uint32_t(e), per = g.ny * g.nz;
+                    xk = ee / per;
+                    const uint32_t rr = ee - xk * per;
+                    xz = rr / g.ny;
+                    xy = rr - xz * g.ny;
+                    xrec = true;
+                }
+            }
             uint64_t ka, kb;
             uint32_t ba, bb;
-            if (DC_XFACE && e < g.ex) {
+            if (xrec) {
                 // x-face edge: both ends from tile_tmt's compact face records (order key, R)
                 // -- in the grid they sit 128 B apart, one line per lane
-                const uint32_t ee = uint32_t(e), per = g.ny * g.nz;
-                const uint32_t k = ee / per, rr = ee - k * per;
-                const uint32_t z = rr / g.ny, y = rr - z * g.ny;
-                const uint32_t rows = g.ty * g.tz, row = (z % g.tz) * g.ty + y % g.ty;
-                const uint64_t t = k + uint64_t(g.tiles_x) * (y / g.ty + uint64_t(g.tiles_y) * (z / g.tz));
+                const uint32_t rows = g.ty * g.tz, row = (xz % g.tz) * g.ty + xy % g.ty;
+                const uint64_t t = xk + uint64_t(g.tiles_x) * (xy / g.ty + uint64_t(g.tiles_y) * (xz / g.tz));
                 const uint64_t ea = __ldg(xface + (t * 2 + 1) * rows + row);        // right face of tile k
                 const uint64_t eb = __ldg(xface + ((t + 1) * 2) * rows + row);      // left face of tile k + 1
                 ka = key_of(uint32_t(ea >> 32), a);
@@ -184,7 +210,7 @@ dedupe_cross_kernel(const float* __restrict__ f, const uint64_t* __restrict__ T0
             } else {
                 ka = key_of(ord32(__ldg(f + a)) ^ flip, a);
                 kb = key_of(ord32(__ldg(f + b)) ^ flip, b);
-                // tile representative at the vertex's own level (DESIGN.md derivation C'''): the
+                // tile representative at the vertex's own level (DESIGN.md derivation C-3): the
                 // tile store's v for a regular vertex (s = u), the vertex itself for a minimum
                 const uint64_t ta = __ldg(reinterpret_cast<const unsigned long long*>(T0 + a));
                 const uint64_t tb = __ldg(reinterpret_cast<const unsigned long long*>(T0 + b));

@@ -65,8 +65,12 @@ struct ForestView {
         }
         return Cell{F.cells[i].lo, F.cells[i].hi};
     }
+    // f of a remote saddle with a zero value (the only ones the repair gathers): a record's own
+    // f bits, else the saddle table of forest_build
     __device__ __forceinline__ float value(const float* f, uint32_t x) const {
         if (mine(x)) return __ldg(f + x);
+        const uint32_t i = forest_lookup(F, x);
+        if (i != FOREST_MISS) return __uint_as_float(F.recs[i].f_bits);
         uint32_t bits = 0;
         if (!forest_value(F, x, &bits)) atomicOr(F.err, ERR_FOREST);
         return __uint_as_float(bits);

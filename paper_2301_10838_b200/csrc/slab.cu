@@ -118,8 +118,10 @@ forest_build_kernel(const mt_forest_record* __restrict__ all, uint64_t n_all, un
         const mt_forest_record r = all[i];
         cells[i] = Cell{r.key_s, r.hi};
         table_put(table, mask, r.id, uint32_t(i));
-        table_put(vtable, mask, r.id, r.f_bits);
-        table_put(vtable, mask, uint32_t(r.key_s), r.s_f_bits);
+        // the f bits of a record's saddle are needed only where the order key cannot give them
+        // back: a zero value (-0 and +0 share one key, reading R2; diagram values are copied from
+        // the input, R14) -- every other value is the inverse of the key's order bits
+        if ((r.s_f_bits & 0x7fffffffu) == 0u) table_put(vtable, mask, uint32_t(r.key_s), r.s_f_bits);
     }
 }
 

@@ -12,6 +12,8 @@ METRICS = [
     ("lts__t_sector_hit_rate.pct", "L2 hit %"),
     ("sm__throughput.avg.pct_of_peak_sustained_elapsed", "SM %pk"),
     ("smsp__thread_inst_executed_per_inst_executed.ratio", "thr/inst"),
+    ("smsp__inst_executed.sum", "warp inst"),
+    ("smsp__issue_active.avg.pct_of_peak_sustained_active", "issue %"),
     ("sm__warps_active.avg.pct_of_peak_sustained_active", "occ %"),
     ("launch__registers_per_thread", "regs"),
     ("launch__grid_size", "grid"),

@@ -73,3 +73,18 @@ def test_nccl_dist_one_rank_through_c_abi(cfg, scale, split):
         assert (npairs, ness) == (npo, neo)
         assert _lib.pairs_to_numpy(rec).tobytes() == po.tobytes()
     assert _lib.mt_last_launch_count(s.ctx) >= 6
+
+
+def test_virtual_ranks_zero_saddles():
+    """Saddles at -0.0 / +0.0 across slab boundaries: the diagram's death values are the input's
+    bits (reading R14) even when the saddle's record lives on another rank (the forest keeps the f
+    bits of zero-valued saddles, whose order key cannot tell -0 from +0, reading R2)."""
+    dims = (40, 24, 32)
+    z, y, x = np.meshgrid(np.arange(32), np.arange(24), np.arange(40), indexing="ij")
+    rng = np.random.default_rng(11)
+    f = np.where((x + y + z) % 2 == 0, -1.0, 0.0).astype(np.float32)
+    neg = rng.random(f.shape) < 0.5
+    f[(f == 0.0) & neg] = -0.0
+    f = f.reshape(-1)
+    for p in (2, 4):
+        check(f, dims, p)
