@@ -6,6 +6,7 @@ from __future__ import annotations
 
 import glob
 import os
+import tempfile
 import subprocess
 import sys
 
@@ -39,7 +40,9 @@ def build(force: bool = False, verbose: bool = False, defines=(), out: str | Non
     variant builds for A/B experiments, scripts/ab_build.py)."""
     if out is None and not force and not stale():
         return SO
-    objdir = os.path.join(PKG, "build" if out is None else "build_" + os.path.basename(out).replace(".so", ""))
+    # variant builds keep their objects outside the tree (they would travel with every gpurun push)
+    objdir = os.path.join(PKG, "build") if out is None else \
+        os.path.join(tempfile.gettempdir(), "mt_build_" + os.path.basename(out).replace(".so", ""))
     os.makedirs(objdir, exist_ok=True)
     objs = []
     for src in sources():

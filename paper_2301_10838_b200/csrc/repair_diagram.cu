@@ -107,7 +107,7 @@ struct BrickGeom {
     uint32_t by, bx_n, by_n;   // brick rows along y; bricks along x and y (brick mode)
 };
 
-template <class View, int BY, bool TILED>
+template <class View, int BY, bool TILED, bool COUNT>
 __global__ void __launch_bounds__(RB_THREADS, MT_REPAIR_MINB)
 repair_brick_kernel(View view, const Cell* C, uint64_t* __restrict__ T, const float* __restrict__ f, Slab sl,
                     BrickGeom g, uint32_t flip, mt_pair* __restrict__ stage, uint64_t stage_cap,
@@ -292,7 +292,7 @@ repair_brick_kernel(View view, const Cell* C, uint64_t* __restrict__ T, const fl
     }
 
     // Rep(u, key(s)): walk from v through cells with key(s') <= key(s) that are not roots
-    unsigned long long hops = 0;
+    unsigned long long hops = 0;   // (COUNT builds only: mt_set_stats)
     uint32_t moved = 0;       // rows whose walk left its start (bit k)
 #if MT_REPAIR_SEQ
     // one walk after the other (the loop runs the sum of the chain lengths, not RB_PER times
@@ -306,7 +306,7 @@ repair_brick_kernel(View view, const Cell* C, uint64_t* __restrict__ T, const fl
             const Cell c = view.cell(C, x);
             if (cv_of(c) == x || c.lo > key[k]) break;   // Alg. 4, reading R20
             x = cv_of(c);
-            ++hops;
+            if (COUNT) ++hops;
         }
         moved |= uint32_t(x != xs[k]) << k;
         xs[k] = x;
@@ -328,7 +328,7 @@ repair_brick_kernel(View view, const Cell* C, uint64_t* __restrict__ T, const fl
             } else {
                 xs[k] = cv_of(c);
                 moved |= 1u << k;
-                ++hops;
+                if (COUNT) ++hops;
             }
         }
     }
@@ -338,7 +338,7 @@ repair_brick_kernel(View view, const Cell* C, uint64_t* __restrict__ T, const fl
 #pragma unroll
     for (int k = 0; k < RB_PER; ++k)
         if (INB(k) && !((keep >> k) & 1u)) T[UID(k)] = pack(sv[k], xs[k]);
-    if (stats && hops) atomicAdd(stats + ST_REPAIR_HOPS, hops);
+    if (COUNT && hops) atomicAdd(stats + ST_REPAIR_HOPS, hops);
 #undef UID
 #undef INB
 #undef FMASK
@@ -481,20 +481,24 @@ __global__ void finish_diagram_kernel(unsigned long long* __restrict__ counters,
     }
 }
 
+template <class View, int BY, bool TILED, bool COUNT>
+void launch_brick_v(const View& view, const Cell* C, uint64_t* T, const float* f, const Slab& sl, BrickGeom g,
+                    uint64_t nb, uint32_t flip, const RepairOut& o, unsigned long long* stats, cudaStream_t stream) {
+    auto kern = repair_brick_kernel<View, BY, TILED, COUNT>;
+    ensure_smem_attr(reinterpret_cast<const void*>(kern), int(sizeof(RepairSmem)));
+    kern<<<uint32_t(nb), RB_THREADS, sizeof(RepairSmem), stream>>>(view, C, T, f, sl, g, flip, o.stage, o.stage_cap,
+                                                                  o.seg_cnt, o.seg_pos, o.counters, stats);
+}
+
 template <class View, int BY>
 void launch_brick(const View& view, const Cell* C, uint64_t* T, const float* f, const Slab& sl, BrickGeom g,
                   uint64_t nb, uint32_t flip, const RepairOut& o, bool tiled, unsigned long long* stats,
                   cudaStream_t stream) {
-    if (tiled) {
-        ensure_smem_attr(reinterpret_cast<const void*>(repair_brick_kernel<View, BY, true>), int(sizeof(RepairSmem)));
-        repair_brick_kernel<View, BY, true><<<uint32_t(nb), RB_THREADS, sizeof(RepairSmem), stream>>>(
-            view, C, T, f, sl, g, flip, o.stage, o.stage_cap, o.seg_cnt, o.seg_pos, o.counters, stats);
-    } else {
-        ensure_smem_attr(reinterpret_cast<const void*>(repair_brick_kernel<View, BY, false>),
-                         int(sizeof(RepairSmem)));
-        repair_brick_kernel<View, BY, false><<<uint32_t(nb), RB_THREADS, sizeof(RepairSmem), stream>>>(
-            view, C, T, f, sl, g, flip, o.stage, o.stage_cap, o.seg_cnt, o.seg_pos, o.counters, stats);
-    }
+    // the hop counter of the statistics costs an add per walk step: a separate instantiation
+    if (tiled && stats) launch_brick_v<View, BY, true, true>(view, C, T, f, sl, g, nb, flip, o, stats, stream);
+    else if (tiled) launch_brick_v<View, BY, true, false>(view, C, T, f, sl, g, nb, flip, o, stats, stream);
+    else if (stats) launch_brick_v<View, BY, false, true>(view, C, T, f, sl, g, nb, flip, o, stats, stream);
+    else launch_brick_v<View, BY, false, false>(view, C, T, f, sl, g, nb, flip, o, stats, stream);
 }
 
 // brick geometry: 3-D bricks 32 x 16 x (RB_ROWS / 16) on volumes, 32 x RB_ROWS on images, id ranges otherwise

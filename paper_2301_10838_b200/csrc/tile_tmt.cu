@@ -60,9 +60,6 @@ namespace {
 #ifndef TILE_MINB
 #define TILE_MINB 2    // __launch_bounds__ min blocks per SM (register budget knob)
 #endif
-#ifndef TILE_MATCH
-#define TILE_MATCH 0   // hash list: a staged batch of 32 inserts only the lowest edge of each basin pair
-#endif
 #ifndef TILE_REP_SEQ
 #define TILE_REP_SEQ 1 // in-tile repair: walks one after the other (else lock-step rounds)
 #endif
@@ -536,19 +533,7 @@ tile_tmt_kernel(const float* __restrict__ f, TileOut out0, TileOut out1, uint32_
                     const uint64_t e = stage[nst - 32 + lane_c];
                     __syncwarp();
                     nst -= 32;
-#if TILE_MATCH
-                    // lanes holding one basin pair: only the lowest edge of the group is inserted
-                    // (derivation C''): the least order key of its upper end, then the least id
-                    const uint32_t pr = uint32_t(e >> LB) & PMASK, hi = uint32_t(e) & LMASK;
-                    const uint32_t grp = __match_any_sync(FULL_MASK, pr);
-                    const uint32_t o = ord[hi];
-                    const uint32_t omin = __reduce_min_sync(grp, o);
-                    const uint32_t tie = grp & __ballot_sync(FULL_MASK, o == omin);
-                    const bool win = o == omin && hi == __reduce_min_sync(tie, hi);
-                    if (win) insert_entry(e);
-#else
                     insert_entry(e);
-#endif
                 }
             }
         };
