@@ -481,6 +481,7 @@ tile_tmt_kernel(const float* __restrict__ f, TileOut out0, TileOut out1, uint32_
     auto insert_entry = [&](uint64_t entry) {
         const uint32_t pair = uint32_t(entry >> LB) & PMASK;
         const uint64_t mo = TILE_ORDBITS ? (entry >> (3 * LB)) & OBMASK : 0;
+        const uint64_t kh = TILE_ORDBITS ? 0 : key48(ord, uint32_t(entry) & LMASK);
         uint32_t h = pair_hash<TABLE>(pair);
         for (uint32_t probe = 0;;) {
             const uint64_t cur = sld64(table + h);
@@ -496,7 +497,8 @@ tile_tmt_kernel(const float* __restrict__ f, TileOut out0, TileOut out1, uint32_
             }
             const uint64_t co = TILE_ORDBITS ? (cur >> (3 * LB)) & OBMASK : 0;
             if (mo > co) break;                                  // the stored edge is lower
-            if (mo == co && key48(ord, uint32_t(entry) & LMASK) >= key48(ord, uint32_t(cur) & LMASK)) break;
+            if (mo == co && (TILE_ORDBITS ? key48(ord, uint32_t(entry) & LMASK) : kh) >= key48(ord, uint32_t(cur) & LMASK))
+                break;
             if (scas64(table + h, cur, entry) == cur) break;
         }
     };
@@ -686,8 +688,9 @@ tile_tmt_kernel(const float* __restrict__ f, TileOut out0, TileOut out1, uint32_
             if (busy) {
                 if (STATS) ++n_iters;
                 const uint64_t cu = sld64(cell + mu), cv = sld64(cell + mv);
-                const bool up_u = c_v(cu) != mu && c_key(cu) < S;   // l.2-4 + R4
-                const bool up_v = c_v(cv) != mv && c_key(cv) < S;   // l.5-8 + R4
+                const uint64_t S16 = S << 16;                       // c_key(c) < S  <=>  c < S16
+                const bool up_u = c_v(cu) != mu && cu < S16;        // l.2-4 + R4
+                const bool up_v = c_v(cv) != mv && cv < S16;        // l.5-8 + R4
                 if (TILE_BOTHCLIMB && (up_u || up_v)) {
                     // the two climbs are independent under one S: both advance in this iteration
                     if (up_u) mu = c_v(cu);
@@ -702,7 +705,7 @@ tile_tmt_kernel(const float* __restrict__ f, TileOut out0, TileOut out1, uint32_
                     uint32_t uu = mu, vv = mv;
                     uint64_t cvv = cv;
                     if (key48(ord, mv) < key48(ord, mu)) { uu = mv; vv = mu; cvv = cu; }   // l.11-12
-                    const uint64_t got = scas64(cell + vv, cvv, (S << 16) | uu);          // l.14
+                    const uint64_t got = scas64(cell + vv, cvv, S16 | uu);                // l.14
                     mu = uu;
                     if (got == cvv) {
                         if (c_v(cvv) == vv) busy = false;      // R5: displaced a root
@@ -777,11 +780,11 @@ tile_tmt_kernel(const float* __restrict__ f, TileOut out0, TileOut out1, uint32_
         const uint64_t cu = cell[(r0 + k * RSTEP) * TX + lx];
         uint32_t x = c_v(cu);
         if (TILE_STOP == 0 || TILE_STOP > 4) {
-            const uint64_t a = c_key(cu);
+            const uint64_t a16 = cu | 0xffffull;   // c_key(cx) > c_key(cu)  <=>  cx > a16
 #pragma unroll 1
             while (true) {
                 const uint64_t cx = cell[x];
-                if (c_v(cx) == x || c_key(cx) > a) break;
+                if (c_v(cx) == x || cx > a16) break;
                 x = c_v(cx);
                 if (STATS) ++n_rep;
             }
