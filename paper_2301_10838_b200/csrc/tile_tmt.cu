@@ -41,6 +41,11 @@
 //
 // Layout: f float32[n] x fastest (reading R10) read once (coalesced 128-B
 // rows).  One CTA of 512 threads per tile.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <mutex>
+
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -154,6 +159,35 @@ __device__ __forceinline__ void uf_union(uint16_t* uf, const uint32_t* ord, uint
     }
 }
 
+// ---- TMA (cp.async.bulk.tensor) staging of a tile's f into shared memory -----------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "MT_WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra MT_WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(phase)
+        : "memory");
+}
+// one tile box {32, TY, TZ} of f at (x, y, z) (slab-local coordinates) into dst; out-of-grid
+// elements arrive as zeros (the kernel masks them by coordinates)
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int x, int y, int z, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
+            smem_u32(dst)),
+        "l"(map), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+        : "memory");
+}
+
 // Output pointers of one tree.  DUAL launches compute two trees from one read of f: the merge
 // (join) tree into the first set and the split tree (complemented order keys, reading R16) into
 // the second.
@@ -164,10 +198,11 @@ struct TileOut {
     unsigned long long* counters;
 };
 
-template <int TY, int TZ, bool STATS, bool DUAL, int NV = TX * TY * TZ, int THREADS = NV / TILE_VPT,
+template <int TY, int TZ, bool STATS, bool DUAL, bool TMA, int NV = TX * TY * TZ, int THREADS = NV / TILE_VPT,
           int TABLE = table_slots(NV)>
 __global__ void __launch_bounds__(THREADS, TILE_MINB)
-tile_tmt_kernel(const float* __restrict__ f, TileOut out0, TileOut out1, uint32_t nx,
+tile_tmt_kernel(const __grid_constant__ CUtensorMap fmap, const float* __restrict__ f, TileOut out0, TileOut out1,
+                uint32_t nx,
                 uint32_t ny, uint32_t z_begin,
                 uint32_t z_end, uint32_t tiles_x, uint32_t tiles_y, uint32_t flip,
                 unsigned long long* __restrict__ stats) {
@@ -179,7 +214,7 @@ tile_tmt_kernel(const float* __restrict__ f, TileOut out0, TileOut out1, uint32_
     constexpr int LB = NV > 4096 ? 13 : 12;          // bits of a local vertex id
     constexpr uint32_t LMASK = (1u << LB) - 1u, PMASK = (1u << (2 * LB)) - 1u;
     static_assert(NV <= 8192, "local ids: 13 bits (and 16-bit cell fields)");
-    extern __shared__ __align__(16) unsigned char smem[];
+    extern __shared__ __align__(1024) unsigned char smem[];
     uint64_t* cell = reinterpret_cast<uint64_t*>(smem);
     uint32_t* ord = reinterpret_cast<uint32_t*>(smem + NV * 8);
     __shared__ int s_overflow;
@@ -218,18 +253,30 @@ tile_tmt_kernel(const float* __restrict__ f, TileOut out0, TileOut out1, uint32_
 
     // ---- K1: load f once, order keys into shared memory ------------------------------
     bool bad = false;
-#pragma unroll
-    for (int k = 0; k < PER; ++k) {
-        const int r = r0 + k * RSTEP;
-        const int ly = r % TY, lz = r / TY;
-        const uint32_t gx = x0 + lx, gy = y0 + ly, gz = z0 + lz;
-        uint32_t o = ABSENT;
-        if (gx < nx && gy < ny && gz < z_end) {
-            const float val = __ldg(f + (uint64_t(gz) * sxy + uint64_t(gy) * nx + gx));
-            bad |= nonfinite(val);
-            o = ord32(val) ^ flip;
+    __shared__ alignas(8) uint64_t s_fbar;
+    if (TMA) {
+        // the whole tile box in one bulk tensor copy issued by one thread (the f staging is the
+        // ord array itself: 4 B per vertex, converted in place below); the table init overlaps it
+        if (threadIdx.x == 0) {
+            mbar_init(&s_fbar, 1);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+            mbar_expect_tx(&s_fbar, uint32_t(NV) * 4u);
+            tma_load_3d(ord, &fmap, int(x0), int(y0), int(z0 - z_begin), &s_fbar);
         }
-        ord[r * TX + lx] = o;
+    } else {
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+            const int r = r0 + k * RSTEP;
+            const int ly = r % TY, lz = r / TY;
+            const uint32_t gx = x0 + lx, gy = y0 + ly, gz = z0 + lz;
+            uint32_t o = ABSENT;
+            if (gx < nx && gy < ny && gz < z_end) {
+                const float val = __ldg(f + (uint64_t(gz) * sxy + uint64_t(gy) * nx + gx));
+                bad |= nonfinite(val);
+                o = ord32(val) ^ flip;
+            }
+            ord[r * TX + lx] = o;
+        }
     }
 #if TILE_KRUSKAL
     for (int i = threadIdx.x; i < NV; i += THREADS) uf[i] = uint16_t(i);
@@ -242,6 +289,24 @@ tile_tmt_kernel(const float* __restrict__ f, TileOut out0, TileOut out1, uint32_
         s_omin = ~0u;
         s_omax = 0;
         s_nkept = 0;
+    }
+    if (TMA) {
+        __syncthreads();                 // (the barrier's init is visible to every waiting thread)
+        mbar_wait(&s_fbar, 0);
+        const float* fv = reinterpret_cast<const float*>(ord);
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+            const int r = r0 + k * RSTEP;
+            const int ly = r % TY, lz = r / TY;
+            const uint32_t i = r * TX + lx;
+            uint32_t o = ABSENT;
+            if (x0 + lx < nx && y0 + ly < ny && z0 + lz < z_end) {
+                const float val = fv[i];
+                bad |= nonfinite(val);
+                o = ord32(val) ^ flip;
+            }
+            ord[i] = o;                  // in place: every element is owned by one thread
+        }
     }
     if (__syncthreads_or(bad) && threadIdx.x == 0) {
         atomicOr(out0.counters + CTR_ERR, ERR_NONFINITE);
@@ -481,7 +546,7 @@ tile_tmt_kernel(const float* __restrict__ f, TileOut out0, TileOut out1, uint32_
     auto insert_entry = [&](uint64_t entry) {
         const uint32_t pair = uint32_t(entry >> LB) & PMASK;
         const uint64_t mo = TILE_ORDBITS ? (entry >> (3 * LB)) & OBMASK : 0;
-        const uint64_t kh = TILE_ORDBITS ? 0 : key48(ord, uint32_t(entry) & LMASK);
+        const uint32_t hme = uint32_t(entry) & LMASK, ome = ord[hme];
         uint32_t h = pair_hash<TABLE>(pair);
         for (uint32_t probe = 0;;) {
             const uint64_t cur = sld64(table + h);
@@ -497,8 +562,10 @@ tile_tmt_kernel(const float* __restrict__ f, TileOut out0, TileOut out1, uint32_
             }
             const uint64_t co = TILE_ORDBITS ? (cur >> (3 * LB)) & OBMASK : 0;
             if (mo > co) break;                                  // the stored edge is lower
-            if (mo == co && (TILE_ORDBITS ? key48(ord, uint32_t(entry) & LMASK) : kh) >= key48(ord, uint32_t(cur) & LMASK))
-                break;
+            if (mo == co) {                                      // the stored edge is lower or equal
+                const uint32_t hcu = uint32_t(cur) & LMASK, ocu = ord[hcu];
+                if (ome > ocu || (ome == ocu && hme >= hcu)) break;
+            }
             if (scas64(table + h, cur, entry) == cur) break;
         }
     };
@@ -659,7 +726,7 @@ tile_tmt_kernel(const float* __restrict__ f, TileOut out0, TileOut out1, uint32_
 #pragma unroll 1
     for (int mp = 0; mp < NPASS; ++mp) {
         bool busy = false;
-        uint64_t S = 0;
+        uint64_t S = 0, S16 = 0;
         uint32_t mu = 0, mv = 0, run_pos = 0;
         const uint32_t run_n = (TILE_STOP == 0 || TILE_STOP > 3) ? run_len : 0u;
 #pragma unroll 1
@@ -678,6 +745,7 @@ tile_tmt_kernel(const float* __restrict__ f, TileOut out0, TileOut out1, uint32_
 #endif
                             if (STATS) ++n_pairs;
                             run_edge(j, &mu, &mv, &S);
+                            S16 = S << 16;                    // the level as a cell bound
                             busy = true;
                         }
                     }
@@ -687,8 +755,7 @@ tile_tmt_kernel(const float* __restrict__ f, TileOut out0, TileOut out1, uint32_
             if (!__any_sync(FULL_MASK, busy) && run_pos >= run_n) break;
             if (busy) {
                 if (STATS) ++n_iters;
-                const uint64_t cu = sld64(cell + mu), cv = sld64(cell + mv);
-                const uint64_t S16 = S << 16;                       // c_key(c) < S  <=>  c < S16
+                const uint64_t cu = sld64(cell + mu), cv = sld64(cell + mv);   // c_key(c) < S <=> c < S16
                 const bool up_u = c_v(cu) != mu && cu < S16;        // l.2-4 + R4
                 const bool up_v = c_v(cv) != mv && cv < S16;        // l.5-8 + R4
                 if (TILE_BOTHCLIMB && (up_u || up_v)) {
@@ -704,12 +771,13 @@ tile_tmt_kernel(const float* __restrict__ f, TileOut out0, TileOut out1, uint32_
                 } else {
                     uint32_t uu = mu, vv = mv;
                     uint64_t cvv = cv;
-                    if (key48(ord, mv) < key48(ord, mu)) { uu = mv; vv = mu; cvv = cu; }   // l.11-12
+                    const uint32_t omv = ord[mv], omu = ord[mu];
+                    if (omv < omu || (omv == omu && mv < mu)) { uu = mv; vv = mu; cvv = cu; }   // l.11-12
                     const uint64_t got = scas64(cell + vv, cvv, S16 | uu);                // l.14
                     mu = uu;
                     if (got == cvv) {
                         if (c_v(cvv) == vv) busy = false;      // R5: displaced a root
-                        S = c_key(cvv);                       // l.15: Merge(T, u, s_v, v')
+                        S16 = cvv & ~0xffffull;               // l.15: Merge(T, u, s_v, v')
                         mv = c_v(cvv);
                     } else {
                         mv = vv;                              // l.17: restart
@@ -888,26 +956,74 @@ void tile_shape(uint32_t nz_global, uint32_t* ty, uint32_t* tz) {
     }
 }
 
-template <int TY, int TZ, bool STATS, bool DUAL>
-void launch_tile_v(const float* f, const TileOut& o0, const TileOut& o1, const Slab& sl, uint32_t tx, uint32_t tyn,
-                   uint32_t grid, uint32_t flip, unsigned long long* stats, cudaStream_t stream) {
+#ifndef TILE_TMA
+#define TILE_TMA 1     // stage each tile's f with one TMA bulk tensor copy (grids with nx % 4 == 0)
+#endif
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no link-time libcuda)
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    });
+    return fn;
+}
+
+// the slab's f as a 3-D tensor {nx, ny, nz_local} of float32 with tile boxes {32, TY, TZ}; false
+// when TMA does not apply (row stride not a multiple of 16 B, unaligned base, no encoder)
+template <int TY, int TZ>
+bool make_fmap(CUtensorMap* m, const float* f_local, const Slab& sl) {
+    const uint64_t nzl = sl.z_end - sl.z_begin;
+    if (!TILE_TMA || sl.nx % 4 || (reinterpret_cast<uintptr_t>(f_local) % 16) || nzl == 0) return false;
+    PFN_cuTensorMapEncodeTiled_v12000 enc = tensor_map_encoder();
+    if (!enc) return false;
+    const cuuint64_t dims[3] = {sl.nx, sl.ny, nzl};
+    const cuuint64_t strides[2] = {uint64_t(sl.nx) * 4, uint64_t(sl.nx) * sl.ny * 4};
+    const cuuint32_t box[3] = {uint32_t(TX), uint32_t(TY), uint32_t(TZ)};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(f_local), dims, strides, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int TY, int TZ, bool STATS, bool DUAL, bool TMA>
+void launch_tile_v(const CUtensorMap& m, const float* f, const TileOut& o0, const TileOut& o1, const Slab& sl,
+                   uint32_t tx, uint32_t tyn, uint32_t grid, uint32_t flip, unsigned long long* stats,
+                   cudaStream_t stream) {
     constexpr int NV = TX * TY * TZ;
-    auto kern = tile_tmt_kernel<TY, TZ, STATS, DUAL>;
+    auto kern = tile_tmt_kernel<TY, TZ, STATS, DUAL, TMA>;
     ensure_smem_attr(reinterpret_cast<const void*>(kern), int(smem_bytes<NV>()));
-    kern<<<grid, NV / TILE_VPT, smem_bytes<NV>(), stream>>>(f, o0, o1, sl.nx, sl.ny, sl.z_begin, sl.z_end, tx, tyn, flip,
-                                                     stats);
+    kern<<<grid, NV / TILE_VPT, smem_bytes<NV>(), stream>>>(m, f, o0, o1, sl.nx, sl.ny, sl.z_begin, sl.z_end, tx, tyn,
+                                                            flip, stats);
+}
+
+template <int TY, int TZ, bool TMA>
+void launch_tile_t(const CUtensorMap& m, const float* f, const TileOut& o0, const TileOut* o1, const Slab& sl,
+                   uint32_t tx, uint32_t tyn, uint32_t grid, uint32_t flip, unsigned long long* stats,
+                   cudaStream_t stream) {
+    if (o1) {
+        if (stats) launch_tile_v<TY, TZ, true, true, TMA>(m, f, o0, *o1, sl, tx, tyn, grid, 0u, stats, stream);
+        else launch_tile_v<TY, TZ, false, true, TMA>(m, f, o0, *o1, sl, tx, tyn, grid, 0u, stats, stream);
+    } else {
+        if (stats) launch_tile_v<TY, TZ, true, false, TMA>(m, f, o0, o0, sl, tx, tyn, grid, flip, stats, stream);
+        else launch_tile_v<TY, TZ, false, false, TMA>(m, f, o0, o0, sl, tx, tyn, grid, flip, stats, stream);
+    }
 }
 
 template <int TY, int TZ>
 void launch_tile(const float* f, const TileOut& o0, const TileOut* o1, const Slab& sl, uint32_t tx, uint32_t tyn,
                  uint32_t grid, uint32_t flip, unsigned long long* stats, cudaStream_t stream) {
-    if (o1) {
-        if (stats) launch_tile_v<TY, TZ, true, true>(f, o0, *o1, sl, tx, tyn, grid, 0u, stats, stream);
-        else launch_tile_v<TY, TZ, false, true>(f, o0, *o1, sl, tx, tyn, grid, 0u, stats, stream);
-    } else {
-        if (stats) launch_tile_v<TY, TZ, true, false>(f, o0, o0, sl, tx, tyn, grid, flip, stats, stream);
-        else launch_tile_v<TY, TZ, false, false>(f, o0, o0, sl, tx, tyn, grid, flip, stats, stream);
-    }
+    CUtensorMap m;
+    memset(&m, 0, sizeof(m));
+    if (make_fmap<TY, TZ>(&m, f + sl.base + uint64_t(0), sl))   // f is shifted by -base: the slab's own array
+        launch_tile_t<TY, TZ, true>(m, f, o0, o1, sl, tx, tyn, grid, flip, stats, stream);
+    else
+        launch_tile_t<TY, TZ, false>(m, f, o0, o1, sl, tx, tyn, grid, flip, stats, stream);
 }
 
 void launch_tile_any(const float* f, const TileOut& o0, const TileOut* o1, const Slab& sl, uint32_t flip,
