@@ -133,6 +133,7 @@ enum CounterSlot : int {
     CTR_FILT_KEPT = 9,    // mt_filter_diagram: records kept
     CTR_STAGE = 10,       // diagram records staged by the repair bricks
     CTR_FQLEN = 11,       // deduplicated inter-slab edges queued (forest_dedupe)
+    CTR_TILE = 12,        // persistent tile_tmt: next tile ticket
     CTR_COUNT = 16
 };
 

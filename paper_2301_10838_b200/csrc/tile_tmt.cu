@@ -198,11 +198,11 @@ struct TileOut {
     unsigned long long* counters;
 };
 
-template <int TY, int TZ, bool STATS, bool DUAL, bool TMA, int NV = TX * TY * TZ, int THREADS = NV / TILE_VPT,
-          int TABLE = table_slots(NV)>
+template <int TY, int TZ, bool STATS, bool DUAL, bool TMA, bool PERSIST, int NV = TX * TY * TZ,
+          int THREADS = NV / TILE_VPT, int TABLE = table_slots(NV)>
 __global__ void __launch_bounds__(THREADS, TILE_MINB)
 tile_tmt_kernel(const __grid_constant__ CUtensorMap fmap, const float* __restrict__ f, TileOut out0, TileOut out1,
-                uint32_t nx,
+                uint32_t ntiles, uint32_t nx,
                 uint32_t ny, uint32_t z_begin,
                 uint32_t z_end, uint32_t tiles_x, uint32_t tiles_y, uint32_t flip,
                 unsigned long long* __restrict__ stats) {
@@ -214,7 +214,7 @@ tile_tmt_kernel(const __grid_constant__ CUtensorMap fmap, const float* __restric
     constexpr int LB = NV > 4096 ? 13 : 12;          // bits of a local vertex id
     constexpr uint32_t LMASK = (1u << LB) - 1u, PMASK = (1u << (2 * LB)) - 1u;
     static_assert(NV <= 8192, "local ids: 13 bits (and 16-bit cell fields)");
-    extern __shared__ __align__(1024) unsigned char smem[];
+    extern __shared__ __align__(128) unsigned char smem[];
     uint64_t* cell = reinterpret_cast<uint64_t*>(smem);
     uint32_t* ord = reinterpret_cast<uint32_t*>(smem + NV * 8);
     __shared__ int s_overflow;
@@ -240,21 +240,46 @@ tile_tmt_kernel(const __grid_constant__ CUtensorMap fmap, const float* __restric
         }
     };
 
-    const uint32_t b = blockIdx.x;
-    const uint32_t bx = b % tiles_x, by = (b / tiles_x) % tiles_y, bz = b / (tiles_x * tiles_y);
-    // f and C are indexed by GLOBAL vertex id (the caller passes pointers shifted by the
-    // slab's first id); this CTA's tile starts at global plane z0
-    const uint32_t x0 = bx * TX, y0 = by * TY, z0 = z_begin + bz * TZ;
     const uint64_t sxy = uint64_t(nx) * ny;
     const int lx = threadIdx.x & (TX - 1);
     const int r0 = threadIdx.x / TX;
     const int lane_c = threadIdx.x & 31;
     const int warp_d = threadIdx.x >> 5;
+    __shared__ alignas(8) uint64_t s_fbar;
+    // PERSIST (TMA, hash variant): one CTA per resident slot walks the tiles b = blockIdx.x +
+    // i * gridDim.x; tile i+1's f is bulk-copied into the list phase's staging buffer (idle
+    // from the end of tile i's list phase on) while tile i merges, repairs and writes
+    [[maybe_unused]] float* const fpre =
+        reinterpret_cast<float*>(smem + NV * 12 + TABLE * 8);   // NV floats = the staging buffer
+    auto tile_origin = [&](uint32_t t, uint32_t* ox, uint32_t* oy, uint32_t* oz) {
+        *ox = (t % tiles_x) * TX;
+        *oy = ((t / tiles_x) % tiles_y) * TY;
+        *oz = z_begin + (t / (tiles_x * tiles_y)) * TZ;
+    };
+    if (PERSIST) {
+        if (threadIdx.x == 0 && blockIdx.x < ntiles) {
+            uint32_t px, py, pz;
+            tile_origin(blockIdx.x, &px, &py, &pz);
+            mbar_init(&s_fbar, 1);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+            mbar_expect_tx(&s_fbar, uint32_t(NV) * 4u);
+            tma_load_3d(fpre, &fmap, int(px), int(py), int(pz - z_begin), &s_fbar);
+        }
+        __syncthreads();
+    }
+    uint32_t it = 0;
+    __shared__ uint32_t s_next;       // PERSIST: the CTA's next tile (dynamic tickets)
+    if (PERSIST && threadIdx.x == 0) s_next = ntiles;
+#pragma unroll 1
+    for (uint32_t b = blockIdx.x; b < (PERSIST ? ntiles : blockIdx.x + 1); ++it) {
+    uint32_t x0, y0, z0;
+    tile_origin(b, &x0, &y0, &z0);
+    // f and C are indexed by GLOBAL vertex id (the caller passes pointers shifted by the
+    // slab's first id); this tile starts at global plane z0
 
     // ---- K1: load f once, order keys into shared memory ------------------------------
     bool bad = false;
-    __shared__ alignas(8) uint64_t s_fbar;
-    if (TMA) {
+    if (TMA && !PERSIST) {
         // the whole tile box in one bulk tensor copy issued by one thread (the f staging is the
         // ord array itself: 4 B per vertex, converted in place below); the table init overlaps it
         if (threadIdx.x == 0) {
@@ -291,9 +316,9 @@ tile_tmt_kernel(const __grid_constant__ CUtensorMap fmap, const float* __restric
         s_nkept = 0;
     }
     if (TMA) {
-        __syncthreads();                 // (the barrier's init is visible to every waiting thread)
-        mbar_wait(&s_fbar, 0);
-        const float* fv = reinterpret_cast<const float*>(ord);
+        if (!PERSIST) __syncthreads();   // (the barrier's init is visible to every waiting thread)
+        mbar_wait(&s_fbar, PERSIST ? (it & 1u) : 0u);
+        const float* fv = PERSIST ? fpre : reinterpret_cast<const float*>(ord);
 #pragma unroll
         for (int k = 0; k < PER; ++k) {
             const int r = r0 + k * RSTEP;
@@ -662,6 +687,19 @@ tile_tmt_kernel(const __grid_constant__ CUtensorMap fmap, const float* __restric
     }
     __syncthreads();
     phase_time(ST_CYC_LIST);
+    if (PERSIST && threadIdx.x == 0 && pass == (DUAL ? 1 : 0)) {
+        // the staging buffer is idle until the next tile's list phase: the next tile (a dynamic
+        // ticket, so that CTAs with cheap tiles take more) has its f copied there now
+        const uint32_t nb = gridDim.x + uint32_t(atomicAdd(out0.counters + CTR_TILE, 1ull));
+        s_next = nb;
+        if (nb < ntiles) {
+            uint32_t px, py, pz;
+            tile_origin(nb, &px, &py, &pz);
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // after the generic-proxy staging
+            mbar_expect_tx(&s_fbar, uint32_t(NV) * 4u);
+            tma_load_3d(fpre, &fmap, int(px), int(py), int(pz - z_begin), &s_fbar);
+        }
+    }
     // most table slots are empty: every warp compacts its 1/NW of the table in place (a chunk of
     // 32 slots is read before any of its lanes writes, and a write never lands past the chunk
     // being read); the warp then merges the pairs of its own run
@@ -921,6 +959,13 @@ tile_tmt_kernel(const __grid_constant__ CUtensorMap fmap, const float* __restric
     }
     phase_time(ST_CYC_WRITE);
     }   // pass
+    if (PERSIST) {
+        __syncthreads();            // the next tile overwrites ord and the cells
+        b = s_next;
+    } else {
+        b = ntiles;
+    }
+    }   // tile
     if (STATS) {
         atomicAdd(stats + ST_TILE_EDGES, n_edges);
         atomicAdd(stats + ST_TILE_ITERS, n_iters);
@@ -991,15 +1036,29 @@ bool make_fmap(CUtensorMap* m, const float* f_local, const Slab& sl) {
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+#ifndef TILE_PERSIST
+#define TILE_PERSIST 0 // TMA tiles: persistent CTAs, the next tile's f prefetched during the merge
+#endif
+
 template <int TY, int TZ, bool STATS, bool DUAL, bool TMA>
 void launch_tile_v(const CUtensorMap& m, const float* f, const TileOut& o0, const TileOut& o1, const Slab& sl,
                    uint32_t tx, uint32_t tyn, uint32_t grid, uint32_t flip, unsigned long long* stats,
                    cudaStream_t stream) {
     constexpr int NV = TX * TY * TZ;
-    auto kern = tile_tmt_kernel<TY, TZ, STATS, DUAL, TMA>;
+    constexpr bool PERSIST = TMA && TILE_PERSIST && !TILE_KRUSKAL;
+    auto kern = tile_tmt_kernel<TY, TZ, STATS, DUAL, TMA, PERSIST>;
     ensure_smem_attr(reinterpret_cast<const void*>(kern), int(smem_bytes<NV>()));
-    kern<<<grid, NV / TILE_VPT, smem_bytes<NV>(), stream>>>(m, f, o0, o1, sl.nx, sl.ny, sl.z_begin, sl.z_end, tx, tyn,
-                                                            flip, stats);
+    uint32_t blocks = grid;
+    if (PERSIST) {   // one CTA per resident slot
+        int dev = 0, sms = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        const uint64_t slots = uint64_t(sms) *
+                               occupancy_per_sm(reinterpret_cast<const void*>(kern), NV / TILE_VPT, smem_bytes<NV>());
+        if (slots < blocks) blocks = uint32_t(slots);
+    }
+    kern<<<blocks, NV / TILE_VPT, smem_bytes<NV>(), stream>>>(m, f, o0, o1, grid, sl.nx, sl.ny, sl.z_begin, sl.z_end,
+                                                              tx, tyn, flip, stats);
 }
 
 template <int TY, int TZ, bool TMA>
