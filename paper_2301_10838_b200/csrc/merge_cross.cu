@@ -62,6 +62,9 @@ namespace {
 #ifndef DC_XPATCH
 #define DC_XPATCH 1       // the x faces in 32 (y) x 8 (z) patches too
 #endif
+#ifndef DC_NDEDUP
+#define DC_NDEDUP 1       // patch steps: drop edges whose neighbour lane has the same pair lower
+#endif
 #ifndef DC_REDUCE
 #define DC_REDUCE 0       // group minimum by two __reduce_min_sync (else a 32-lane shuffle scan)
 #endif
@@ -250,6 +253,18 @@ dedupe_cross_kernel(const float* __restrict__ f, const uint64_t* __restrict__ T0
             if ((lane > 0 && pu == pair && lu < en.L) || (lane < 31 && pd == pair && ld < en.L)) keep = false;
         }
 #endif
+#if DC_NDEDUP
+        if (zpatch) {
+            // neighbouring lanes of a patch hold neighbouring edges of one face, mostly between the
+            // same two tile representatives: an edge with a lower one of its pair in the next or
+            // previous lane is dropped before the CTA table (derivation C''; upper ends differ, so
+            // levels never tie)
+            const uint64_t pu = __shfl_up_sync(FULL_MASK, pair, 1), pd = __shfl_down_sync(FULL_MASK, pair, 1);
+            const uint64_t lu = __shfl_up_sync(FULL_MASK, en.L, 1), ld = __shfl_down_sync(FULL_MASK, en.L, 1);
+            if (keep && ((lane > 0 && pu == pair && lu < en.L) || (lane < 31 && pd == pair && ld < en.L)))
+                keep = false;
+        }
+#endif
         if (DC_PATCH && zpatch) {
             // CTA-wide: the warps' survivors keep the lowest edge of each pair over the patch
             s_key[threadIdx.x] = ~0ull;
@@ -316,11 +331,18 @@ merge_queue_kernel(Cell* C, const QEntry* __restrict__ q, uint64_t cap, const un
     uint64_t pool_next = 0, pool_end = 0;  // warp-uniform
     bool exhausted = false;                // warp-uniform
 
+    // The state that lives from one round trip to the next, shared between the phases (the
+    // phases are exclusive, so one set of registers serves all of them):
+    //   climbs (CLIMB_HI / CLIMB_LO): lev = L, p0 = x (walk position), p1 = xp (previous cell),
+    //     p2 = lo (the other end's representative), p3 = rh (where the first walk stopped),
+    //     held = the previous cell's value (path splitting);
+    //   Alg. 3 (MERGE_LD / MERGE_CAS): lev = S, p0 = u, p1 = v, held = T[v] as loaded (the
+    //     expected value of the CAS; the desired value is rebuilt from it).
     int phase = IDLE;
-    uint64_t L = 0, ks = 0;
-    uint32_t x = 0, xp = 0, lo = 0, rh = 0, u = 0, v = 0;
+    uint64_t lev = 0;
+    uint32_t p0 = 0, p1 = 0, p2 = 0, p3 = 0;
     bool has_prev = false;
-    Cell c{0, 0}, cp{0, 0}, cu{0, 0}, cv{0, 0}, desired{0, 0}, got{0, 0};
+    Cell held{0, 0};
     unsigned long long n_edges = 0, n_hops = 0, n_iters = 0, n_fail = 0, n_skip = 0;
 
     while (true) {
@@ -339,15 +361,13 @@ merge_queue_kernel(Cell* C, const QEntry* __restrict__ q, uint64_t cap, const un
             if (phase == IDLE) {
                 if (rank < avail) {
                     const QEntry en = q[pool_next + rank];
-                    L = en.L;
-                    x = en.m_hi;                      // walk the upper end's basin first
-                    lo = en.m_lo;
+                    lev = en.L;
+                    p0 = en.m_hi;                     // walk the upper end's basin first
+                    p2 = en.m_lo;
                     has_prev = false;
                     phase = CLIMB_HI;
                     if (!MQ_WALK) {                   // Merge(T, R_hi, hi, R_lo) straight away
-                        u = en.m_hi;
-                        v = en.m_lo;
-                        ks = L;
+                        p1 = en.m_lo;
                         phase = MERGE_LD;
                     }
                     if (STATS) n_edges++;
@@ -359,74 +379,66 @@ merge_queue_kernel(Cell* C, const QEntry* __restrict__ q, uint64_t cap, const un
         }
         if (__ballot_sync(FULL_MASK, phase != DONE) == 0) break;
 
-        // ---- one memory round-trip ----
-        if (phase == MERGE_LD) {
-            cu = ld_cell(C + u);
-            cv = ld_cell(C + v);
-        } else if (phase == CLIMB_HI || phase == CLIMB_LO) {
-            c = ld_cell(C + x);
-        } else if (phase == MERGE_CAS) {
-            got = cas_cell(C + v, cv, desired);
-        }
-
-        // ---- advance ----
+        // ---- one memory round-trip, then advance ----
         if (phase == CLIMB_HI || phase == CLIMB_LO) {
-            if (cv_of(c) != x && c.lo <= L) {          // followable at level L
+            const Cell c = ld_cell(C + p0);
+            if (cv_of(c) != p0 && c.lo <= lev) {       // followable at level L
                 if (STATS) n_hops++;
-                const bool split = MQ_SPLIT && has_prev && c.lo <= cp.lo;
+                const bool split = MQ_SPLIT && has_prev && c.lo <= held.lo;
                 if (split)                                 // path splitting: prev skips x
-                    cas_cell(C + xp, cp, Cell{cp.lo, (cp.hi & 0xffffffff00000000ull) | cv_of(c)});
+                    cas_cell(C + p1, held, Cell{held.lo, (held.hi & 0xffffffff00000000ull) | cv_of(c)});
                 if (MQ_SPLIT == 2 && split) {
                     has_prev = false;                      // path halving: every other cell
                 } else {
-                    xp = x;
-                    cp = c;
+                    p1 = p0;
+                    held = c;
                     has_prev = true;
                 }
-                x = cv_of(c);
+                p0 = cv_of(c);
             } else if (phase == CLIMB_HI) {
-                rh = x;
-                x = lo;
+                p3 = p0;
+                p0 = p2;
                 has_prev = false;
                 phase = CLIMB_LO;
-            } else if (x == rh) {                      // walks met: nothing to join
+            } else if (p0 == p3) {                     // walks met: nothing to join
                 if (STATS) n_skip++;
                 phase = IDLE;
             } else {
-                u = rh;                                // Merge(T, r_hi, hi, r_lo) at level L
-                v = x;
-                ks = L;
+                p1 = p0;                               // Merge(T, r_hi, hi, r_lo) at level L
+                p0 = p3;
                 phase = MERGE_LD;
             }
         } else if (phase == MERGE_LD) {
+            Cell cu = ld_cell(C + p0), cv = ld_cell(C + p1);
             if (STATS) n_iters++;
-            const bool up_u = cv_of(cu) != u && cu.lo < ks;   // l.2-4 (+ R4)
-            const bool up_v = cv_of(cv) != v && cv.lo < ks;   // l.5-8 (+ R4)
-            if (MQ_BOTHCLIMB && (up_u || up_v)) {             // independent climbs: both advance
-                if (up_u) u = cv_of(cu);
-                if (up_v) v = cv_of(cv);
+            const bool up_u = cv_of(cu) != p0 && cu.lo < lev;   // l.2-4 (+ R4)
+            const bool up_v = cv_of(cv) != p1 && cv.lo < lev;   // l.5-8 (+ R4)
+            if (MQ_BOTHCLIMB && (up_u || up_v)) {               // independent climbs: both advance
+                if (up_u) p0 = cv_of(cu);
+                if (up_v) p1 = cv_of(cv);
             } else if (up_u) {                         // climb u, restart
-                u = cv_of(cu);
+                p0 = cv_of(cu);
             } else if (up_v) {                         // climb v, restart
-                v = cv_of(cv);
-            } else if (u == v) {                       // l.9-10
+                p1 = cv_of(cv);
+            } else if (p0 == p1) {                     // l.9-10
                 phase = IDLE;
             } else {
-                if (self_key(cv, v) < self_key(cu, u)) {   // l.11-12: swap
-                    const uint32_t t = u; u = v; v = t;
-                    const Cell tc = cu; cu = cv; cv = tc;
+                if (self_key(cv, p1) < self_key(cu, p0)) {   // l.11-12: swap
+                    const uint32_t t = p0; p0 = p1; p1 = t;
+                    cv = cu;
                 }
-                desired = Cell{ks, (cv.hi & 0xffffffff00000000ull) | u};  // l.14: (s, u) into T[v]
+                held = cv;                             // l.14: (s, u) into T[v], next round trip
                 phase = MERGE_CAS;
             }
         } else if (phase == MERGE_CAS) {
-            if (got.lo == cv.lo && got.hi == cv.hi) {
-                const uint32_t vp = cv_of(cv);
-                if (vp == v) {
+            const Cell got = cas_cell(C + p1, held, Cell{lev, (held.hi & 0xffffffff00000000ull) | p0});
+            if (got.lo == held.lo && got.hi == held.hi) {
+                const uint32_t vp = cv_of(held);
+                if (vp == p1) {
                     phase = IDLE;                      // displaced a root (R5)
                 } else {
-                    ks = cv.lo;                        // l.15: Merge(T, u, s_v, v')
-                    v = vp;
+                    lev = held.lo;                     // l.15: Merge(T, u, s_v, v')
+                    p1 = vp;
                     phase = MERGE_LD;
                 }
             } else {
