@@ -219,12 +219,23 @@ forest_merge_kernel(ForestRef F, const FQEntry* __restrict__ q, const unsigned l
     uint64_t pool_next = 0, pool_end = 0;
     bool exhausted = false;
     int phase = IDLE;
-    uint64_t L = 0, ks = 0;
-    uint32_t x = 0, lo = 0, rh = 0, u = 0, v = 0;
-    uint32_t ix = 0, ixp = 0, iu = 0, iv = 0, ilo = 0, irh = 0;   // table indices
+    // merge_queue_kernel's state machine with every cell reached through the id table; one set
+    // of registers serves the exclusive phases (ids p*, table indices i*):
+    //   climbs: lev = L, p0/i0 = x, i1 = previous cell, p2/i2 = lo, p3/i3 = rh, held = previous cell;
+    //   Alg. 3: lev = S, p0/i0 = u, p1/i1 = v, held = T[v] as loaded (the CAS's expected value).
+    uint64_t lev = 0;
+    uint32_t p0 = 0, p1 = 0, p2 = 0, p3 = 0, i0 = 0, i1 = 0, i2 = 0, i3 = 0;
     bool has_prev = false;
-    Cell c{0, 0}, cp{0, 0}, cu{0, 0}, cv{0, 0}, desired{0, 0}, got{0, 0};
+    Cell held{0, 0};
     auto at = [&](uint32_t i) { return F.cells + i; };
+    auto lookup = [&](uint32_t id, uint32_t* i) {
+        *i = forest_lookup(F, id);
+        if (*i == FOREST_MISS) {
+            atomicOr(F.err, ERR_FOREST);
+            return false;
+        }
+        return true;
+    };
     while (true) {
         const uint32_t need = __ballot_sync(FULL_MASK, phase == IDLE);
         if (need) {
@@ -242,17 +253,11 @@ forest_merge_kernel(ForestRef F, const FQEntry* __restrict__ q, const unsigned l
                 if (rank < avail) {
                     // a deduplicated edge: walk from R_hi, then R_lo, at level L (forest_dedupe_kernel)
                     const FQEntry en = q[pool_next + rank];
-                    L = en.L;
-                    x = en.r_hi;
-                    lo = en.r_lo;
-                    ix = forest_lookup(F, x);
-                    ilo = forest_lookup(F, lo);
+                    lev = en.L;
+                    p0 = en.r_hi;
+                    p2 = en.r_lo;
                     has_prev = false;
-                    phase = CLIMB_HI;
-                    if (ix == FOREST_MISS || ilo == FOREST_MISS) {
-                        atomicOr(F.err, ERR_FOREST);
-                        phase = IDLE;
-                    }
+                    phase = (lookup(p0, &i0) && lookup(p2, &i2)) ? CLIMB_HI : IDLE;
                 } else if (exhausted) {
                     phase = DONE;
                 }
@@ -261,76 +266,66 @@ forest_merge_kernel(ForestRef F, const FQEntry* __restrict__ q, const unsigned l
         }
         if (__ballot_sync(FULL_MASK, phase != DONE) == 0) break;
 
-        if (phase == MERGE_LD) {
-            cu = ld_cell(at(iu));
-            cv = ld_cell(at(iv));
-        } else if (phase == CLIMB_HI || phase == CLIMB_LO) {
-            c = ld_cell(at(ix));
-        } else if (phase == MERGE_CAS) {
-            got = cas_cell(at(iv), cv, desired);
-        }
-
         if (phase == CLIMB_HI || phase == CLIMB_LO) {
-            if (cv_of(c) != x && c.lo <= L) {                       // followable at level L
-                if (has_prev && c.lo <= cp.lo)                      // path splitting
-                    cas_cell(at(ixp), cp, Cell{cp.lo, (cp.hi & 0xffffffff00000000ull) | cv_of(c)});
-                ixp = ix;
-                cp = c;
+            const Cell c = ld_cell(at(i0));
+            if (cv_of(c) != p0 && c.lo <= lev) {                    // followable at level L
+                if (has_prev && c.lo <= held.lo)                    // path splitting
+                    cas_cell(at(i1), held, Cell{held.lo, (held.hi & 0xffffffff00000000ull) | cv_of(c)});
+                i1 = i0;
+                held = c;
                 has_prev = true;
-                x = cv_of(c);
-                ix = forest_lookup(F, x);
-                if (ix == FOREST_MISS) {
-                    atomicOr(F.err, ERR_FOREST);
-                    phase = IDLE;
-                }
+                p0 = cv_of(c);
+                if (!lookup(p0, &i0)) phase = IDLE;
             } else if (phase == CLIMB_HI) {
-                rh = x;
-                irh = ix;
-                x = lo;
-                ix = ilo;
+                p3 = p0;
+                i3 = i0;
+                p0 = p2;
+                i0 = i2;
                 has_prev = false;
                 phase = CLIMB_LO;
-            } else if (x == rh) {
+            } else if (p0 == p3) {
                 phase = IDLE;                                       // already joined below L
             } else {
-                u = rh;                                             // Merge(T, r_hi, hi, r_lo) at level L
-                iu = irh;
-                v = x;
-                iv = ix;
-                ks = L;
+                p1 = p0;                                            // Merge(T, r_hi, hi, r_lo) at level L
+                i1 = i0;
+                p0 = p3;
+                i0 = i3;
                 phase = MERGE_LD;
             }
         } else if (phase == MERGE_LD) {
-            if (cv_of(cu) != u && cu.lo < ks) {                     // l.2-4 (+ R4)
-                u = cv_of(cu);
-                iu = forest_lookup(F, u);
-                if (iu == FOREST_MISS) { atomicOr(F.err, ERR_FOREST); phase = IDLE; }
-            } else if (cv_of(cv) != v && cv.lo < ks) {              // l.5-8 (+ R4)
-                v = cv_of(cv);
-                iv = forest_lookup(F, v);
-                if (iv == FOREST_MISS) { atomicOr(F.err, ERR_FOREST); phase = IDLE; }
-            } else if (u == v) {                                    // l.9-10
+            Cell cu = ld_cell(at(i0)), cv = ld_cell(at(i1));
+            const bool up_u = cv_of(cu) != p0 && cu.lo < lev;       // l.2-4 (+ R4)
+            const bool up_v = cv_of(cv) != p1 && cv.lo < lev;       // l.5-8 (+ R4)
+            if (up_u || up_v) {                                     // independent climbs (derivation J)
+                if (up_u) {
+                    p0 = cv_of(cu);
+                    if (!lookup(p0, &i0)) phase = IDLE;
+                }
+                if (up_v) {
+                    p1 = cv_of(cv);
+                    if (!lookup(p1, &i1)) phase = IDLE;
+                }
+            } else if (p0 == p1) {                                  // l.9-10
                 phase = IDLE;
             } else {
-                if (self_key(cv, v) < self_key(cu, u)) {            // l.11-12
-                    uint32_t t = u; u = v; v = t;
-                    t = iu; iu = iv; iv = t;
-                    const Cell tc = cu; cu = cv; cv = tc;
+                if (self_key(cv, p1) < self_key(cu, p0)) {          // l.11-12
+                    uint32_t t = p0; p0 = p1; p1 = t;
+                    t = i0; i0 = i1; i1 = t;
+                    cv = cu;
                 }
-                desired = Cell{ks, (cv.hi & 0xffffffff00000000ull) | u};   // l.14
+                held = cv;                                          // l.14, next round trip
                 phase = MERGE_CAS;
             }
         } else if (phase == MERGE_CAS) {
-            if (got.lo == cv.lo && got.hi == cv.hi) {
-                const uint32_t vp = cv_of(cv);
-                if (vp == v) {
+            const Cell got = cas_cell(at(i1), held, Cell{lev, (held.hi & 0xffffffff00000000ull) | p0});
+            if (got.lo == held.lo && got.hi == held.hi) {
+                const uint32_t vp = cv_of(held);
+                if (vp == p1) {
                     phase = IDLE;                                   // displaced a root (R5)
                 } else {
-                    ks = cv.lo;                                     // l.15
-                    v = vp;
-                    iv = forest_lookup(F, vp);
-                    phase = MERGE_LD;
-                    if (iv == FOREST_MISS) { atomicOr(F.err, ERR_FOREST); phase = IDLE; }
+                    lev = held.lo;                                  // l.15
+                    p1 = vp;
+                    phase = lookup(p1, &i1) ? MERGE_LD : IDLE;
                 }
             } else {
                 phase = MERGE_LD;                                   // l.17

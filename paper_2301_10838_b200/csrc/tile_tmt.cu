@@ -931,10 +931,12 @@ tile_tmt_kernel(const __grid_constant__ CUtensorMap fmap, const float* __restric
     // crossing edges start at tile representatives, which are minima, and every cell on a v
     // chain from a minimum is a minimum's; DESIGN.md derivation C'''), so regular vertices need
     // none (the x-face records carry (order key, R) for the tile's x faces, coalesced).
-    const uint64_t gbase = uint64_t(z0) * sxy + uint64_t(y0) * nx + x0;
+    // global ids in 32-bit arithmetic: every id and every partial sum is below n < 2^32
+    const uint32_t sxy32 = nx * ny;
+    const uint32_t gbase = z0 * sxy32 + y0 * nx + x0;
     auto gid = [&](uint32_t l) -> uint32_t {
         const uint32_t l_x = l % TX, l_r = l / TX;
-        return uint32_t(gbase + uint64_t(l_r / TY) * sxy + uint64_t(l_r % TY) * nx + l_x);
+        return gbase + (l_r / TY) * sxy32 + (l_r % TY) * nx + l_x;
     };
 #pragma unroll
     for (int k = 0; k < PER; ++k) {
@@ -945,8 +947,8 @@ tile_tmt_kernel(const __grid_constant__ CUtensorMap fmap, const float* __restric
         if (ou == ABSENT) continue;
         const uint64_t cu = cell[u];
         const uint32_t s = c_s(cu), v = rep[k];
-        const uint64_t g = gbase + uint64_t(lz) * sxy + uint64_t(ly) * nx + lx;
-        const uint32_t gu = uint32_t(g), gv = gid(v);
+        const uint32_t gu = gbase + uint32_t(lz) * sxy32 + uint32_t(ly) * nx + lx, gv = gid(v);
+        const uint64_t g = gu;
         const bool minimum = s != u || v == u;
         const uint32_t gs = s == u ? gu : gid(s);
         T0[g] = pack(gs, gv);
