@@ -204,9 +204,9 @@ def _ecross(dims):
 
 ALG_BYTES = {
     "tile_tmt": lambda n, rec, ec: 12 * n,                 # read f (4) + write the tile store (8)
-    "dedupe_cross": lambda n, rec, ec: 24 * ec,            # f + tile store of both ends of every crossing edge
+    "dedupe_cross": lambda n, rec, ec: 16 * ec,            # the tile store (order key, R) of both ends
     "merge_queue": lambda n, rec, ec: 2 * 8 * ec,          # (lower bound) both end cells of every crossing edge
-    "repair": lambda n, rec, ec: 20 * n,                   # read the tile store (8) + f (4), write T (8)
+    "repair": lambda n, rec, ec: 16 * n,                   # read the tile store (8), write T (8)
     "diagram": lambda n, rec, ec: 4 * n + 16 * rec,        # one 4-B word per vertex to find the minima + records
     "finish_diagram": lambda n, rec, ec: 0,
 }

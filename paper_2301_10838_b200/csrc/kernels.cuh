@@ -124,6 +124,7 @@ struct RepairOut {
 uint64_t repair_segments(const Slab& sl);     // segments of the slab
 uint64_t repair_segments_bound(uint64_t n);   // >= repair_segments of any slab of n vertices
 uint64_t diagram_tiles(uint64_t nseg);        // diagram tiles; one 16-B status record each
+uint64_t diagram_tiles_bound(uint64_t nseg);  // >= diagram_tiles of any nseg' <= nseg (status sizing)
 // tiled: T holds tile_tmt's T0 and only tile minima have cells (grids); else every vertex has a
 // cell and T is output only (explicit graphs)
 void launch_repair(const Cell* C, uint64_t* T, const float* f, const Slab& sl, uint32_t flip, const RepairOut& o,

@@ -211,14 +211,14 @@ dedupe_cross_kernel(const float* __restrict__ f, const uint64_t* __restrict__ T0
                 ba = uint32_t(ea);
                 bb = uint32_t(eb);
             } else {
-                ka = key_of(ord32(__ldg(f + a)) ^ flip, a);
-                kb = key_of(ord32(__ldg(f + b)) ^ flip, b);
-                // tile representative at the vertex's own level (DESIGN.md derivation C-3): the
-                // tile store's v for a regular vertex (s = u), the vertex itself for a minimum
+                // the tile store holds each vertex's order key and its tile representative at its
+                // own level (DESIGN.md derivation C-3): ord(u) << 32 | R(u)
                 const uint64_t ta = __ldg(reinterpret_cast<const unsigned long long*>(T0 + a));
                 const uint64_t tb = __ldg(reinterpret_cast<const unsigned long long*>(T0 + b));
-                ba = cell_s(ta) == a ? cell_v(ta) : a;
-                bb = cell_s(tb) == b ? cell_v(tb) : b;
+                ka = key_of(uint32_t(ta >> 32), a);
+                kb = key_of(uint32_t(tb >> 32), b);
+                ba = uint32_t(ta);
+                bb = uint32_t(tb);
             }
             en = ka > kb ? QEntry{ka, ba, bb} : QEntry{kb, bb, ba};
             pair = ba < bb ? (uint64_t(ba) << 32 | bb) : (uint64_t(bb) << 32 | ba);

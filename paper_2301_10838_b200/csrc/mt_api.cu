@@ -86,7 +86,7 @@ Layout layout_for(uint64_t n, uint64_t ncross, bool slab = false, uint64_t ess_c
     L.pairs_cap = n ? (ess_cap >= n ? n : (n + 1) / 2 + 1) : 0;
     L.seg_cap = n ? mt::repair_segments_bound(n) : 0;
     // tile records of the diagram compaction (16 B) / of mt_filter_diagram (8 B)
-    L.status_bytes = std::max(mt::diagram_tiles(L.seg_cap) * sizeof(mt::Cell),
+    L.status_bytes = std::max(mt::diagram_tiles_bound(L.seg_cap) * sizeof(mt::Cell),
                               mt::filter_tiles(L.pairs_cap + ess_cap) * sizeof(uint64_t));
     size_t off = 0;
     L.counters = off;

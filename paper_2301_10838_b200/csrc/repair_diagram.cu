@@ -169,19 +169,16 @@ repair_brick_kernel(View view, const Cell* C, uint64_t* __restrict__ T, const fl
     uint32_t xs[RB_PER];      // walk start (then position)
     uint32_t mins = 0;        // rows k whose vertex has a working cell (bit k)
     if (TILED) {
-        // every load of the thread in flight at once: the tile store and f of all its vertices,
-        // then the working cells of the (few) tile minima among them
+        // every load of the thread in flight at once: the tile store of all its vertices (its
+        // order key and tile representative), then the working cells of the tile minima among them
         uint64_t t0[RB_PER];
-        uint32_t fo[RB_PER];
 #pragma unroll
         for (int k = 0; k < RB_PER; ++k) t0[k] = INB(k) ? T[UID(k)] : 0;
 #pragma unroll
-        for (int k = 0; k < RB_PER; ++k) fo[k] = INB(k) ? ord32(__ldg(f + UID(k))) ^ flip : 0u;
-#pragma unroll
         for (int k = 0; k < RB_PER; ++k) {
             const uint32_t u = uint32_t(UID(k));
-            if (cell_s(t0[k]) == u && cell_v(t0[k]) != u) {   // regular in its tile: s = u is final
-                key[k] = key_of(fo[k], u);
+            if (cell_v(t0[k]) != u) {            // regular in its tile: s = u is final
+                key[k] = key_of(cell_s(t0[k]), u);
                 sv[k] = u;
                 xs[k] = cell_v(t0[k]);
             } else {
@@ -350,11 +347,12 @@ repair_brick_kernel(View view, const Cell* C, uint64_t* __restrict__ T, const fl
 // place in the diagram (ordered compaction: CTA scan + decoupled look-back);
 // the records are copied from the staging runs the repair wrote.
 constexpr int THREADS = 256;
-#ifndef DG_SPT
-#define DG_SPT 1            // diagram: segments per thread (4: c5 1.31 -> 1.07 ms, c4 0.39 -> 0.56 ms)
-#endif
+#ifndef DG_BIG
+#define DG_BIG (1ull << 24) // diagram: from this many segments on, 4 segments per thread (fewer tiles in the
+#endif                      // look-back chain: c5 1.31 -> 1.07 ms in round 1; 1 below: c4 0.39 vs 0.56 ms)
 constexpr uint64_t ST_AGG = 1ull << 62, ST_PRE = 2ull << 62, ST_VAL = (1ull << 62) - 1;
 
+template <int DG_SPT>
 __global__ void __launch_bounds__(THREADS)
 diagram_kernel(const uint16_t* __restrict__ seg_cnt, const uint32_t* __restrict__ seg_pos, uint64_t nseg,
                const mt_pair* __restrict__ stage, unsigned long long* __restrict__ counters, Cell* __restrict__ status,
@@ -540,7 +538,12 @@ uint64_t repair_segments(const Slab& sl) {
     return nseg;
 }
 uint64_t repair_segments_bound(uint64_t n) { return n / 16 + 2; }
-uint64_t diagram_tiles(uint64_t nseg) { return (nseg + THREADS * DG_SPT - 1) / (THREADS * DG_SPT); }
+static int diagram_spt(uint64_t nseg) { return nseg >= DG_BIG ? 4 : 1; }
+uint64_t diagram_tiles(uint64_t nseg) {
+    const uint64_t per = uint64_t(THREADS) * diagram_spt(nseg);
+    return (nseg + per - 1) / per;
+}
+uint64_t diagram_tiles_bound(uint64_t nseg) { return (nseg + THREADS - 1) / THREADS; }
 
 void launch_repair(const Cell* C, uint64_t* T, const float* f, const Slab& sl, uint32_t flip, const RepairOut& o,
                    bool tiled, unsigned long long* stats, const ForestRef* forest, cudaStream_t stream) {
@@ -554,9 +557,14 @@ void launch_diagram(const Slab& sl, const RepairOut& o, void* status, mt_pair* o
     const uint64_t nseg = sl.n ? repair_segments(sl) : 0;
     const uint64_t ntiles = diagram_tiles(nseg);
     if (ntiles == 0) return;
-    diagram_kernel<<<uint32_t(ntiles), THREADS, 0, stream>>>(o.seg_cnt, o.seg_pos, nseg, o.stage, o.counters,
-                                                             static_cast<Cell*>(status), out, out_cap, ess, ess_cap,
-                                                             ntiles);
+    if (diagram_spt(nseg) == 4)
+        diagram_kernel<4><<<uint32_t(ntiles), THREADS, 0, stream>>>(o.seg_cnt, o.seg_pos, nseg, o.stage, o.counters,
+                                                                    static_cast<Cell*>(status), out, out_cap, ess,
+                                                                    ess_cap, ntiles);
+    else
+        diagram_kernel<1><<<uint32_t(ntiles), THREADS, 0, stream>>>(o.seg_cnt, o.seg_pos, nseg, o.stage, o.counters,
+                                                                    static_cast<Cell*>(status), out, out_cap, ess,
+                                                                    ess_cap, ntiles);
 }
 
 void launch_finish_diagram(unsigned long long* counters, mt_pair* out, uint64_t out_cap, mt_pair* ess,

@@ -26,11 +26,13 @@ namespace mt {
 
 namespace {
 
-// a vertex that is regular in its tile has no working cell: its tile triplet (u, u, R) is in T0
-__device__ __forceinline__ bool tile_regular(const uint64_t* T0, uint32_t x, uint32_t* rep) {
+// a vertex that is regular in its tile has no working cell: T0 = ord(x) << 32 | R(x) with its
+// tile representative R(x) != x (a tile minimum has R(x) == x and a cell)
+__device__ __forceinline__ bool tile_regular(const uint64_t* T0, uint32_t x, uint32_t* rep, uint32_t* ord_x) {
     const uint64_t t = T0[x];
     *rep = cell_v(t);
-    return cell_s(t) == x && cell_v(t) != x;
+    *ord_x = cell_s(t);
+    return cell_v(t) != x;
 }
 
 __global__ void __launch_bounds__(256)
@@ -48,8 +50,8 @@ forest_mark_kernel(const Cell* C, const uint64_t* T0, uint32_t nx, uint32_t ny, 
         uint8_t* fl = flag + (uint64_t(x) - base);
         if (*reinterpret_cast<volatile uint8_t*>(fl)) continue;
         *reinterpret_cast<volatile uint8_t*>(fl) = 1;
-        uint32_t rep;
-        if (tile_regular(T0, x, &rep)) {
+        uint32_t rep, ox;
+        if (tile_regular(T0, x, &rep, &ox)) {
             x = rep;
         } else {
             const Cell c = ld_cell(C + x);
@@ -83,12 +85,11 @@ forest_compact_kernel(const Cell* C, const uint64_t* T0, const float* f, uint32_
         if (take) {
             const uint64_t pos = b + __popc(m & ((1u << lane) - 1u));
             const uint32_t u = uint32_t(base + l);
-            uint32_t rep;
+            uint32_t rep, o;
             const uint32_t fb = __float_as_uint(f[u]);
             mt_forest_record rec;
-            if (tile_regular(T0, u, &rep)) {
+            if (tile_regular(T0, u, &rep, &o)) {
                 // the cell the vertex would have: (u, u, R) at its own key
-                const uint32_t o = ord32(f[u]) ^ flip;
                 rec = mt_forest_record{u, fb, key_of(o, u), (uint64_t(o) << 32) | rep, fb, 0u};
             } else {
                 const Cell c = ld_cell(C + u);
@@ -339,9 +340,9 @@ forest_writeback_kernel(ForestRef F, uint64_t n_all, Cell* C, const uint64_t* T0
     for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n_all;
          i += uint64_t(gridDim.x) * blockDim.x) {
         const uint32_t id = F.recs[i].id;
-        uint32_t rep;
+        uint32_t rep, o;
         // (a tile-regular face vertex keeps its T0: the repair walks from its R through the forest)
-        if (uint64_t(id) - base < n && !tile_regular(T0, id, &rep)) {
+        if (uint64_t(id) - base < n && !tile_regular(T0, id, &rep, &o)) {
             const Cell c = F.cells[i];
             st_cell(C + id, c);
         }

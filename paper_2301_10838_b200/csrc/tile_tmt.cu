@@ -127,6 +127,8 @@ __device__ __forceinline__ uint64_t sld64(const uint64_t* p) {
 __device__ __forceinline__ uint64_t scas64(uint64_t* p, uint64_t cmp, uint64_t val) {
     return atomicCAS(reinterpret_cast<unsigned long long*>(p), cmp, val);
 }
+
+#if TILE_KRUSKAL
 __device__ __forceinline__ uint32_t sld16(const uint16_t* p) { return *reinterpret_cast<const volatile uint16_t*>(p); }
 
 // union-find over basin minima (local ids, 16-bit parents): find with path halving -- the
@@ -158,6 +160,7 @@ __device__ __forceinline__ void uf_union(uint16_t* uf, const uint32_t* ord, uint
             return;
     }
 }
+#endif
 
 // ---- TMA (cp.async.bulk.tensor) staging of a tile's f into shared memory -----------------
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -924,9 +927,9 @@ tile_tmt_kernel(const __grid_constant__ CUtensorMap fmap, const float* __restric
     phase_time(ST_CYC_REPAIR);
 
     // ---- f. write the tile store T0 (8 B per vertex) and the tile minima's 16-byte cells ------
-    // T0[u] = s << 32 | v with global ids, into the caller's triplet buffer: for a regular vertex
-    // (u, Rep_tile(u, key(u))) -- its s is final and the repair only re-points v; for a tile
-    // minimum its tile triplet.  Only tile minima (s != u, or the tile root) get a 16-byte
+    // T0[u] (into the caller's triplet buffer) = ord(u) << 32 | R(u): for a tile-regular vertex
+    // R = Rep_tile(u, key(u)) -- its s = u is final and the repair only re-points v, starting at
+    // R with threshold key(u); for a tile minimum R = u.  Only tile minima (s != u, or the tile root) get a 16-byte
     // working cell: the global merge only ever reads or writes cells of tile minima (the
     // crossing edges start at tile representatives, which are minima, and every cell on a v
     // chain from a minimum is a minimum's; DESIGN.md derivation C'''), so regular vertices need
@@ -945,19 +948,19 @@ tile_tmt_kernel(const __grid_constant__ CUtensorMap fmap, const float* __restric
         const uint32_t u = r * TX + lx;
         const uint32_t ou = ord[u];
         if (ou == ABSENT) continue;
-        const uint64_t cu = cell[u];
-        const uint32_t s = c_s(cu), v = rep[k];
+        const uint32_t v = rep[k];
         const uint32_t gu = gbase + uint32_t(lz) * sxy32 + uint32_t(ly) * nx + lx, gv = gid(v);
-        const uint64_t g = gu;
+        const uint64_t cu = cell[u];
+        const uint32_t s = c_s(cu);
         const bool minimum = s != u || v == u;
-        const uint32_t gs = s == u ? gu : gid(s);
-        T0[g] = pack(gs, gv);
-        if (minimum) C[g] = make_cell(key_of(uint32_t(cu >> 32), gs), ou, gv);
-        // the tile's x faces (lanes 0 and 31) again, compactly: (order key, R) per row, R =
-        // Rep_tile(u, key(u)) for a regular vertex, u for a minimum, so that the crossing edges of
-        // the x faces read them coalesced (in the grid they are 128 B apart)
-        if (lx == 0 || lx == TX - 1)
-            xface[(uint64_t(b) * 2 + (lx == TX - 1)) * ROWS + r] = (uint64_t(ou) << 32) | (s == u ? gv : gu);
+        // T0 = ord(u) << 32 | R(u), R = Rep_tile(u, key(u)) for a tile-regular vertex, u itself for
+        // a tile minimum (so R(u) == u tells a minimum apart); the crossing edges read their key and
+        // tile representative from it, the repair its threshold and walk start
+        const uint64_t t0 = (uint64_t(ou) << 32) | (minimum ? gu : gv);
+        T0[gu] = t0;
+        // the tile's x faces (lanes 0 and 31) again, compactly (in the grid they are 128 B apart)
+        if (lx == 0 || lx == TX - 1) xface[(uint64_t(b) * 2 + (lx == TX - 1)) * ROWS + r] = t0;
+        if (minimum) C[gu] = make_cell(key_of(uint32_t(cu >> 32), s == u ? gu : gid(s)), ou, gv);
     }
     phase_time(ST_CYC_WRITE);
     }   // pass
