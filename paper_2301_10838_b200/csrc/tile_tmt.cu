@@ -441,37 +441,44 @@ tile_tmt_kernel(const __grid_constant__ CUtensorMap fmap, const float* __restric
 
 #if TILE_KRUSKAL
     // ---- c. bucketed Kruskal filter over the basin graph --------------------------------
-    // Level buckets: the order keys' range of the tile split at a power-of-two shift, so that a
-    // bucket is (ord - omin) >> sh (at least NB/2 of the NB buckets in use).
-    {
-        uint32_t omin = ~0u, omax = 0;
+    // Level buckets at sample quantiles: warp 0 sorts 32 order keys spread over the tile
+    // (bitonic, in registers) and keeps NB - 1 of them as splitters; a vertex's bucket is the
+    // number of splitters <= its key, so the buckets hold roughly equal numbers of vertices
+    // whatever the value distribution (a skewed field would put most of a tile into one bucket
+    // of a range split).
+    __shared__ uint32_t s_split[TILE_NB];
+    if (warp_d == 0) {
+        uint32_t o = ord[(uint32_t(lane_c) * (NV / 32) + NV / 64) % NV];   // ABSENT sorts last
 #pragma unroll
-        for (int k = 0; k < PER; ++k) {
-            const uint32_t o = ord[(r0 + k * RSTEP) * TX + lx];
-            if (o != ABSENT) {
-                omin = min(omin, o);
-                omax = max(omax, o);
+        for (int k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+            for (int j = k >> 1; j > 0; j >>= 1) {
+                const uint32_t p = __shfl_xor_sync(FULL_MASK, o, j);
+                const bool up = ((lane_c & k) == 0), lower = (lane_c & j) == 0;
+                o = (lower == up) ? min(o, p) : max(o, p);
             }
         }
-        omin = __reduce_min_sync(FULL_MASK, omin);
-        omax = __reduce_max_sync(FULL_MASK, omax);
-        if (lane_c == 0) {
-            atomicMin(&s_omin, omin);
-            atomicMax(&s_omax, omax);
-        }
+        // lane i holds the i-th smallest sample; splitter j = sample (j + 1) * 32 / NB
+        if (lane_c % (32 / TILE_NB) == (32 / TILE_NB) - 1 && lane_c / (32 / TILE_NB) < TILE_NB - 1)
+            s_split[lane_c / (32 / TILE_NB)] = o;
     }
     __syncthreads();
-    const uint32_t omin = s_omin;
-    const uint32_t range = s_omax >= omin ? s_omax - omin : 0u;
-    const int rbits = range ? 32 - __clz(range) : 0;
-    const int sh = rbits > LOG2NB ? rbits - LOG2NB : 0;
+    auto bucket_of = [&](uint32_t o) {
+        int lo = 0, hi = TILE_NB - 1;           // number of splitters <= o, by binary search
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (s_split[mid] <= o) lo = mid + 1;
+            else hi = mid;
+        }
+        return lo;
+    };
     // counting sort of the vertices by bucket: per-warp counts, bucket-major prefix, scatter
     {
         uint32_t rank[PER];
 #pragma unroll
         for (int k = 0; k < PER; ++k) {
             const uint32_t o = ord[(r0 + k * RSTEP) * TX + lx];
-            rank[k] = o != ABSENT ? atomicAdd(&s_hist[(o - omin) >> sh][warp_d], 1u) : 0u;
+            rank[k] = o != ABSENT ? atomicAdd(&s_hist[bucket_of(o)][warp_d], 1u) : 0u;
         }
         __syncthreads();
         if (warp_d == 0) {                     // exclusive prefix over (bucket, warp), bucket-major
@@ -504,7 +511,7 @@ tile_tmt_kernel(const __grid_constant__ CUtensorMap fmap, const float* __restric
         for (int k = 0; k < PER; ++k) {
             const uint32_t u = (r0 + k * RSTEP) * TX + lx;
             const uint32_t o = ord[u];
-            if (o != ABSENT) vlist[s_hist[(o - omin) >> sh][warp_d] + rank[k]] = uint16_t(u);
+            if (o != ABSENT) vlist[s_hist[bucket_of(o)][warp_d] + rank[k]] = uint16_t(u);
         }
     }
     __syncthreads();
