@@ -80,3 +80,13 @@ def test_dist_host_entry_points_without_gpu(lib):
     assert lib.mt_create_dist(ctypes.byref(h), dims, 6, 3, 2, idbuf, 0, None, 0) == _lib.MT_ERR_INVALID_ARG
     assert lib.mt_create_dist(ctypes.byref(h), dims, 6, 0, 65, idbuf, 0, None, 0) == _lib.MT_ERR_INVALID_ARG
     assert lib.mt_create_dist(ctypes.byref(h), dims, 6, 0, 2, None, 0, None, 0) == _lib.MT_ERR_INVALID_ARG
+
+
+def test_host_pipeline_and_dual_entry_points_validate_without_gpu(lib):
+    """mt_compute_host / mt_compute_join_split reject bad arguments before touching the device."""
+    vp = ctypes.c_void_p
+    lib.mt_host_staging_bytes.restype = ctypes.c_size_t
+    lib.mt_host_staging_bytes.argtypes = [vp]
+    assert lib.mt_host_staging_bytes(None) == 0
+    assert lib.mt_compute_host(None, 1, None, None, None, 0, None, 0, None, 0, None) == _lib.MT_ERR_INVALID_ARG
+    assert lib.mt_compute_join_split(None, None, None, None, None, None) == _lib.MT_ERR_INVALID_ARG
