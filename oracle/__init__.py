@@ -72,6 +72,10 @@ def _load():
             lib.oracle_triplet_at.argtypes = [
                 ctypes.c_void_p, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_int, ctypes.c_int,
                 ctypes.c_uint32, ctypes.c_uint64, ctypes.POINTER(ctypes.c_uint32), ctypes.POINTER(ctypes.c_uint32)]
+            lib.oracle_triplet_at64.restype = ctypes.c_int
+            lib.oracle_triplet_at64.argtypes = [
+                ctypes.c_void_p, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_int, ctypes.c_int,
+                ctypes.c_uint64, ctypes.c_uint64, ctypes.POINTER(ctypes.c_uint64), ctypes.POINTER(ctypes.c_uint64)]
             lib.oracle_merge_tree_graph.restype = ctypes.c_int
             lib.oracle_merge_tree_graph.argtypes = [
                 ctypes.c_void_p, ctypes.c_uint32, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int,
@@ -111,13 +115,15 @@ def merge_tree(f: np.ndarray, dims, conn: int = 6, split: bool = False, want_pai
 
 def triplet_at(f: np.ndarray, dims, conn: int, u: int, split: bool = False, cap: int = 1 << 20):
     """O4: the triplet (s, v) of the single vertex u from the definition by
-    bounded floods (oracle/mt_oracle.c: oracle_triplet_at), or None when a flood would visit
-    more than ``cap`` vertices.  For sampled checks of full-size outputs."""
+    bounded floods (oracle/mt_oracle.c: oracle_triplet_at64, 64-bit ids: any grid size), or None
+    when a flood would visit more than ``cap`` vertices.  For sampled checks of full-size outputs."""
     f = np.ascontiguousarray(f, dtype=np.float32).reshape(-1)
     nx, ny, nz = (int(d) for d in dims)
-    s, v = ctypes.c_uint32(0), ctypes.c_uint32(0)
-    rc = _load().oracle_triplet_at(f.ctypes.data, nx, ny, nz, int(conn), int(bool(split)), int(u), int(cap),
-                                   ctypes.byref(s), ctypes.byref(v))
+    if f.size != nx * ny * nz:
+        raise ValueError("f size does not match dims")
+    s, v = ctypes.c_uint64(0), ctypes.c_uint64(0)
+    rc = _load().oracle_triplet_at64(f.ctypes.data, nx, ny, nz, int(conn), int(bool(split)), int(u), int(cap),
+                                     ctypes.byref(s), ctypes.byref(v))
     if rc < 0:
         raise OracleError(rc)
     return (int(s.value), int(v.value)) if rc == 1 else None

@@ -306,34 +306,61 @@ int oracle_abi_version(void) { return 1; }
  * Returns 1 and (s, v) on success, 0 when a flood would visit more than `cap` vertices
  * (the caller skips that sample), negative on bad arguments or memory.
  * ------------------------------------------------------------------------------------------ */
-typedef struct { uint32_t *keys; uint64_t mask, count; } idset;
+/* O4 works with 64-bit vertex ids so that it also checks grids past 2^32 vertices (SURVEY.md 8f
+ * row f3; PAPER.md:389-396 limits the paper's ids to 32 bits).  key_less / the grid adjacency
+ * are the ones above, widened. */
+typedef struct {
+    float g;
+    uint64_t id;
+} vkey64;
+
+static int key_less64(float ga, uint64_t a, float gb, uint64_t b) {   /* reading R1, as key_less */
+    if (ga < gb) return 1;
+    if (ga == gb && a < b) return 1;
+    return 0;
+}
+
+static int grid_neighbours64(uint64_t u, uint32_t nx, uint32_t ny, uint32_t nz, uint64_t out[6]) {
+    uint64_t x = u % nx, y = (u / nx) % ny, z = u / ((uint64_t)nx * ny);
+    uint64_t sxy = (uint64_t)nx * ny;
+    int k = 0;
+    if (x > 0) out[k++] = u - 1;
+    if (x + 1 < nx) out[k++] = u + 1;
+    if (y > 0) out[k++] = u - nx;
+    if (y + 1 < ny) out[k++] = u + nx;
+    if (z > 0) out[k++] = u - sxy;
+    if (z + 1 < nz) out[k++] = u + sxy;
+    return k;
+}
+
+typedef struct { uint64_t *keys; uint64_t mask, count; } idset;
 
 static int set_init(idset *S, uint64_t cap) {
     uint64_t m = 1;
     while (m < 2 * cap + 2) m <<= 1;
-    S->keys = (uint32_t *)malloc(m * sizeof(uint32_t));
+    S->keys = (uint64_t *)malloc(m * sizeof(uint64_t));
     if (!S->keys) return 0;
-    memset(S->keys, 0xff, m * sizeof(uint32_t));
+    memset(S->keys, 0xff, m * sizeof(uint64_t));
     S->mask = m - 1;
     S->count = 0;
     return 1;
 }
-/* 1 if inserted, 0 if already present (ids are < 2^32 - 1: 0xffffffff marks a free slot) */
-static int set_add(idset *S, uint32_t x) {
-    uint64_t h = ((uint64_t)x * 0x9E3779B97F4A7C15ull) >> 20;
+/* 1 if inserted, 0 if already present (ids are < 2^63: all-ones marks a free slot) */
+static int set_add(idset *S, uint64_t x) {
+    uint64_t h = (x * 0x9E3779B97F4A7C15ull) >> 20;
     for (;; ++h) {
-        uint32_t *k = &S->keys[h & S->mask];
-        if (*k == 0xffffffffu) { *k = x; ++S->count; return 1; }
+        uint64_t *k = &S->keys[h & S->mask];
+        if (*k == ~0ull) { *k = x; ++S->count; return 1; }
         if (*k == x) return 0;
     }
 }
 
-typedef struct { vkey *a; uint64_t n, cap; } vheap;
-static int heap_less(const vkey *x, const vkey *y) { return key_less(x->g, x->id, y->g, y->id); }
-static int heap_push(vheap *H, vkey k) {
+typedef struct { vkey64 *a; uint64_t n, cap; } vheap;
+static int heap_less(const vkey64 *x, const vkey64 *y) { return key_less64(x->g, x->id, y->g, y->id); }
+static int heap_push(vheap *H, vkey64 k) {
     if (H->n == H->cap) {
         uint64_t nc = H->cap ? 2 * H->cap : 1024;
-        vkey *na = (vkey *)realloc(H->a, nc * sizeof(vkey));
+        vkey64 *na = (vkey64 *)realloc(H->a, nc * sizeof(vkey64));
         if (!na) return 0;
         H->a = na;
         H->cap = nc;
@@ -341,13 +368,13 @@ static int heap_push(vheap *H, vkey k) {
     uint64_t i = H->n++;
     H->a[i] = k;
     while (i && heap_less(&H->a[i], &H->a[(i - 1) / 2])) {
-        vkey t = H->a[i]; H->a[i] = H->a[(i - 1) / 2]; H->a[(i - 1) / 2] = t;
+        vkey64 t = H->a[i]; H->a[i] = H->a[(i - 1) / 2]; H->a[(i - 1) / 2] = t;
         i = (i - 1) / 2;
     }
     return 1;
 }
-static vkey heap_pop(vheap *H) {
-    vkey top = H->a[0];
+static vkey64 heap_pop(vheap *H) {
+    vkey64 top = H->a[0];
     H->a[0] = H->a[--H->n];
     uint64_t i = 0;
     for (;;) {
@@ -355,39 +382,42 @@ static vkey heap_pop(vheap *H) {
         if (l < H->n && heap_less(&H->a[l], &H->a[m])) m = l;
         if (r < H->n && heap_less(&H->a[r], &H->a[m])) m = r;
         if (m == i) break;
-        vkey t = H->a[i]; H->a[i] = H->a[m]; H->a[m] = t;
+        vkey64 t = H->a[i]; H->a[i] = H->a[m]; H->a[m] = t;
         i = m;
     }
     return top;
 }
 
-int oracle_triplet_at(const float *f, uint32_t nx, uint32_t ny, uint32_t nz, int conn, int split, uint32_t u,
-                      uint64_t cap, uint32_t *s_out, uint32_t *v_out) {
-    const uint64_t n = (uint64_t)nx * ny * nz;
-    if (!f || u >= n || (conn != 4 && conn != 6) || (conn == 4 && nz != 1) || n >= 0xffffffffull) return -1;
+int oracle_triplet_at64(const float *f, uint32_t nx, uint32_t ny, uint32_t nz, int conn, int split, uint64_t u,
+                        uint64_t cap, uint64_t *s_out, uint64_t *v_out) {
+    const uint64_t sxy = (uint64_t)nx * ny;
+    if (!f || (conn != 4 && conn != 6) || (conn == 4 && nz != 1) || sxy == 0 || nz > (1ull << 63) / sxy) return -1;
+    const uint64_t n = sxy * nz;
+    if (u >= n) return -1;
     const float sg = split ? -1.0f : 1.0f;
 #define G_OF(x) (sg * f[(x)] + 0.0f)
-    uint32_t nb[6];
+    uint64_t nb[6];
     int rc = -2;
     idset S = {0}, B = {0};
     vheap H = {0};
-    uint32_t *queue = NULL;
+    uint64_t *queue = NULL;
     if (!set_init(&S, cap) || !set_init(&B, cap)) goto out;
     /* s: Prim flood from u */
     const float gu = G_OF(u);
-    uint32_t s = u, found = 0;
+    uint64_t s = u;
+    int found = 0;
     float gs = gu;
     set_add(&S, u);
-    if (!heap_push(&H, (vkey){gu, u})) goto out;
+    if (!heap_push(&H, (vkey64){gu, u})) goto out;
     while (H.n) {
-        vkey x = heap_pop(&H);
-        if (key_less(x.g, x.id, gu, u)) { found = 1; break; }   /* entered a deeper vertex */
-        if (key_less(gs, s, x.g, x.id)) { gs = x.g; s = x.id; } /* the level rises to key(x) */
-        int d = grid_neighbours(x.id, nx, ny, nz, nb);
+        vkey64 x = heap_pop(&H);
+        if (key_less64(x.g, x.id, gu, u)) { found = 1; break; }   /* entered a deeper vertex */
+        if (key_less64(gs, s, x.g, x.id)) { gs = x.g; s = x.id; } /* the level rises to key(x) */
+        int d = grid_neighbours64(x.id, nx, ny, nz, nb);
         for (int i = 0; i < d; ++i)
             if (set_add(&S, nb[i])) {
                 if (S.count > cap) { rc = 0; goto out; }
-                if (!heap_push(&H, (vkey){G_OF(nb[i]), nb[i]})) goto out;
+                if (!heap_push(&H, (vkey64){G_OF(nb[i]), nb[i]})) goto out;
             }
     }
     if (!found) {                 /* the whole component lies above u: u is its minimum */
@@ -397,21 +427,21 @@ int oracle_triplet_at(const float *f, uint32_t nx, uint32_t ny, uint32_t nz, int
         goto out;
     }
     /* v: deepest vertex of u's component of {x : key(x) <= key(s)} */
-    queue = (uint32_t *)malloc((cap + 1) * sizeof(uint32_t));
+    queue = (uint64_t *)malloc((cap + 1) * sizeof(uint64_t));
     if (!queue) goto out;
     uint64_t qh = 0, qt = 0;
-    uint32_t v = u;
+    uint64_t v = u;
     float gv = gu;
     set_add(&B, u);
     queue[qt++] = u;
     while (qh < qt) {
-        const uint32_t x = queue[qh++];
+        const uint64_t x = queue[qh++];
         const float gx = G_OF(x);
-        if (key_less(gx, x, gv, v)) { gv = gx; v = x; }
-        int d = grid_neighbours(x, nx, ny, nz, nb);
+        if (key_less64(gx, x, gv, v)) { gv = gx; v = x; }
+        int d = grid_neighbours64(x, nx, ny, nz, nb);
         for (int i = 0; i < d; ++i) {
             const float gy = G_OF(nb[i]);
-            if (!key_less(gy, nb[i], gs, s) && nb[i] != s) continue;   /* above level key(s) */
+            if (!key_less64(gy, nb[i], gs, s) && nb[i] != s) continue;   /* above level key(s) */
             if (set_add(&B, nb[i])) {
                 if (B.count > cap) { rc = 0; goto out; }
                 queue[qt++] = nb[i];
@@ -427,5 +457,18 @@ out:
     free(B.keys);
     free(H.a);
     free(queue);
+    return rc;
+}
+
+/* the 32-bit form (grids below 2^32 - 1 vertices) */
+int oracle_triplet_at(const float *f, uint32_t nx, uint32_t ny, uint32_t nz, int conn, int split, uint32_t u,
+                      uint64_t cap, uint32_t *s_out, uint32_t *v_out) {
+    if ((uint64_t)nx * ny * nz >= 0xffffffffull) return -1;
+    uint64_t s = 0, v = 0;
+    const int rc = oracle_triplet_at64(f, nx, ny, nz, conn, split, u, cap, &s, &v);
+    if (rc == 1) {
+        *s_out = (uint32_t)s;
+        *v_out = (uint32_t)v;
+    }
     return rc;
 }

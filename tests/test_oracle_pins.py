@@ -239,3 +239,37 @@ def test_o4_cap_skips():
     root = int(np.flatnonzero((T >> np.uint64(32)) == (T & np.uint64(0xffffffff)))[0])
     assert oracle.triplet_at(f, dims, conn, root, cap=100) is None   # the global minimum floods everything
     assert oracle.triplet_at(f, dims, conn, root, cap=f.size) == (root, root)
+
+
+def test_o4_ids_past_2_32_hand_derived():
+    """O4 with 64-bit ids (PAPER.md:389-396 stops at 32 bits) on a
+    2048 x 2048 x 1032 grid (4.33e9 vertices; plane 1024 starts at id 2^32 exactly), f = 0
+    except two pits joined by a path along +z that crosses id 2^32 (an anonymous zero mapping:
+    only the touched pages exist).  By the definition:
+      B = -1 (plane 1022) -> p1 = -0.9 -> p2 = -0.8 (plane 1024, id >= 2^32) -> p3 = -0.7 -> A = -2;
+      T[p1] = (p1, B): p1 has a lower neighbour, its component at level f(p1) is {B, p1};
+      T[p3] = (p3, A): at level f(p3) the path joins A, the deepest vertex;
+      T[B]  = (p3, A): B's component first reaches a deeper vertex (A) at level f(p3);
+    truncating any id (or a neighbour offset) to 32 bits breaks one of these."""
+    import mmap
+    dims = (2048, 2048, 1032)
+    nx, ny, nz = dims
+    n, sxy = nx * ny * nz, nx * ny
+    m = mmap.mmap(-1, n * 4)
+    try:
+        f = np.frombuffer(m, dtype=np.float32)
+        b = 1022 * sxy + 9 * nx + 7
+        p1, p2, p3, a = b + sxy, b + 2 * sxy, b + 3 * sxy, b + 4 * sxy
+        assert p1 < 2 ** 32 <= p2
+        for x, val in ((b, -1.0), (p1, -0.9), (p2, -0.8), (p3, -0.7), (a, -2.0)):
+            f[x] = val
+        assert oracle.triplet_at(f, dims, 6, p1, cap=64) == (p1, b)
+        assert oracle.triplet_at(f, dims, 6, p2, cap=64) == (p2, b)
+        assert oracle.triplet_at(f, dims, 6, p3, cap=64) == (p3, a)
+        assert oracle.triplet_at(f, dims, 6, b, cap=64) == (p3, a)
+        assert oracle.triplet_at(f, dims, 6, a, cap=64) is None          # the global minimum floods all
+        # a zero vertex's sublevel component holds every lower-id zero: far past the cap
+        assert oracle.triplet_at(f, dims, 6, a + 1, cap=64) is None
+        del f
+    finally:
+        m.close()
