@@ -48,7 +48,7 @@ typedef void *mt_stream_t;    /* a cudaStream_t (0 = legacy default stream) */
 typedef enum {
     MT_OK = 0,
     MT_ERR_INVALID_ARG = 1, /* NULL pointer, conn not in {4,6}, conn 4 with nz != 1, bad rank */
-    MT_ERR_TOO_LARGE = 2,   /* nx*ny*nz > 2^32 - 1: 32-bit vertex ids */
+    MT_ERR_TOO_LARGE = 2,   /* ids past 32 bits where they must fit (one GPU: nx*ny*nz <= 2^32 - 1) */
     MT_ERR_NONFINITE = 3,   /* NaN or +-Inf in f (reading R3); sticky */
     MT_ERR_CUDA = 4,        /* a CUDA runtime call failed */
     MT_ERR_NCCL = 5,        /* NCCL missing or an NCCL call failed (mt_create_dist contexts) */
@@ -168,33 +168,67 @@ int mt_kernel_times(mt_ctx *ctx, const char **names, float *ms, int max);
 
 /* ---- Multi-GPU: z-slab decomposition (distribution is the
  * paper's future work) --------------------------------
- * Rank r of P owns planes [z_begin, z_end) of the global grid; vertex ids stay
- * GLOBAL everywhere (triplets and diagram records hold global ids).  3D grids
- * only (conn 6), at most 64 slabs.  Per step:
+ * Rank r of P owns planes [z_begin, z_end) of the global grid; 3D grids only
+ * (conn 6), at most 64 slabs.  Per step:
  *   1. mt_compute_local  -- merge tree of the slab subgraph + its boundary
  *      forest (the cells reachable from the slab's inter-slab faces);
  *   2. mt_forest_view    -- the forest records (the caller all-gathers them,
- *      e.g. with NCCL, concatenating every rank's records in any order);
+ *      e.g. with NCCL, concatenating the slabs' records in SLAB ORDER);
  *   3. mt_compute_global -- merges every inter-slab edge on the union of the
  *      forests, then repairs the slab and extracts its diagram: the slab's
  *      finite pairs (births in the slab, ascending) and, on the rank owning
- *      the global minimum, the essential class; mt_diagram as usual.
+ *      the global minimum, the essential class.
  * The result equals the single-GPU result (the store is unique, PAPER.md:
- * 196-200).  Forest record: the vertex id, its cell, and the f bits of the
- * vertex and of its saddle s (a saddle travels with displaced pairs across
- * slabs, and diagram values are copied from the input f, reading R14). */
+ * 196-200).
+ *
+ * Vertex ids.  The paper packs two 32-bit ids into one
+ * 64-bit CAS word and names that limit as the obstacle to distribution
+ * (PAPER.md:389-396, 1063-1066).  Here every kernel keeps 32-bit ids and the
+ * packed 8-B store; the global ids may pass 2^32:
+ *   - 32-bit mode (nx*ny*nz <= 2^32 - 1): the triplets and the diagram hold
+ *     GLOBAL ids (mt_diagram as on one GPU);
+ *   - wide mode (nx*ny*nz > 2^32 - 1, or MT_SLAB_WIDE_IDS): each context works
+ *     in its own 32-bit VIEW of the id space -- its slab's vertices at a fixed
+ *     offset, the vertices of other slabs that the gathered forest references
+ *     compressed below and above it in global order (each slab numbers its
+ *     referenced vertices by rank, an order-preserving compression, so every
+ *     comparison of the method -- the (value, id) key, reading R1 -- gives the
+ *     global answer).  mt_triplets64 / mt_diagram64 translate the results to
+ *     64-bit global ids; mt_diagram returns MT_ERR_TOO_LARGE.
+ *   A wide slab needs (z_end - z_begin + 2) * nx * ny < 2^32 and the
+ *   gathered forest must fit the view beside it (MT_ERR_TOO_LARGE otherwise).
+ *
+ * Forest record (32 B): the vertex, its cell (s, v) and the f bits of the
+ * vertex and of s (a saddle travels with displaced pairs across slabs;
+ * diagram values are copied from the input f, reading R14; the order keys
+ * are recomputed from the bits).  Ids are slab-local (global id minus
+ * nx*ny*z_begin); the *_c fields are the compressed ids of wide mode (equal
+ * to the local ids in 32-bit mode). */
 typedef struct {
-    uint32_t id;       /* global vertex id */
+    uint32_t id;       /* slab-local vertex id */
+    uint32_t s;        /* slab-local id of its saddle s */
+    uint32_t v;        /* slab-local id of v */
     uint32_t f_bits;   /* bits of f[id] */
-    uint64_t key_s;    /* order key of s: ord(f[s]) << 32 | s */
-    uint64_t hi;       /* ord(f[id]) << 32 | v */
-    uint32_t s_f_bits; /* bits of f[s] (diagram values of saddles owned by other ranks) */
-    uint32_t reserved;
+    uint32_t s_f_bits; /* bits of f[s] */
+    uint32_t id_c, s_c, v_c;  /* compressed ids (wide mode) */
 } mt_forest_record;    /* 32 bytes */
 
+enum { MT_SLAB_WIDE_IDS = 1u }; /* mt_create_slab / mt_create_dist option: wide mode at any size */
+
+/* 64-bit results (wide mode; also valid, widened, in 32-bit mode and on one GPU). */
+typedef struct {
+    uint64_t s, v;
+} mt_triplet64;
+typedef struct {
+    uint64_t birth_v, death_v;
+    float birth, death;
+} mt_pair64;           /* 24 bytes */
+
 size_t mt_slab_workspace_bytes(const uint32_t global_dims[3], int conn, uint32_t z_begin, uint32_t z_end);
+/* options: 0 or MT_SLAB_WIDE_IDS (wide mode is automatic past 2^32 - 1 vertices). */
 mt_status mt_create_slab(mt_ctx **out, const uint32_t global_dims[3], int conn, uint32_t z_begin,
-                         uint32_t z_end, int cuda_device, void *workspace, size_t workspace_bytes);
+                         uint32_t z_end, uint32_t options, int cuda_device, void *workspace,
+                         size_t workspace_bytes);
 /* f_slab (device): the slab's nx*ny*(z_end-z_begin) values, borrowed until
  * mt_compute_global's work completes; triplets_slab (device, n_local uint64):
  * receives the slab's tile store now and the final triplets from
@@ -208,21 +242,34 @@ mt_status mt_forest_view(mt_ctx *ctx, const mt_forest_record **records, uint64_t
 /* Device scratch bytes mt_compute_global needs for n_all gathered records; 0 when the id
  * tables would pass 2^31 slots (n_all > 2^29: mt_compute_global returns MT_ERR_TOO_LARGE). */
 size_t mt_forest_scratch_bytes(uint64_t n_all);
-/* all (device): the records of every slab, n_all of them; z_bounds (host):
- * the P+1 plane boundaries of all slabs (z_bounds[0] = 0, z_bounds[P] = nz);
- * scratch (device, >= mt_forest_scratch_bytes(n_all), 256-B aligned);
- * triplets_slab (device): the buffer given to mt_compute_local (MT_ERR_INVALID_ARG
- * otherwise), overwritten with the slab's n_local cells.  Asynchronous. */
-mt_status mt_compute_global(mt_ctx *ctx, const mt_forest_record *all, uint64_t n_all,
+/* all (device): the records of every slab concatenated in slab order, counts[k]
+ * (host) of slab k, nslabs of them (n_all = their sum); z_bounds (host): the
+ * P+1 plane boundaries of all slabs (z_bounds[0] = 0, z_bounds[P] = nz);
+ * scratch (device, >= mt_forest_scratch_bytes(n_all), 256-B aligned; it also
+ * holds the id translation of wide mode and must stay intact until the last
+ * mt_triplets64 / mt_diagram64 of this step); triplets_slab (device): the
+ * buffer given to mt_compute_local (MT_ERR_INVALID_ARG otherwise), overwritten
+ * with the slab's n_local triplets.  Asynchronous. */
+mt_status mt_compute_global(mt_ctx *ctx, const mt_forest_record *all, const uint64_t *counts,
                             const uint32_t *z_bounds, uint32_t nslabs, void *scratch,
                             size_t scratch_bytes, uint64_t *triplets_slab, mt_stream_t stream);
+
+/* Triplets first .. first+count-1 of the context's last result (triplets: the
+ * buffer mt_compute / mt_compute_global wrote, device) with 64-bit global ids
+ * into out (device, count records).  Asynchronous. */
+mt_status mt_triplets64(mt_ctx *ctx, const uint64_t *triplets, uint64_t first, uint64_t count,
+                        mt_triplet64 *out, mt_stream_t stream);
+/* mt_diagram with 64-bit global ids (out: device, capacity records). */
+mt_status mt_diagram64(mt_ctx *ctx, mt_pair64 *out, uint64_t capacity, uint64_t *n_pairs,
+                       uint64_t *n_essential, mt_stream_t stream);
 
 /* ---- Multi-GPU with the exchange inside the library ----------
  * One process per GPU.  Rank 0 calls mt_get_unique_id and the caller
  * broadcasts the 128 bytes to every rank (e.g. over torch.distributed); each
  * rank then creates its context with mt_create_dist and calls mt_compute /
- * mt_diagram exactly as on one GPU, with its slab of f and of the triplets
- * (planes [z_begin, z_end) of mt_dist_slab_bounds; global vertex ids).
+ * mt_diagram (mt_triplets64 / mt_diagram64 in wide mode) exactly as on one
+ * GPU, with its slab of f and of the triplets (planes [z_begin, z_end) of
+ * mt_dist_slab_bounds).
  * mt_compute on such a context runs the local phase, then on `stream` an
  * ncclAllGather of the boundary-forest sizes (8 B per rank), ONE host sync to
  * read them, a grouped ncclBroadcast of every rank's records (exact length,
@@ -239,7 +286,7 @@ mt_status mt_get_unique_id(uint8_t id[128]);
 mt_status mt_dist_slab_bounds(uint32_t nz, int nranks, uint32_t *bounds);
 size_t mt_dist_workspace_bytes(const uint32_t global_dims[3], int conn, int rank, int nranks);
 mt_status mt_create_dist(mt_ctx **out, const uint32_t global_dims[3], int conn, int rank, int nranks,
-                         const uint8_t nccl_id[128], int cuda_device, void *workspace,
+                         const uint8_t nccl_id[128], uint32_t options, int cuda_device, void *workspace,
                          size_t workspace_bytes);
 
 /* ---- Explicit graphs ----------------------------------
@@ -280,7 +327,8 @@ const char *mt_status_string(mt_status s);
 void mt_destroy(mt_ctx *ctx);
 
 /* Version of this ABI (bumped on any signature change; 2: mt_compute_local takes the
- * triplet buffer). */
+ * triplet buffer; 3: wide ids -- forest record v3, slab counts in mt_compute_global,
+ * options in mt_create_slab / mt_create_dist, mt_triplets64, mt_diagram64). */
 int mt_abi_version(void);
 
 #ifdef __cplusplus

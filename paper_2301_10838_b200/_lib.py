@@ -24,7 +24,10 @@ MT_ERR_NCCL, MT_ERR_STATE, MT_ERR_CAPACITY, MT_ERR_WORKSPACE = 5, 6, 7, 8
 MT_FLAG_SPLIT_TREE = 1
 
 PAIR_DTYPE = np.dtype([("birth_v", "<u4"), ("death_v", "<u4"), ("birth", "<f4"), ("death", "<f4")])
+PAIR64_DTYPE = np.dtype([("birth_v", "<u8"), ("death_v", "<u8"), ("birth", "<f4"), ("death", "<f4")])
+TRIPLET64_DTYPE = np.dtype([("s", "<u8"), ("v", "<u8")])
 FOREST_RECORD_BYTES = 32  # mt_forest_record
+MT_SLAB_WIDE_IDS = 1      # mt_create_slab / mt_create_dist option
 
 # every symbol include/mt.h declares (checked by tests/test_abi_cpu.py)
 EXPORTS = ["mt_workspace_bytes", "mt_create", "mt_compute", "mt_set_diagram_output", "mt_diagram",
@@ -33,7 +36,7 @@ EXPORTS = ["mt_workspace_bytes", "mt_create", "mt_compute", "mt_set_diagram_outp
            "mt_create_slab", "mt_compute_local", "mt_forest_view", "mt_forest_scratch_bytes", "mt_compute_global",
            "mt_filter_diagram", "mt_graph_workspace_bytes", "mt_create_graph", "mt_compute_graph",
            "mt_get_unique_id", "mt_dist_slab_bounds", "mt_dist_workspace_bytes", "mt_create_dist",
-           "mt_compute_join_split", "mt_host_staging_bytes", "mt_compute_host"]
+           "mt_compute_join_split", "mt_host_staging_bytes", "mt_compute_host", "mt_triplets64", "mt_diagram64"]
 
 
 class MTError(RuntimeError):
@@ -88,18 +91,19 @@ def load(build_if_missing: bool = False):
         "mt_destroy": (None, [vp]),
         "mt_slab_workspace_bytes": (ctypes.c_size_t, [u32p, ctypes.c_int, ctypes.c_uint32, ctypes.c_uint32]),
         "mt_create_slab": (ctypes.c_int, [ctypes.POINTER(vp), u32p, ctypes.c_int, ctypes.c_uint32, ctypes.c_uint32,
-                                          ctypes.c_int, vp, ctypes.c_size_t]),
+                                          ctypes.c_uint32, ctypes.c_int, vp, ctypes.c_size_t]),
         "mt_compute_local": (ctypes.c_int, [vp, vp, vp, ctypes.c_uint32, vp]),
         "mt_forest_view": (ctypes.c_int, [vp, ctypes.POINTER(vp), u64p, vp]),
         "mt_forest_scratch_bytes": (ctypes.c_size_t, [ctypes.c_uint64]),
-        "mt_compute_global": (ctypes.c_int, [vp, vp, ctypes.c_uint64, u32p, ctypes.c_uint32, vp, ctypes.c_size_t,
-                                             vp, vp]),
+        "mt_compute_global": (ctypes.c_int, [vp, vp, u64p, u32p, ctypes.c_uint32, vp, ctypes.c_size_t, vp, vp]),
+        "mt_triplets64": (ctypes.c_int, [vp, vp, ctypes.c_uint64, ctypes.c_uint64, vp, vp]),
+        "mt_diagram64": (ctypes.c_int, [vp, vp, ctypes.c_uint64, u64p, u64p, vp]),
         "mt_abi_version": (ctypes.c_int, []),
         "mt_get_unique_id": (ctypes.c_int, [ctypes.c_void_p]),
         "mt_dist_slab_bounds": (ctypes.c_int, [ctypes.c_uint32, ctypes.c_int, u32p]),
         "mt_dist_workspace_bytes": (ctypes.c_size_t, [u32p, ctypes.c_int, ctypes.c_int, ctypes.c_int]),
         "mt_create_dist": (ctypes.c_int, [ctypes.POINTER(vp), u32p, ctypes.c_int, ctypes.c_int, ctypes.c_int,
-                                          ctypes.c_void_p, ctypes.c_int, vp, ctypes.c_size_t]),
+                                          ctypes.c_void_p, ctypes.c_uint32, ctypes.c_int, vp, ctypes.c_size_t]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -249,10 +253,12 @@ def mt_slab_workspace_bytes(dims, conn: int, z_begin: int, z_end: int) -> int:
     return int(load().mt_slab_workspace_bytes(_dims(dims), int(conn), int(z_begin), int(z_end)))
 
 
-def mt_create_slab(dims, conn: int, z_begin: int, z_end: int, device: int, workspace_ptr: int, workspace_bytes: int):
+def mt_create_slab(dims, conn: int, z_begin: int, z_end: int, device: int, workspace_ptr: int, workspace_bytes: int,
+                   options: int = 0):
     h = ctypes.c_void_p()
-    _check(load().mt_create_slab(ctypes.byref(h), _dims(dims), int(conn), int(z_begin), int(z_end), int(device),
-                                 ctypes.c_void_p(workspace_ptr), ctypes.c_size_t(workspace_bytes)), "mt_create_slab")
+    _check(load().mt_create_slab(ctypes.byref(h), _dims(dims), int(conn), int(z_begin), int(z_end), int(options),
+                                 int(device), ctypes.c_void_p(workspace_ptr), ctypes.c_size_t(workspace_bytes)),
+           "mt_create_slab")
     return h
 
 
@@ -271,12 +277,30 @@ def mt_forest_scratch_bytes(n_all: int) -> int:
     return int(load().mt_forest_scratch_bytes(ctypes.c_uint64(n_all)))
 
 
-def mt_compute_global(ctx, all_ptr: int, n_all: int, z_bounds, scratch_ptr: int, scratch_bytes: int,
+def mt_compute_global(ctx, all_ptr: int, counts, z_bounds, scratch_ptr: int, scratch_bytes: int,
                       triplets_ptr: int, stream=None):
+    """``counts``: records per slab (the gathered array holds them in slab order)."""
+    if len(counts) != len(z_bounds) - 1:
+        raise ValueError("one record count per slab")
     zb = (ctypes.c_uint32 * len(z_bounds))(*[int(z) for z in z_bounds])
-    _check(load().mt_compute_global(ctx, ctypes.c_void_p(all_ptr or None), ctypes.c_uint64(n_all), zb,
+    cn = (ctypes.c_uint64 * len(counts))(*[int(c) for c in counts])
+    _check(load().mt_compute_global(ctx, ctypes.c_void_p(all_ptr or None), cn, zb,
                                     len(z_bounds) - 1, ctypes.c_void_p(scratch_ptr), ctypes.c_size_t(scratch_bytes),
                                     ctypes.c_void_p(triplets_ptr), _stream_handle(stream)), "mt_compute_global")
+
+
+def mt_triplets64(ctx, triplets_ptr: int, first: int, count: int, out_ptr: int, stream=None):
+    _check(load().mt_triplets64(ctx, ctypes.c_void_p(triplets_ptr or None), ctypes.c_uint64(first),
+                                ctypes.c_uint64(count), ctypes.c_void_p(out_ptr or None), _stream_handle(stream)),
+           "mt_triplets64")
+
+
+def mt_diagram64(ctx, out_ptr: int, capacity: int, stream=None):
+    """Syncs; (status, n_pairs, n_essential); records copied to out_ptr (device) when non-zero."""
+    a, b = ctypes.c_uint64(0), ctypes.c_uint64(0)
+    st = load().mt_diagram64(ctx, ctypes.c_void_p(out_ptr or None), ctypes.c_uint64(capacity), ctypes.byref(a),
+                             ctypes.byref(b), _stream_handle(stream))
+    return st, a.value, b.value
 
 
 # ---- multi-GPU with the NCCL exchange inside the library -------------------------
@@ -298,13 +322,14 @@ def mt_dist_workspace_bytes(dims, conn: int, rank: int, nranks: int) -> int:
 
 
 def mt_create_dist(dims, conn: int, rank: int, nranks: int, nccl_id: bytes, device: int, workspace_ptr: int,
-                   workspace_bytes: int):
+                   workspace_bytes: int, options: int = 0):
     if len(nccl_id) != 128:
         raise ValueError("an NCCL unique id is 128 bytes")
     h = ctypes.c_void_p()
     idbuf = (ctypes.c_uint8 * 128)(*nccl_id)
     _check(load().mt_create_dist(ctypes.byref(h), _dims(dims), int(conn), int(rank), int(nranks), idbuf,
-                                 int(device), ctypes.c_void_p(workspace_ptr), ctypes.c_size_t(workspace_bytes)),
+                                 int(options), int(device), ctypes.c_void_p(workspace_ptr),
+                                 ctypes.c_size_t(workspace_bytes)),
            "mt_create_dist")
     return h
 

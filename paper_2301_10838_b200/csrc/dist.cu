@@ -10,7 +10,8 @@
 //   ncclAllGather     (every rank's forest record count, 8 B each)
 //   one host sync     (the counts size the exact-length exchange below)
 //   ncclBroadcast x P (grouped: each rank's records, exact length, into one
-//                      contiguous array in rank order -- no padding)
+//                      contiguous array in rank order -- no padding; in wide
+//                      mode the records carry compressed ids, slab.cu)
 //   mt_compute_global (forest merge, write-back, repair, diagram: kernels)
 // so a rank calls mt_compute / mt_diagram exactly as on one GPU.  NCCL is
 // loaded at run time (dlopen of libnccl.so.2; the copy torch already loaded
@@ -155,8 +156,8 @@ mt_status dist_compute(mt_ctx* c, DistState* d, const float* f, uint64_t* T, uin
     }
     if (N.GroupEnd() != ncclSuccess || nr != ncclSuccess) return MT_ERR_NCCL;
     char* sp = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(d->scratch) + 255) / 256 * 256);
-    return mt_compute_global(c, reinterpret_cast<const mt_forest_record*>(d->gather), n_all, d->bounds.data(),
-                             uint32_t(d->nranks), sp, need, T, s);
+    return mt_compute_global(c, reinterpret_cast<const mt_forest_record*>(d->gather), d->counts_host,
+                             d->bounds.data(), uint32_t(d->nranks), sp, need, T, s);
 }
 
 }  // namespace mt
@@ -187,7 +188,8 @@ size_t mt_dist_workspace_bytes(const uint32_t global_dims[3], int conn, int rank
 }
 
 mt_status mt_create_dist(mt_ctx** out, const uint32_t global_dims[3], int conn, int rank, int nranks,
-                         const uint8_t nccl_id[128], int cuda_device, void* workspace, size_t workspace_bytes) {
+                         const uint8_t nccl_id[128], uint32_t options, int cuda_device, void* workspace,
+                         size_t workspace_bytes) {
     if (!out) return MT_ERR_INVALID_ARG;
     *out = nullptr;
     if (!global_dims || !nccl_id || rank < 0 || rank >= nranks) return MT_ERR_INVALID_ARG;
@@ -196,7 +198,7 @@ mt_status mt_create_dist(mt_ctx** out, const uint32_t global_dims[3], int conn, 
     const mt::NcclApi& N = mt::nccl();
     if (!N.ok) return MT_ERR_NCCL;
     mt_ctx* c = nullptr;
-    mt_status st = mt_create_slab(&c, global_dims, conn, b[rank], b[rank + 1], cuda_device, workspace,
+    mt_status st = mt_create_slab(&c, global_dims, conn, b[rank], b[rank + 1], options, cuda_device, workspace,
                                   workspace_bytes);
     if (st != MT_OK) return st;
     mt::DistState* d = new (std::nothrow) mt::DistState();

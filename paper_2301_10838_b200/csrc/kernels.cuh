@@ -28,15 +28,49 @@ struct Slab {
 };
 
 // Boundary forest of all slabs (multi-GPU, slab.cu): records of every rank in one
-// array, an open-addressing table global id -> record index, 16-B cells with global
+// array, an open-addressing table view id -> record index, 16-B cells with view
 // ids after the forest merge, and the f bits of each record's vertex.
 struct ForestRef {
     const uint64_t* table;      // (id << 32 | index) or ~0 (empty); size mask + 1
-    const uint64_t* vtable;     // (id << 32 | f bits) of every record's vertex and saddle; same size
+    const uint64_t* vtable;     // (id << 32 | f bits) of the zero-valued saddles; same size
     uint32_t mask;
-    Cell* cells;                // merged cells, global ids
+    Cell* cells;                // merged cells, view ids
     const mt_forest_record* recs;
+    const uint32_t* vid;        // view id of each record's vertex
     unsigned long long* err;    // error bits (ERR_FOREST on a missing id)
+};
+
+constexpr int MAX_SLABS = 64;
+
+// The gathered records in this rank's view (slab.cu header): slab k's ids at voff[k] + local id
+// (own slab, k == self) or voff[k] + compressed id (other slabs; in 32-bit mode the compressed id
+// is the local id and voff[k] = nx ny z_begin(k), so view ids are global ids).
+struct ForestXlate {
+    uint32_t nslabs, self, flip;
+    bool wide;
+    uint64_t rec_off[MAX_SLABS + 1];   // first record of slab k
+    uint32_t voff[MAX_SLABS];
+    uint64_t real_base[MAX_SLABS];     // global id of slab k's first vertex
+    uint32_t dec_lo, own_lo;           // wide: lowest remote view id, first own view id
+    uint64_t own_n;
+    // index of remote view id y in the decode array (the own range is skipped)
+    __device__ __forceinline__ uint64_t dec_index(uint32_t y) const {
+        return y < own_lo ? uint64_t(y - dec_lo) : uint64_t(own_lo - dec_lo) + (uint64_t(y) - own_lo - own_n);
+    }
+};
+
+// view id -> 64-bit global id (identity in 32-bit mode)
+struct IdDecode {
+    bool wide;
+    uint32_t dec_lo, own_lo;
+    uint64_t own_n, own_gid0;
+    const uint64_t* dec;
+    __device__ __forceinline__ uint64_t gid(uint32_t y) const {
+        if (!wide) return y;
+        const uint64_t k = uint64_t(y) - own_lo;
+        if (k < own_n) return own_gid0 + k;
+        return y < own_lo ? dec[y - dec_lo] : dec[uint64_t(own_lo - dec_lo) + (uint64_t(y) - own_lo - own_n)];
+    }
 };
 
 __device__ __forceinline__ uint32_t forest_hash(uint32_t id, uint32_t mask) {
@@ -140,26 +174,38 @@ void launch_filter_diagram(const mt_pair* in, uint64_t n_fin, uint64_t n_all, fl
                            unsigned long long* ctl, uint64_t* status, cudaStream_t stream);
 
 // multi-GPU boundary forest (slab.cu)
-constexpr int MAX_SLABS = 64;
-struct SlabBounds {
-    uint32_t z[MAX_SLABS + 1];
-    uint32_t count;             // number of slabs
-};
-// T0: the slab's tile store (regular vertices have no working cell, see launch_tile_tmt)
-void launch_forest_mark(const Cell* C, const uint64_t* T0, const Slab& sl, uint8_t* flag, cudaStream_t stream);
-void launch_forest_compact(const Cell* C, const uint64_t* T0, const float* f, const Slab& sl, uint32_t flip,
-                           const uint8_t* flag, mt_forest_record* recs, uint64_t cap, unsigned long long* count,
-                           int num_sms, cudaStream_t stream);
+// T0: the slab's tile store (regular vertices have no working cell, see launch_tile_tmt); the
+// faces marked are the slab's inter-slab faces (below / above)
+void launch_forest_mark(const Cell* C, const uint64_t* T0, const Slab& sl, bool has_bottom, bool has_top,
+                        uint8_t* flag, cudaStream_t stream);
+// records with slab-local ids (compressed ids = local ids)
+void launch_forest_compact(const Cell* C, const uint64_t* T0, const float* f, const Slab& sl, const uint8_t* flag,
+                           mt_forest_record* recs, uint64_t cap, unsigned long long* count, int num_sms,
+                           cudaStream_t stream);
+// wide mode: the records' compressed ids (top face from local id top_begin on; UINT64_MAX: none);
+// scratch >= forest_compress_scratch_bytes(n); returns the kernels launched
+size_t forest_compress_scratch_bytes(uint64_t n);
+int launch_forest_compress(mt_forest_record* recs, const unsigned long long* count, uint64_t n, uint64_t top_begin,
+                           void* scratch, int num_sms, cudaStream_t stream);
 // open-addressing table slots for n_all gathered records (>= 4 n_all, a power of two), or 0
 // when that exceeds 2^31 (32-bit table indices)
 uint64_t forest_table_size(uint64_t n_all);
-void launch_forest_build(const mt_forest_record* all, uint64_t n_all, uint64_t* table, uint64_t* vtable,
-                         uint32_t mask, Cell* cells, int num_sms, cudaStream_t stream);
-// inter-slab edges: deduplicated by tile-representative pairs into `queue`, then merged
+// cells, view ids and (wide) the decode array of the gathered records
+void launch_forest_build(const mt_forest_record* all, uint64_t n_all, const ForestXlate& X, uint64_t* table,
+                         uint64_t* vtable, uint32_t mask, Cell* cells, uint32_t* vid, uint64_t* dec, int num_sms,
+                         cudaStream_t stream);
+// inter-slab edges: deduplicated by tile-representative pairs into `queue`, then merged;
+// boundary k joins view ids a0[k] + r and b0[k] + r, r < nx ny
 size_t forest_queue_entry_bytes();
-void launch_forest_merge(const ForestRef& F, const Slab& sl, const SlabBounds& b, void* queue,
-                         unsigned long long* qlen, unsigned long long* fetch, int num_sms, cudaStream_t stream);
+void launch_forest_merge(const ForestRef& F, const Slab& sl, uint32_t nslabs, const uint32_t* a0, const uint32_t* b0,
+                         void* queue, unsigned long long* qlen, unsigned long long* fetch, int num_sms,
+                         cudaStream_t stream);
 void launch_forest_writeback(const ForestRef& F, uint64_t n_all, Cell* C, const uint64_t* T0, const Slab& sl,
                              int num_sms, cudaStream_t stream);
+// view ids -> 64-bit global ids
+void launch_triplets64(const uint64_t* T, uint64_t count, const IdDecode& d, mt_triplet64* out, int num_sms,
+                       cudaStream_t stream);
+void launch_pairs64(const mt_pair* in, uint64_t count, const IdDecode& d, mt_pair64* out, int num_sms,
+                    cudaStream_t stream);
 
 }  // namespace mt

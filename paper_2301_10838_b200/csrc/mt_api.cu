@@ -113,9 +113,10 @@ Layout layout_for(uint64_t n, uint64_t ncross, bool slab = false, uint64_t ess_c
     off += align_up(L.seg_cap * sizeof(uint16_t));
     L.seg_pos = off;
     off += align_up(L.seg_cap * sizeof(uint32_t));
-    if (slab) {  // boundary forest of the slab: a flag per vertex, at most n records
+    if (slab) {  // boundary forest of the slab: a flag per vertex (then the wide-mode compression
+                 // scratch), at most n records
         L.flags = off;
-        off += align_up(n);
+        off += align_up(std::max<size_t>(n, mt::forest_compress_scratch_bytes(n)));
         L.recs = off;
         L.recs_cap = n;
         off += align_up(n * sizeof(mt_forest_record));
@@ -136,7 +137,13 @@ Layout grid_layout(const uint32_t dims[3], uint32_t z_begin, uint32_t z_end, boo
 struct mt_ctx {
     uint32_t nx, ny, nz;
     uint64_t n;              // vertices this context owns
-    mt::Slab slab;           // owned planes of the global grid (all of them for mt_create)
+    mt::Slab slab;           // owned planes of the global grid (all of them for mt_create), in the
+                             // context's id view (slab.cu header; wide mode: a virtual grid)
+    uint32_t z_begin, z_end; // owned planes of the real grid
+    uint64_t gid0;           // global id of the first owned vertex
+    bool wide = false;       // wide ids (f3): view ids != global ids
+    mt::IdDecode decode{};   // view -> global ids of the last result
+    bool decode_ok = false;
     bool multi = false;      // created by mt_create_slab
     bool graph = false;      // created by mt_create_graph (CSR adjacency instead of a grid)
     bool local_done = false; // mt_compute_local ran, mt_compute_global pending
@@ -238,12 +245,35 @@ mt_status sync_counters(mt_ctx* c, cudaStream_t s) {
 extern "C" void mt_destroy(mt_ctx* c);
 namespace {
 
+// wide mode: the slab's planes in a virtual grid of 32-bit ids, centred so that the other slabs'
+// referenced vertices fit below and above (slab.cu header); false if the slab itself cannot fit
+bool wide_view(const uint32_t dims[3], uint32_t z_begin, uint32_t z_end, mt::Slab* v) {
+    const uint64_t sxy = uint64_t(dims[0]) * dims[1], nzl = z_end - z_begin;
+    if (sxy == 0 || sxy > 0xffffffffull) return false;
+    const uint64_t planes = 0xffffffffull / sxy;   // view ids stay below 2^32 - 1
+    if (planes < nzl + 2) return false;
+    const uint64_t zb = (planes - nzl) / 2;
+    *v = mt::Slab{dims[0], dims[1], uint32_t(planes), uint32_t(zb), uint32_t(zb + nzl), zb * sxy, nzl * sxy};
+    return true;
+}
+
+bool n_global_fits(const uint32_t dims[3]) {   // nx ny nz < 2^63 (64-bit global ids)
+    const uint64_t sxy = uint64_t(dims[0]) * dims[1];
+    return sxy == 0 || dims[2] <= (1ull << 63) / sxy;
+}
+
 mt_status create_ctx(mt_ctx** out, const uint32_t dims[3], int conn, uint32_t z_begin, uint32_t z_end, bool multi,
-                     int cuda_device, void* workspace, size_t workspace_bytes, const Layout* graph_layout = nullptr) {
+                     int cuda_device, void* workspace, size_t workspace_bytes, const Layout* graph_layout = nullptr,
+                     uint32_t options = 0) {
     if (!out) return MT_ERR_INVALID_ARG;
     *out = nullptr;
     if (!graph_layout && !valid_dims(dims, conn)) return MT_ERR_INVALID_ARG;
-    if (uint64_t(dims[0]) * dims[1] * dims[2] > 0xffffffffull) return MT_ERR_TOO_LARGE;
+    if (!n_global_fits(dims)) return MT_ERR_TOO_LARGE;
+    const bool wide = multi && ((options & MT_SLAB_WIDE_IDS) ||
+                                uint64_t(dims[0]) * dims[1] * dims[2] > 0xffffffffull);
+    mt::Slab view{};
+    if (wide && !wide_view(dims, z_begin, z_end, &view)) return MT_ERR_TOO_LARGE;
+    if (!wide && uint64_t(dims[0]) * dims[1] * dims[2] > 0xffffffffull) return MT_ERR_TOO_LARGE;
     const uint64_t n = uint64_t(dims[0]) * dims[1] * (z_end - z_begin);
     const Layout L = graph_layout ? *graph_layout
                                   : grid_layout(dims, z_begin, z_end, multi);
@@ -260,7 +290,12 @@ mt_status create_ctx(mt_ctx** out, const uint32_t dims[3], int conn, uint32_t z_
     c->ny = dims[1];
     c->nz = dims[2];
     c->n = n;
-    c->slab = mt::Slab{dims[0], dims[1], dims[2], z_begin, z_end, uint64_t(dims[0]) * dims[1] * z_begin, n};
+    c->slab = wide ? view : mt::Slab{dims[0], dims[1], dims[2], z_begin, z_end, uint64_t(dims[0]) * dims[1] * z_begin, n};
+    c->z_begin = z_begin;
+    c->z_end = z_end;
+    c->gid0 = uint64_t(dims[0]) * dims[1] * z_begin;
+    c->wide = wide;
+    c->decode_ok = !wide;
     c->multi = multi;
     c->graph = graph_layout != nullptr;
     c->conn = conn;
@@ -286,6 +321,8 @@ mt_status create_ctx(mt_ctx** out, const uint32_t dims[3], int conn, uint32_t z_
 // caller's triplet buffer, indexed from the slab's first vertex) receives the tile store T0
 // reset the context for a new compute: state, statistics, counters and chunk status records
 mt_status prepare_compute(mt_ctx* c, const float* f, uint32_t flags, cudaStream_t s) {
+    c->decode = mt::IdDecode{};   // 32-bit mode: view ids are global ids
+    c->decode_ok = !c->wide;
     c->launches = 0;
     c->nev = 0;
     c->sticky = MT_OK;
@@ -360,13 +397,13 @@ mt_status finish_compute(mt_ctx* c, uint64_t* T, const mt::ForestRef* forest, cu
 
 extern "C" {
 
-int mt_abi_version(void) { return 2; }
+int mt_abi_version(void) { return 3; }
 
 const char* mt_status_string(mt_status s) {
     switch (s) {
         case MT_OK: return "ok";
         case MT_ERR_INVALID_ARG: return "invalid argument";
-        case MT_ERR_TOO_LARGE: return "grid too large for 32-bit vertex ids";
+        case MT_ERR_TOO_LARGE: return "vertex ids do not fit (32-bit ids on one GPU / in a slab's view)";
         case MT_ERR_NONFINITE: return "non-finite value in f";
         case MT_ERR_CUDA: return "CUDA error";
         case MT_ERR_NCCL: return "NCCL error";
@@ -392,16 +429,19 @@ mt_status mt_create(mt_ctx** out, const uint32_t dims[3], int conn, int cuda_dev
 
 size_t mt_slab_workspace_bytes(const uint32_t dims[3], int conn, uint32_t z_begin, uint32_t z_end) {
     if (!valid_dims(dims, conn) || dims[2] < 2 || z_begin >= z_end || z_end > dims[2]) return 0;
-    if (uint64_t(dims[0]) * dims[1] * dims[2] > 0xffffffffull) return 0;
+    mt::Slab v{};
+    if (!n_global_fits(dims) || !wide_view(dims, z_begin, z_end, &v)) return 0;   // the slab fits 32-bit ids
     return grid_layout(dims, z_begin, z_end, true).total;
 }
 
 mt_status mt_create_slab(mt_ctx** out, const uint32_t dims[3], int conn, uint32_t z_begin, uint32_t z_end,
-                         int cuda_device, void* workspace, size_t workspace_bytes) {
+                         uint32_t options, int cuda_device, void* workspace, size_t workspace_bytes) {
     if (!out) return MT_ERR_INVALID_ARG;
     *out = nullptr;
     if (!dims || dims[2] < 2 || conn != 6 || z_begin >= z_end || z_end > dims[2]) return MT_ERR_INVALID_ARG;
-    return create_ctx(out, dims, conn, z_begin, z_end, true, cuda_device, workspace, workspace_bytes);
+    if (options & ~uint32_t(MT_SLAB_WIDE_IDS)) return MT_ERR_INVALID_ARG;
+    return create_ctx(out, dims, conn, z_begin, z_end, true, cuda_device, workspace, workspace_bytes, nullptr,
+                      options);
 }
 
 mt_status mt_set_diagram_output(mt_ctx* c, mt_pair* buf, uint64_t capacity) {
@@ -631,14 +671,22 @@ mt_status mt_compute_local(mt_ctx* c, const float* f, uint64_t* T, uint32_t flag
     mt_status st = start_compute(c, f, T, flags, s);
     if (st != MT_OK) return st;
     c->local_T = T;
+    const bool has_bottom = c->z_begin > 0, has_top = c->z_end < c->nz;
     mark(c, "forest_mark", s);
-    mt::launch_forest_mark(cells_of(c), T - c->slab.base, c->slab, flag, s);
+    mt::launch_forest_mark(cells_of(c), T - c->slab.base, c->slab, has_bottom, has_top, flag, s);
     mark(c, "forest_compact", s);
-    mt::launch_forest_compact(cells_of(c), T - c->slab.base, f - c->slab.base, c->slab, c->flip, flag,
-                              reinterpret_cast<mt_forest_record*>(c->ws + c->L.recs), c->L.recs_cap,
-                              counters_of(c) + mt::CTR_FCOUNT, c->num_sms, s);
-    mark(c, "exchange", s);  // closes at mt_compute_global's first mark: host sync + all-gather
+    mt_forest_record* recs = reinterpret_cast<mt_forest_record*>(c->ws + c->L.recs);
+    unsigned long long* fcount = counters_of(c) + mt::CTR_FCOUNT;
+    mt::launch_forest_compact(cells_of(c), T - c->slab.base, f - c->slab.base, c->slab, flag, recs, c->L.recs_cap,
+                              fcount, c->num_sms, s);
     c->launches += 2;
+    if (c->wide) {   // the flags are dead after the compaction: their space holds the bitmap
+        mark(c, "forest_compress", s);
+        const uint64_t sxy = uint64_t(c->nx) * c->ny;
+        c->launches += mt::launch_forest_compress(recs, fcount, c->n, has_top ? c->n - sxy : ~0ull, flag,
+                                                  c->num_sms, s);
+    }
+    mark(c, "exchange", s);  // closes at mt_compute_global's first mark: host sync + all-gather
     c->local_done = true;
     if (cudaGetLastError() != cudaSuccess) return c->sticky = MT_ERR_CUDA;
     return MT_OK;
@@ -659,58 +707,106 @@ mt_status mt_forest_view(mt_ctx* c, const mt_forest_record** records, uint64_t* 
 
 // id tables (2) | merged cells | queue of deduplicated inter-slab edges (every face vertex of a
 // boundary has a record, so a boundary's nx ny edges are at most half of the records)
+// + the view id of each record and (wide mode) the global id of every remote view id (at most
+// 2 per record)
 size_t mt_forest_scratch_bytes(uint64_t n_all) {
     const uint64_t t = mt::forest_table_size(n_all);
     if (t == 0) return 0;
     return 2 * align_up(size_t(t) * sizeof(uint64_t)) + align_up(n_all * sizeof(mt::Cell)) +
-           align_up((n_all / 2 + 1) * mt::forest_queue_entry_bytes());
+           align_up((n_all / 2 + 1) * mt::forest_queue_entry_bytes()) + align_up(n_all * sizeof(uint32_t)) +
+           align_up(2 * n_all * sizeof(uint64_t));
 }
 
-mt_status mt_compute_global(mt_ctx* c, const mt_forest_record* all, uint64_t n_all, const uint32_t* z_bounds,
+mt_status mt_compute_global(mt_ctx* c, const mt_forest_record* all, const uint64_t* counts, const uint32_t* z_bounds,
                             uint32_t nslabs, void* scratch, size_t scratch_bytes, uint64_t* T, mt_stream_t stream) {
-    if (!c || !z_bounds || !T || (n_all && !all)) return MT_ERR_INVALID_ARG;
+    if (!c || !z_bounds || !counts || !T) return MT_ERR_INVALID_ARG;
     if (!c->multi || !c->local_done) return MT_ERR_STATE;
     if (T != c->local_T) return MT_ERR_INVALID_ARG;   // the buffer holding mt_compute_local's tile store
     if (nslabs < 1 || nslabs > uint32_t(mt::MAX_SLABS) || z_bounds[0] != 0 || z_bounds[nslabs] != c->nz)
         return MT_ERR_INVALID_ARG;
-    bool found = false;
+    uint32_t self = nslabs;
+    uint64_t n_all = 0;
     for (uint32_t k = 0; k < nslabs; ++k) {
         if (z_bounds[k] >= z_bounds[k + 1]) return MT_ERR_INVALID_ARG;
-        found |= z_bounds[k] == c->slab.z_begin && z_bounds[k + 1] == c->slab.z_end;
+        if (z_bounds[k] == c->z_begin && z_bounds[k + 1] == c->z_end) self = k;
+        n_all += counts[k];
     }
-    if (!found) return MT_ERR_INVALID_ARG;
+    if (self == nslabs) return MT_ERR_INVALID_ARG;
+    if (n_all && !all) return MT_ERR_INVALID_ARG;
     if (n_all > 0xffffffffull || mt::forest_table_size(n_all) == 0) return MT_ERR_TOO_LARGE;
     if (!scratch || scratch_bytes < mt_forest_scratch_bytes(n_all) || reinterpret_cast<uintptr_t>(scratch) % ALIGN)
         return MT_ERR_WORKSPACE;
+    // this rank's view of every slab's ids (slab.cu header)
+    const uint64_t sxy = uint64_t(c->nx) * c->ny;
+    mt::ForestXlate X{};
+    X.nslabs = nslabs;
+    X.self = self;
+    X.flip = c->flip;
+    X.wide = c->wide;
+    uint64_t span[mt::MAX_SLABS];
+    for (uint32_t k = 0; k < nslabs; ++k) {
+        X.rec_off[k + 1] = X.rec_off[k] + counts[k];
+        X.real_base[k] = uint64_t(z_bounds[k]) * sxy;
+        span[k] = k == self ? c->n : c->wide ? 2 * counts[k] : uint64_t(z_bounds[k + 1] - z_bounds[k]) * sxy;
+    }
+    if (c->wide) {
+        const uint64_t own = c->slab.base;
+        uint64_t below = 0, above = 0;
+        for (uint32_t k = 0; k < self; ++k) below += span[k];
+        for (uint32_t k = self + 1; k < nslabs; ++k) above += span[k];
+        if (below > own || own + c->n + above > 0xffffffffull) return MT_ERR_TOO_LARGE;
+        uint64_t at = own - below;
+        for (uint32_t k = 0; k < nslabs; ++k) {
+            X.voff[k] = uint32_t(at);
+            at += span[k];
+        }
+        X.dec_lo = X.voff[0];
+        X.own_lo = uint32_t(own);
+        X.own_n = c->n;
+    } else {
+        for (uint32_t k = 0; k < nslabs; ++k) X.voff[k] = uint32_t(X.real_base[k]);
+    }
+    uint32_t a0[mt::MAX_SLABS], b0[mt::MAX_SLABS];
+    for (uint32_t k = 0; k + 1 < nslabs; ++k) {   // the faces of boundary k in the view
+        a0[k] = uint32_t(X.voff[k] + span[k] - sxy);
+        b0[k] = X.voff[k + 1];
+    }
     DeviceGuard g(c->device);
     if (!g.ok) return MT_ERR_CUDA;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const uint32_t tsize = uint32_t(mt::forest_table_size(n_all));
-    uint64_t* table = static_cast<uint64_t*>(scratch);
-    uint64_t* vtable = reinterpret_cast<uint64_t*>(static_cast<char*>(scratch) + align_up(size_t(tsize) * 8));
-    mt::Cell* fcells = reinterpret_cast<mt::Cell*>(static_cast<char*>(scratch) + 2 * align_up(size_t(tsize) * 8));
-    mt::ForestRef F{table, vtable, tsize - 1, fcells, all, counters_of(c) + mt::CTR_ERR};
-    mt::SlabBounds b{};
-    b.count = nslabs;
-    for (uint32_t k = 0; k <= nslabs; ++k) b.z[k] = z_bounds[k];
+    char* p = static_cast<char*>(scratch);
+    uint64_t* table = reinterpret_cast<uint64_t*>(p);
+    uint64_t* vtable = reinterpret_cast<uint64_t*>(p + align_up(size_t(tsize) * 8));
+    p += 2 * align_up(size_t(tsize) * 8);
+    mt::Cell* fcells = reinterpret_cast<mt::Cell*>(p);
+    p += align_up(n_all * sizeof(mt::Cell));
+    void* fqueue = p;
+    p += align_up((n_all / 2 + 1) * mt::forest_queue_entry_bytes());
+    uint32_t* vid = reinterpret_cast<uint32_t*>(p);
+    p += align_up(n_all * sizeof(uint32_t));
+    uint64_t* dec = reinterpret_cast<uint64_t*>(p);
+    mt::ForestRef F{table, vtable, tsize - 1, fcells, all, vid, counters_of(c) + mt::CTR_ERR};
     mark(c, "forest_build", s);
     if (cudaMemsetAsync(table, 0xff, 2 * align_up(size_t(tsize) * 8), s) != cudaSuccess)
         return c->sticky = MT_ERR_CUDA;
-    mt::launch_forest_build(all, n_all, table, vtable, tsize - 1, fcells, c->num_sms, s);
+    mt::launch_forest_build(all, n_all, X, table, vtable, tsize - 1, fcells, vid, dec, c->num_sms, s);
     mark(c, "forest_merge", s);
-    void* fqueue = static_cast<char*>(scratch) + 2 * align_up(size_t(tsize) * 8) + align_up(n_all * sizeof(mt::Cell));
-    mt::launch_forest_merge(F, c->slab, b, fqueue, counters_of(c) + mt::CTR_FQLEN, counters_of(c) + mt::CTR_FFETCH,
-                            c->num_sms, s);
+    mt::launch_forest_merge(F, c->slab, nslabs, a0, b0, fqueue, counters_of(c) + mt::CTR_FQLEN,
+                            counters_of(c) + mt::CTR_FFETCH, c->num_sms, s);
     mark(c, "forest_writeback", s);
     mt::launch_forest_writeback(F, n_all, cells_of(c), T - c->slab.base, c->slab, c->num_sms, s);
     c->launches += 3;
     c->local_done = false;
+    c->decode = mt::IdDecode{c->wide, X.dec_lo, X.own_lo, X.own_n, c->gid0, dec};
+    c->decode_ok = true;
     return finish_compute(c, T, &F, s);
 }
 
 mt_status mt_diagram(mt_ctx* c, mt_pair* out, uint64_t capacity, uint64_t* n_pairs, uint64_t* n_essential,
                      mt_stream_t stream) {
     if (!c) return MT_ERR_INVALID_ARG;
+    if (c->wide) return MT_ERR_TOO_LARGE;   // view ids: mt_diagram64
     DeviceGuard g(c->device);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const mt_status st = sync_counters(c, s);
@@ -735,6 +831,7 @@ mt_status mt_diagram(mt_ctx* c, mt_pair* out, uint64_t capacity, uint64_t* n_pai
 mt_status mt_diagram_view(mt_ctx* c, const mt_pair** records, uint64_t* n_pairs, uint64_t* n_essential,
                           mt_stream_t stream) {
     if (!c) return MT_ERR_INVALID_ARG;
+    if (c->wide) return MT_ERR_TOO_LARGE;
     DeviceGuard g(c->device);
     const mt_status st = sync_counters(c, static_cast<cudaStream_t>(stream));
     if (st == MT_ERR_STATE || st == MT_ERR_CUDA) return st;
@@ -743,6 +840,39 @@ mt_status mt_diagram_view(mt_ctx* c, const mt_pair** records, uint64_t* n_pairs,
     uint64_t cap = 0;
     if (records) *records = target_of(c, &cap);
     return st;
+}
+
+mt_status mt_triplets64(mt_ctx* c, const uint64_t* T, uint64_t first, uint64_t count, mt_triplet64* out,
+                        mt_stream_t stream) {
+    if (!c) return MT_ERR_INVALID_ARG;
+    if (!c->computed || !c->decode_ok || c->local_done) return MT_ERR_STATE;
+    if (first > c->n || count > c->n - first) return MT_ERR_INVALID_ARG;
+    if (count == 0) return MT_OK;
+    if (!T || !out) return MT_ERR_INVALID_ARG;
+    DeviceGuard g(c->device);
+    if (!g.ok) return MT_ERR_CUDA;
+    mt::launch_triplets64(T + first, count, c->decode, out, c->num_sms, static_cast<cudaStream_t>(stream));
+    return cudaGetLastError() == cudaSuccess ? MT_OK : MT_ERR_CUDA;
+}
+
+mt_status mt_diagram64(mt_ctx* c, mt_pair64* out, uint64_t capacity, uint64_t* n_pairs, uint64_t* n_essential,
+                       mt_stream_t stream) {
+    if (!c) return MT_ERR_INVALID_ARG;
+    DeviceGuard g(c->device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const mt_status st = sync_counters(c, s);
+    if (st == MT_ERR_STATE || st == MT_ERR_CUDA) return st;
+    if (!c->decode_ok || c->local_done) return MT_ERR_STATE;
+    const uint64_t nfin = c->host_ctr[mt::CTR_FIN], ness = c->host_ctr[mt::CTR_ESS];
+    if (n_pairs) *n_pairs = nfin;
+    if (n_essential) *n_essential = ness;
+    if (st != MT_OK || !out || nfin + ness == 0) return st;
+    if (capacity < nfin + ness) return MT_ERR_CAPACITY;
+    uint64_t cap = 0;
+    const mt_pair* src = target_of(c, &cap);
+    mt::launch_pairs64(src, nfin + ness, c->decode, out, c->num_sms, s);
+    if (cudaGetLastError() != cudaSuccess || cudaStreamSynchronize(s) != cudaSuccess) return c->sticky = MT_ERR_CUDA;
+    return MT_OK;
 }
 
 mt_status mt_last_error(mt_ctx* c, mt_stream_t stream) {
@@ -755,6 +885,7 @@ mt_status mt_last_error(mt_ctx* c, mt_stream_t stream) {
 mt_status mt_filter_diagram(mt_ctx* c, float eps, mt_pair* out, uint64_t capacity, uint64_t* n_pairs_kept,
                             uint64_t* n_essential, mt_stream_t stream) {
     if (!c || !(eps >= 0.f)) return MT_ERR_INVALID_ARG;
+    if (c->wide) return MT_ERR_TOO_LARGE;
     DeviceGuard g(c->device);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const mt_status st = sync_counters(c, s);

@@ -19,6 +19,20 @@
 // then the repair walks local cells and, past a remote id, the merged forest
 // (repair_diagram.cu, ForestView).  Every rank merges the whole forest
 // redundantly; the post-repair store is unique, so the ranks agree.
+//
+// Ids (PAPER.md:389-396 and 1063-1066 name the 32-bit
+// packing as the obstacle to distribution).  Every kernel of a context works in
+// the context's 32-bit VIEW of the id space: its own vertices at view ids
+// [base, base + n), the vertices of other slabs the gathered forest references
+// at view ids below and above, in global order.  32-bit mode: the view is the
+// global id (base = nx ny z_begin).  Wide mode (global ids past 2^32): each
+// slab numbers the vertices its records reference (ids and saddles) by rank --
+// an order-preserving compression (forest_refmark / popc_* / forest_compress)
+// -- and each receiver places slab k's compressed ids at its own offset voff[k]
+// (forest_build).  Every decision of the method compares (value, id) keys or
+// tests ids for equality (Alg. 3-5, reading R1), and an order-preserving
+// relabelling keeps all of them, so each rank computes its slab's result with
+// view ids, which mt_triplets64 / mt_diagram64 translate (id_decode).
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -70,33 +84,149 @@ forest_mark_kernel(const Cell* C, const uint64_t* T0, uint32_t nx, uint32_t ny, 
 }
 
 __global__ void __launch_bounds__(256)
-forest_compact_kernel(const Cell* C, const uint64_t* T0, const float* f, uint32_t flip, uint64_t base, uint64_t n,
+forest_compact_kernel(const Cell* C, const uint64_t* T0, const float* f, uint64_t base, uint64_t n,
                       const uint8_t* __restrict__ flag, mt_forest_record* __restrict__ recs, uint64_t cap,
                       unsigned long long* count) {
     const int lane = threadIdx.x & 31;
     const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+    const uint32_t b = uint32_t(base);
     for (uint64_t l0 = uint64_t(blockIdx.x) * blockDim.x; l0 < n; l0 += stride) {
         const uint64_t l = l0 + threadIdx.x;
         const bool take = l < n && flag[l];
         const uint32_t m = __ballot_sync(FULL_MASK, take);
-        unsigned long long b = 0;
-        if (lane == 0 && m) b = atomicAdd(count, (unsigned long long)__popc(m));
-        b = __shfl_sync(FULL_MASK, b, 0);
+        unsigned long long b0 = 0;
+        if (lane == 0 && m) b0 = atomicAdd(count, (unsigned long long)__popc(m));
+        b0 = __shfl_sync(FULL_MASK, b0, 0);
         if (take) {
-            const uint64_t pos = b + __popc(m & ((1u << lane) - 1u));
+            const uint64_t pos = b0 + __popc(m & ((1u << lane) - 1u));
             const uint32_t u = uint32_t(base + l);
             uint32_t rep, o;
             const uint32_t fb = __float_as_uint(f[u]);
+            const uint32_t lu = uint32_t(l);
             mt_forest_record rec;
             if (tile_regular(T0, u, &rep, &o)) {
                 // the cell the vertex would have: (u, u, R) at its own key
-                rec = mt_forest_record{u, fb, key_of(o, u), (uint64_t(o) << 32) | rep, fb, 0u};
+                rec = mt_forest_record{lu, lu, rep - b, fb, fb, lu, lu, rep - b};
             } else {
                 const Cell c = ld_cell(C + u);
-                rec = mt_forest_record{u, fb, c.lo, c.hi, __float_as_uint(f[cs_of(c)]), 0u};
+                const uint32_t ls = cs_of(c) - b, lv = cv_of(c) - b;
+                rec = mt_forest_record{lu, ls, lv, fb, __float_as_uint(f[cs_of(c)]), lu, ls, lv};
             }
             if (pos < cap) recs[pos] = rec;
         }
+    }
+}
+
+// ---- wide mode, sender side: order-preserving compression of the referenced local ids ----
+// referenced = the records' vertices and their saddles (every v is a record's vertex: the forest
+// is closed under v).  c(l) = #referenced ids below l, plus a gap before the top face so that the
+// top face of a slab with count records sits at [2 count - nx ny, 2 count) -- the receivers know
+// where a face is without the slab's exact number of referenced ids (2 count bounds it).
+__global__ void __launch_bounds__(256)
+forest_refmark_kernel(const mt_forest_record* __restrict__ recs, const unsigned long long* __restrict__ count,
+                      uint32_t* __restrict__ bits) {
+    const uint64_t nrec = *count;
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < nrec;
+         i += uint64_t(gridDim.x) * blockDim.x) {
+        const uint32_t id = recs[i].id, sd = recs[i].s;
+        atomicOr(bits + (id >> 5), 1u << (id & 31));
+        if (sd != id) atomicOr(bits + (sd >> 5), 1u << (sd & 31));
+    }
+}
+
+constexpr int PC_THREADS = 1024, PC_WORDS = 8;   // one CTA: 8192 bitmap words
+__device__ __forceinline__ uint32_t cta_exclusive_scan(uint32_t x, uint32_t* s_warp, uint32_t* total) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t incl = x;
+    for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t y = __shfl_up_sync(FULL_MASK, incl, d);
+        if (lane >= d) incl += y;
+    }
+    if (lane == 31) s_warp[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+        uint32_t w = lane < int(blockDim.x >> 5) ? s_warp[lane] : 0u, wi = w;
+        for (int d = 1; d < 32; d <<= 1) {
+            const uint32_t y = __shfl_up_sync(FULL_MASK, wi, d);
+            if (lane >= d) wi += y;
+        }
+        s_warp[lane] = wi - w;
+        if (lane == 31) s_warp[32] = wi;
+    }
+    __syncthreads();
+    const uint32_t r = s_warp[warp] + incl - x;
+    *total = s_warp[32];
+    __syncthreads();
+    return r;
+}
+
+__global__ void __launch_bounds__(PC_THREADS)
+popc_block_kernel(const uint32_t* __restrict__ bits, uint64_t nwords, uint32_t* __restrict__ bsum) {
+    __shared__ uint32_t s_warp[33];
+    const uint64_t w0 = uint64_t(blockIdx.x) * PC_THREADS * PC_WORDS + uint64_t(threadIdx.x) * PC_WORDS;
+    uint32_t c = 0;
+    for (int k = 0; k < PC_WORDS; ++k)
+        if (w0 + k < nwords) c += __popc(bits[w0 + k]);
+    uint32_t tot = 0;
+    cta_exclusive_scan(c, s_warp, &tot);
+    if (threadIdx.x == 0) bsum[blockIdx.x] = tot;
+}
+
+// one CTA: exclusive scan of the block sums in place, the total into bsum[nblocks]
+__global__ void __launch_bounds__(PC_THREADS) popc_scan_kernel(uint32_t* __restrict__ bsum, uint32_t nblocks) {
+    __shared__ uint32_t s_warp[33];
+    const uint32_t per = (nblocks + PC_THREADS - 1) / PC_THREADS;
+    const uint32_t b0 = threadIdx.x * per;
+    uint32_t c = 0;
+    for (uint32_t k = 0; k < per; ++k)
+        if (b0 + k < nblocks) c += bsum[b0 + k];
+    uint32_t tot = 0;
+    uint32_t run = cta_exclusive_scan(c, s_warp, &tot);
+    for (uint32_t k = 0; k < per; ++k)
+        if (b0 + k < nblocks) {
+            const uint32_t x = bsum[b0 + k];
+            bsum[b0 + k] = run;
+            run += x;
+        }
+    if (threadIdx.x == 0) bsum[nblocks] = tot;
+}
+
+__global__ void __launch_bounds__(PC_THREADS)
+popc_prefix_kernel(const uint32_t* __restrict__ bits, uint64_t nwords, const uint32_t* __restrict__ bsum,
+                   uint32_t* __restrict__ pre) {
+    __shared__ uint32_t s_warp[33];
+    const uint64_t w0 = uint64_t(blockIdx.x) * PC_THREADS * PC_WORDS + uint64_t(threadIdx.x) * PC_WORDS;
+    uint32_t w[PC_WORDS], c = 0;
+    for (int k = 0; k < PC_WORDS; ++k) {
+        w[k] = w0 + k < nwords ? bits[w0 + k] : 0u;
+        c += __popc(w[k]);
+    }
+    uint32_t tot = 0;
+    uint32_t run = bsum[blockIdx.x] + cta_exclusive_scan(c, s_warp, &tot);
+    for (int k = 0; k < PC_WORDS; ++k)
+        if (w0 + k < nwords) {
+            pre[w0 + k] = run;
+            run += __popc(w[k]);
+        }
+}
+
+__global__ void __launch_bounds__(256)
+forest_compress_kernel(mt_forest_record* __restrict__ recs, const unsigned long long* __restrict__ count,
+                       const uint32_t* __restrict__ bits, const uint32_t* __restrict__ pre,
+                       const uint32_t* __restrict__ total, uint64_t top_begin) {
+    const uint64_t nrec = *count;
+    const uint64_t gap = 2 * nrec - *total;   // >= 0: at most 2 referenced ids per record
+    auto rank = [&](uint32_t l) -> uint32_t {
+        const uint32_t c = pre[l >> 5] + __popc(bits[l >> 5] & ((1u << (l & 31)) - 1u));
+        return uint32_t(c + (l >= top_begin ? gap : 0));
+    };
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < nrec;
+         i += uint64_t(gridDim.x) * blockDim.x) {
+        mt_forest_record r = recs[i];
+        r.id_c = rank(r.id);
+        r.s_c = rank(r.s);
+        r.v_c = rank(r.v);
+        recs[i] = r;
     }
 }
 
@@ -111,25 +241,51 @@ __device__ __forceinline__ void table_put(unsigned long long* t, uint32_t mask, 
     }
 }
 
+// slab of gathered record i (records concatenated in slab order)
+__device__ __forceinline__ uint32_t slab_of(const ForestXlate& X, uint64_t i) {
+    uint32_t lo = 0, hi = X.nslabs - 1;
+    while (lo < hi) {
+        const uint32_t mid = (lo + hi + 1) >> 1;
+        if (X.rec_off[mid] <= i) lo = mid;
+        else hi = mid - 1;
+    }
+    return lo;
+}
+
 __global__ void __launch_bounds__(256)
-forest_build_kernel(const mt_forest_record* __restrict__ all, uint64_t n_all, unsigned long long* table,
-                    unsigned long long* vtable, uint32_t mask, Cell* cells) {
+forest_build_kernel(const mt_forest_record* __restrict__ all, uint64_t n_all, ForestXlate X,
+                    unsigned long long* table, unsigned long long* vtable, uint32_t mask, Cell* cells,
+                    uint32_t* __restrict__ vid, uint64_t* __restrict__ dec) {
     for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n_all;
          i += uint64_t(gridDim.x) * blockDim.x) {
         const mt_forest_record r = all[i];
-        cells[i] = Cell{r.key_s, r.hi};
-        table_put(table, mask, r.id, uint32_t(i));
+        const uint32_t k = slab_of(X, i);
+        const bool own = k == X.self;
+        // the record in this rank's view: own slab at base + local id, slab k's compressed ids at voff[k]
+        const uint32_t id = X.voff[k] + (own ? r.id : r.id_c);
+        const uint32_t sv = X.voff[k] + (own ? r.s : r.s_c);
+        const uint32_t vv = X.voff[k] + (own ? r.v : r.v_c);
+        const uint32_t ou = ord32(__uint_as_float(r.f_bits)) ^ X.flip;
+        const uint32_t os = ord32(__uint_as_float(r.s_f_bits)) ^ X.flip;
+        cells[i] = Cell{key_of(os, sv), key_of(ou, vv)};
+        vid[i] = id;
+        table_put(table, mask, id, uint32_t(i));
         // the f bits of a record's saddle are needed only where the order key cannot give them
         // back: a zero value (-0 and +0 share one key, reading R2; diagram values are copied from
         // the input, R14) -- every other value is the inverse of the key's order bits
-        if ((r.s_f_bits & 0x7fffffffu) == 0u) table_put(vtable, mask, uint32_t(r.key_s), r.s_f_bits);
+        if ((r.s_f_bits & 0x7fffffffu) == 0u) table_put(vtable, mask, sv, r.s_f_bits);
+        if (X.wide && !own) {                      // 64-bit global ids of the remote view ids
+            dec[X.dec_index(id)] = X.real_base[k] + r.id;
+            dec[X.dec_index(sv)] = X.real_base[k] + r.s;
+        }
     }
 }
 
 struct BoundaryGeom {
     uint32_t nx, ny;
     uint32_t nb;                   // inter-slab boundaries
-    uint32_t zb[MAX_SLABS];        // plane index of the upper side of boundary k
+    uint32_t a0[MAX_SLABS];        // view id of vertex (0, 0) of the lower face of boundary k
+    uint32_t b0[MAX_SLABS];        // ... and of its upper face (faces are consecutive view ids)
 };
 
 // Inter-slab edges reduced to pairs of tile representatives (DESIGN.md derivation C-3, the
@@ -160,7 +316,7 @@ forest_dedupe_kernel(ForestRef F, BoundaryGeom g, FQEntry* __restrict__ q, unsig
         uint64_t pair = ~0ull;
         if (e < total) {
             const uint64_t k = e / sxy, r = e % sxy;
-            const uint32_t a = uint32_t((uint64_t(g.zb[k]) - 1) * sxy + r), b = uint32_t(a + sxy);
+            const uint32_t a = g.a0[k] + uint32_t(r), b = g.b0[k] + uint32_t(r);
             const uint32_t ia = forest_lookup(F, a), ib = forest_lookup(F, b);
             if (ia == FOREST_MISS || ib == FOREST_MISS) {
                 atomicOr(F.err, ERR_FOREST);
@@ -339,13 +495,32 @@ __global__ void __launch_bounds__(256)
 forest_writeback_kernel(ForestRef F, uint64_t n_all, Cell* C, const uint64_t* T0, uint64_t base, uint64_t n) {
     for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n_all;
          i += uint64_t(gridDim.x) * blockDim.x) {
-        const uint32_t id = F.recs[i].id;
+        const uint32_t id = F.vid[i];
         uint32_t rep, o;
         // (a tile-regular face vertex keeps its T0: the repair walks from its R through the forest)
         if (uint64_t(id) - base < n && !tile_regular(T0, id, &rep, &o)) {
             const Cell c = F.cells[i];
             st_cell(C + id, c);
         }
+    }
+}
+
+// ---- view ids -> 64-bit global ids (mt_triplets64 / mt_diagram64) ----
+__global__ void __launch_bounds__(256)
+triplets64_kernel(const uint64_t* __restrict__ T, uint64_t count, IdDecode d, mt_triplet64* __restrict__ out) {
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < count;
+         i += uint64_t(gridDim.x) * blockDim.x) {
+        const uint64_t t = T[i];
+        out[i] = mt_triplet64{d.gid(cell_s(t)), d.gid(cell_v(t))};
+    }
+}
+
+__global__ void __launch_bounds__(256)
+pairs64_kernel(const mt_pair* __restrict__ in, uint64_t count, IdDecode d, mt_pair64* __restrict__ out) {
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < count;
+         i += uint64_t(gridDim.x) * blockDim.x) {
+        const mt_pair p = in[i];
+        out[i] = mt_pair64{d.gid(p.birth_v), d.gid(p.death_v), p.birth, p.death};
     }
 }
 
@@ -358,8 +533,8 @@ uint32_t grid_for(uint64_t work, int num_sms) {
 
 }  // namespace
 
-void launch_forest_mark(const Cell* C, const uint64_t* T0, const Slab& sl, uint8_t* flag, cudaStream_t stream) {
-    const bool has_bottom = sl.z_begin > 0, has_top = sl.z_end < sl.nz;
+void launch_forest_mark(const Cell* C, const uint64_t* T0, const Slab& sl, bool has_bottom, bool has_top,
+                        uint8_t* flag, cudaStream_t stream) {
     if (!has_bottom && !has_top) return;
     const uint64_t sxy = uint64_t(sl.nx) * sl.ny;
     const uint64_t work = sxy * (uint64_t(has_bottom) + uint64_t(has_top));
@@ -368,12 +543,34 @@ void launch_forest_mark(const Cell* C, const uint64_t* T0, const Slab& sl, uint8
                                                                 sl.base, flag);
 }
 
-void launch_forest_compact(const Cell* C, const uint64_t* T0, const float* f, const Slab& sl, uint32_t flip,
-                           const uint8_t* flag, mt_forest_record* recs, uint64_t cap, unsigned long long* count,
-                           int num_sms, cudaStream_t stream) {
+void launch_forest_compact(const Cell* C, const uint64_t* T0, const float* f, const Slab& sl, const uint8_t* flag,
+                           mt_forest_record* recs, uint64_t cap, unsigned long long* count, int num_sms,
+                           cudaStream_t stream) {
     if (sl.n == 0) return;
-    forest_compact_kernel<<<grid_for(sl.n, num_sms), 256, 0, stream>>>(C, T0, f, flip, sl.base, sl.n, flag, recs, cap,
+    forest_compact_kernel<<<grid_for(sl.n, num_sms), 256, 0, stream>>>(C, T0, f, sl.base, sl.n, flag, recs, cap,
                                                                        count);
+}
+
+size_t forest_compress_scratch_bytes(uint64_t n) {
+    const uint64_t words = (n + 31) / 32, blocks = (words + PC_THREADS * PC_WORDS - 1) / (PC_THREADS * PC_WORDS);
+    return size_t(2 * words + blocks + 1) * sizeof(uint32_t) + 512;
+}
+
+int launch_forest_compress(mt_forest_record* recs, const unsigned long long* count, uint64_t n, uint64_t top_begin,
+                           void* scratch, int num_sms, cudaStream_t stream) {
+    if (n == 0) return 0;
+    const uint64_t words = (n + 31) / 32, blocks = (words + PC_THREADS * PC_WORDS - 1) / (PC_THREADS * PC_WORDS);
+    uint32_t* bits = static_cast<uint32_t*>(scratch);
+    uint32_t* pre = bits + words;
+    uint32_t* bsum = pre + words;
+    cudaMemsetAsync(bits, 0, words * sizeof(uint32_t), stream);
+    const uint32_t g = uint32_t(num_sms) * 8;
+    forest_refmark_kernel<<<g, 256, 0, stream>>>(recs, count, bits);
+    popc_block_kernel<<<uint32_t(blocks), PC_THREADS, 0, stream>>>(bits, words, bsum);
+    popc_scan_kernel<<<1, PC_THREADS, 0, stream>>>(bsum, uint32_t(blocks));
+    popc_prefix_kernel<<<uint32_t(blocks), PC_THREADS, 0, stream>>>(bits, words, bsum, pre);
+    forest_compress_kernel<<<g, 256, 0, stream>>>(recs, count, bits, pre, bsum + blocks, top_begin);
+    return 5;
 }
 
 uint64_t forest_table_size(uint64_t n_all) {
@@ -382,24 +579,29 @@ uint64_t forest_table_size(uint64_t n_all) {
     return s > (1ull << 31) ? 0 : s; // table indices and the mask are 32-bit
 }
 
-void launch_forest_build(const mt_forest_record* all, uint64_t n_all, uint64_t* table, uint64_t* vtable,
-                         uint32_t mask, Cell* cells, int num_sms, cudaStream_t stream) {
+void launch_forest_build(const mt_forest_record* all, uint64_t n_all, const ForestXlate& X, uint64_t* table,
+                         uint64_t* vtable, uint32_t mask, Cell* cells, uint32_t* vid, uint64_t* dec, int num_sms,
+                         cudaStream_t stream) {
     if (n_all == 0) return;
     forest_build_kernel<<<grid_for(n_all, num_sms), 256, 0, stream>>>(
-        all, n_all, reinterpret_cast<unsigned long long*>(table), reinterpret_cast<unsigned long long*>(vtable), mask,
-        cells);
+        all, n_all, X, reinterpret_cast<unsigned long long*>(table), reinterpret_cast<unsigned long long*>(vtable),
+        mask, cells, vid, dec);
 }
 
 size_t forest_queue_entry_bytes() { return sizeof(FQEntry); }
 
-void launch_forest_merge(const ForestRef& F, const Slab& sl, const SlabBounds& b, void* queue,
-                         unsigned long long* qlen, unsigned long long* fetch, int num_sms, cudaStream_t stream) {
-    if (b.count < 2) return;
+void launch_forest_merge(const ForestRef& F, const Slab& sl, uint32_t nslabs, const uint32_t* a0, const uint32_t* b0,
+                         void* queue, unsigned long long* qlen, unsigned long long* fetch, int num_sms,
+                         cudaStream_t stream) {
+    if (nslabs < 2) return;
     BoundaryGeom g{};
     g.nx = sl.nx;
     g.ny = sl.ny;
-    g.nb = b.count - 1;
-    for (uint32_t k = 0; k + 1 < b.count; ++k) g.zb[k] = b.z[k + 1];
+    g.nb = nslabs - 1;
+    for (uint32_t k = 0; k + 1 < nslabs; ++k) {
+        g.a0[k] = a0[k];
+        g.b0[k] = b0[k];
+    }
     FQEntry* q = static_cast<FQEntry*>(queue);
     const uint64_t total = uint64_t(g.nx) * g.ny * g.nb;
     uint64_t blocks = (total + FD_THREADS - 1) / FD_THREADS;
@@ -412,6 +614,18 @@ void launch_forest_writeback(const ForestRef& F, uint64_t n_all, Cell* C, const 
                              int num_sms, cudaStream_t stream) {
     if (n_all == 0) return;
     forest_writeback_kernel<<<grid_for(n_all, num_sms), 256, 0, stream>>>(F, n_all, C, T0, sl.base, sl.n);
+}
+
+void launch_triplets64(const uint64_t* T, uint64_t count, const IdDecode& d, mt_triplet64* out, int num_sms,
+                       cudaStream_t stream) {
+    if (count == 0) return;
+    triplets64_kernel<<<grid_for(count, num_sms), 256, 0, stream>>>(T, count, d, out);
+}
+
+void launch_pairs64(const mt_pair* in, uint64_t count, const IdDecode& d, mt_pair64* out, int num_sms,
+                    cudaStream_t stream) {
+    if (count == 0) return;
+    pairs64_kernel<<<grid_for(count, num_sms), 256, 0, stream>>>(in, count, d, out);
 }
 
 }  // namespace mt

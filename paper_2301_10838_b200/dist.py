@@ -10,13 +10,16 @@ Two transports for the one exchange step:
       2. all-gather of the forest records over the process group (``torch.distributed``);
       3. ``mt_compute_global``  -- every rank merges all inter-slab edges on the gathered
          forest, writes back its cells, repairs its slab and extracts its part of the diagram.
-The triplets hold global ids; the finite pairs of rank r are the branches born in its slab
+The triplets hold global ids (32-bit mode) or the context's view ids (wide mode, SURVEY.md 8f row
+f3: global grids past 2^32 vertices, or ``wide=True``), which ``triplets64`` / ``diagram64``
+translate to 64-bit global ids; the finite pairs of rank r are the branches born in its slab
 (ascending), so concatenating the ranks in order gives the single-GPU diagram.
 This module is plumbing (argument marshalling + the collective); all computation runs in
 libmt_b200.so.
 """
 from __future__ import annotations
 
+import numpy as np
 import torch
 
 from . import _lib
@@ -33,8 +36,9 @@ def slab_bounds(nz: int, nranks: int) -> list[int]:
     return _lib.mt_dist_slab_bounds(nz, nranks)
 
 
-def allgather_varsize(t: torch.Tensor, group=None) -> torch.Tensor:
-    """All-gather 1-D uint8 tensors of different lengths; returns the concatenation in rank order."""
+def allgather_varsize(t: torch.Tensor, group=None, sizes_out=None) -> torch.Tensor:
+    """All-gather 1-D uint8 tensors of different lengths; returns the concatenation in rank order
+    (the per-rank lengths are appended to ``sizes_out`` when given)."""
     import torch.distributed as dist
 
     world = dist.get_world_size(group)
@@ -42,6 +46,8 @@ def allgather_varsize(t: torch.Tensor, group=None) -> torch.Tensor:
     sizes = [torch.zeros_like(n) for _ in range(world)]
     dist.all_gather(sizes, n, group=group)
     sizes = [int(s.item()) for s in sizes]
+    if sizes_out is not None:
+        sizes_out.extend(sizes)
     m = max(sizes)
     padded = torch.zeros(m, dtype=t.dtype, device=t.device)
     padded[: t.numel()] = t
@@ -53,7 +59,7 @@ def allgather_varsize(t: torch.Tensor, group=None) -> torch.Tensor:
 class SlabMergeTree:
     """Context for planes [z_begin, z_end) of an nx x ny x nz grid on one device."""
 
-    def __init__(self, dims, z_begin: int, z_end: int, device=None):
+    def __init__(self, dims, z_begin: int, z_end: int, device=None, wide: bool = False, workspace=None):
         self.dims = tuple(int(d) for d in dims)
         self.z_begin, self.z_end = int(z_begin), int(z_end)
         nx, ny, _ = self.dims
@@ -64,9 +70,14 @@ class SlabMergeTree:
         nbytes = _lib.mt_slab_workspace_bytes(self.dims, 6, self.z_begin, self.z_end)
         if nbytes == 0:
             raise _lib.MTError(_lib.MT_ERR_INVALID_ARG, "mt_slab_workspace_bytes")
-        self.workspace = torch.empty(nbytes + 256, dtype=torch.uint8, device=dev)
+        # a caller may share one workspace between contexts used one after another (tests)
+        self.workspace = workspace if workspace is not None else \
+            torch.empty(nbytes + 256, dtype=torch.uint8, device=dev)
+        if self.workspace.numel() < nbytes + 256:
+            raise ValueError("workspace too small")
         ptr = (self.workspace.data_ptr() + 255) // 256 * 256
-        self.ctx = _lib.mt_create_slab(self.dims, 6, self.z_begin, self.z_end, dev.index, ptr, nbytes)
+        self.ctx = _lib.mt_create_slab(self.dims, 6, self.z_begin, self.z_end, dev.index, ptr, nbytes,
+                                       _lib.MT_SLAB_WIDE_IDS if wide else 0)
         self._scratch = None
         self._f = None
         self._T = None
@@ -98,17 +109,41 @@ class SlabMergeTree:
         off = ptr - self.workspace.data_ptr()
         return self.workspace[off: off + n * RECORD_BYTES]
 
-    def compute_global(self, all_records: torch.Tensor, z_bounds, stream=None) -> torch.Tensor:
-        """Global phase into the triplet buffer of compute_local (returned)."""
+    def compute_global(self, all_records: torch.Tensor, z_bounds, counts, stream=None) -> torch.Tensor:
+        """Global phase into the triplet buffer of compute_local (returned); ``all_records``: every
+        slab's records in slab order, ``counts`` of them per slab."""
         n_all = all_records.numel() // RECORD_BYTES
+        if sum(counts) != n_all:
+            raise ValueError("counts do not add up to the gathered records")
         need = _lib.mt_forest_scratch_bytes(n_all)
         if self._scratch is None or self._scratch.numel() < need + 256:
             self._scratch = torch.empty(need + 256, dtype=torch.uint8, device=self.device)
         sp = (self._scratch.data_ptr() + 255) // 256 * 256
         triplets = self._T
-        _lib.mt_compute_global(self.ctx, all_records.data_ptr() if n_all else 0, n_all, z_bounds, sp, need,
+        _lib.mt_compute_global(self.ctx, all_records.data_ptr() if n_all else 0, counts, z_bounds, sp, need,
                                triplets.data_ptr(), stream)
         return triplets
+
+    def triplets64(self, triplets: torch.Tensor, first: int = 0, count: int | None = None, stream=None):
+        """(count, 2) int64 tensor (s, v) of 64-bit global ids of triplets[first:first+count]."""
+        if count is None:
+            count = self.n - first
+        out = torch.empty((count, 2), dtype=torch.int64, device=self.device)
+        _lib.mt_triplets64(self.ctx, triplets.data_ptr(), first, count, out.data_ptr(), stream)
+        return out
+
+    def diagram64(self, stream=None):
+        """Synchronises; (records as a PAIR64_DTYPE numpy array, n_pairs, n_essential)."""
+        st, npairs, ness = _lib.mt_diagram64(self.ctx, 0, 0, stream)
+        if st != _lib.MT_OK:
+            raise _lib.MTError(st, "mt_diagram64")
+        k = npairs + ness
+        out = torch.empty(k * 24, dtype=torch.uint8, device=self.device)
+        if k:
+            st, _, _ = _lib.mt_diagram64(self.ctx, out.data_ptr(), k, stream)
+            if st != _lib.MT_OK:
+                raise _lib.MTError(st, "mt_diagram64")
+        return out.cpu().numpy().view(_lib.PAIR64_DTYPE), npairs, ness
 
     def diagram(self, stream=None):
         """Synchronises; (records (k,4) int32, n_pairs, n_essential) of this slab."""
@@ -127,7 +162,7 @@ class SlabMergeTree:
 class NcclSlab:
     """A ``mt_create_dist`` context: the rank's slab with the NCCL exchange inside the library."""
 
-    def __init__(self, dims, rank: int, nranks: int, nccl_id: bytes, device=None):
+    def __init__(self, dims, rank: int, nranks: int, nccl_id: bytes, device=None, wide: bool = False):
         self.dims = tuple(int(d) for d in dims)
         self.z_bounds = slab_bounds(self.dims[2], nranks)
         self.z_begin, self.z_end = self.z_bounds[rank], self.z_bounds[rank + 1]
@@ -141,7 +176,8 @@ class NcclSlab:
             raise _lib.MTError(_lib.MT_ERR_INVALID_ARG, "mt_dist_workspace_bytes")
         self.workspace = torch.empty(nbytes + 256, dtype=torch.uint8, device=dev)
         ptr = (self.workspace.data_ptr() + 255) // 256 * 256
-        self.ctx = _lib.mt_create_dist(self.dims, 6, rank, nranks, nccl_id, dev.index, ptr, nbytes)
+        self.ctx = _lib.mt_create_dist(self.dims, 6, rank, nranks, nccl_id, dev.index, ptr, nbytes,
+                                       _lib.MT_SLAB_WIDE_IDS if wide else 0)
         self._f = None
 
     def __del__(self):
@@ -162,6 +198,8 @@ class NcclSlab:
         return triplets
 
     diagram = SlabMergeTree.diagram
+    diagram64 = SlabMergeTree.diagram64
+    triplets64 = SlabMergeTree.triplets64
 
 
 def broadcast_unique_id(group=None) -> bytes:
@@ -201,26 +239,37 @@ class DistMergeTree:
             return self.slab.compute(f_slab, split, triplets)
         self.slab.compute_local(f_slab, split, triplets)
         mine = self.slab.forest()
-        everything = allgather_varsize(mine, self.group)
+        sizes = []
+        everything = allgather_varsize(mine, self.group, sizes)
         self.forest_records = everything.numel() // RECORD_BYTES
-        return self.slab.compute_global(everything, self.z_bounds)
+        return self.slab.compute_global(everything, self.z_bounds, [b // RECORD_BYTES for b in sizes])
 
     def diagram(self):
         return self.slab.diagram()
 
 
-def virtual_compute(f: torch.Tensor, dims, nranks: int, split: bool = False):
+def virtual_compute(f: torch.Tensor, dims, nranks: int, split: bool = False, wide: bool = False):
     """All slabs on ONE device, the all-gather replaced by a concatenation: the device code of
     the multi-GPU path exercised without several GPUs (tests).  Returns (T, diagram records,
-    n_pairs, n_essential) assembled in the single-GPU order."""
+    n_pairs, n_essential, gathered records) assembled in the single-GPU order; wide mode: T as
+    (n, 2) int64 global (s, v) and the records as a PAIR64_DTYPE array."""
     nx, ny, nz = dims
     zb = slab_bounds(nz, nranks)
-    slabs = [SlabMergeTree(dims, zb[r], zb[r + 1], f.device) for r in range(nranks)]
+    slabs = [SlabMergeTree(dims, zb[r], zb[r + 1], f.device, wide=wide) for r in range(nranks)]
     plane = nx * ny
     for r, s in enumerate(slabs):
         s.compute_local(f[zb[r] * plane: zb[r + 1] * plane].contiguous(), split)
-    everything = torch.cat([s.forest() for s in slabs])
-    Ts = [s.compute_global(everything, zb) for s in slabs]
+    forests = [s.forest() for s in slabs]
+    counts = [x.numel() // RECORD_BYTES for x in forests]
+    everything = torch.cat(forests)
+    Ts = [s.compute_global(everything, zb, counts) for s in slabs]
+    if wide:
+        T64 = torch.cat([s.triplets64(T) for s, T in zip(slabs, Ts)])
+        diags = [s.diagram64() for s in slabs]
+        fin = np.concatenate([d[0][: d[1]] for d in diags])
+        ess = np.concatenate([d[0][d[1]:] for d in diags])
+        return (T64, np.concatenate([fin, ess]), sum(d[1] for d in diags), sum(d[2] for d in diags),
+                everything.numel() // RECORD_BYTES)
     diags = [s.diagram() for s in slabs]
     fin = torch.cat([d[0][: d[1]] for d in diags])
     ess = torch.cat([d[0][d[1]:] for d in diags])

@@ -21,10 +21,12 @@ for r, s in enumerate(slabs):
     s.compute_local(fd[zb[r] * nx * ny: zb[r + 1] * nx * ny].contiguous())
     torch.cuda.synchronize()
     print("local", r, "forest", s.forest().numel() // 32, flush=True)
-allr = torch.cat([s.forest() for s in slabs])
+recs = [s.forest() for s in slabs]
+counts = [x.numel() // 32 for x in recs]
+allr = torch.cat(recs)
 for r, s in enumerate(slabs):
     t = time.time()
-    s.compute_global(allr, zb)
+    s.compute_global(allr, zb, counts)
     torch.cuda.synchronize()
     st = _lib.mt_last_error(s.ctx)
     print("global", r, "status", st, round(time.time() - t, 3), flush=True)

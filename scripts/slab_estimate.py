@@ -37,8 +37,9 @@ for P in Ps:
     for rep in range(3):   # per rank, the best of the last two passes
         loc = [timed(lambda r=r: slabs[r].compute_local(parts[r])) for r in range(P)]
         recs = [s.forest() for s in slabs]
+        counts = [x.numel() // 32 for x in recs]
         allr = torch.cat(recs)
-        glob = [timed(lambda r=r: slabs[r].compute_global(allr, zb)) for r in range(P)]
+        glob = [timed(lambda r=r: slabs[r].compute_global(allr, zb, counts)) for r in range(P)]
         if rep:
             best_loc = [min(a, b) for a, b in zip(best_loc, loc)]
             best_glob = [min(a, b) for a, b in zip(best_glob, glob)]
@@ -47,7 +48,7 @@ for P in Ps:
     from paper_2301_10838_b200 import _lib
     _lib.mt_set_profiling(slabs[-1].ctx, True)
     slabs[-1].compute_local(parts[-1])
-    slabs[-1].compute_global(allr, zb)
+    slabs[-1].compute_global(allr, zb, counts)
     torch.cuda.synchronize()
     split = _lib.mt_kernel_times(slabs[-1].ctx)
     _lib.mt_set_profiling(slabs[-1].ctx, False)

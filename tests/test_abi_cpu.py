@@ -14,7 +14,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 def header_functions():
     src = open(os.path.join(ROOT, "include", "mt.h")).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    return sorted(set(re.findall(r"\b(mt_[a-z_]+)\s*\(", src)))
+    return sorted(set(re.findall(r"\b(mt_[a-z0-9_]+)\s*\(", src)))
 
 
 @pytest.fixture(scope="module")
@@ -32,7 +32,7 @@ def test_exports_every_declared_symbol(lib):
 
 
 def test_abi_version_and_status_strings(lib):
-    assert lib.mt_abi_version() == 2
+    assert lib.mt_abi_version() == 3
     for st in range(9):
         assert lib.mt_status_string(st)
     assert b"non-finite" in lib.mt_status_string(3)
@@ -77,9 +77,35 @@ def test_dist_host_entry_points_without_gpu(lib):
     h = ctypes.c_void_p()
     dims = (ctypes.c_uint32 * 3)(64, 64, 64)
     idbuf = (ctypes.c_uint8 * 128)(*uid)
-    assert lib.mt_create_dist(ctypes.byref(h), dims, 6, 3, 2, idbuf, 0, None, 0) == _lib.MT_ERR_INVALID_ARG
-    assert lib.mt_create_dist(ctypes.byref(h), dims, 6, 0, 65, idbuf, 0, None, 0) == _lib.MT_ERR_INVALID_ARG
-    assert lib.mt_create_dist(ctypes.byref(h), dims, 6, 0, 2, None, 0, None, 0) == _lib.MT_ERR_INVALID_ARG
+    assert lib.mt_create_dist(ctypes.byref(h), dims, 6, 3, 2, idbuf, 0, 0, None, 0) == _lib.MT_ERR_INVALID_ARG
+    assert lib.mt_create_dist(ctypes.byref(h), dims, 6, 0, 65, idbuf, 0, 0, None, 0) == _lib.MT_ERR_INVALID_ARG
+    assert lib.mt_create_dist(ctypes.byref(h), dims, 6, 0, 2, None, 0, 0, None, 0) == _lib.MT_ERR_INVALID_ARG
+
+
+def test_wide_id_host_logic_without_gpu(lib):
+    """a slab of a grid past 2^32 vertices is sized (its own ids fit the 32-bit
+    view with room below and above); a slab too thick for the view is refused; the 64-bit entry
+    points and the slab options validate their arguments before touching the device."""
+    big = (2048, 2048, 1032)                                  # 4.33e9 vertices
+    assert big[0] * big[1] * big[2] > 2 ** 32
+    assert _lib.mt_workspace_bytes(big, 6) == 0               # one GPU: 32-bit ids
+    assert _lib.mt_slab_workspace_bytes(big, 6, 0, 129) > 0   # a slab of 5.4e8 vertices
+    assert _lib.mt_slab_workspace_bytes(big, 6, 0, 1023) == 0  # 1023 planes + 2 do not fit 2^32 - 1
+    assert _lib.mt_dist_workspace_bytes(big, 6, 3, 8) > 0
+    assert _lib.mt_dist_workspace_bytes(big, 6, 0, 1) == 0
+    h = ctypes.c_void_p()
+    dims = (ctypes.c_uint32 * 3)(*big)
+    assert lib.mt_create_slab(ctypes.byref(h), dims, 6, 0, 129, 2, 0, None, 0) == _lib.MT_ERR_INVALID_ARG  # options
+    assert lib.mt_create_slab(ctypes.byref(h), dims, 6, 0, 129, 0, 0, None, 0) == _lib.MT_ERR_WORKSPACE
+    huge = (ctypes.c_uint32 * 3)(0xffffffff, 0xffffffff, 0xffffffff)    # ids past 2^63
+    assert lib.mt_create_slab(ctypes.byref(h), huge, 6, 0, 1, 0, 0, None, 0) == _lib.MT_ERR_TOO_LARGE
+    assert lib.mt_triplets64(None, None, 0, 0, None, None) == _lib.MT_ERR_INVALID_ARG
+    a, b = ctypes.c_uint64(), ctypes.c_uint64()
+    assert lib.mt_diagram64(None, None, 0, ctypes.byref(a), ctypes.byref(b), None) == _lib.MT_ERR_INVALID_ARG
+    zb = (ctypes.c_uint32 * 3)(0, 8, 16)
+    cnt = (ctypes.c_uint64 * 2)(0, 0)
+    assert lib.mt_compute_global(None, None, cnt, zb, 2, None, 0, None, None) == _lib.MT_ERR_INVALID_ARG
+    assert _lib.PAIR64_DTYPE.itemsize == 24 and _lib.TRIPLET64_DTYPE.itemsize == 16
 
 
 def test_host_pipeline_and_dual_entry_points_validate_without_gpu(lib):

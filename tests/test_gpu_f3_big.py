@@ -1,0 +1,151 @@
+"""a grid past 2^32 vertices (the paper packs two 32-bit ids into one 64-bit
+CAS word and names that limit as the obstacle to distribution).
+
+2048 x 2048 x 1032 white noise (4.33e9 vertices; plane 1024 starts at id 2^32) in 8 z-slabs
+(wide mode: every slab works in its own 32-bit view, the 64-bit translation at the end).  The
+ranks run one after another on one GPU, sharing one workspace: pass 1 computes every slab's
+boundary forest, pass 2 recomputes each slab's local phase (the same store: it is unique) and runs
+its global phase on the gathered forests.  O1 cannot run at this size in a test, so
+  (1) invariants that hold at any size, per slab on the 64-bit triplets with plain torch ops:
+      I1 key order of v and s, I2 s = u iff a lower neighbour exists, I3 one root in the grid,
+      I4 #pairs = #strict minima - 1; each slab's diagram equals its branch triplets (births,
+      deaths) and carries the input's bits at both ids;
+  (2) exact triplets of stratified samples against O4 with 64-bit ids (the definition by bounded
+      floods, oracle.triplet_at; pinned past 2^32 in tests/test_oracle_pins.py), every sample
+      checked: ids >= 2^32, branches, and triplets whose s or v lies in another slab.
+~120 GB of device memory and 18 GB of host memory: opt-in with MT_F3_BIG=1 (its own gpurun call)."""
+import os
+import resource
+import time
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+import oracle  # noqa: E402
+from paper_2301_10838_b200 import _lib, fields  # noqa: E402
+from paper_2301_10838_b200.dist import RECORD_BYTES, SlabMergeTree, slab_bounds  # noqa: E402
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+T0 = time.time()
+
+
+def _log(msg):
+    print(f"[f3 {time.time() - T0:6.1f}s] {msg} (maxrss {resource.getrusage(resource.RUSAGE_SELF).ru_maxrss >> 20} GB, "
+          f"device {torch.cuda.memory_allocated() / 2 ** 30:.1f} GiB)", flush=True)
+
+
+@pytest.mark.skipif(os.environ.get("MT_F3_BIG") != "1", reason="4.33e9-vertex grid: set MT_F3_BIG=1")
+def test_ids_past_2_32_in_slabs():
+    dims = (2048, 2048, 1032)
+    nx, ny, nz = dims
+    sxy, n = nx * ny, nx * ny * nz
+    assert n > 2 ** 32
+    P = 8
+    zb = slab_bounds(nz, P)
+    f = fields.white_noise(dims, 5)
+    _log(f"field {dims}, n = {n}, slabs {zb}")
+    fd = torch.from_numpy(f).cuda()
+    nbytes = max(_lib.mt_slab_workspace_bytes(dims, 6, zb[r], zb[r + 1]) for r in range(P))
+    ws = torch.empty(nbytes + 256, dtype=torch.uint8, device="cuda")
+    fsl = [fd[zb[r] * sxy: zb[r + 1] * sxy] for r in range(P)]
+    forests = []
+    for r in range(P):   # pass 1: the boundary forests
+        s = SlabMergeTree(dims, zb[r], zb[r + 1], workspace=ws)
+        s.compute_local(fsl[r])
+        forests.append(s.forest().clone())
+        del s
+    counts = [x.numel() // RECORD_BYTES for x in forests]
+    everything = torch.cat(forests)
+    del forests
+    _log(f"forests: {counts} records")
+    rng = np.random.default_rng(32)
+    q20 = float(np.quantile(f[rng.integers(0, n, 1 << 22)], 0.2))
+    tot = dict(root=0, fin=0, ess=0, minima=0, remote_v=0, remote_s=0, hi_ref=0)
+    samples = []   # (u, s, v, kind)
+    g = fd.view(nz, ny, nx)
+    for r in range(P):   # pass 2: local phase again, global phase, 64-bit results, checks
+        z0, z1 = zb[r], zb[r + 1]
+        s = SlabMergeTree(dims, z0, z1, workspace=ws)
+        s.compute_local(fsl[r])
+        s.compute_global(everything, zb, counts)
+        T64 = s.triplets64(s._T)
+        rec, npairs, ness = s.diagram64()
+        del s
+        gid0, nr = z0 * sxy, (z1 - z0) * sxy
+        ids = torch.arange(gid0, gid0 + nr, device="cuda", dtype=torch.int64)
+        sv, vv = T64[:, 0], T64[:, 1]
+        del T64
+        fu = fsl[r]
+        # I2 on the slab's planes, neighbours from the whole field (across the slab faces too)
+        lo, hi = max(z0 - 1, 0), min(z1 + 1, nz)
+        gg = g[lo:hi]
+        hl = torch.zeros_like(gg, dtype=torch.bool)
+        hl[:, :, 1:] |= gg[:, :, :-1] <= gg[:, :, 1:]
+        hl[:, :, :-1] |= gg[:, :, 1:] < gg[:, :, :-1]
+        hl[:, 1:, :] |= gg[:, :-1, :] <= gg[:, 1:, :]
+        hl[:, :-1, :] |= gg[:, 1:, :] < gg[:, :-1, :]
+        hl[1:] |= gg[:-1] <= gg[1:]
+        hl[:-1] |= gg[1:] < gg[:-1]
+        has_lower = hl[z0 - lo: z0 - lo + (z1 - z0)].reshape(-1)
+        del hl, gg
+        is_reg = sv == ids
+        root = is_reg & (vv == ids)
+        n_min = int((~has_lower).sum())
+        bad_i2 = int(((is_reg != has_lower) & ~root).sum())
+        del has_lower
+        fv = fd[vv]
+        bad_v = int((~(root | (fv < fu) | ((fv == fu) & (vv < ids)))).sum())
+        del fv
+        fs = fd[sv]
+        bad_s = int((~(root | (fs > fu) | ((fs == fu) & (sv >= ids)))).sum())
+        del fs
+        assert bad_i2 == 0 and bad_v == 0 and bad_s == 0, (r, bad_i2, bad_v, bad_s)
+        remote_v = (vv < gid0) | (vv >= gid0 + nr)
+        remote_s = (sv < gid0) | (sv >= gid0 + nr)
+        tot["root"] += int(root.sum())
+        tot["fin"] += npairs
+        tot["ess"] += ness
+        tot["minima"] += n_min
+        tot["remote_v"] += int(remote_v.sum())
+        tot["remote_s"] += int(remote_s.sum())
+        tot["hi_ref"] += int(((vv >= 2 ** 32) | (sv >= 2 ** 32)).sum())
+        # the slab's diagram = its branch triplets, ascending, with the input's bits at both ids
+        br = torch.nonzero(~is_reg).view(-1)
+        recd = torch.from_numpy(rec.view(np.uint8).copy()).cuda()
+        r64 = recd.view(torch.int64).view(-1, 3)
+        assert npairs == br.numel() and torch.equal(r64[:npairs, 0], ids[br]) and torch.equal(r64[:npairs, 1], sv[br])
+        bits = recd.view(torch.int32).view(-1, 6)
+        fbits = fd.view(torch.int32)
+        assert torch.equal(bits[:npairs, 4], fbits[r64[:npairs, 0]]) and torch.equal(bits[:npairs, 5],
+                                                                                       fbits[r64[:npairs, 1]])
+        del br, recd, r64, bits
+        # stratified samples at low levels: regular, branch, remote s or v (ids past 2^32 in the top slabs)
+        low = fu <= q20
+        for kind, mask in (("regular", is_reg & ~root & low), ("branch", ~is_reg & (fd[sv] <= q20)),
+                           ("remote", (remote_v | remote_s) & low)):
+            cand = torch.nonzero(mask).view(-1)
+            if cand.numel() == 0:
+                continue
+            pick = cand[torch.from_numpy(rng.integers(0, cand.numel(), 8)).cuda()]
+            for i, a, b in zip(pick.tolist(), sv[pick].tolist(), vv[pick].tolist()):
+                samples.append((gid0 + i, a, b, kind))
+        _log(f"slab {r} [{z0}, {z1}): ok; {npairs} pairs, {ness} essential, remote v {int(remote_v.sum())}, "
+             f"remote s {int(remote_s.sum())}")
+        del ids, sv, vv, is_reg, root, remote_v, remote_s, low, mask, cand
+        torch.cuda.empty_cache()
+    _log(f"totals {tot}")
+    assert tot["root"] == 1 and tot["ess"] == 1 and tot["fin"] == tot["minima"] - 1
+    assert tot["remote_v"] > 0 and tot["remote_s"] > 0 and tot["hi_ref"] > 0
+    del fd, ws, fsl, everything, g
+    torch.cuda.empty_cache()
+    kinds = {}
+    for u, a, b, kind in samples:
+        o = oracle.triplet_at(f, dims, 6, u, cap=1 << 23)
+        assert o is not None, f"O4 flood of u={u} passed 2^23 vertices"
+        assert o == (a, b), (kind, u, o, (a, b))
+        kinds[kind] = kinds.get(kind, 0) + 1
+    n_hi = sum(1 for u, *_ in samples if u >= 2 ** 32)
+    _log(f"all {len(samples)} samples equal O4: {kinds}, {n_hi} with ids >= 2^32")
+    assert kinds.get("remote", 0) >= 16 and n_hi >= 8
