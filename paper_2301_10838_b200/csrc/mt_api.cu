@@ -683,8 +683,10 @@ mt_status mt_compute_local(mt_ctx* c, const float* f, uint64_t* T, uint32_t flag
     if (c->wide) {   // the flags are dead after the compaction: their space holds the bitmap
         mark(c, "forest_compress", s);
         const uint64_t sxy = uint64_t(c->nx) * c->ny;
-        c->launches += mt::launch_forest_compress(recs, fcount, c->n, has_top ? c->n - sxy : ~0ull, flag,
-                                                  c->num_sms, s);
+        // the top face moves to the end of the compressed range (a one-plane slab's only plane is
+        // its bottom face too and keeps compressed ids 0 .. nx ny - 1)
+        c->launches += mt::launch_forest_compress(recs, fcount, c->n, has_top && c->n > sxy ? c->n - sxy : ~0ull,
+                                                  flag, c->num_sms, s);
     }
     mark(c, "exchange", s);  // closes at mt_compute_global's first mark: host sync + all-gather
     c->local_done = true;
@@ -768,7 +770,8 @@ mt_status mt_compute_global(mt_ctx* c, const mt_forest_record* all, const uint64
     }
     uint32_t a0[mt::MAX_SLABS], b0[mt::MAX_SLABS];
     for (uint32_t k = 0; k + 1 < nslabs; ++k) {   // the faces of boundary k in the view
-        a0[k] = uint32_t(X.voff[k] + span[k] - sxy);
+        const bool one_plane = z_bounds[k + 1] - z_bounds[k] == 1;   // its top face is its bottom face
+        a0[k] = uint32_t(one_plane ? X.voff[k] : X.voff[k] + span[k] - sxy);
         b0[k] = X.voff[k + 1];
     }
     DeviceGuard g(c->device);

@@ -121,7 +121,8 @@ forest_compact_kernel(const Cell* C, const uint64_t* T0, const float* f, uint64_
 // referenced = the records' vertices and their saddles (every v is a record's vertex: the forest
 // is closed under v).  c(l) = #referenced ids below l, plus a gap before the top face so that the
 // top face of a slab with count records sits at [2 count - nx ny, 2 count) -- the receivers know
-// where a face is without the slab's exact number of referenced ids (2 count bounds it).
+// where a face is without the slab's exact number of referenced ids (2 count bounds it); the
+// bottom face, the lowest referenced ids, is [0, nx ny) (a one-plane slab: both faces).
 __global__ void __launch_bounds__(256)
 forest_refmark_kernel(const mt_forest_record* __restrict__ recs, const unsigned long long* __restrict__ count,
                       uint32_t* __restrict__ bits) {

@@ -191,6 +191,13 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, i
         : "memory");
 }
 
+// L2 prefetch of a tile box (no shared memory, no barrier): the tile a later CTA will load
+__device__ __forceinline__ void tma_prefetch_3d(const CUtensorMap* map, int x, int y, int z) {
+    asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(map), "r"(x), "r"(y),
+                 "r"(z)
+                 : "memory");
+}
+
 // Output pointers of one tree.  DUAL launches compute two trees from one read of f: the merge
 // (join) tree into the first set and the split tree (complemented order keys, reading R16) into
 // the second.
@@ -208,7 +215,7 @@ tile_tmt_kernel(const __grid_constant__ CUtensorMap fmap, const float* __restric
                 uint32_t ntiles, uint32_t nx,
                 uint32_t ny, uint32_t z_begin,
                 uint32_t z_end, uint32_t tiles_x, uint32_t tiles_y, uint32_t flip,
-                unsigned long long* __restrict__ stats) {
+                unsigned long long* __restrict__ stats, uint32_t pf_dist) {
     constexpr int ROWS = TY * TZ;               // 128 rows of 32
     static_assert(TX * ROWS == NV, "tile size");
     constexpr int RSTEP = THREADS / TX;         // 16 rows per pass
@@ -290,6 +297,13 @@ tile_tmt_kernel(const __grid_constant__ CUtensorMap fmap, const float* __restric
             asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
             mbar_expect_tx(&s_fbar, uint32_t(NV) * 4u);
             tma_load_3d(ord, &fmap, int(x0), int(y0), int(z0 - z_begin), &s_fbar);
+            // the tile the CTA pf_dist launches later will load (about one wave of resident CTAs
+            // later): into L2 now, so its load meets L2 latency instead of HBM's
+            if (pf_dist && b + pf_dist < ntiles) {
+                uint32_t px, py, pz;
+                tile_origin(b + pf_dist, &px, &py, &pz);
+                tma_prefetch_3d(&fmap, int(px), int(py), int(pz - z_begin));
+            }
         }
     } else {
 #pragma unroll
@@ -1048,6 +1062,10 @@ bool make_fmap(CUtensorMap* m, const float* f_local, const Slab& sl) {
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+#ifndef TILE_L2PF
+#define TILE_L2PF 1    // TMA tiles: L2-prefetch the tile TILE_L2PF waves of resident CTAs ahead (0: off)
+#endif
+
 #ifndef TILE_PERSIST
 #define TILE_PERSIST 0 // TMA tiles: persistent CTAs, the next tile's f prefetched during the merge
 #endif
@@ -1060,17 +1078,18 @@ void launch_tile_v(const CUtensorMap& m, const float* f, const TileOut& o0, cons
     constexpr bool PERSIST = TMA && TILE_PERSIST && !TILE_KRUSKAL;
     auto kern = tile_tmt_kernel<TY, TZ, STATS, DUAL, TMA, PERSIST>;
     ensure_smem_attr(reinterpret_cast<const void*>(kern), int(smem_bytes<NV>()));
-    uint32_t blocks = grid;
-    if (PERSIST) {   // one CTA per resident slot
+    uint32_t blocks = grid, pf = 0;
+    if (PERSIST || (TMA && TILE_L2PF)) {
         int dev = 0, sms = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         const uint64_t slots = uint64_t(sms) *
                                occupancy_per_sm(reinterpret_cast<const void*>(kern), NV / TILE_VPT, smem_bytes<NV>());
-        if (slots < blocks) blocks = uint32_t(slots);
+        if (PERSIST && slots < blocks) blocks = uint32_t(slots);   // one CTA per resident slot
+        if (!PERSIST) pf = uint32_t(slots * TILE_L2PF);
     }
     kern<<<blocks, NV / TILE_VPT, smem_bytes<NV>(), stream>>>(m, f, o0, o1, grid, sl.nx, sl.ny, sl.z_begin, sl.z_end,
-                                                              tx, tyn, flip, stats);
+                                                              tx, tyn, flip, stats, pf);
 }
 
 template <int TY, int TZ, bool TMA>
