@@ -312,10 +312,13 @@ dedupe_cross_kernel(const float* __restrict__ f, const uint64_t* __restrict__ T0
 #define MQ_BOTHCLIMB 1    // Alg. 3 step: climb u and v in the same round trip when both can climb
 #endif
 #ifndef MQ_WALK
-#define MQ_WALK 1         // filter walks (with path splitting) before Alg. 3
+#define MQ_WALK 0         // filter walks (with path splitting) before Alg. 3 (measured slower than MQ_CSPLIT)
+#endif
+#ifndef MQ_CSPLIT
+#define MQ_CSPLIT 1       // path splitting inside the Alg. 3 climbs (with MQ_WALK 0)
 #endif
 #ifndef MQ_MIN_BLOCKS
-#define MQ_MIN_BLOCKS 6   // 6 x 256 threads per SM: <= 42 registers, 48 warps of loads in flight
+#define MQ_MIN_BLOCKS 4   // 4 x 256 threads per SM: <= 64 registers (the climbs keep their previous cells), 32 warps of loads in flight
 #endif
 
 enum Phase : int { IDLE = 0, CLIMB_HI = 2, CLIMB_LO = 3, MERGE_LD = 4, MERGE_CAS = 5, DONE = 6 };
@@ -343,6 +346,10 @@ merge_queue_kernel(Cell* C, const QEntry* __restrict__ q, uint64_t cap, const un
     uint32_t p0 = 0, p1 = 0, p2 = 0, p3 = 0;
     bool has_prev = false;
     Cell held{0, 0};
+    // MQ_CSPLIT: the previous cell of each Alg. 3 climb (path splitting)
+    [[maybe_unused]] Cell hu{0, 0}, hv{0, 0};
+    [[maybe_unused]] uint32_t xu = 0, xv = 0;
+    [[maybe_unused]] bool has_u = false, has_v = false;
     unsigned long long n_edges = 0, n_hops = 0, n_iters = 0, n_fail = 0, n_skip = 0;
 
     while (true) {
@@ -369,6 +376,7 @@ merge_queue_kernel(Cell* C, const QEntry* __restrict__ q, uint64_t cap, const un
                     if (!MQ_WALK) {                   // Merge(T, R_hi, hi, R_lo) straight away
                         p1 = en.m_lo;
                         phase = MERGE_LD;
+                        has_u = has_v = false;
                     }
                     if (STATS) n_edges++;
                 } else if (exhausted) {
@@ -413,7 +421,28 @@ merge_queue_kernel(Cell* C, const QEntry* __restrict__ q, uint64_t cap, const un
             if (STATS) n_iters++;
             const bool up_u = cv_of(cu) != p0 && cu.lo < lev;   // l.2-4 (+ R4)
             const bool up_v = cv_of(cv) != p1 && cv.lo < lev;   // l.5-8 (+ R4)
-            if (MQ_BOTHCLIMB && (up_u || up_v)) {               // independent climbs: both advance
+            if (MQ_CSPLIT && (up_u || up_v)) {
+                // both climbs advance, each splitting its path: the cell climbed from before
+                // (x -> y) is re-pointed past y when y's saddle is not above x's (x then joins
+                // v(y) at its own level; any value a cell holds stays a valid triplet), so the
+                // repair later walks shorter chains
+                if (up_u) {
+                    if (has_u && cu.lo <= hu.lo)
+                        cas_cell(C + xu, hu, Cell{hu.lo, (hu.hi & 0xffffffff00000000ull) | cv_of(cu)});
+                    xu = p0;
+                    hu = cu;
+                    has_u = true;
+                    p0 = cv_of(cu);
+                }
+                if (up_v) {
+                    if (has_v && cv.lo <= hv.lo)
+                        cas_cell(C + xv, hv, Cell{hv.lo, (hv.hi & 0xffffffff00000000ull) | cv_of(cv)});
+                    xv = p1;
+                    hv = cv;
+                    has_v = true;
+                    p1 = cv_of(cv);
+                }
+            } else if (MQ_BOTHCLIMB && (up_u || up_v)) {        // independent climbs: both advance
                 if (up_u) p0 = cv_of(cu);
                 if (up_v) p1 = cv_of(cv);
             } else if (up_u) {                         // climb u, restart
@@ -429,6 +458,7 @@ merge_queue_kernel(Cell* C, const QEntry* __restrict__ q, uint64_t cap, const un
                 }
                 held = cv;                             // l.14: (s, u) into T[v], next round trip
                 phase = MERGE_CAS;
+                has_u = has_v = false;                 // (the climbs start afresh after the CAS)
             }
         } else if (phase == MERGE_CAS) {
             const Cell got = cas_cell(C + p1, held, Cell{lev, (held.hi & 0xffffffff00000000ull) | p0});

@@ -282,8 +282,16 @@ tile_tmt_kernel(const __grid_constant__ CUtensorMap fmap, const float* __restric
     if (PERSIST && threadIdx.x == 0) s_next = ntiles;
 #pragma unroll 1
     for (uint32_t b = blockIdx.x; b < (PERSIST ? ntiles : blockIdx.x + 1); ++it) {
-    uint32_t x0, y0, z0;
-    tile_origin(b, &x0, &y0, &z0);
+    uint32_t x0 = 0, y0 = 0, z0 = 0;
+    // (TMA tiles: thread 0 alone divides -- it issues the copy -- and the others read the origin
+    // after the barrier that publishes the mbarrier's init)
+    __shared__ uint32_t s_org[3];
+    if (!(TMA && !PERSIST) || threadIdx.x == 0) tile_origin(b, &x0, &y0, &z0);
+    if (TMA && !PERSIST && threadIdx.x == 0) {
+        s_org[0] = x0;
+        s_org[1] = y0;
+        s_org[2] = z0;
+    }
     // f and C are indexed by GLOBAL vertex id (the caller passes pointers shifted by the
     // slab's first id); this tile starts at global plane z0
 
@@ -333,7 +341,12 @@ tile_tmt_kernel(const __grid_constant__ CUtensorMap fmap, const float* __restric
         s_nkept = 0;
     }
     if (TMA) {
-        if (!PERSIST) __syncthreads();   // (the barrier's init is visible to every waiting thread)
+        if (!PERSIST) {
+            __syncthreads();             // (the barrier's init is visible to every waiting thread)
+            x0 = s_org[0];
+            y0 = s_org[1];
+            z0 = s_org[2];
+        }
         mbar_wait(&s_fbar, PERSIST ? (it & 1u) : 0u);
         const float* fv = PERSIST ? fpre : reinterpret_cast<const float*>(ord);
 #pragma unroll
