@@ -39,6 +39,12 @@ namespace {
 #ifndef MT_REPAIR_SEQ
 #define MT_REPAIR_SEQ 1     // walks one after the other (else lock-step rounds over the thread's vertices)
 #endif
+#ifndef MT_REPAIR_ZPAIR
+#define MT_REPAIR_ZPAIR 1   // volumes: launch the bricks of one tile depth back to back (c5 repair 10.15 -> 9.99 ms)
+#endif
+#ifndef MT_REPAIR_CHAIN
+#define MT_REPAIR_CHAIN 0   // a thread's walks in threshold order, chained from a shared start
+#endif
 #ifndef MT_REPAIR_SKIPW
 #define MT_REPAIR_SKIPW 0   // tiled: no store for a tile-regular vertex whose T0 is already final
 #endif
@@ -131,11 +137,14 @@ repair_brick_kernel(View view, const Cell* C, uint64_t* __restrict__ T, const fl
         u0 = uint64_t(blockIdx.x) * RB_NV;
         seg0 = uint64_t(blockIdx.x) * RB_ROWS;
     } else {
-        const uint32_t b = blockIdx.x;
+        // (MT_REPAIR_ZPAIR, volumes: the two bricks of one tile depth run back to back, so that
+        // the second finds the tile's minima cells still in L2)
+        constexpr bool ZP = MT_REPAIR_ZPAIR && BY == 16;
+        const uint32_t b = ZP ? blockIdx.x >> 1 : blockIdx.x;
         bxi = b % g.bx_n;
         x0 = bxi * 32;
         y0 = ((b / g.bx_n) % g.by_n) * BYD;
-        z0 = sl.z_begin + (b / g.bx_n / g.by_n) * (RB_ROWS / BYD);
+        z0 = sl.z_begin + ((b / g.bx_n / g.by_n) * (ZP ? 2 : 1) + (ZP ? (blockIdx.x & 1) : 0)) * (RB_ROWS / BYD);
     }
     // the warp's rows (item k = row warp + 16 k): first id, valid lanes and segment number, computed
     // once by lanes 0..RB_PER-1 (integer divisions) and read back from shared memory
@@ -291,7 +300,61 @@ repair_brick_kernel(View view, const Cell* C, uint64_t* __restrict__ T, const fl
     // Rep(u, key(s)): walk from v through cells with key(s') <= key(s) that are not roots
     unsigned long long hops = 0;   // (COUNT builds only: mt_set_stats)
     uint32_t moved = 0;       // rows whose walk left its start (bit k)
-#if MT_REPAIR_SEQ
+#if MT_REPAIR_CHAIN
+    // The thread's walks in ascending threshold order, each continuing from the result of the
+    // previous walk when both start at the same vertex: the cells are read-only here, so the
+    // chain from a start vertex is fixed and Rep(x, a') for a' >= a lies on it past Rep(x, a)
+    // (Alg. 4 stops at the first cell that is a root or has key(s) > a).  A thread's vertices
+    // form a z column and mostly share their tile representative, so the chain is walked about
+    // once instead of once per vertex.  Sorted in registers (5 compare-exchanges); T is written
+    // in that order.
+    static_assert(RB_PER == 4 && !MT_REPAIR_SKIPW, "repair chaining: 4 vertices per thread");
+    {
+        uint64_t tk[RB_PER];
+        uint32_t tx[RB_PER], ts[RB_PER], ti[RB_PER];
+#pragma unroll
+        for (int k = 0; k < RB_PER; ++k) {
+            const bool walk = INB(k) && xs[k] != uint32_t(UID(k));
+            tk[k] = INB(k) ? key[k] : ~0ull;
+            tx[k] = xs[k];
+            ts[k] = sv[k];
+            ti[k] = uint32_t(k) | (uint32_t(walk) << 8) | (uint32_t(INB(k)) << 9);
+        }
+        auto cx = [&](int a, int b) {
+            if (tk[b] < tk[a]) {
+                uint64_t t = tk[a]; tk[a] = tk[b]; tk[b] = t;
+                uint32_t u = tx[a]; tx[a] = tx[b]; tx[b] = u;
+                u = ts[a]; ts[a] = ts[b]; ts[b] = u;
+                u = ti[a]; ti[a] = ti[b]; ti[b] = u;
+            }
+        };
+        cx(0, 1);
+        cx(2, 3);
+        cx(0, 2);
+        cx(1, 3);
+        cx(1, 2);
+        uint32_t memo_x0 = ~0u, memo_res = 0;
+#pragma unroll
+        for (int r = 0; r < RB_PER; ++r) {
+            if (!((ti[r] >> 9) & 1u)) continue;
+            uint32_t x = tx[r];
+            if ((ti[r] >> 8) & 1u) {
+                const uint32_t x0 = x;
+                if (x0 == memo_x0) x = memo_res;
+#pragma unroll 1
+                while (true) {
+                    const Cell c = view.cell(C, x);
+                    if (cv_of(c) == x || c.lo > tk[r]) break;   // Alg. 4, reading R20
+                    x = cv_of(c);
+                    if (COUNT) ++hops;
+                }
+                memo_x0 = x0;
+                memo_res = x;
+            }
+            T[S.rowbase[warp + 16 * (ti[r] & 0xffu)] + lane] = pack(ts[r], x);
+        }
+    }
+#elif MT_REPAIR_SEQ
     // one walk after the other (the loop runs the sum of the chain lengths, not RB_PER times
     // the longest)
 #pragma unroll
@@ -330,11 +393,13 @@ repair_brick_kernel(View view, const Cell* C, uint64_t* __restrict__ T, const fl
         }
     }
 #endif
+#if !MT_REPAIR_CHAIN
     // a tile-regular vertex whose walk stayed at its tile representative keeps T0 = (u, R)
     const uint32_t keep = (TILED && MT_REPAIR_SKIPW) ? ~(moved | mins) : 0u;
 #pragma unroll
     for (int k = 0; k < RB_PER; ++k)
         if (INB(k) && !((keep >> k) & 1u)) T[UID(k)] = pack(sv[k], xs[k]);
+#endif
     if (COUNT && hops) atomicAdd(stats + ST_REPAIR_HOPS, hops);
 #undef UID
 #undef INB
@@ -509,7 +574,7 @@ bool brick_mode(const Slab& sl, BrickGeom* g, uint64_t* nb, uint64_t* nseg) {
         const uint32_t bz = RB_ROWS / by;
         const uint32_t bx_n = (sl.nx + 31) / 32, by_n = (sl.ny + by - 1) / by, bz_n = (nzl + bz - 1) / bz;
         *g = BrickGeom{by, bx_n, by_n};
-        *nb = uint64_t(bx_n) * by_n * bz_n;
+        *nb = uint64_t(bx_n) * by_n * ((MT_REPAIR_ZPAIR && by == 16) ? (bz_n + 1) / 2 * 2 : bz_n);
         *nseg = uint64_t(bx_n) * sl.ny * nzl;
         return true;
     }

@@ -367,6 +367,9 @@ forest_dedupe_kernel(ForestRef F, BoundaryGeom g, FQEntry* __restrict__ q, unsig
 
 enum Phase : int { IDLE = 0, CLIMB_HI = 2, CLIMB_LO = 3, MERGE_LD = 4, MERGE_CAS = 5, DONE = 6 };
 
+#ifndef FM_CSPLIT
+#define FM_CSPLIT 1   // forest_merge: Alg. 3 straight from the representatives, path splitting in the climbs
+#endif
 // merge_cross.cu's state machine on the forest: every cell access goes through the table
 __global__ void __launch_bounds__(256)
 forest_merge_kernel(ForestRef F, const FQEntry* __restrict__ q, const unsigned long long* __restrict__ qlen,
@@ -385,6 +388,10 @@ forest_merge_kernel(ForestRef F, const FQEntry* __restrict__ q, const unsigned l
     uint32_t p0 = 0, p1 = 0, p2 = 0, p3 = 0, i0 = 0, i1 = 0, i2 = 0, i3 = 0;
     bool has_prev = false;
     Cell held{0, 0};
+    // FM_CSPLIT: the previous cell (table index, value) of each Alg. 3 climb
+    [[maybe_unused]] Cell hu{0, 0}, hv{0, 0};
+    [[maybe_unused]] uint32_t ju = 0, jv = 0;
+    [[maybe_unused]] bool has_u = false, has_v = false;
     auto at = [&](uint32_t i) { return F.cells + i; };
     auto lookup = [&](uint32_t id, uint32_t* i) {
         *i = forest_lookup(F, id);
@@ -416,6 +423,12 @@ forest_merge_kernel(ForestRef F, const FQEntry* __restrict__ q, const unsigned l
                     p2 = en.r_lo;
                     has_prev = false;
                     phase = (lookup(p0, &i0) && lookup(p2, &i2)) ? CLIMB_HI : IDLE;
+                    if (FM_CSPLIT && phase == CLIMB_HI) {   // Merge(T, R_hi, hi, R_lo) straight away
+                        p1 = p2;
+                        i1 = i2;
+                        has_u = has_v = false;
+                        phase = MERGE_LD;
+                    }
                 } else if (exhausted) {
                     phase = DONE;
                 }
@@ -454,7 +467,27 @@ forest_merge_kernel(ForestRef F, const FQEntry* __restrict__ q, const unsigned l
             Cell cu = ld_cell(at(i0)), cv = ld_cell(at(i1));
             const bool up_u = cv_of(cu) != p0 && cu.lo < lev;       // l.2-4 (+ R4)
             const bool up_v = cv_of(cv) != p1 && cv.lo < lev;       // l.5-8 (+ R4)
-            if (up_u || up_v) {                                     // independent climbs (derivation J)
+            if (FM_CSPLIT && (up_u || up_v)) {
+                // independent climbs, each splitting its path (merge_cross.cu, MQ_CSPLIT)
+                if (up_u) {
+                    if (has_u && cu.lo <= hu.lo)
+                        cas_cell(at(ju), hu, Cell{hu.lo, (hu.hi & 0xffffffff00000000ull) | cv_of(cu)});
+                    ju = i0;
+                    hu = cu;
+                    has_u = true;
+                    p0 = cv_of(cu);
+                    if (!lookup(p0, &i0)) phase = IDLE;
+                }
+                if (up_v) {
+                    if (has_v && cv.lo <= hv.lo)
+                        cas_cell(at(jv), hv, Cell{hv.lo, (hv.hi & 0xffffffff00000000ull) | cv_of(cv)});
+                    jv = i1;
+                    hv = cv;
+                    has_v = true;
+                    p1 = cv_of(cv);
+                    if (!lookup(p1, &i1)) phase = IDLE;
+                }
+            } else if (up_u || up_v) {                              // independent climbs (derivation J)
                 if (up_u) {
                     p0 = cv_of(cu);
                     if (!lookup(p0, &i0)) phase = IDLE;
@@ -473,6 +506,7 @@ forest_merge_kernel(ForestRef F, const FQEntry* __restrict__ q, const unsigned l
                 }
                 held = cv;                                          // l.14, next round trip
                 phase = MERGE_CAS;
+                has_u = has_v = false;
             }
         } else if (phase == MERGE_CAS) {
             const Cell got = cas_cell(at(i1), held, Cell{lev, (held.hi & 0xffffffff00000000ull) | p0});

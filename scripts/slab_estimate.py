@@ -34,7 +34,7 @@ for P in Ps:
     slabs = [SlabMergeTree(dims, zb[r], zb[r + 1]) for r in range(P)]
     parts = [fd[zb[r] * nx * ny: zb[r + 1] * nx * ny].contiguous() for r in range(P)]
     best_loc, best_glob = [1e30] * P, [1e30] * P
-    for rep in range(3):   # per rank, the best of the last two passes
+    for rep in range(5):   # per rank, the best of the last four passes
         loc = [timed(lambda r=r: slabs[r].compute_local(parts[r])) for r in range(P)]
         recs = [s.forest() for s in slabs]
         counts = [x.numel() // 32 for x in recs]
