@@ -65,6 +65,9 @@ namespace {
 #ifndef DC_NDEDUP
 #define DC_NDEDUP 1       // patch steps: drop edges whose neighbour lane has the same pair lower
 #endif
+#ifndef DC_MIN32
+#define DC_MIN32 1        // patch table: the lowest level by two native 32-bit minima (order key, id)
+#endif
 #ifndef DC_REDUCE
 #define DC_REDUCE 0       // group minimum by two __reduce_min_sync (else a 32-lane shuffle scan)
 #endif
@@ -123,7 +126,12 @@ dedupe_cross_kernel(const float* __restrict__ f, const uint64_t* __restrict__ T0
                     unsigned long long* __restrict__ stats) {
     __shared__ uint32_t s_warp[DC_THREADS / 32];
     __shared__ unsigned long long s_base;
-    __shared__ unsigned long long s_key[2 * DC_THREADS], s_min[2 * DC_THREADS];   // DC_PATCH: pair -> lowest level
+    __shared__ unsigned long long s_key[2 * DC_THREADS];   // DC_PATCH: pair -> lowest level
+#if DC_MIN32
+    __shared__ uint32_t s_mo[2 * DC_THREADS], s_mi[2 * DC_THREADS];   // its order key, then its id
+#else
+    __shared__ unsigned long long s_min[2 * DC_THREADS];
+#endif
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint64_t total = g.ex + g.ey + g.ez;
     const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
@@ -269,8 +277,15 @@ dedupe_cross_kernel(const float* __restrict__ f, const uint64_t* __restrict__ T0
             // CTA-wide: the warps' survivors keep the lowest edge of each pair over the patch
             s_key[threadIdx.x] = ~0ull;
             s_key[threadIdx.x + DC_THREADS] = ~0ull;
+#if DC_MIN32
+            s_mo[threadIdx.x] = ~0u;
+            s_mo[threadIdx.x + DC_THREADS] = ~0u;
+            s_mi[threadIdx.x] = ~0u;
+            s_mi[threadIdx.x + DC_THREADS] = ~0u;
+#else
             s_min[threadIdx.x] = ~0ull;
             s_min[threadIdx.x + DC_THREADS] = ~0ull;
+#endif
             __syncthreads();
             uint32_t h = 0;
             if (keep) {
@@ -280,10 +295,22 @@ dedupe_cross_kernel(const float* __restrict__ f, const uint64_t* __restrict__ T0
                     if (k == ~0ull || k == pair) break;
                     h = (h + 1) & (2u * DC_THREADS - 1u);
                 }
+#if DC_MIN32
+                atomicMin(&s_mo[h], uint32_t(en.L >> 32));   // (native 32-bit minima: no CAS loop)
+#else
                 atomicMin(&s_min[h], (unsigned long long)en.L);
+#endif
             }
             __syncthreads();
+#if DC_MIN32
+            // the lowest order key first, then the lowest id among the edges that have it
+            if (keep && s_mo[h] != uint32_t(en.L >> 32)) keep = false;
+            if (keep) atomicMin(&s_mi[h], uint32_t(en.L));
+            __syncthreads();
+            if (keep && s_mi[h] != uint32_t(en.L)) keep = false;
+#else
             if (keep && s_min[h] != en.L) keep = false;
+#endif
         }
         const uint32_t km = __ballot_sync(FULL_MASK, keep);
         if (lane == 0) s_warp[warp] = __popc(km);

@@ -440,6 +440,15 @@ diagram_kernel(const uint16_t* __restrict__ seg_cnt, const uint32_t* __restrict_
         cf += cnts[j] & 0xffu;
         ce += cnts[j] >> 8;
     }
+    // the staging offsets and every segment's first record are loaded before the scans and the
+    // look-back, so those loads overlap the chain instead of following it
+    uint32_t spos[DG_SPT];
+    mt_pair first[DG_SPT];
+#pragma unroll
+    for (int j = 0; j < DG_SPT; ++j) {
+        spos[j] = cnts[j] ? seg_pos[seg + j] : 0u;
+        if (cnts[j]) first[j] = stage[spos[j]];
+    }
     // block-wide exclusive scans (finite, essential)
     uint32_t incl = cf, eincl = ce;
 #pragma unroll
@@ -517,13 +526,13 @@ diagram_kernel(const uint16_t* __restrict__ seg_cnt, const uint32_t* __restrict_
     for (int j = 0; j < DG_SPT; ++j) {
         const uint32_t fj = cnts[j] & 0xffu, ej = cnts[j] >> 8;
         if (!(fj | ej)) continue;
-        const mt_pair* src = stage + seg_pos[seg + j];
+        const mt_pair* src = stage + spos[j];
         for (uint32_t i = 0; i < fj; ++i) {
-            if (p + i < out_cap) out[p + i] = src[i];
+            if (p + i < out_cap) out[p + i] = i ? src[i] : first[j];
             else atomicOr(counters + CTR_ERR, ERR_CAPACITY);
         }
         for (uint32_t i = 0; i < ej; ++i) {
-            if (ep + i < ess_cap) ess[ep + i] = src[fj + i];
+            if (ep + i < ess_cap) ess[ep + i] = (fj + i) ? src[fj + i] : first[j];
             else atomicOr(counters + CTR_ERR, ERR_ESS_CAPACITY);
         }
         p += fj;

@@ -18,23 +18,19 @@
 //      (derivation B);
 //   b. compress by synchronous pointer jumping: every regular cell points at
 //      its basin minimum (derivations F, F');
-//   c. choose the inter-basin edges the merge needs (TILE_KRUSKAL, default):
-//      the vertices are counting-sorted into NB level buckets; bucket by
-//      bucket, an edge (u, w) from u down to a lower neighbour w of another
-//      basin is kept only if a union-find over the basins, holding every kept
-//      edge of the LOWER buckets, does not already join the two basins (an
-//      edge whose basins are joined below its level changes no sublevel
-//      component: derivation K); then the bucket's kept edges are united.
-//      This is Kruskal's filter at bucket granularity: the kept edges are the
-//      basin graph's minimum spanning forest plus the few edges that close a
-//      cycle inside one bucket.  (TILE_KRUSKAL=0: the earlier lowest-edge-per-
-//      basin-pair hash table, derivation C''.)
-//   d. merge the kept edges: Alg. 3 from the two basins at the edge's level
+//   c. one edge per pair of adjacent basins, the lowest (derivation C''): every in-tile edge
+//      (u, w) between two basins is a candidate; a shared-memory hash table keyed by the basin
+//      pair keeps the one of lowest level (64-bit CAS).  Candidates go through a per-warp ring
+//      of staged entries and every lane runs its insert as a state machine, one probe per loop
+//      iteration, taking the next staged entry as soon as its insert is done (TILE_RINS), so a
+//      warp pays the lanes' average probe count rather than their maximum.  (TILE_KRUSKAL=1: a
+//      bucketed Kruskal filter instead, derivation K -- measured slower.)
+//   d. merge the kept edges (one per basin pair): Alg. 3 from the two basins at the edge's level
 //      with 64-bit shared-memory CAS and the root guards R4/R5,
 //      one lane per edge, one shared-memory round trip per loop iteration; a
 //      lane whose edge is done takes the next one of the warp's slice;
 //   e. repair (Alg. 5 with Alg. 4's walk, reading R20): the tile store is
-//      minimal for G_t (each thread's walks in lock-step rounds);
+//      minimal for G_t (each thread walks its vertices one after the other);
 //   f. write the tile store T0 (8 B per vertex) and the tile minima's 16-byte
 //      working cells (common.cuh) with global ids, and the x-face records.
 // No halo is needed: only in-tile edges are used here.
@@ -76,6 +72,9 @@ namespace {
 #endif
 #ifndef TILE_BOTHCLIMB
 #define TILE_BOTHCLIMB 1  // Alg. 3 loop: climb u and v in the same iteration when both can climb
+#endif
+#ifndef TILE_RINS
+#define TILE_RINS 1    // hash list: refilling insert loop over a per-warp ring (lanes' average probes)
 #endif
 #ifndef TILE_ZRUN
 #define TILE_ZRUN 0    // hash list: a thread's z column keeps one edge per run of equal basin pairs
@@ -647,6 +646,85 @@ tile_tmt_kernel(const __grid_constant__ CUtensorMap fmap, const float* __restric
                  (uint64_t(pair) << LB) | hi;
         return true;
     };
+#if TILE_RINS
+    if (TILE_STOP == 0 || TILE_STOP > 2) {
+        // The warp's candidates go through a ring of 128 staged entries; every lane runs one
+        // insert as a state machine, one table probe per loop iteration, and a lane whose insert
+        // is done takes the next staged entry at the top of the next iteration (as in the merge
+        // loop below), so the warp's iterations are the lanes' average probe count instead of
+        // their maximum.  After each vertex row at most 32 entries stay pending (+ <= 96 new).
+        constexpr uint32_t RING = 128;
+        static_assert(NV / (2 * NW) == int(RING), "staging ring: 128 entries per warp");
+        uint64_t* stage = reinterpret_cast<uint64_t*>(smem + NV * 12 + TABLE * 8) + warp_d * RING;
+        const uint32_t lt = (1u << lane_c) - 1u;
+        uint32_t head = 0, tail = 0;          // warp-uniform ring positions
+        bool ibusy = false;
+        uint64_t ient = 0;
+        uint32_t ih = 0, ipair = 0, iprobe = 0;
+        // run the warp's inserts until at most `keep` entries are pending (keep == 0: all done)
+        auto pump = [&](uint32_t keep) {
+#pragma unroll 1
+            while (true) {
+                const uint32_t pend = tail - head;
+                const uint32_t need = __ballot_sync(FULL_MASK, !ibusy);
+                if (pend <= keep && (keep || need == FULL_MASK)) break;
+                if (need && pend) {
+                    if (!ibusy) {
+                        const uint32_t r = __popc(need & lt);
+                        if (r < pend) {
+                            ient = stage[(head + r) & (RING - 1)];
+                            ipair = uint32_t(ient >> LB) & PMASK;
+                            ih = pair_hash<TABLE>(ipair);
+                            iprobe = 0;
+                            ibusy = true;
+                        }
+                    }
+                    head += min(__popc(need), pend);
+                }
+                if (ibusy) {                 // one probe of the insert (insert_entry's loop body)
+                    const uint64_t cur = sld64(table + ih);
+                    if (cur == EMPTY) {
+                        if (scas64(table + ih, EMPTY, ient) == EMPTY) ibusy = false;
+                    } else if ((uint32_t(cur >> LB) & PMASK) != ipair) {
+                        ih = ih + 1 == uint32_t(TABLE) ? 0u : ih + 1;
+                        if (++iprobe >= uint32_t(TABLE)) {
+                            s_overflow = 1;          // table full: merge every edge
+                            ibusy = false;
+                        }
+                    } else {
+                        const uint32_t hme = uint32_t(ient) & LMASK, hcu = uint32_t(cur) & LMASK;
+                        const uint32_t ome = ord[hme], ocu = ord[hcu];
+                        if (ome > ocu || (ome == ocu && hme >= hcu)) ibusy = false;   // stored edge is lower
+                        else if (scas64(table + ih, cur, ient) == cur) ibusy = false;
+                    }
+                }
+            }
+        };
+#pragma unroll 1
+        for (int k = 0; k < PER; ++k) {
+            const int r = r0 + k * RSTEP;
+            const int ly = r % TY, lz = r / TY;
+            const uint32_t u = r * TX + lx;
+            const uint32_t ou = ord[u];
+            const uint32_t bu = c_v(cell[u]);      // basin (a minimum points at itself)
+            const bool ok[3] = {lx + 1 < TX, ly + 1 < TY, lz + 1 < TZ};
+            const uint32_t off[3] = {1u, uint32_t(TX), uint32_t(TX * TY)};
+#pragma unroll
+            for (int d = 0; d < 3; ++d) {
+                uint64_t entry = 0;
+                const bool valid = candidate(u, ou, bu, ok[d], off[d], &entry);
+                if (STATS && valid) ++n_edges;
+                const uint32_t m = __ballot_sync(FULL_MASK, valid);
+                if (valid) stage[(tail + __popc(m & lt)) & (RING - 1)] = entry;
+                tail += __popc(m);
+            }
+            __syncwarp();
+            pump(32);
+        }
+        __syncwarp();
+        pump(0);
+    }
+#else
     if (TILE_STOP == 0 || TILE_STOP > 2) {
         constexpr int STAGE = NV / (2 * NW);   // per-warp staging entries (>= 64: flushed per direction)
         static_assert(STAGE >= 64, "staging buffer");
@@ -722,6 +800,7 @@ tile_tmt_kernel(const __grid_constant__ CUtensorMap fmap, const float* __restric
 #endif
         if (uint32_t(lane_c) < nst) insert_entry(stage[lane_c]);
     }
+#endif
     __syncthreads();
     phase_time(ST_CYC_LIST);
     if (PERSIST && threadIdx.x == 0 && pass == (DUAL ? 1 : 0)) {
