@@ -73,6 +73,12 @@ namespace {
 #ifndef TILE_BOTHCLIMB
 #define TILE_BOTHCLIMB 1  // Alg. 3 loop: climb u and v in the same iteration when both can climb
 #endif
+#ifndef TILE_TQ
+#define TILE_TQ 6      // basin-pair table: TILE_TQ / 4 slots per tile vertex
+#endif
+#ifndef TILE_ZREG
+#define TILE_ZREG 1    // volumes: the +-z neighbours' order keys / basins from the thread's own registers
+#endif
 #ifndef TILE_RINS
 #define TILE_RINS 1    // hash list: refilling insert loop over a per-warp ring (lanes' average probes)
 #endif
@@ -91,8 +97,8 @@ constexpr uint32_t ABSENT = 0xffffffffu;       // order key of a tile slot outsi
 constexpr uint64_t EMPTY = ~0ull;
 constexpr int LOG2NB = TILE_NB == 32 ? 5 : TILE_NB == 16 ? 4 : TILE_NB == 8 ? 3 : 2;
 static_assert((1 << LOG2NB) == TILE_NB, "TILE_NB: 4, 8, 16 or 32");
-// hash variant: basin-pair table of 1.5 NV slots + a staging buffer of 128 entries per warp
-constexpr int table_slots(int nv) { return 3 * nv / 2; }
+// hash variant: basin-pair table of TILE_TQ / 4 NV slots + a staging buffer of 128 entries per warp
+constexpr int table_slots(int nv) { return TILE_TQ * nv / 4; }
 template <int NV>
 constexpr size_t smem_bytes() {
     return TILE_KRUSKAL ? size_t(NV) * 8 + size_t(NV) * 4 + size_t(NV) * 2 /* uf */ + size_t(NV) * 2 /* vlist */ +
@@ -400,12 +406,20 @@ tile_tmt_kernel(const __grid_constant__ CUtensorMap fmap, const float* __restric
     // the key-least of u and its neighbours: visiting them in ascending id order (-z, -y, -x,
     // u, +x, +y, +z: local ids are lexicographic in (z, y, x) like global ids) and taking a
     // strictly smaller order key breaks ties by id (reading R1) with 32-bit compares only
+    {
+        // (ZREG, volumes: the +-z neighbours of vertex k are the thread's own vertices k -+ 1)
+        constexpr bool ZREG = TILE_ZREG && TY == RSTEP;
+        uint32_t oreg[PER];
+        if (ZREG) {
+#pragma unroll
+            for (int k = 0; k < PER; ++k) oreg[k] = ord[(r0 + k * RSTEP) * TX + lx];
+        }
 #pragma unroll
     for (int k = 0; k < PER; ++k) {
         const int r = r0 + k * RSTEP;
         const int ly = r % TY, lz = r / TY;
         const uint32_t u = r * TX + lx;
-        const uint32_t ou = ord[u];
+        const uint32_t ou = ZREG ? oreg[k] : ord[u];
         uint32_t best = u;
         if (ou != ABSENT) {
             uint32_t bo = ABSENT;
@@ -417,15 +431,25 @@ tile_tmt_kernel(const __grid_constant__ CUtensorMap fmap, const float* __restric
                     best = w;
                 }
             };
-            visit(lz > 0, u - TX * TY);
+            auto visit_kn = [&](bool ok, uint32_t w, uint32_t ow) {
+                if (ok && ow < bo) {
+                    bo = ow;
+                    best = w;
+                }
+            };
+            if (ZREG) visit_kn(k > 0, u - TX * TY, oreg[k > 0 ? k - 1 : 0]);
+            else visit(lz > 0, u - TX * TY);
             visit(ly > 0, u - TX);
             visit(lx > 0, u - 1);
-            visit(true, u);
+            if (ZREG) visit_kn(true, u, ou);
+            else visit(true, u);
             visit(lx + 1 < TX, u + 1);
             visit(ly + 1 < TY, u + TX);
-            visit(lz + 1 < TZ, u + TX * TY);
+            if (ZREG) visit_kn(k + 1 < PER, u + TX * TY, oreg[k + 1 < PER ? k + 1 : k]);
+            else visit(lz + 1 < TZ, u + TX * TY);
         }
         cell[u] = c_make(ou, u, best);
+    }
     }
     __syncthreads();
     phase_time(ST_CYC_DESCENT);
@@ -630,6 +654,18 @@ tile_tmt_kernel(const __grid_constant__ CUtensorMap fmap, const float* __restric
             if (scas64(table + h, cur, entry) == cur) break;
         }
     };
+    // (candidate_kn: the neighbour's order key and basin already in registers)
+    auto candidate_kn = [&](uint32_t u, uint32_t ou, uint32_t bu, bool ok, uint32_t w, uint32_t ow, uint32_t bw,
+                            uint64_t* entry) {
+        if (ou == ABSENT || !ok || ow == ABSENT || bw == bu) return false;
+        const bool u_hi = ow < ou;   // w has the larger id: on a tie w is the upper end
+        const uint32_t hi = u_hi ? u : w, oh = u_hi ? ou : ow;
+        const bool lo_first = bu < bw;
+        const uint32_t pair = lo_first ? (bu << LB) | bw : (bw << LB) | bu;
+        *entry = (uint64_t(u_hi == lo_first) << 63) | (TILE_ORDBITS ? uint64_t(oh >> (32 - OB)) << (3 * LB) : 0ull) |
+                 (uint64_t(pair) << LB) | hi;
+        return true;
+    };
     auto candidate = [&](uint32_t u, uint32_t ou, uint32_t bu, bool ok, uint32_t off, uint64_t* entry) {
         if (ou == ABSENT || !ok) return false;
         const uint32_t w = u + off;
@@ -700,19 +736,38 @@ tile_tmt_kernel(const __grid_constant__ CUtensorMap fmap, const float* __restric
                 }
             }
         };
+        // (ZREG, volumes: the +z neighbour of vertex k is the thread's own vertex k + 1, so its order
+        // key and basin are loaded once and carried to the next iteration)
+        constexpr bool ZREG = TILE_ZREG && TY == RSTEP;
+        uint32_t ou_n = 0, bu_n = 0;
+        if (ZREG) {
+            ou_n = ord[r0 * TX + lx];
+            bu_n = c_v(cell[r0 * TX + lx]);
+        }
 #pragma unroll 1
         for (int k = 0; k < PER; ++k) {
             const int r = r0 + k * RSTEP;
             const int ly = r % TY, lz = r / TY;
             const uint32_t u = r * TX + lx;
-            const uint32_t ou = ord[u];
-            const uint32_t bu = c_v(cell[u]);      // basin (a minimum points at itself)
+            uint32_t ou, bu;
+            if (ZREG) {
+                ou = ou_n;
+                bu = bu_n;
+                if (k + 1 < PER) {
+                    ou_n = ord[u + TX * TY];
+                    bu_n = c_v(cell[u + TX * TY]);
+                }
+            } else {
+                ou = ord[u];
+                bu = c_v(cell[u]);                 // basin (a minimum points at itself)
+            }
             const bool ok[3] = {lx + 1 < TX, ly + 1 < TY, lz + 1 < TZ};
             const uint32_t off[3] = {1u, uint32_t(TX), uint32_t(TX * TY)};
 #pragma unroll
             for (int d = 0; d < 3; ++d) {
                 uint64_t entry = 0;
-                const bool valid = candidate(u, ou, bu, ok[d], off[d], &entry);
+                const bool valid = (ZREG && d == 2) ? candidate_kn(u, ou, bu, ok[d], u + TX * TY, ou_n, bu_n, &entry)
+                                                    : candidate(u, ou, bu, ok[d], off[d], &entry);
                 if (STATS && valid) ++n_edges;
                 const uint32_t m = __ballot_sync(FULL_MASK, valid);
                 if (valid) stage[(tail + __popc(m & lt)) & (RING - 1)] = entry;
