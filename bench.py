@@ -134,13 +134,29 @@ def oracle_rate(f, dims, conn, planes, split=False):
     return n / dt / 1e6, n, dt, sub_dims
 
 
-def cpu_sample_planes(cfg, target_s):
+def paper_cpu_rate(f, dims, conn, planes, split=False):
+    """The paper's Alg. 1-5 with CAS on all host cores (OpenMP; baseline/paper_cpu) on the first
+    `planes` z-planes; the second of two runs is timed.  Returns (Mv/s, n, seconds, dims, threads)."""
+    from baseline import paper_cpu
+    nx, ny, nz = dims
+    sub_dims = (nx, ny, min(planes, nz)) if nz > 1 else (nx, min(max(1, planes * 64), ny), 1)
+    n = sub_dims[0] * sub_dims[1] * sub_dims[2]
+    sub = np.ascontiguousarray(f[:n])
+    conn = 4 if sub_dims[2] == 1 else conn
+    dt = 0.0
+    for _ in range(2):
+        t0 = time.perf_counter()
+        paper_cpu.merge_tree(sub, sub_dims, conn=conn, split=split)
+        dt = time.perf_counter() - t0
+    return n / dt / 1e6, n, dt, sub_dims, paper_cpu.max_threads()
+
+
+def cpu_sample_planes(cfg, target_s, rate=1.3e6):
     # oracle throughput is ~1-2 Mv/s on one core; pick the number of planes that
     # gives about target_s seconds of work
     from paper_2301_10838_b200.fields import CONFIGS
     nx, ny, nz = CONFIGS[cfg]["dims"]
     per_plane = nx * ny if nz > 1 else nx * 64
-    rate = 1.3e6
     return max(1, int(target_s * rate / per_plane))
 
 
@@ -429,13 +445,23 @@ def run_mt(args, rank, world):
                "overlap": "mt_compute_host (C ABI): H2D(i+1) | compute(i) | D2H(i-1) on the library's 3 streams"
                if world == 1 else "none"}
 
-    cpu = None
+    cpu = cpu_paper = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         planes = cpu_sample_planes(args.config, 15.0)
         r, nv, dt, sub = oracle_rate(f_np, dims, conn, planes, args.split)
         cpu = {"value": r, "unit": "Mvertices/s", "cores": 1, "kind": "oracle",
                "sample": f"O1 (serial C union-find + elder rule) on the first {sub} sub-grid "
                          f"({nv} vertices, {dt:.1f} s) of the same field, 1 of {os.cpu_count()} host cores"}
+        # the paper's own method on every host core (optional second CPU baseline,
+        # the analogue of the paper's OpenMP column) -- a reported baseline, not the oracle
+        try:
+            pplanes = cpu_sample_planes(args.config, 2.0, rate=3e7)
+            pr, pnv, pdt, psub, pthr = paper_cpu_rate(f_np, dims, conn, pplanes, args.split)
+            cpu_paper = {"value": pr, "unit": "Mvertices/s", "cores": pthr, "kind": "paper Alg. 1-5, OpenMP + CAS",
+                         "sample": f"baseline/paper_cpu on the first {psub} sub-grid ({pnv} vertices, {pdt:.2f} s, "
+                                   f"second of two runs) of the same field, {pthr} of {os.cpu_count()} host threads"}
+        except Exception as e:   # a missing OpenMP toolchain must not void the GPU measurement
+            cpu_paper = {"unavailable": str(e)[:200]}
 
     if rank == 0:
         line = {
@@ -446,7 +472,8 @@ def run_mt(args, rank, world):
             "config": _config(args, dims, conn, world),
             "pairs": npairs, "essential": ness,
             "step_ms": {"median": statistics.median(step_ms), "min": min(step_ms), "max": max(step_ms)},
-            "roofline": roofline, "secondary_ceilings": secondary, "cpu_baseline": cpu, "e2e": e2e,
+            "roofline": roofline, "secondary_ceilings": secondary, "cpu_baseline": cpu,
+            "cpu_paper_method": cpu_paper, "e2e": e2e,
             "gpu_launches": launches,
             "clocks": clk.summary(),
         }
