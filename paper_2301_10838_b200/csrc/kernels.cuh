@@ -130,13 +130,19 @@ void launch_tile_tmt_dual(const float* f, Cell* C_join, uint64_t* T0_join, uint6
 uint64_t cross_edges(const Slab& sl);
 size_t cross_queue_entry_bytes();
 // returns 0 when the slab has a single tile (no crossing edges, no kernel launched)
+// Stepped queue (cross_stepped()): every 512-edge step of the enumeration writes its survivors at
+// its own edge positions and their count to qcnt[step] (cross_steps() steps), no global counter.
 int launch_dedupe_cross(const float* f, const uint64_t* T0, const uint64_t* xface, const Slab& sl, uint32_t flip,
                         void* queue,
-                        uint64_t cap, unsigned long long* qlen, unsigned long long* stats, int num_sms,
-                        cudaStream_t stream);
+                        uint64_t cap, unsigned long long* qlen, uint32_t* qcnt, unsigned long long* stats,
+                        int num_sms, cudaStream_t stream);
+uint64_t cross_steps(const Slab& sl);
+bool cross_stepped();
 
-// the queue consumer alone (queue entries: {uint64 L, uint32 basin_hi, uint32 basin_lo})
+// the queue consumer alone (queue entries: {uint64 L, uint32 basin_hi, uint32 basin_lo}); qcnt null:
+// a compact queue of *qlen entries, else nsteps steps of 512 entries with qcnt[step] of them used
 void launch_merge_queue(Cell* C, const void* queue, uint64_t cap, const unsigned long long* qlen,
+                        const uint32_t* qcnt, uint64_t nsteps,
                         unsigned long long* fetch, unsigned long long* stats, int num_sms, cudaStream_t stream);
 
 // explicit graphs in CSR form (graph.cu)
@@ -157,6 +163,9 @@ struct RepairOut {
 };
 uint64_t repair_segments(const Slab& sl);     // segments of the slab
 uint64_t repair_segments_bound(uint64_t n);   // >= repair_segments of any slab of n vertices
+// staging records the repair of this slab addresses when its bricks stage at fixed offsets (0: it
+// uses a global counter and needs at most one record per minimum)
+uint64_t repair_stage_records(const Slab& sl);
 uint64_t diagram_tiles(uint64_t nseg);        // diagram tiles; one 16-B status record each
 uint64_t diagram_tiles_bound(uint64_t nseg);  // >= diagram_tiles of any nseg' <= nseg (status sizing)
 // tiled: T holds tile_tmt's T0 and only tile minima have cells (grids); else every vertex has a

@@ -65,6 +65,9 @@ namespace {
 #ifndef DC_NDEDUP
 #define DC_NDEDUP 1       // patch steps: drop edges whose neighbour lane has the same pair lower
 #endif
+#ifndef DC_STEPQ
+#define DC_STEPQ 0        // stepped crossing-edge queue: survivors at their step's own positions + a count per step (measured slower)
+#endif
 #ifndef DC_MIN32
 #define DC_MIN32 1        // patch table: the lowest level by two native 32-bit minima (order key, id)
 #endif
@@ -123,7 +126,7 @@ __global__ void __launch_bounds__(DC_THREADS)
 dedupe_cross_kernel(const float* __restrict__ f, const uint64_t* __restrict__ T0,
                     const uint64_t* __restrict__ xface, CrossGeom g, uint32_t flip,
                     QEntry* __restrict__ q, uint64_t cap, unsigned long long* __restrict__ qlen,
-                    unsigned long long* __restrict__ stats) {
+                    uint32_t* __restrict__ qcnt, unsigned long long* __restrict__ stats) {
     __shared__ uint32_t s_warp[DC_THREADS / 32];
     __shared__ unsigned long long s_base;
     __shared__ unsigned long long s_key[2 * DC_THREADS];   // DC_PATCH: pair -> lowest level
@@ -322,7 +325,14 @@ dedupe_cross_kernel(const float* __restrict__ f, const uint64_t* __restrict__ T0
                 s_warp[w] = tot;
                 tot += t;
             }
-            s_base = tot ? atomicAdd(qlen, (unsigned long long)tot) : 0;
+            if (qcnt) {
+                // stepped queue: this step's survivors at its own edge positions [e0, e0 + tot)
+                // and their count -- no global atomic (merge_queue reads step by step)
+                qcnt[e0 / DC_THREADS] = tot;
+                s_base = e0;
+            } else {
+                s_base = tot ? atomicAdd(qlen, (unsigned long long)tot) : 0;
+            }
         }
         __syncthreads();
         const uint64_t pos = s_base + s_warp[warp] + __popc(km & ((1u << lane) - 1u));
@@ -353,8 +363,10 @@ enum Phase : int { IDLE = 0, CLIMB_HI = 2, CLIMB_LO = 3, MERGE_LD = 4, MERGE_CAS
 template <bool STATS>
 __global__ void __launch_bounds__(256, MQ_MIN_BLOCKS)
 merge_queue_kernel(Cell* C, const QEntry* __restrict__ q, uint64_t cap, const unsigned long long* __restrict__ qlen,
-                   unsigned long long* __restrict__ fetch, unsigned long long* __restrict__ stats) {
+                   const uint32_t* __restrict__ qcnt, uint64_t nsteps, unsigned long long* __restrict__ fetch,
+                   unsigned long long* __restrict__ stats) {
     constexpr uint64_t BATCH = 256;
+    constexpr uint64_t STEP = DC_THREADS;   // stepped queue: entries per dedupe_cross step
     const int lane = threadIdx.x & 31;
     const uint64_t qn = *reinterpret_cast<const volatile unsigned long long*>(qlen);
     const uint64_t total = qn < cap ? qn : cap;
@@ -382,7 +394,21 @@ merge_queue_kernel(Cell* C, const QEntry* __restrict__ q, uint64_t cap, const un
     while (true) {
         const uint32_t need = __ballot_sync(FULL_MASK, phase == IDLE);
         if (need) {
-            if (pool_next == pool_end && !exhausted) {
+            if (qcnt) {
+                // stepped queue (dedupe_cross): one step's survivors at a time, empty steps skipped
+                while (pool_next == pool_end && !exhausted) {
+                    unsigned long long st = 0;
+                    if (lane == 0) st = atomicAdd(fetch, 1ull);
+                    st = __shfl_sync(FULL_MASK, st, 0);
+                    if (st >= nsteps) {
+                        exhausted = true;
+                    } else {
+                        const uint32_t c = qcnt[st];
+                        pool_next = st * STEP;
+                        pool_end = pool_next + (c < STEP ? c : STEP);
+                    }
+                }
+            } else if (pool_next == pool_end && !exhausted) {
                 unsigned long long b0 = 0;
                 if (lane == 0) b0 = atomicAdd(fetch, (unsigned long long)BATCH);
                 b0 = __shfl_sync(FULL_MASK, b0, 0);
@@ -517,8 +543,8 @@ merge_queue_kernel(Cell* C, const QEntry* __restrict__ q, uint64_t cap, const un
 
 int launch_dedupe_cross(const float* f, const uint64_t* T0, const uint64_t* xface, const Slab& sl, uint32_t flip,
                         void* queue,
-                        uint64_t cap, unsigned long long* qlen, unsigned long long* stats, int num_sms,
-                        cudaStream_t stream) {
+                        uint64_t cap, unsigned long long* qlen, uint32_t* qcnt, unsigned long long* stats,
+                        int num_sms, cudaStream_t stream) {
     CrossGeom g{};
     g.nx = sl.nx;
     g.ny = sl.ny;
@@ -541,11 +567,17 @@ int launch_dedupe_cross(const float* f, const uint64_t* T0, const uint64_t* xfac
     QEntry* q = static_cast<QEntry*>(queue);
     uint64_t blocks = (total + DC_THREADS - 1) / DC_THREADS;
     if (blocks > uint64_t(num_sms) * 32) blocks = uint64_t(num_sms) * 32;
-    dedupe_cross_kernel<<<uint32_t(blocks), DC_THREADS, 0, stream>>>(f, T0, xface, g, flip, q, cap, qlen, stats);
+    dedupe_cross_kernel<<<uint32_t(blocks), DC_THREADS, 0, stream>>>(f, T0, xface, g, flip, q, cap, qlen,
+                                                                      DC_STEPQ ? qcnt : nullptr, stats);
     return 1;
 }
 
+static_assert(DC_THREADS >= 128, "the workspace sizes the stepped queue's counts for steps of >= 128 edges");
+uint64_t cross_steps(const Slab& sl) { return (cross_edges(sl) + DC_THREADS - 1) / DC_THREADS; }
+bool cross_stepped() { return DC_STEPQ != 0; }
+
 void launch_merge_queue(Cell* C, const void* queue, uint64_t cap, const unsigned long long* qlen,
+                        const uint32_t* qcnt, uint64_t nsteps,
                         unsigned long long* fetch, unsigned long long* stats, int num_sms, cudaStream_t stream) {
     const QEntry* q = static_cast<const QEntry*>(queue);
     // persistent grid: as many CTAs as fit on every SM of this device
@@ -553,9 +585,9 @@ void launch_merge_queue(Cell* C, const void* queue, uint64_t cap, const unsigned
                              : occupancy_per_sm(reinterpret_cast<const void*>(merge_queue_kernel<false>), 256, 0);
     const uint32_t pblocks = uint32_t(num_sms) * per_sm;
     if (stats)
-        merge_queue_kernel<true><<<pblocks, 256, 0, stream>>>(C, q, cap, qlen, fetch, stats);
+        merge_queue_kernel<true><<<pblocks, 256, 0, stream>>>(C, q, cap, qlen, qcnt, nsteps, fetch, stats);
     else
-        merge_queue_kernel<false><<<pblocks, 256, 0, stream>>>(C, q, cap, qlen, fetch, stats);
+        merge_queue_kernel<false><<<pblocks, 256, 0, stream>>>(C, q, cap, qlen, qcnt, nsteps, fetch, stats);
 }
 
 uint64_t cross_edges(const Slab& sl) {

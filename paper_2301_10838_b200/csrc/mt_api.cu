@@ -65,9 +65,9 @@ constexpr int MAX_EVENTS = 16;
 size_t align_up(size_t x) { return (x + ALIGN - 1) / ALIGN * ALIGN; }
 
 struct Layout {
-    size_t counters, status, status_bytes, stats, ess, cells, xface, queue, pairs, stage, seg_cnt, seg_pos, flags, recs,
-        total;
-    uint64_t pairs_cap, recs_cap, queue_cap, ess_cap, seg_cap;
+    size_t counters, status, status_bytes, stats, ess, cells, xface, queue, qcnt, pairs, stage, seg_cnt, seg_pos, flags,
+        recs, total;
+    uint64_t pairs_cap, recs_cap, queue_cap, ess_cap, seg_cap, stage_cap;
 };
 
 bool valid_dims(const uint32_t dims[3], int conn) {
@@ -79,7 +79,8 @@ bool valid_dims(const uint32_t dims[3], int conn) {
 
 // n vertices; ncross queue entries; ess_cap essential records (components);
 // slab: add the boundary-forest buffers
-Layout layout_for(uint64_t n, uint64_t ncross, bool slab = false, uint64_t ess_cap = ESS_CAP, uint64_t nxface = 0) {
+Layout layout_for(uint64_t n, uint64_t ncross, bool slab = false, uint64_t ess_cap = ESS_CAP, uint64_t nxface = 0,
+                  uint64_t stage_recs = 0) {
     Layout L{};
     // records = #minima.  On a grid the strict minima form an independent set,
     // so at most ceil(n/2) (+1 slack); a general graph (ess_cap = n) may have n.
@@ -105,10 +106,13 @@ Layout layout_for(uint64_t n, uint64_t ncross, bool slab = false, uint64_t ess_c
     L.queue = off;  // deduplicated tile-crossing edges
     L.queue_cap = ncross;
     off += align_up(ncross * mt::cross_queue_entry_bytes());
+    L.qcnt = off;   // stepped queue: survivors per step of the enumeration (steps of >= 128 edges)
+    off += align_up((ncross + 127) / 128 * sizeof(uint32_t));
     L.pairs = off;
     off += align_up(L.pairs_cap * sizeof(mt_pair));
-    L.stage = off;    // diagram records staged by the repair (at most one per minimum)
-    off += align_up(L.pairs_cap * sizeof(mt_pair));
+    L.stage = off;    // diagram records staged by the repair (at most one per minimum, or fixed brick runs)
+    L.stage_cap = std::max(L.pairs_cap, stage_recs);
+    off += align_up(L.stage_cap * sizeof(mt_pair));
     L.seg_cnt = off;
     off += align_up(L.seg_cap * sizeof(uint16_t));
     L.seg_pos = off;
@@ -129,7 +133,7 @@ Layout layout_for(uint64_t n, uint64_t ncross, bool slab = false, uint64_t ess_c
 Layout grid_layout(const uint32_t dims[3], uint32_t z_begin, uint32_t z_end, bool slab) {
     const uint64_t n = uint64_t(dims[0]) * dims[1] * (z_end - z_begin);
     const mt::Slab sl{dims[0], dims[1], dims[2], z_begin, z_end, uint64_t(dims[0]) * dims[1] * z_begin, n};
-    return layout_for(n, mt::cross_edges(sl), slab, ESS_CAP, mt::xface_entries(sl));
+    return layout_for(n, mt::cross_edges(sl), slab, ESS_CAP, mt::xface_entries(sl), mt::repair_stage_records(sl));
 }
 
 }  // namespace
@@ -346,12 +350,13 @@ void launch_cross(mt_ctx* c, uint64_t* T0, cudaStream_t s) {
     unsigned long long* ctr = counters_of(c);
     unsigned long long* stats = stats_of(c);
     mark(c, "dedupe_cross", s);
+    uint32_t* qcnt = mt::cross_stepped() ? reinterpret_cast<uint32_t*>(c->ws + c->L.qcnt) : nullptr;
     int nl = mt::launch_dedupe_cross(c->f - c->slab.base, T0, xface_of(c), c->slab, c->flip, c->ws + c->L.queue,
-                                     c->L.queue_cap, ctr + mt::CTR_QLEN, stats, c->num_sms, s);
+                                     c->L.queue_cap, ctr + mt::CTR_QLEN, qcnt, stats, c->num_sms, s);
     if (nl) {
         mark(c, "merge_queue", s);
-        mt::launch_merge_queue(cells_of(c), c->ws + c->L.queue, c->L.queue_cap, ctr + mt::CTR_QLEN,
-                               ctr + mt::CTR_QFETCH, stats, c->num_sms, s);
+        mt::launch_merge_queue(cells_of(c), c->ws + c->L.queue, c->L.queue_cap, ctr + mt::CTR_QLEN, qcnt,
+                               mt::cross_steps(c->slab), ctr + mt::CTR_QFETCH, stats, c->num_sms, s);
         ++nl;
     }
     c->launches += nl;
@@ -378,7 +383,7 @@ mt_status finish_compute(mt_ctx* c, uint64_t* T, const mt::ForestRef* forest, cu
     mt_pair* out = target_of(c, &cap);
     mt_pair* ess = reinterpret_cast<mt_pair*>(c->ws + c->L.ess);
     const uint64_t base = c->slab.base;
-    const mt::RepairOut ro{reinterpret_cast<mt_pair*>(c->ws + c->L.stage), c->L.pairs_cap,
+    const mt::RepairOut ro{reinterpret_cast<mt_pair*>(c->ws + c->L.stage), c->L.stage_cap,
                            reinterpret_cast<uint16_t*>(c->ws + c->L.seg_cnt),
                            reinterpret_cast<uint32_t*>(c->ws + c->L.seg_pos), ctr};
     mark(c, "repair", s);
@@ -497,8 +502,8 @@ mt_status mt_compute_graph(mt_ctx* c, const float* f, const uint64_t* row, const
     mt::launch_graph_edges(row, col, uint32_t(c->n), cells, nullptr, c->ws + c->L.queue, c->L.queue_cap,
                            ctr + mt::CTR_QLEN, ctr, c->num_sms, s);
     mark(c, "merge_queue", s);
-    mt::launch_merge_queue(cells, c->ws + c->L.queue, c->L.queue_cap, ctr + mt::CTR_QLEN, ctr + mt::CTR_QFETCH, stats,
-                           c->num_sms, s);
+    mt::launch_merge_queue(cells, c->ws + c->L.queue, c->L.queue_cap, ctr + mt::CTR_QLEN, nullptr, 0,
+                           ctr + mt::CTR_QFETCH, stats, c->num_sms, s);
     c->launches = 4;
     return finish_compute(c, T, nullptr, s);
 }

@@ -45,6 +45,15 @@ namespace {
 #ifndef MT_REPAIR_BLOCK
 #define MT_REPAIR_BLOCK 1   // volumes (with ZPAIR): bricks in 4 x 4 x 4 blocks of tile columns (c5 repair 9.89 -> 9.67 ms)
 #endif
+#ifndef MT_REPAIR_STOP
+#define MT_REPAIR_STOP 0    // timing only (WRONG results): 1 the T0 -> T stream alone, 2 + cells and records
+#endif
+#ifndef MT_REPAIR_FIXSTAGE
+#define MT_REPAIR_FIXSTAGE 1  // grid bricks stage their records at a fixed offset (no global atomic; c5 repair 9.67 -> 8.91 ms)
+#endif
+#ifndef MT_REPAIR_PRE
+#define MT_REPAIR_PRE 0     // walks: the first cells of this many walks loaded together (0: off; 1, 2 or 4)
+#endif
 #ifndef MT_REPAIR_CHAIN
 #define MT_REPAIR_CHAIN 0   // a thread's walks in threshold order, chained from a shared start
 #endif
@@ -221,6 +230,12 @@ repair_brick_kernel(View view, const Cell* C, uint64_t* __restrict__ T, const fl
     } else {
         mins = inb;
     }
+    if (MT_REPAIR_STOP == 1 && TILED) {   // timing only (WRONG results): the T0 -> T stream alone
+#pragma unroll
+        for (int k = 0; k < RB_PER; ++k)
+            if (INB(k)) T[UID(k)] = pack(sv[k], xs[k]);
+        return;
+    }
 #pragma unroll
     for (int k = 0; k < RB_PER; ++k) {
         if (!((mins >> k) & 1u)) continue;
@@ -268,7 +283,14 @@ repair_brick_kernel(View view, const Cell* C, uint64_t* __restrict__ T, const fl
         }
         const uint32_t all = __shfl_sync(FULL_MASK, incl, 31);
         uint32_t base = 0;
-        if (lane == 0 && all) base = uint32_t(atomicAdd(counters + CTR_STAGE, (unsigned long long)all));
+        if (MT_REPAIR_FIXSTAGE && !LINEAR) {
+            // grid bricks: a fixed run of RB_NV / 2 records per brick (its records are strict
+            // minima, an independent set of the bipartite brick, so at most half its vertices):
+            // no global atomic, no wait for one
+            base = uint32_t(blockIdx.x) * uint32_t(RB_NV / 2);
+        } else if (lane == 0 && all) {
+            base = uint32_t(atomicAdd(counters + CTR_STAGE, (unsigned long long)all));
+        }
         if (lane == 0) S.base = base;
     }
 
@@ -318,9 +340,15 @@ repair_brick_kernel(View view, const Cell* C, uint64_t* __restrict__ T, const fl
         else atomicOr(counters + CTR_ERR, ERR_CAPACITY);
     }
 
+    if (MT_REPAIR_STOP == 2 && TILED) {   // timing only (WRONG results): no walks
+#pragma unroll
+        for (int k = 0; k < RB_PER; ++k)
+            if (INB(k)) T[UID(k)] = pack(sv[k], xs[k]);
+        return;
+    }
     // Rep(u, key(s)): walk from v through cells with key(s') <= key(s) that are not roots
     unsigned long long hops = 0;   // (COUNT builds only: mt_set_stats)
-    uint32_t moved = 0;       // rows whose walk left its start (bit k)
+    [[maybe_unused]] uint32_t moved = 0;   // rows whose walk left its start (bit k)
 #if MT_REPAIR_CHAIN
     // The thread's walks in ascending threshold order, each continuing from the result of the
     // previous walk when both start at the same vertex: the cells are read-only here, so the
@@ -354,30 +382,81 @@ repair_brick_kernel(View view, const Cell* C, uint64_t* __restrict__ T, const fl
         cx(0, 2);
         cx(1, 3);
         cx(1, 2);
+        // memo: the previous walk's start, result and the result's cell (which stopped that walk:
+        // a root or a saddle above its threshold) -- a chained walk first tests that cell in
+        // registers, so it loads nothing when the same cell stops it too
         uint32_t memo_x0 = ~0u, memo_res = 0;
+        Cell memo_c{0, 0};
 #pragma unroll
         for (int r = 0; r < RB_PER; ++r) {
             if (!((ti[r] >> 9) & 1u)) continue;
             uint32_t x = tx[r];
             if ((ti[r] >> 8) & 1u) {
                 const uint32_t x0 = x;
-                if (x0 == memo_x0) x = memo_res;
+                Cell c{0, 0};
+                bool have = false;
+                if (x0 == memo_x0) {
+                    x = memo_res;
+                    c = memo_c;
+                    have = true;
+                }
 #pragma unroll 1
                 while (true) {
-                    const Cell c = view.cell(C, x);
+                    if (!have) c = view.cell(C, x);
+                    have = false;
                     if (cv_of(c) == x || c.lo > tk[r]) break;   // Alg. 4, reading R20
                     x = cv_of(c);
                     if (COUNT) ++hops;
                 }
                 memo_x0 = x0;
                 memo_res = x;
+                memo_c = c;
             }
             T[S.rowbase[warp + 16 * (ti[r] & 0xffu)] + lane] = pack(ts[r], x);
         }
     }
 #elif MT_REPAIR_SEQ
     // one walk after the other (the loop runs the sum of the chain lengths, not RB_PER times
-    // the longest)
+    // the longest); MT_REPAIR_PRE: the first cells of MT_REPAIR_PRE walks are loaded together
+    // (independent loads in flight), the walks then continue one after the other
+#if MT_REPAIR_PRE
+    static_assert(RB_PER % MT_REPAIR_PRE == 0, "MT_REPAIR_PRE divides the vertices per thread");
+#pragma unroll
+    for (int k0 = 0; k0 < RB_PER; k0 += MT_REPAIR_PRE) {
+        uint64_t plo[MT_REPAIR_PRE];
+        uint32_t pv[MT_REPAIR_PRE];
+#pragma unroll
+        for (int j = 0; j < MT_REPAIR_PRE; ++j) {
+            const int k = k0 + j;
+            plo[j] = 0;
+            pv[j] = 0;
+            if (INB(k) && xs[k] != uint32_t(UID(k))) {
+                const Cell c = view.cell(C, xs[k]);
+                plo[j] = c.lo;
+                pv[j] = cv_of(c);
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < MT_REPAIR_PRE; ++j) {
+            const int k = k0 + j;
+            if (!INB(k) || xs[k] == uint32_t(UID(k))) continue;
+            uint32_t x = xs[k];
+            uint64_t clo = plo[j];
+            uint32_t cv = pv[j];
+#pragma unroll 1
+            while (true) {
+                if (cv == x || clo > key[k]) break;   // Alg. 4, reading R20
+                x = cv;
+                if (COUNT) ++hops;
+                const Cell c = view.cell(C, x);
+                clo = c.lo;
+                cv = cv_of(c);
+            }
+            moved |= uint32_t(x != xs[k]) << k;
+            xs[k] = x;
+        }
+    }
+#else
 #pragma unroll
     for (int k = 0; k < RB_PER; ++k) {
         if (!INB(k) || xs[k] == uint32_t(UID(k))) continue;
@@ -392,6 +471,7 @@ repair_brick_kernel(View view, const Cell* C, uint64_t* __restrict__ T, const fl
         moved |= uint32_t(x != xs[k]) << k;
         xs[k] = x;
     }
+#endif
 #else
     // the thread's walks advance in lock-step rounds: independent load chains in flight
     uint32_t act = 0;
@@ -635,6 +715,12 @@ uint64_t repair_segments(const Slab& sl) {
     return nseg;
 }
 uint64_t repair_segments_bound(uint64_t n) { return n / 16 + 2; }
+uint64_t repair_stage_records(const Slab& sl) {
+    BrickGeom g;
+    uint64_t nb, nseg;
+    if (!MT_REPAIR_FIXSTAGE || sl.n == 0 || !brick_mode(sl, &g, &nb, &nseg)) return 0;
+    return nb * uint64_t(RB_NV / 2);
+}
 static int diagram_spt(uint64_t nseg) { return nseg >= DG_BIG ? 4 : 1; }
 uint64_t diagram_tiles(uint64_t nseg) {
     const uint64_t per = uint64_t(THREADS) * diagram_spt(nseg);
