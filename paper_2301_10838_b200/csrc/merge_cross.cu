@@ -354,6 +354,9 @@ dedupe_cross_kernel(const float* __restrict__ f, const uint64_t* __restrict__ T0
 #ifndef MQ_CSPLIT
 #define MQ_CSPLIT 1       // path splitting inside the Alg. 3 climbs (with MQ_WALK 0)
 #endif
+#ifndef MQ_BATCH
+#define MQ_BATCH 256      // queue entries a warp takes per fetch (one global atomic each)
+#endif
 #ifndef MQ_MIN_BLOCKS
 #define MQ_MIN_BLOCKS 4   // 4 x 256 threads per SM: <= 64 registers (the climbs keep their previous cells), 32 warps of loads in flight
 #endif
@@ -365,7 +368,7 @@ __global__ void __launch_bounds__(256, MQ_MIN_BLOCKS)
 merge_queue_kernel(Cell* C, const QEntry* __restrict__ q, uint64_t cap, const unsigned long long* __restrict__ qlen,
                    const uint32_t* __restrict__ qcnt, uint64_t nsteps, unsigned long long* __restrict__ fetch,
                    unsigned long long* __restrict__ stats) {
-    constexpr uint64_t BATCH = 256;
+    constexpr uint64_t BATCH = MQ_BATCH;
     constexpr uint64_t STEP = DC_THREADS;   // stepped queue: entries per dedupe_cross step
     const int lane = threadIdx.x & 31;
     const uint64_t qn = *reinterpret_cast<const volatile unsigned long long*>(qlen);

@@ -54,6 +54,9 @@ namespace {
 #ifndef MT_REPAIR_PRE
 #define MT_REPAIR_PRE 0     // walks: the first cells of this many walks loaded together (0: off; 1, 2 or 4)
 #endif
+#ifndef MT_REPAIR_SEGSTAGE
+#define MT_REPAIR_SEGSTAGE 0  // grid bricks: 16 staging slots per segment (no prefix, no barrier)
+#endif
 #ifndef MT_REPAIR_CHAIN
 #define MT_REPAIR_CHAIN 0   // a thread's walks in threshold order, chained from a shared start
 #endif
@@ -258,10 +261,15 @@ repair_brick_kernel(View view, const Cell* C, uint64_t* __restrict__ T, const fl
             S.rowem[warp + 16 * k] = em;
         }
     }
-    __syncthreads();   // hash set initialised, row counts in
+    // MT_REPAIR_SEGSTAGE (grid bricks): every segment (row) stages its records at a fixed run of
+    // 16 (strict minima of <= 32 x-consecutive vertices: an independent set of a path, so at most
+    // half of them), so a warp needs nothing from the other warps: no barrier, no brick prefix
+    constexpr bool SEGST = MT_REPAIR_SEGSTAGE && !LINEAR;
+    if (SEGST) __syncwarp();
+    else __syncthreads();   // row counts in
 
     // warp 0: the brick's staging run (one global atomic) and each row's offset in it
-    if (warp == 0) {
+    if (!SEGST && warp == 0) {
         uint32_t c[RB_ROWS / 32], tot = 0;
 #pragma unroll
         for (int j = 0; j < RB_ROWS / 32; ++j) {
@@ -294,19 +302,19 @@ repair_brick_kernel(View view, const Cell* C, uint64_t* __restrict__ T, const fl
         if (lane == 0) S.base = base;
     }
 
-    __syncthreads();   // staging base and row offsets in
+    if (!SEGST) __syncthreads();   // staging base and row offsets in
 
     // staging records of every row, in id order within the row: finite pairs, then roots.
     // Lanes 0..7 publish the counts and staging offsets of the warp's 8 rows; then every lane
     // stages only its own records (few: ~5 % of the vertices at c5), so the record code runs
     // max-over-lanes times instead of once per row
-    const uint32_t sbase = S.base;
+    const uint32_t sbase = SEGST ? 0u : S.base;
     if (lane < RB_PER) {
         const int r = warp + 16 * lane;
         if (S.rowlim[r] > 0) {   // every row holding a vertex of the grid is a segment
             const uint64_t seg = S.rowseg[r];
             seg_cnt[seg] = uint16_t(S.rowcnt[r] & 0xffffu) | uint16_t((S.rowcnt[r] >> 16) << 8);
-            seg_pos[seg] = sbase + S.rowoff[r];
+            if (!SEGST) seg_pos[seg] = sbase + S.rowoff[r];
         }
     }
     uint32_t rm = (recbits | (recbits >> 8)) & 0xffu;
@@ -322,7 +330,7 @@ repair_brick_kernel(View view, const Cell* C, uint64_t* __restrict__ T, const fl
         // than a dynamically indexed register array
         const Cell cu = ld_cell_ro(C + u);
         const uint32_t s = cs_of(cu), ou = uint32_t(cu.hi >> 32), os = uint32_t(cu.lo >> 32);
-        const uint64_t pos = uint64_t(sbase) + S.rowoff[r] +
+        const uint64_t pos = (SEGST ? S.rowseg[r] * 16u : uint64_t(sbase) + S.rowoff[r]) +
                              (isf ? __popc(fm & lt) : __popc(fm) + __popc(em & lt));
         mt_pair rec;
         if (isf) {
@@ -523,7 +531,7 @@ __global__ void __launch_bounds__(THREADS)
 diagram_kernel(const uint16_t* __restrict__ seg_cnt, const uint32_t* __restrict__ seg_pos, uint64_t nseg,
                const mt_pair* __restrict__ stage, unsigned long long* __restrict__ counters, Cell* __restrict__ status,
                mt_pair* __restrict__ out, uint64_t out_cap, mt_pair* __restrict__ ess, uint64_t ess_cap,
-               uint64_t ntiles) {
+               uint64_t ntiles, bool seg16) {
     __shared__ uint64_t s_tile;
     __shared__ uint32_t s_w[THREADS / 32], s_we[THREADS / 32];
     __shared__ uint64_t s_prefix, s_eprefix;
@@ -547,7 +555,7 @@ diagram_kernel(const uint16_t* __restrict__ seg_cnt, const uint32_t* __restrict_
     mt_pair first[DG_SPT];
 #pragma unroll
     for (int j = 0; j < DG_SPT; ++j) {
-        spos[j] = cnts[j] ? seg_pos[seg + j] : 0u;
+        spos[j] = cnts[j] ? (seg16 ? uint32_t((seg + j) * 16u) : seg_pos[seg + j]) : 0u;
         if (cnts[j]) first[j] = stage[spos[j]];
     }
     // block-wide exclusive scans (finite, essential)
@@ -718,8 +726,9 @@ uint64_t repair_segments_bound(uint64_t n) { return n / 16 + 2; }
 uint64_t repair_stage_records(const Slab& sl) {
     BrickGeom g;
     uint64_t nb, nseg;
-    if (!MT_REPAIR_FIXSTAGE || sl.n == 0 || !brick_mode(sl, &g, &nb, &nseg)) return 0;
-    return nb * uint64_t(RB_NV / 2);
+    if (sl.n == 0 || !brick_mode(sl, &g, &nb, &nseg)) return 0;
+    if (MT_REPAIR_SEGSTAGE) return nseg * 16;
+    return MT_REPAIR_FIXSTAGE ? nb * uint64_t(RB_NV / 2) : 0;
 }
 static int diagram_spt(uint64_t nseg) { return nseg >= DG_BIG ? 4 : 1; }
 uint64_t diagram_tiles(uint64_t nseg) {
@@ -738,16 +747,19 @@ void launch_repair(const Cell* C, uint64_t* T, const float* f, const Slab& sl, u
 void launch_diagram(const Slab& sl, const RepairOut& o, void* status, mt_pair* out, uint64_t out_cap, mt_pair* ess,
                     uint64_t ess_cap, cudaStream_t stream) {
     const uint64_t nseg = sl.n ? repair_segments(sl) : 0;
+    BrickGeom bg;
+    uint64_t bnb, bns;
+    const bool seg16 = MT_REPAIR_SEGSTAGE && sl.n && brick_mode(sl, &bg, &bnb, &bns);   // as the repair staged
     const uint64_t ntiles = diagram_tiles(nseg);
     if (ntiles == 0) return;
     if (diagram_spt(nseg) == 4)
         diagram_kernel<4><<<uint32_t(ntiles), THREADS, 0, stream>>>(o.seg_cnt, o.seg_pos, nseg, o.stage, o.counters,
                                                                     static_cast<Cell*>(status), out, out_cap, ess,
-                                                                    ess_cap, ntiles);
+                                                                    ess_cap, ntiles, seg16);
     else
         diagram_kernel<1><<<uint32_t(ntiles), THREADS, 0, stream>>>(o.seg_cnt, o.seg_pos, nseg, o.stage, o.counters,
                                                                     static_cast<Cell*>(status), out, out_cap, ess,
-                                                                    ess_cap, ntiles);
+                                                                    ess_cap, ntiles, seg16);
 }
 
 void launch_finish_diagram(unsigned long long* counters, mt_pair* out, uint64_t out_cap, mt_pair* ess,
