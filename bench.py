@@ -393,7 +393,7 @@ def run_mt(args, rank, world):
     # sequential copies around each distributed step.
     e2e = None
     if not args.no_e2e:
-        e2e_steps = max(2, min(args.steps, 5))
+        e2e_steps = max(2, min(args.steps, 10))   # (a longer run amortises the pipeline fill: H2D(0) + compute(0))
         f_host = torch.from_numpy(f_np).pin_memory()
         cap = (n_local + 1) // 2 + 2
         if world == 1:
