@@ -76,6 +76,12 @@ namespace {
 #ifndef TILE_TQ
 #define TILE_TQ 6      // basin-pair table: TILE_TQ / 4 slots per tile vertex
 #endif
+#ifndef TILE_CLIMB2
+#define TILE_CLIMB2 0  // merge loop: two climb steps per iteration
+#endif
+#ifndef TILE_RCHAIN
+#define TILE_RCHAIN 1  // in-tile repair: a walk continues the thread's previous one (same start, higher threshold)
+#endif
 #ifndef TILE_ZREG
 #define TILE_ZREG 1    // volumes: the +-z neighbours' order keys / basins from the thread's own registers
 #endif
@@ -971,6 +977,13 @@ tile_tmt_kernel(const __grid_constant__ CUtensorMap fmap, const float* __restric
                     // the two climbs are independent under one S: both advance in this iteration
                     if (up_u) mu = c_v(cu);
                     if (up_v) mv = c_v(cv);
+                    if (TILE_CLIMB2) {
+                        // (one more step of each climb still under way: the loop's refill and vote
+                        // overhead is paid once for two climb steps)
+                        const uint64_t cu2 = up_u ? sld64(cell + mu) : 0ull, cv2 = up_v ? sld64(cell + mv) : 0ull;
+                        if (up_u && c_v(cu2) != mu && cu2 < S16) mu = c_v(cu2);
+                        if (up_v && c_v(cv2) != mv && cv2 < S16) mv = c_v(cv2);
+                    }
                 } else if (up_u) {
                     mu = c_v(cu);
                 } else if (up_v) {
@@ -1051,19 +1064,32 @@ tile_tmt_kernel(const __grid_constant__ CUtensorMap fmap, const float* __restric
     // reads them, so the representatives stay in registers and go straight to phase f
     uint32_t rep[PER];
 #if TILE_REP_SEQ
-    // one walk after the other (the loops run the sum of the chain lengths)
+    // one walk after the other (the loops run the sum of the chain lengths).  TILE_RCHAIN: a walk
+    // that starts where the previous one of the thread started, at a threshold not below it,
+    // continues from the previous result (the cells are read-only here, so the chain from a start
+    // is fixed and Rep(x, a') for a' >= a lies on it past Rep(x, a)); the thread's vertices form a
+    // z column and mostly share their basin
+    [[maybe_unused]] uint32_t pc_x0 = 0xffffffffu, pc_res = 0;
+    [[maybe_unused]] uint64_t pc_a16 = 0;
 #pragma unroll
     for (int k = 0; k < PER; ++k) {
         const uint64_t cu = cell[(r0 + k * RSTEP) * TX + lx];
         uint32_t x = c_v(cu);
         if (TILE_STOP == 0 || TILE_STOP > 4) {
             const uint64_t a16 = cu | 0xffffull;   // c_key(cx) > c_key(cu)  <=>  cx > a16
+            const uint32_t x0 = x;
+            if (TILE_RCHAIN && x0 == pc_x0 && a16 >= pc_a16) x = pc_res;
 #pragma unroll 1
             while (true) {
                 const uint64_t cx = cell[x];
                 if (c_v(cx) == x || cx > a16) break;
                 x = c_v(cx);
                 if (STATS) ++n_rep;
+            }
+            if (TILE_RCHAIN) {
+                pc_x0 = x0;
+                pc_a16 = a16;
+                pc_res = x;
             }
         }
         rep[k] = x;
