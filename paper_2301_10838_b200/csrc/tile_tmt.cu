@@ -76,6 +76,9 @@ namespace {
 #ifndef TILE_TQ
 #define TILE_TQ 6      // basin-pair table: TILE_TQ / 4 slots per tile vertex
 #endif
+#ifndef TILE_FULLSECTOR
+#define TILE_FULLSECTOR 0  // tile minima cells written as whole 32-B sectors (a copy in the partner slot)
+#endif
 #ifndef TILE_CLIMB2
 #define TILE_CLIMB2 0  // merge loop: two climb steps per iteration
 #endif
@@ -1154,7 +1157,18 @@ tile_tmt_kernel(const __grid_constant__ CUtensorMap fmap, const float* __restric
         T0[gu] = t0;
         // the tile's x faces (lanes 0 and 31) again, compactly (in the grid they are 128 B apart)
         if (lx == 0 || lx == TX - 1) xface[(uint64_t(b) * 2 + (lx == TX - 1)) * ROWS + r] = t0;
-        if (minimum) C[gu] = make_cell(key_of(uint32_t(cu >> 32), s == u ? gu : gid(s)), ou, gv);
+        if (minimum) {
+            const Cell cc = make_cell(key_of(uint32_t(cu >> 32), s == u ? gu : gid(s)), ou, gv);
+            // TILE_FULLSECTOR, even nx: the cell's 32-B sector partner is its x neighbour gu ^ 1 in
+            // the same row and tile, never a tile minimum, so one 256-bit store writes the cell into
+            // both slots: the whole sector is written and L2 needs no DRAM fill for a partial write
+            if (TILE_FULLSECTOR && !(nx & 1u))
+                asm volatile("st.global.v4.b64 [%0], {%1, %2, %1, %2};" ::"l"(C + (gu & ~1u)), "l"(cc.lo),
+                             "l"(cc.hi)
+                             : "memory");
+            else
+                C[gu] = cc;
+        }
     }
     phase_time(ST_CYC_WRITE);
     }   // pass
