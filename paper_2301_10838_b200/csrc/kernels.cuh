@@ -188,9 +188,11 @@ void launch_filter_diagram(const mt_pair* in, uint64_t n_fin, uint64_t n_all, fl
 void launch_forest_mark(const Cell* C, const uint64_t* T0, const Slab& sl, bool has_bottom, bool has_top,
                         uint8_t* flag, cudaStream_t stream);
 // records with slab-local ids (compressed ids = local ids)
-void launch_forest_compact(const Cell* C, const uint64_t* T0, const float* f, const Slab& sl, const uint8_t* flag,
-                           mt_forest_record* recs, uint64_t cap, unsigned long long* count, int num_sms,
-                           cudaStream_t stream);
+// (the face vertices' records at fixed slots: the bottom face first, then the top face, then the
+// rest; returns the kernels launched)
+int launch_forest_compact(const Cell* C, const uint64_t* T0, const float* f, const Slab& sl, const uint8_t* flag,
+                          mt_forest_record* recs, uint64_t cap, unsigned long long* count, bool has_bottom,
+                          bool has_top, int num_sms, cudaStream_t stream);
 // wide mode: the records' compressed ids (top face from local id top_begin on; UINT64_MAX: none);
 // scratch >= forest_compress_scratch_bytes(n); returns the kernels launched
 size_t forest_compress_scratch_bytes(uint64_t n);
@@ -206,9 +208,10 @@ void launch_forest_build(const mt_forest_record* all, uint64_t n_all, const Fore
 // inter-slab edges: deduplicated by tile-representative pairs into `queue`, then merged;
 // boundary k joins view ids a0[k] + r and b0[k] + r, r < nx ny
 size_t forest_queue_entry_bytes();
+// ia0 / ib0 (or null): record index of vertex (0, 0) of each boundary's lower / upper face
 void launch_forest_merge(const ForestRef& F, const Slab& sl, uint32_t nslabs, const uint32_t* a0, const uint32_t* b0,
-                         void* queue, unsigned long long* qlen, unsigned long long* fetch, int num_sms,
-                         cudaStream_t stream);
+                         const uint32_t* ia0, const uint32_t* ib0, void* queue, unsigned long long* qlen,
+                         unsigned long long* fetch, int num_sms, cudaStream_t stream);
 void launch_forest_writeback(const ForestRef& F, uint64_t n_all, Cell* C, const uint64_t* T0, const Slab& sl,
                              int num_sms, cudaStream_t stream);
 // view ids -> 64-bit global ids

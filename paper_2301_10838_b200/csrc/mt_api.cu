@@ -682,9 +682,8 @@ mt_status mt_compute_local(mt_ctx* c, const float* f, uint64_t* T, uint32_t flag
     mark(c, "forest_compact", s);
     mt_forest_record* recs = reinterpret_cast<mt_forest_record*>(c->ws + c->L.recs);
     unsigned long long* fcount = counters_of(c) + mt::CTR_FCOUNT;
-    mt::launch_forest_compact(cells_of(c), T - c->slab.base, f - c->slab.base, c->slab, flag, recs, c->L.recs_cap,
-                              fcount, c->num_sms, s);
-    c->launches += 2;
+    c->launches += 1 + mt::launch_forest_compact(cells_of(c), T - c->slab.base, f - c->slab.base, c->slab, flag, recs,
+                                                 c->L.recs_cap, fcount, has_bottom, has_top, c->num_sms, s);
     if (c->wide) {   // the flags are dead after the compaction: their space holds the bitmap
         mark(c, "forest_compress", s);
         const uint64_t sxy = uint64_t(c->nx) * c->ny;
@@ -773,11 +772,15 @@ mt_status mt_compute_global(mt_ctx* c, const mt_forest_record* all, const uint64
     } else {
         for (uint32_t k = 0; k < nslabs; ++k) X.voff[k] = uint32_t(X.real_base[k]);
     }
-    uint32_t a0[mt::MAX_SLABS], b0[mt::MAX_SLABS];
+    uint32_t a0[mt::MAX_SLABS], b0[mt::MAX_SLABS], ia0[mt::MAX_SLABS], ib0[mt::MAX_SLABS];
     for (uint32_t k = 0; k + 1 < nslabs; ++k) {   // the faces of boundary k in the view
         const bool one_plane = z_bounds[k + 1] - z_bounds[k] == 1;   // its top face is its bottom face
         a0[k] = uint32_t(one_plane ? X.voff[k] : X.voff[k] + span[k] - sxy);
         b0[k] = X.voff[k + 1];
+        // their records' fixed slots (forest_compact): slab k's top face after its bottom face
+        // (none for slab 0; a one-plane slab has one face region), slab k + 1's bottom face first
+        ia0[k] = uint32_t(X.rec_off[k] + ((k > 0 && !one_plane) ? sxy : 0));
+        ib0[k] = uint32_t(X.rec_off[k + 1]);
     }
     DeviceGuard g(c->device);
     if (!g.ok) return MT_ERR_CUDA;
@@ -800,7 +803,7 @@ mt_status mt_compute_global(mt_ctx* c, const mt_forest_record* all, const uint64
         return c->sticky = MT_ERR_CUDA;
     mt::launch_forest_build(all, n_all, X, table, vtable, tsize - 1, fcells, vid, dec, c->num_sms, s);
     mark(c, "forest_merge", s);
-    mt::launch_forest_merge(F, c->slab, nslabs, a0, b0, fqueue, counters_of(c) + mt::CTR_FQLEN,
+    mt::launch_forest_merge(F, c->slab, nslabs, a0, b0, ia0, ib0, fqueue, counters_of(c) + mt::CTR_FQLEN,
                             counters_of(c) + mt::CTR_FFETCH, c->num_sms, s);
     mark(c, "forest_writeback", s);
     mt::launch_forest_writeback(F, n_all, cells_of(c), T - c->slab.base, c->slab, c->num_sms, s);

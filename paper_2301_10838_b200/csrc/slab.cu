@@ -36,6 +36,10 @@
 #include "common.cuh"
 #include "kernels.cuh"
 
+#ifndef FOREST_FACEIDX
+#define FOREST_FACEIDX 1   // face records at fixed slots; forest_dedupe indexes them directly
+#endif
+
 namespace mt {
 
 namespace {
@@ -86,19 +90,25 @@ forest_mark_kernel(const Cell* C, const uint64_t* T0, uint32_t nx, uint32_t ny, 
 __global__ void __launch_bounds__(256)
 forest_compact_kernel(const Cell* C, const uint64_t* T0, const float* f, uint64_t base, uint64_t n,
                       const uint8_t* __restrict__ flag, mt_forest_record* __restrict__ recs, uint64_t cap,
-                      unsigned long long* count) {
+                      unsigned long long* count, uint64_t bot_hi, uint64_t top_lo, uint64_t top_at, uint64_t nf) {
+    // FOREST_FACEIDX: the face vertices (every one is a record) take fixed slots -- the bottom face
+    // (local ids [0, bot_hi)) at its local id, the top face (from top_lo on) at top_at + offset --
+    // and the rest are appended after the nf face slots, so a face vertex's record index follows
+    // from its position (forest_dedupe reads the boundary records without id lookups)
     const int lane = threadIdx.x & 31;
     const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
     const uint32_t b = uint32_t(base);
     for (uint64_t l0 = uint64_t(blockIdx.x) * blockDim.x; l0 < n; l0 += stride) {
         const uint64_t l = l0 + threadIdx.x;
         const bool take = l < n && flag[l];
-        const uint32_t m = __ballot_sync(FULL_MASK, take);
+        const bool face = l < bot_hi || l >= top_lo;
+        const uint32_t m = __ballot_sync(FULL_MASK, take && !face);
         unsigned long long b0 = 0;
         if (lane == 0 && m) b0 = atomicAdd(count, (unsigned long long)__popc(m));
         b0 = __shfl_sync(FULL_MASK, b0, 0);
         if (take) {
-            const uint64_t pos = b0 + __popc(m & ((1u << lane) - 1u));
+            const uint64_t pos = l < bot_hi ? l : l >= top_lo ? top_at + (l - top_lo)
+                                                              : nf + b0 + __popc(m & ((1u << lane) - 1u));
             const uint32_t u = uint32_t(base + l);
             uint32_t rep, o;
             const uint32_t fb = __float_as_uint(f[u]);
@@ -285,8 +295,11 @@ forest_build_kernel(const mt_forest_record* __restrict__ all, uint64_t n_all, Fo
 struct BoundaryGeom {
     uint32_t nx, ny;
     uint32_t nb;                   // inter-slab boundaries
+    uint32_t direct;               // ia0 / ib0 valid (FOREST_FACEIDX)
     uint32_t a0[MAX_SLABS];        // view id of vertex (0, 0) of the lower face of boundary k
     uint32_t b0[MAX_SLABS];        // ... and of its upper face (faces are consecutive view ids)
+    uint32_t ia0[MAX_SLABS];       // record index of vertex (0, 0) of the lower face of boundary k
+    uint32_t ib0[MAX_SLABS];       // ... and of its upper face
 };
 
 // Inter-slab edges reduced to pairs of tile representatives (DESIGN.md derivation C-3, the
@@ -318,7 +331,15 @@ forest_dedupe_kernel(ForestRef F, BoundaryGeom g, FQEntry* __restrict__ q, unsig
         if (e < total) {
             const uint64_t k = e / sxy, r = e % sxy;
             const uint32_t a = g.a0[k] + uint32_t(r), b = g.b0[k] + uint32_t(r);
-            const uint32_t ia = forest_lookup(F, a), ib = forest_lookup(F, b);
+            uint32_t ia = FOREST_MISS, ib = FOREST_MISS;
+            if (g.direct) {   // the face records' fixed slots (forest_compact), checked against their ids
+                ia = g.ia0[k] + uint32_t(r);
+                ib = g.ib0[k] + uint32_t(r);
+                if (F.vid[ia] != a) ia = FOREST_MISS;
+                if (F.vid[ib] != b) ib = FOREST_MISS;
+            }
+            if (ia == FOREST_MISS) ia = forest_lookup(F, a);
+            if (ib == FOREST_MISS) ib = forest_lookup(F, b);
             if (ia == FOREST_MISS || ib == FOREST_MISS) {
                 atomicOr(F.err, ERR_FOREST);
             } else {
@@ -578,12 +599,29 @@ void launch_forest_mark(const Cell* C, const uint64_t* T0, const Slab& sl, bool 
                                                                 sl.base, flag);
 }
 
-void launch_forest_compact(const Cell* C, const uint64_t* T0, const float* f, const Slab& sl, const uint8_t* flag,
-                           mt_forest_record* recs, uint64_t cap, unsigned long long* count, int num_sms,
-                           cudaStream_t stream) {
-    if (sl.n == 0) return;
+__global__ void add_count_kernel(unsigned long long* count, uint64_t add) { *count += add; }
+
+int launch_forest_compact(const Cell* C, const uint64_t* T0, const float* f, const Slab& sl, const uint8_t* flag,
+                          mt_forest_record* recs, uint64_t cap, unsigned long long* count, bool has_bottom,
+                          bool has_top, int num_sms, cudaStream_t stream) {
+    if (sl.n == 0) return 0;
+    const uint64_t sxy = uint64_t(sl.nx) * sl.ny;
+    uint64_t bot_hi = 0, top_lo = ~0ull, top_at = 0, nf = 0;
+    if (FOREST_FACEIDX && sxy && sl.n % sxy == 0) {
+        if (has_bottom) bot_hi = sxy;
+        if (has_top && !(has_bottom && sl.n == sxy)) {   // (a one-plane slab's only plane: the bottom region)
+            top_lo = sl.n - sxy;
+            top_at = bot_hi;
+        }
+        nf = bot_hi + (top_lo == ~0ull ? 0 : sxy);
+    }
     forest_compact_kernel<<<grid_for(sl.n, num_sms), 256, 0, stream>>>(C, T0, f, sl.base, sl.n, flag, recs, cap,
-                                                                       count);
+                                                                       count, bot_hi, top_lo, top_at, nf);
+    if (nf) {
+        add_count_kernel<<<1, 1, 0, stream>>>(count, nf);   // the count covers the face slots too
+        return 2;
+    }
+    return 1;
 }
 
 size_t forest_compress_scratch_bytes(uint64_t n) {
@@ -626,16 +664,19 @@ void launch_forest_build(const mt_forest_record* all, uint64_t n_all, const Fore
 size_t forest_queue_entry_bytes() { return sizeof(FQEntry); }
 
 void launch_forest_merge(const ForestRef& F, const Slab& sl, uint32_t nslabs, const uint32_t* a0, const uint32_t* b0,
-                         void* queue, unsigned long long* qlen, unsigned long long* fetch, int num_sms,
-                         cudaStream_t stream) {
+                         const uint32_t* ia0, const uint32_t* ib0, void* queue, unsigned long long* qlen,
+                         unsigned long long* fetch, int num_sms, cudaStream_t stream) {
     if (nslabs < 2) return;
     BoundaryGeom g{};
     g.nx = sl.nx;
     g.ny = sl.ny;
     g.nb = nslabs - 1;
+    g.direct = (FOREST_FACEIDX && ia0 && ib0) ? 1u : 0u;
     for (uint32_t k = 0; k + 1 < nslabs; ++k) {
         g.a0[k] = a0[k];
         g.b0[k] = b0[k];
+        g.ia0[k] = g.direct ? ia0[k] : 0u;
+        g.ib0[k] = g.direct ? ib0[k] : 0u;
     }
     FQEntry* q = static_cast<FQEntry*>(queue);
     const uint64_t total = uint64_t(g.nx) * g.ny * g.nb;
