@@ -521,6 +521,9 @@ repair_brick_kernel(View view, const Cell* C, uint64_t* __restrict__ T, const fl
 // place in the diagram (ordered compaction: CTA scan + decoupled look-back);
 // the records are copied from the staging runs the repair wrote.
 constexpr int THREADS = 256;
+#ifndef DG_SPT_BIG
+#define DG_SPT_BIG 4        // diagram: segments per thread on grids of >= DG_BIG segments
+#endif
 #ifndef DG_BIG
 #define DG_BIG (1ull << 24) // diagram: from this many segments on, 4 segments per thread (fewer tiles in the
 #endif                      // look-back chain: c5 1.31 -> 1.07 ms in round 1; 1 below: c4 0.39 vs 0.56 ms)
@@ -730,7 +733,7 @@ uint64_t repair_stage_records(const Slab& sl) {
     if (MT_REPAIR_SEGSTAGE) return nseg * 16;
     return MT_REPAIR_FIXSTAGE ? nb * uint64_t(RB_NV / 2) : 0;
 }
-static int diagram_spt(uint64_t nseg) { return nseg >= DG_BIG ? 4 : 1; }
+static int diagram_spt(uint64_t nseg) { return nseg >= DG_BIG ? DG_SPT_BIG : 1; }
 uint64_t diagram_tiles(uint64_t nseg) {
     const uint64_t per = uint64_t(THREADS) * diagram_spt(nseg);
     return (nseg + per - 1) / per;
@@ -752,8 +755,8 @@ void launch_diagram(const Slab& sl, const RepairOut& o, void* status, mt_pair* o
     const bool seg16 = MT_REPAIR_SEGSTAGE && sl.n && brick_mode(sl, &bg, &bnb, &bns);   // as the repair staged
     const uint64_t ntiles = diagram_tiles(nseg);
     if (ntiles == 0) return;
-    if (diagram_spt(nseg) == 4)
-        diagram_kernel<4><<<uint32_t(ntiles), THREADS, 0, stream>>>(o.seg_cnt, o.seg_pos, nseg, o.stage, o.counters,
+    if (diagram_spt(nseg) == DG_SPT_BIG)
+        diagram_kernel<DG_SPT_BIG><<<uint32_t(ntiles), THREADS, 0, stream>>>(o.seg_cnt, o.seg_pos, nseg, o.stage, o.counters,
                                                                     static_cast<Cell*>(status), out, out_cap, ess,
                                                                     ess_cap, ntiles, seg16);
     else
