@@ -522,7 +522,7 @@ repair_brick_kernel(View view, const Cell* C, uint64_t* __restrict__ T, const fl
 // the records are copied from the staging runs the repair wrote.
 constexpr int THREADS = 256;
 #ifndef DG_SPT_BIG
-#define DG_SPT_BIG 4        // diagram: segments per thread on grids of >= DG_BIG segments
+#define DG_SPT_BIG 2        // diagram: segments per thread on grids of >= DG_BIG segments (c5: 2 0.98 ms, 4 1.04, 8 1.14)
 #endif
 #ifndef DG_BIG
 #define DG_BIG (1ull << 24) // diagram: from this many segments on, 4 segments per thread (fewer tiles in the
